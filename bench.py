@@ -1,0 +1,453 @@
+#!/usr/bin/env python3
+"""bench.py -- validate + transcode throughput on B200 (BASELINE.json metric), one JSON line.
+
+Workload: BASELINE config 4, the one the metric is quoted on at
+1/2/4/8 GPUs -- 8 GiB of mixed UTF-8 (config-0 mix), sharded over N ranks at character
+boundaries.  One STEP is one pass of the whole hot path over it:
+    utf16_length_from_utf8            (a11, exact output sizing)
+    utf8_to_utf16le   (validate+transcode, a1-a8, a10)
+    [N>1: NCCL all-gather of the 32-B shard records + combine kernel]
+    utf8_length_from_utf16le          (a11)
+    utf16le_to_utf8   (validate+transcode back, a9, a5-a8, a10)
+    [N>1: all-gather + combine]
+value = input bytes of both transcoding passes (n8 + 2*n16, all ranks) / step time, in GB/s
+(1e9).  Inputs (>= 1 GiB per rank) exceed the 126 MB L2, so no flush is needed.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+Under torchrun one process per GPU (NCCL); rank 0 prints the line.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "validate+transcode input GB/s per GPU at 1/2/4/8 (UTF-8->UTF-16LE->UTF-8), % of HBM roofline"
+UNIT = "GB/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="c4")
+    p.add_argument("--size-mib", type=int, default=0, help="override the config size (debug)")
+    p.add_argument("--e2e-steps", type=int, default=2)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--out", default="")
+    return p.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ------------------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.file = None
+
+    def start(self):
+        try:
+            self.file = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=self.file, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.file.flush()
+        self.file.seek(0)
+        rows = [ln.split(",") for ln in self.file.read().strip().splitlines() if ln.strip()]
+        os.unlink(self.file.name)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            r = [x.strip() for x in r]
+            try:
+                sm.append(float(r[1]))
+                smax.append(float(r[2]))
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, r[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------ peaks
+def hbm_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def ncu_traffic():
+    """DRAM bytes per launch of the dominant kernel from the committed ncu summary."""
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            d = json.load(f)
+        return d
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------------------------ sharding
+def plan(n: int, G: int):
+    """Nominal cuts k*floor(n/G) aligned down to 16 bytes."""
+    return [0] + [(k * (n // G)) & ~15 for k in range(1, G)] + [n]
+
+
+def load_shard(cfg, rank, G, size):
+    """Generate this rank's bytes [c_k - 16, c_{k+1} + 16) and back the two cuts off to
+    character starts with the library's cut rule.  Returns (host array, lo, hi, base)."""
+    import paper_2111_08692_b200 as ug
+    nom = plan(size, G)
+    c0, c1 = nom[rank], nom[rank + 1]
+    base = max(0, c0 - 16)
+    buf = synth.generate_range(cfg, base, min(size, c1 + 16))
+
+    def back(c):
+        if c in (0, size):
+            return c
+        i = c - base
+        return c - ug.utf8_cut_backoff(buf[max(0, i - 8):i + 8].tobytes(), i - max(0, i - 8))
+    return buf, back(c0), back(c1), base
+
+
+# ------------------------------------------------------------------------------ ours
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2111_08692_b200 as ug
+
+    G, rank, local = dist_env()
+    assert G == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={G}"
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if G > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = synth.CONFIGS[args.config]
+    size = cfg.size if not args.size_mib else args.size_mib << 20
+    t_gen = time.time()
+    host, lo, hi, base = load_shard(cfg, rank, G, size)
+    t_gen = time.time() - t_gen
+    n8 = hi - lo
+    hb, ha = min(lo, 3), min(size - hi, 3)
+    t_all = torch.from_numpy(host).to(dev)                      # bytes [base, ...)
+    t_in = t_all[lo - base: hi - base]
+    stream = torch.cuda.current_stream()
+
+    out16 = torch.empty(n8, dtype=torch.int16, device=dev)      # worst case: 1 unit per byte
+    out8 = torch.empty(n8, dtype=torch.uint8, device=dev)       # valid input: round trip = n8
+    rec = ug.record_buffer(dev, 2)
+    allrec = ug.record_buffer(dev, 2 * G)
+    res = ug.result_buffer(dev, 4)
+    lens = torch.zeros(2, dtype=torch.int64, device=dev)
+    offs = torch.zeros(2, dtype=torch.int64, device=dev)
+    R = ug.RECORD_BYTES
+
+    # setup pass (untimed): learn this rank's UTF-16 length for the reverse launch
+    ug.utf8_to_utf16le_shard_async(t_all, lo - base, n8, hb, ha, lo, out16, rec)
+    torch.cuda.synchronize()
+    r0 = ug.decode_records(rec[:R])[0]
+    assert r0.first_err == ug.NONE and r0.too_small == 0, r0
+    n16 = r0.count
+    u16 = out16[:n16]
+    # code points of this rank (reporting only): non-continuation bytes
+    nchar = int(((t_in & 0xC0) != 0x80).sum())
+    tot16 = torch.tensor([n16], dtype=torch.int64, device=dev)
+    if G > 1:
+        dist.all_reduce(tot16)
+    N16_global = int(tot16[0])
+
+    ev_f = []  # (start, end) events around each forward launch
+
+    def gather_combine(which):
+        if G > 1:
+            dist.all_gather_into_tensor(allrec[which * G * R:(which + 1) * G * R],
+                                        rec[which * R:(which + 1) * R])
+            ug.combine_records_async(allrec[which * G * R:], G, rank,
+                                     size if which == 0 else N16_global,
+                                     res[(2 + which) * 24:],
+                                     offs[which:])
+
+    def step(record_events=False):
+        ug.utf16_length_from_utf8_async(t_in, lens)
+        if record_events:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+        ug.utf8_to_utf16le_shard_async(t_all, lo - base, n8, hb, ha, lo, out16, rec)
+        if record_events:
+            e1.record(stream)
+            ev_f.append((e0, e1))
+        gather_combine(0)
+        ug.utf8_length_from_utf16le_async(u16, lens, len_off=8)
+        ug.utf16le_to_utf8_shard_async(u16, 0, n16, 0, 0, 0, out8, rec, rec_off=R)
+        gather_combine(1)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if G > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(torch.cuda.current_device() if "CUDA_VISIBLE_DEVICES" not in os.environ
+                          else local)
+    clocks.start()
+    launches0 = ug.launch_count()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for _ in range(args.steps):
+        step(record_events=True)
+    t1.record(stream)
+    torch.cuda.synchronize()
+    if G > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    launches = ug.launch_count() - launches0
+    clk = clocks.stop()
+    ms = t0.elapsed_time(t1)
+    fwd_ms = statistics.mean(a.elapsed_time(b) for a, b in ev_f)
+
+    # ---- verification (untimed): results, lengths, round trip on the device
+    r = ug.decode_records(rec)
+    assert r[0].first_err == ug.NONE and r[0].count == n16, r[0]
+    assert r[1].first_err == ug.NONE and r[1].count == n8, r[1]
+    assert int(lens[0]) == n16 and int(lens[1]) == n8
+    assert torch.equal(out8[:n8], t_in), "round trip differs from the input"
+    glob = None
+    if G > 1:
+        glob = ug.decode_results(res[48:96])
+        assert glob[0].error == 0 and glob[1].error == 0, glob
+
+    # ---- aggregate over ranks: max time, total units
+    tot = torch.tensor([ms, fwd_ms, float(n8), float(n16), float(nchar)], dtype=torch.float64,
+                       device=dev)
+    if G > 1:
+        mx = tot[:2].clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        sm = tot[2:].clone()
+        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        ms, fwd_ms = float(mx[0]), float(mx[1])
+        N8, N16, NCH = int(sm[0]), int(sm[1]), int(sm[2])
+    else:
+        N8, N16, NCH = n8, n16, nchar
+
+    ms_step = ms / args.steps
+    in_bytes = N8 + 2 * N16                      # both transcoding passes' inputs
+    value = in_bytes / (ms_step * 1e-3) / 1e9
+    gchar = 2 * NCH / (ms_step * 1e-3) / 1e9     # code points transcoded per step (both ways)
+    peak, peak_src = hbm_peak()
+    fwd_bytes = n8 + 2 * n16                     # algorithmic bytes of one forward launch
+    achieved = fwd_bytes / (fwd_ms * 1e-3) / 1e9
+    traffic = ncu_traffic()
+
+    # ---- end to end through the host-buffer API (pinned host memory, copies timed)
+    e2e = None
+    if not args.no_e2e:
+        e2e = run_e2e(args, ug, host[lo - base: hi - base], n16, G, rank, dev, dist)
+
+    cpu = None
+    if rank == 0 and G == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, size)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": G,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "u8/u16 (integer)", "data": "synthetic (seeded; DESIGN.md section 4)",
+            "config": {"workload": f"config 4: {size / 2**30:g} GiB mixed UTF-8 "
+                                   "(60% ASCII/25% 2B/10% 3B/5% 4B), validate + UTF-8->UTF-16LE "
+                                   "and back, sharded at character boundaries",
+                       "bytes_utf8": N8, "units_utf16": N16,
+                       "step": "len16 + utf8_to_utf16le + [allgather+combine] + len8 + "
+                               "utf16le_to_utf8 + [allgather+combine]",
+                       "parallelism": f"shard{G}", "l2": "inputs >= 1 GiB per rank > 126 MB L2; no flush",
+                       "per_gpu_gbs": round(value / G, 2),
+                       "gchar_per_s": round(gchar, 2), "gchar_per_s_per_gpu": round(gchar / G, 2),
+                       "chars": NCH,
+                       "forward_input_gbs": round(N8 / (fwd_ms * 1e-3) / 1e9 * 1, 2),
+                       "gen_seconds": round(t_gen, 1)},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(achieved / peak, 4),
+                         "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
+                         "kernel": "k_utf8<true> (utf8_to_utf16le)",
+                         "algorithmic_bytes_per_launch": fwd_bytes,
+                         "avg_launch_ms": round(fwd_ms, 4), "peak_source": peak_src},
+            "clocks": clk,
+            "gpu_launches": int(launches),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        s = json.dumps(line)
+        print(s, flush=True)
+        if args.out:
+            with open(args.out, "w") as f:
+                f.write(s + "\n")
+    if G > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def run_e2e(args, ug, host_shard, n16, G, rank, dev, dist):
+    """Same step through the public host-buffer API: H2D of the step's input from pinned host
+    memory, the fused kernel, D2H of the result, both directions; wall clock, max over ranks."""
+    import torch
+    n8 = host_shard.size
+    hin = torch.from_numpy(host_shard).pin_memory()
+    h16 = torch.empty(n8, dtype=torch.int16).pin_memory()
+    h8 = torch.empty(n8, dtype=torch.uint8).pin_memory()
+    K = max(1, args.e2e_steps)
+    ug.utf8_to_utf16le_host(hin[:1 << 20], h16)      # warm the staging buffers
+    times = []
+    for _ in range(K + 1):
+        if G > 1:
+            dist.barrier()
+        t = time.perf_counter()
+        r1 = ug.utf8_to_utf16le_host(hin, h16)
+        r2 = ug.utf16le_to_utf8_host(h16[: r1.written], h8)
+        times.append(time.perf_counter() - t)
+        assert r1 == (0, n8, n16) and r2 == (0, n16, n8), (r1, r2)
+    dt = min(times[1:]) if len(times) > 1 else times[0]
+    tt = torch.tensor([dt, float(n8), float(n16)], dtype=torch.float64, device=dev)
+    if G > 1:
+        a = tt[:1].clone()
+        dist.all_reduce(a, op=dist.ReduceOp.MAX)
+        b = tt[1:].clone()
+        dist.all_reduce(b, op=dist.ReduceOp.SUM)
+        dt, N8, N16 = float(a[0]), int(b[0]), int(b[1])
+    else:
+        N8, N16 = n8, n16
+    assert bytes(h8[:1 << 16].numpy()) == host_shard[:1 << 16].tobytes()
+    return {"value": round((N8 + 2 * N16) / dt / 1e9, 3), "unit": UNIT,
+            "h2d_bytes_per_step": N8 + 2 * N16, "d2h_bytes_per_step": 2 * N16 + N8,
+            "steps": K, "api": "utf8_to_utf16le_host + utf16le_to_utf8_host (pinned)",
+            "seconds_per_step": round(dt, 4)}
+
+
+# ------------------------------------------------------------------------------ CPU legs
+def oracle_step(oracle, chunk: np.ndarray):
+    """The hot path on the CPU oracle, as it stands: sizing, forward, sizing, reverse."""
+    n16 = oracle.utf16_length_from_utf8(chunk)
+    r1, u = oracle.utf8_to_utf16le(chunk, out_cap=n16)
+    n8 = oracle.utf8_length_from_utf16le(u)
+    r2, back = oracle.utf16le_to_utf8(u, out_cap=n8)
+    assert r1.error == 0 and r2.error == 0 and back.size == chunk.size
+    return chunk.size + 2 * u.size
+
+
+def cpu_baseline(cfg, size, chunks=None):
+    """The oracle on the host cores: independent 64 MiB generator chunks (each is whole,
+    valid text, so the unmodified oracle runs on each), one per thread (ctypes releases the
+    GIL).  Bounded sample: min(#cores, 16) chunks."""
+    import oracle
+    oracle.build()
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    nch = chunks or max(1, min(cores, 16, size // synth.CHUNK))
+    data = [np.frombuffer(synth.gen_chunk(cfg.mix, cfg.encoding, min(synth.CHUNK, size),
+                                          cfg.seed, c), dtype=np.uint8) for c in range(nch)]
+    t = time.perf_counter()
+    with ThreadPoolExecutor(nch) as ex:
+        tot = sum(ex.map(lambda c: oracle_step(oracle, c), data))
+    dt = time.perf_counter() - t
+    return {"value": round(tot / dt / 1e9, 4), "unit": UNIT, "cores": nch, "kind": "oracle",
+            "sample": f"{nch} x 64 MiB chunks of config {cfg.key} (first chunks), one per "
+                      f"thread; step = len16 + utf8->utf16le + len8 + utf16le->utf8",
+            "seconds": round(dt, 2), "host_cpus": cores}
+
+
+def run_reference(args):
+    """--impl reference: the oracle (no reference implementation exists for this paper) on
+    the host cores, same metric/unit/config, each step a bounded sample."""
+    G, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    cfg = synth.CONFIGS[args.config]
+    size = cfg.size if not args.size_mib else args.size_mib << 20
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    nch = max(1, min(cores, 8, size // synth.CHUNK))
+    data = [np.frombuffer(synth.gen_chunk(cfg.mix, cfg.encoding, min(synth.CHUNK, size),
+                                          cfg.seed, c), dtype=np.uint8) for c in range(nch)]
+    ex = ThreadPoolExecutor(nch)
+    for _ in range(min(args.warmup, 1)):
+        sum(ex.map(lambda c: oracle_step(oracle, c), data))
+    K = max(1, min(args.steps, 3))
+    t = time.perf_counter()
+    tot = 0
+    for _ in range(K):
+        tot += sum(ex.map(lambda c: oracle_step(oracle, c), data))
+    dt = (time.perf_counter() - t) / K
+    v = (tot / K) / dt / 1e9
+    line = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": UNIT,
+            "n_gpus": G, "steps": K, "warmup": min(args.warmup, 1),
+            "ms_per_step": round(dt * 1e3, 2), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u8/u16 (integer)", "data": "synthetic",
+            "config": {"workload": f"config 4 sample: {nch} x 64 MiB of the {cfg.key} stream",
+                       "parallelism": f"{nch} host threads"},
+            "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": nch, "kind": "oracle",
+                             "sample": f"{nch} x 64 MiB chunks per step"},
+            "e2e": {"value": round(v, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,206 @@
+/*
+ * unigpu.h -- C-ABI of paper_2111_08692_b200 (libunigpu.so): B200-native (sm_100a) UTF-8 /
+ * UTF-16LE validation and validating transcoding, after D. Lemire, "Unicode at Gigabytes per
+ * Second", arXiv 2111.08692.
+ *
+ * What each entry point computes is the paper's statement of the problem:
+ *   - UTF-8 validity = the six exhaustive rules of PAPER.md:76-83 (Section 3);
+ *   - UTF-16 validity = surrogate pairing, PAPER.md:85-87 ("only the possible surrogate pairs
+ *     require attention");
+ *   - transcoding = decode with the payload layout of PAPER.md:75 and re-encode with the
+ *     surrogate-pair formula of PAPER.md:87 (or its inverse), validation fused in
+ *     ("All of our transcoding tests include validation").
+ * The result conventions the paper leaves open are DESIGN.md section 3 (R1..R21).
+ *
+ * Conventions shared by every function below
+ * -------------------------------------------
+ *  - Pointers named in/out are DEVICE pointers (cudaMalloc'd or torch CUDA tensors) on the
+ *    current CUDA device, unless the name ends in _host.  The caller owns every input and
+ *    output buffer; the library never allocates output.  It owns a small workspace per
+ *    (device, stream) (tile status words, ticket counters, a result slot), allocated lazily on
+ *    first use and reused; calls on different streams never share a workspace.
+ *  - Lengths are in CODE UNITS: bytes for UTF-8, 16-bit words for UTF-16LE.  UTF-16LE is
+ *    little-endian, the GPU's native order; a BOM is ordinary data (R7, R9).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = the legacy default stream).
+ *  - Validity failures are DATA, returned in ug_result, not API failures.
+ *  - API misuse (NULL pointer with n > 0, odd address for a UTF-16 pointer, output capacity
+ *    larger than the buffer can be checked for is the caller's duty) returns UG_ERR_ARG; CUDA
+ *    failures return UG_ERR_CUDA.  n = 0 returns {UG_OK, 0, 0} without launching anything.
+ *  - Synchronous functions enqueue on `stream`, then synchronise `stream` and return the
+ *    result.  *_async functions only enqueue; they write the result into a caller-provided
+ *    DEVICE (or pinned, device-mapped) pointer and return UG_OK or an API error code.
+ *  - Nothing is ever written at or beyond out[out_cap].  out[0..written) is exact; output
+ *    units beyond `written` are unspecified (R5).
+ *  - Every device function is one kernel launch (no memset, no host round trip): per-call
+ *    state is epoch-tagged and self-resetting.
+ */
+#ifndef UNIGPU_H
+#define UNIGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define UNIGPU_ABI_VERSION 1
+
+/* Data verdicts: one per validity rule of PAPER.md:77-82, lone or
+ * misordered UTF-16 surrogates reuse UG_SURROGATE.  Negative values are API
+ * outcomes. */
+typedef enum {
+  UG_OK = 0,
+  UG_HEADER_BITS = 1, /* rule 1: byte F8..FF                                         */
+  UG_TOO_SHORT = 2,   /* rule 2: lead without enough continuation bytes (incl. at end) */
+  UG_TOO_LONG = 3,    /* rule 3: continuation byte not preceded by a lead             */
+  UG_OVERLONG = 4,    /* rule 4: value not larger than 7F / 7FF / FFFF                 */
+  UG_TOO_LARGE = 5,   /* rule 5: value >= 0x110000                                     */
+  UG_SURROGATE = 6,   /* rule 6 (D800..DFFF in UTF-8) and unpaired UTF-16 surrogates   */
+  UG_ERR_ARG = -1,
+  UG_ERR_CUDA = -2,
+  UG_ERR_OUTPUT_TOO_SMALL = -3
+} ug_error;
+
+/* 24-byte result, SPEC.md S:39-44 / BASELINE north_star ("output length or a validity
+ * verdict with the first-error offset"):
+ *   success:            error = UG_OK, position = n (input units consumed),
+ *                       written = output units (0 for validators)
+ *   invalid input:      error = kind of the first error, position = e, the offset of the
+ *                       first code unit of the sequence a left-to-right decoder fails on
+ *                       (R1), written = output units for in[0..e)
+ *   output too small:   error = UG_ERR_OUTPUT_TOO_SMALL, position = units required for
+ *                       in[0..e) (e = first error or n), written = 0
+ *   API error:          error = UG_ERR_ARG / UG_ERR_CUDA, position = written = 0          */
+typedef struct {
+  int32_t error;
+  uint32_t reserved;
+  uint64_t position;
+  uint64_t written;
+} ug_result;
+
+/* ------------------------------------------------------------------ synchronous, device
+ * Validate UTF-8 in[0..n).  Read-only. */
+ug_result utf8_validate(const uint8_t *in, size_t n, void *stream);
+
+/* Validate UTF-16LE in[0..n) words.  `in` must be 2-byte aligned. */
+ug_result utf16le_validate(const uint16_t *in, size_t n, void *stream);
+
+/* Validate UTF-8 in[0..n) and transcode to UTF-16LE out[0..out_cap) words, in one fused pass
+ * (PAPER.md:95-100 + 120).  out_cap = n always suffices (one unit per input byte at most,
+ * SPEC.md S:175); utf16_length_from_utf8() gives the exact size for valid input.  `out` must
+ * be 2-byte aligned. */
+ug_result utf8_to_utf16le(const uint8_t *in, size_t n, uint16_t *out, size_t out_cap,
+                          void *stream);
+
+/* Validate UTF-16LE in[0..n) and transcode to UTF-8 out[0..out_cap) bytes (PAPER.md:104-107
+ * + 120).  out_cap = 3n always suffices; utf8_length_from_utf16le() is exact for valid
+ * input. */
+ug_result utf16le_to_utf8(const uint16_t *in, size_t n, uint8_t *out, size_t out_cap,
+                          void *stream);
+
+/* Number of UTF-16 units the UTF-8 input transcodes to, for ANY input defined as
+ * #(bytes b with (b & 0xC0) != 0x80) + #(bytes b >= 0xF0) (R15); equals
+ * utf8_to_utf16le's `written` on valid input.  Read-only reduction. */
+uint64_t utf16_length_from_utf8(const uint8_t *in, size_t n, void *stream);
+
+/* Number of UTF-8 bytes the UTF-16LE input transcodes to, defined as the sum over words of
+ * 1 (< 0x80), 2 (< 0x800), 2 (surrogate), 3 (other); exact on valid input. */
+uint64_t utf8_length_from_utf16le(const uint16_t *in, size_t n, void *stream);
+
+/* ------------------------------------------------------------------ asynchronous, device
+ * Same operations; the result is written by the GPU into *d_result (a device pointer, or
+ * pinned host memory mapped into the device).  Return UG_OK once enqueued, or UG_ERR_ARG /
+ * UG_ERR_CUDA (then nothing was enqueued and *d_result is untouched). */
+int ug_utf8_validate_async(const uint8_t *in, size_t n, ug_result *d_result, void *stream);
+int ug_utf16le_validate_async(const uint16_t *in, size_t n, ug_result *d_result, void *stream);
+int ug_utf8_to_utf16le_async(const uint8_t *in, size_t n, uint16_t *out, size_t out_cap,
+                             ug_result *d_result, void *stream);
+int ug_utf16le_to_utf8_async(const uint16_t *in, size_t n, uint8_t *out, size_t out_cap,
+                             ug_result *d_result, void *stream);
+int ug_utf16_length_from_utf8_async(const uint8_t *in, size_t n, uint64_t *d_len, void *stream);
+int ug_utf8_length_from_utf16le_async(const uint16_t *in, size_t n, uint64_t *d_len,
+                                      void *stream);
+
+/* ------------------------------------------------------------------ sharded (multi-GPU)
+ * One rank's share of a buffer cut at character boundaries (BASELINE
+ * north_star item 3).  `in` points at the first OWNED code unit; the owned range is
+ * in[0..n), which starts at offset `in_global_offset` of the whole (unsharded) input.
+ * in[-halo_before .. -1] and in[n .. n+halo_after-1] must be readable context from the
+ * neighbouring shards (0 at the global start / end; 3 bytes / 1 word suffice, more is
+ * ignored).  Every per-position quantity reads only in[i-3 .. i+3] (D2), so the
+ * counts and the first error are exact wherever the cuts fall.
+ *
+ * The kernel writes one 32-byte record to *d_rec (device memory):
+ *   count     output units produced for the owned range (exact for valid input),
+ *   first_err GLOBAL offset (in_global_offset + local) of the first error among owned
+ *             positions, UINT64_MAX if none,
+ *   written   output units for in[0..first_err) (0 if none),
+ *   kind      ug_error kind at first_err (UG_OK if none).
+ * Output goes to out[0..out_cap) of this rank (outputs stay sharded).  Ranks exchange the
+ * records (one all-gather of 32 B per rank) and call ug_combine_records. */
+typedef struct {
+  uint64_t count;
+  uint64_t first_err;
+  uint64_t written;
+  int32_t kind;
+  int32_t reserved;
+} ug_shard_record;
+
+int ug_utf8_to_utf16le_shard_async(const uint8_t *in, size_t n, size_t halo_before,
+                                   size_t halo_after, uint64_t in_global_offset, uint16_t *out,
+                                   size_t out_cap, ug_shard_record *d_rec, void *stream);
+int ug_utf16le_to_utf8_shard_async(const uint16_t *in, size_t n, size_t halo_before,
+                                   size_t halo_after, uint64_t in_global_offset, uint8_t *out,
+                                   size_t out_cap, ug_shard_record *d_rec, void *stream);
+int ug_utf8_validate_shard_async(const uint8_t *in, size_t n, size_t halo_before,
+                                 size_t halo_after, uint64_t in_global_offset,
+                                 ug_shard_record *d_rec, void *stream);
+int ug_utf16le_validate_shard_async(const uint16_t *in, size_t n, size_t halo_before,
+                                    size_t halo_after, uint64_t in_global_offset,
+                                    ug_shard_record *d_rec, void *stream);
+
+/* Combine the all-gathered records of `nranks` shards (d_recs[0..nranks), device memory, in
+ * rank order).  Writes the global result to *d_result: {OK, total_in, total count} if no rank
+ * saw an error, else {kind, e, written} for the smallest first_err e, written = the output
+ * offset of e's rank + that rank's local written.  total_in is the global input length.
+ * Writes this rank's global output offset (exclusive prefix of counts) to *d_out_offset
+ * (may be NULL).  One single-thread kernel; no host synchronisation. */
+int ug_combine_records_async(const ug_shard_record *d_recs, int nranks, int rank,
+                             uint64_t total_in, ug_result *d_result, uint64_t *d_out_offset,
+                             void *stream);
+/* The same combine on host memory (for hosts that gather records themselves). */
+ug_result ug_combine_records_host(const ug_shard_record *recs, int nranks, int rank,
+                                  uint64_t total_in, uint64_t *out_offset);
+
+/* Cut rule on HOST memory: how many units to move a nominal cut back
+ * so that it falls on a character start.  `at` points at the unit at the nominal cut; up to
+ * `avail_before` units before it are readable.  UTF-8: back off over at most 3 continuation
+ * bytes (stop early at a non-continuation byte); UTF-16: back off 1 word off a low
+ * surrogate. */
+size_t ug_utf8_cut_backoff(const uint8_t *at, size_t avail_before);
+size_t ug_utf16_cut_backoff(const uint16_t *at, size_t avail_before);
+
+/* ------------------------------------------------------------------ host buffers
+ * End-to-end variants on HOST memory (pinned memory gives DMA-speed copies): copy the input
+ * to the device, run the fused kernel, copy out[0..written) back, synchronise.  Uses a
+ * library-owned device staging area per (device, stream), grown on demand. */
+ug_result utf8_to_utf16le_host(const uint8_t *in_host, size_t n, uint16_t *out_host,
+                               size_t out_cap, void *stream);
+ug_result utf16le_to_utf8_host(const uint16_t *in_host, size_t n, uint8_t *out_host,
+                               size_t out_cap, void *stream);
+
+/* ------------------------------------------------------------------ misc */
+/* Human-readable name of a ug_error value (static string). */
+const char *ug_error_name(int err);
+/* Number of kernel launches this process has issued through the library (for the bench's
+ * gpu_launches accounting). */
+uint64_t ug_launch_count(void);
+/* Free the workspaces of the current device (all streams). */
+void ug_release_workspaces(void);
+int ug_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* UNIGPU_H */

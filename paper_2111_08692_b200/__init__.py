@@ -1,0 +1,327 @@
+"""paper_2111_08692_b200 -- B200-native (sm_100a) UTF-8 / UTF-16LE validation and validating
+transcoding (D. Lemire, "Unicode at Gigabytes per Second", arXiv 2111.08692).
+
+Thin ctypes binding over libunigpu.so (C-ABI declared in include/unigpu.h).  Argument
+marshalling only: torch tensors are passed as device pointers plus the current CUDA stream;
+every step of the computation runs in the CUDA kernels.  There is no CPU fallback: if the
+library is missing or was not built, importing the binding raises.
+
+Names mirror the C-ABI:
+    utf8_validate, utf16le_validate, utf8_to_utf16le, utf16le_to_utf8,
+    utf16_length_from_utf8, utf8_length_from_utf16le
+plus *_async, *_shard_async, combine_records(_host), cut backoff and *_host variants.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from typing import NamedTuple
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libunigpu.so")
+
+OK, HEADER_BITS, TOO_SHORT, TOO_LONG, OVERLONG, TOO_LARGE, SURROGATE = range(7)
+ERR_ARG, ERR_CUDA, ERR_OUTPUT_TOO_SMALL = -1, -2, -3
+NONE = (1 << 64) - 1
+
+
+class Result(NamedTuple):
+    error: int
+    position: int
+    written: int
+
+
+class _CResult(ctypes.Structure):
+    _fields_ = [("error", ctypes.c_int32), ("reserved", ctypes.c_uint32),
+                ("position", ctypes.c_uint64), ("written", ctypes.c_uint64)]
+
+
+class ShardRecord(NamedTuple):
+    count: int
+    first_err: int
+    written: int
+    kind: int
+    too_small: int
+
+
+class _CRecord(ctypes.Structure):
+    _fields_ = [("count", ctypes.c_uint64), ("first_err", ctypes.c_uint64),
+                ("written", ctypes.c_uint64), ("kind", ctypes.c_int32),
+                ("reserved", ctypes.c_int32)]
+
+
+RESULT_BYTES = ctypes.sizeof(_CResult)   # 24
+RECORD_BYTES = ctypes.sizeof(_CRecord)   # 32
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; "
+            "g.build()'` (nvcc, sm_100a).  There is no CPU fallback.")
+    L = ctypes.CDLL(LIB_PATH)
+    P, S, U64, I = ctypes.c_void_p, ctypes.c_size_t, ctypes.c_uint64, ctypes.c_int
+    sig = {
+        "utf8_validate": ([P, S, P], _CResult),
+        "utf16le_validate": ([P, S, P], _CResult),
+        "utf8_to_utf16le": ([P, S, P, S, P], _CResult),
+        "utf16le_to_utf8": ([P, S, P, S, P], _CResult),
+        "utf16_length_from_utf8": ([P, S, P], U64),
+        "utf8_length_from_utf16le": ([P, S, P], U64),
+        "ug_utf8_validate_async": ([P, S, P, P], I),
+        "ug_utf16le_validate_async": ([P, S, P, P], I),
+        "ug_utf8_to_utf16le_async": ([P, S, P, S, P, P], I),
+        "ug_utf16le_to_utf8_async": ([P, S, P, S, P, P], I),
+        "ug_utf16_length_from_utf8_async": ([P, S, P, P], I),
+        "ug_utf8_length_from_utf16le_async": ([P, S, P, P], I),
+        "ug_utf8_to_utf16le_shard_async": ([P, S, S, S, U64, P, S, P, P], I),
+        "ug_utf16le_to_utf8_shard_async": ([P, S, S, S, U64, P, S, P, P], I),
+        "ug_utf8_validate_shard_async": ([P, S, S, S, U64, P, P], I),
+        "ug_utf16le_validate_shard_async": ([P, S, S, S, U64, P, P], I),
+        "ug_combine_records_async": ([P, I, I, U64, P, P, P], I),
+        "ug_combine_records_host": ([P, I, I, U64, P], _CResult),
+        "ug_utf8_cut_backoff": ([P, S], S),
+        "ug_utf16_cut_backoff": ([P, S], S),
+        "utf8_to_utf16le_host": ([P, S, P, S, P], _CResult),
+        "utf16le_to_utf8_host": ([P, S, P, S, P], _CResult),
+        "ug_error_name": ([I], ctypes.c_char_p),
+        "ug_launch_count": ([], U64),
+        "ug_release_workspaces": ([], None),
+        "ug_abi_version": ([], I),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    return L
+
+
+lib = _load()
+EXPORTED = ("utf8_validate", "utf16le_validate", "utf8_to_utf16le", "utf16le_to_utf8",
+            "utf16_length_from_utf8", "utf8_length_from_utf16le")
+
+
+# --------------------------------------------------------------------------- helpers
+def _res(r: _CResult) -> Result:
+    return Result(int(r.error), int(r.position), int(r.written))
+
+
+def _stream(stream):
+    """cudaStream_t handle: explicit int / torch.cuda.Stream, else torch's current stream."""
+    if stream is None:
+        import torch
+        return ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    if isinstance(stream, int):
+        return ctypes.c_void_p(stream)
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else ctypes.c_void_p(0)
+
+
+def _units(t):
+    return t.numel() if t is not None else 0
+
+
+def _check(rc: int, what: str):
+    if rc != OK:
+        raise RuntimeError(f"{what}: {lib.ug_error_name(rc).decode()} ({rc})")
+
+
+def error_name(err: int) -> str:
+    return lib.ug_error_name(err).decode()
+
+
+def launch_count() -> int:
+    return int(lib.ug_launch_count())
+
+
+# --------------------------------------------------------------------------- synchronous
+def utf8_validate(t_in, n: int | None = None, stream=None) -> Result:
+    """Validate UTF-8 bytes (CUDA uint8 tensor).  PAPER.md:76-83."""
+    return _res(lib.utf8_validate(_ptr(t_in), _units(t_in) if n is None else n, _stream(stream)))
+
+
+def utf16le_validate(t_in, n: int | None = None, stream=None) -> Result:
+    """Validate UTF-16LE words (CUDA int16/uint16 tensor).  PAPER.md:85-87."""
+    return _res(lib.utf16le_validate(_ptr(t_in), _units(t_in) if n is None else n,
+                                     _stream(stream)))
+
+
+def utf8_to_utf16le(t_in, t_out, n: int | None = None, out_cap: int | None = None,
+                    stream=None) -> Result:
+    """Validate + transcode UTF-8 -> UTF-16LE into t_out (int16/uint16, capacity numel)."""
+    return _res(lib.utf8_to_utf16le(_ptr(t_in), _units(t_in) if n is None else n, _ptr(t_out),
+                                    _units(t_out) if out_cap is None else out_cap,
+                                    _stream(stream)))
+
+
+def utf16le_to_utf8(t_in, t_out, n: int | None = None, out_cap: int | None = None,
+                    stream=None) -> Result:
+    """Validate + transcode UTF-16LE -> UTF-8 into t_out (uint8, capacity numel)."""
+    return _res(lib.utf16le_to_utf8(_ptr(t_in), _units(t_in) if n is None else n, _ptr(t_out),
+                                    _units(t_out) if out_cap is None else out_cap,
+                                    _stream(stream)))
+
+
+def utf16_length_from_utf8(t_in, n: int | None = None, stream=None) -> int:
+    return int(lib.utf16_length_from_utf8(_ptr(t_in), _units(t_in) if n is None else n,
+                                          _stream(stream)))
+
+
+def utf8_length_from_utf16le(t_in, n: int | None = None, stream=None) -> int:
+    return int(lib.utf8_length_from_utf16le(_ptr(t_in), _units(t_in) if n is None else n,
+                                            _stream(stream)))
+
+
+# --------------------------------------------------------------------------- asynchronous
+def result_buffer(device=None, count: int = 1):
+    """Device buffer for `count` ug_result slots (read back with decode_results)."""
+    import torch
+    return torch.zeros(RESULT_BYTES * count, dtype=torch.uint8, device=device or "cuda")
+
+
+def record_buffer(device=None, count: int = 1):
+    import torch
+    return torch.zeros(RECORD_BYTES * count, dtype=torch.uint8, device=device or "cuda")
+
+
+def decode_results(buf) -> list[Result]:
+    raw = bytes(buf.cpu().numpy().tobytes())
+    out = []
+    for i in range(len(raw) // RESULT_BYTES):
+        r = _CResult.from_buffer_copy(raw[i * RESULT_BYTES:(i + 1) * RESULT_BYTES])
+        out.append(_res(r))
+    return out
+
+
+def decode_records(buf) -> list[ShardRecord]:
+    raw = bytes(buf.cpu().numpy().tobytes())
+    out = []
+    for i in range(len(raw) // RECORD_BYTES):
+        r = _CRecord.from_buffer_copy(raw[i * RECORD_BYTES:(i + 1) * RECORD_BYTES])
+        out.append(ShardRecord(int(r.count), int(r.first_err), int(r.written), int(r.kind),
+                               int(r.reserved)))
+    return out
+
+
+def _at(t, byte_off=0):
+    return ctypes.c_void_p(t.data_ptr() + byte_off)
+
+
+def utf8_validate_async(t_in, d_result, n=None, stream=None, result_off=0):
+    _check(lib.ug_utf8_validate_async(_ptr(t_in), _units(t_in) if n is None else n,
+                                      _at(d_result, result_off), _stream(stream)),
+           "utf8_validate_async")
+
+
+def utf16le_validate_async(t_in, d_result, n=None, stream=None, result_off=0):
+    _check(lib.ug_utf16le_validate_async(_ptr(t_in), _units(t_in) if n is None else n,
+                                         _at(d_result, result_off), _stream(stream)),
+           "utf16le_validate_async")
+
+
+def utf8_to_utf16le_async(t_in, t_out, d_result, n=None, out_cap=None, stream=None,
+                          result_off=0):
+    _check(lib.ug_utf8_to_utf16le_async(_ptr(t_in), _units(t_in) if n is None else n,
+                                        _ptr(t_out),
+                                        _units(t_out) if out_cap is None else out_cap,
+                                        _at(d_result, result_off), _stream(stream)),
+           "utf8_to_utf16le_async")
+
+
+def utf16le_to_utf8_async(t_in, t_out, d_result, n=None, out_cap=None, stream=None,
+                          result_off=0):
+    _check(lib.ug_utf16le_to_utf8_async(_ptr(t_in), _units(t_in) if n is None else n,
+                                        _ptr(t_out),
+                                        _units(t_out) if out_cap is None else out_cap,
+                                        _at(d_result, result_off), _stream(stream)),
+           "utf16le_to_utf8_async")
+
+
+def utf16_length_from_utf8_async(t_in, d_len, n=None, stream=None, len_off=0):
+    _check(lib.ug_utf16_length_from_utf8_async(_ptr(t_in), _units(t_in) if n is None else n,
+                                               _at(d_len, len_off), _stream(stream)),
+           "utf16_length_from_utf8_async")
+
+
+def utf8_length_from_utf16le_async(t_in, d_len, n=None, stream=None, len_off=0):
+    _check(lib.ug_utf8_length_from_utf16le_async(_ptr(t_in), _units(t_in) if n is None else n,
+                                                 _at(d_len, len_off), _stream(stream)),
+           "utf8_length_from_utf16le_async")
+
+
+# --------------------------------------------------------------------------- sharded
+def utf8_to_utf16le_shard_async(t_in, offset, n, halo_before, halo_after, global_off, t_out,
+                                d_rec, out_cap=None, stream=None, rec_off=0):
+    """Shard [offset, offset+n) of the UTF-8 tensor t_in (element offsets)."""
+    _check(lib.ug_utf8_to_utf16le_shard_async(
+        _at(t_in, offset), n, halo_before, halo_after, global_off, _ptr(t_out),
+        _units(t_out) if out_cap is None else out_cap, _at(d_rec, rec_off), _stream(stream)),
+        "utf8_to_utf16le_shard_async")
+
+
+def utf16le_to_utf8_shard_async(t_in, offset, n, halo_before, halo_after, global_off, t_out,
+                                d_rec, out_cap=None, stream=None, rec_off=0):
+    _check(lib.ug_utf16le_to_utf8_shard_async(
+        _at(t_in, 2 * offset), n, halo_before, halo_after, global_off, _ptr(t_out),
+        _units(t_out) if out_cap is None else out_cap, _at(d_rec, rec_off), _stream(stream)),
+        "utf16le_to_utf8_shard_async")
+
+
+def utf8_validate_shard_async(t_in, offset, n, halo_before, halo_after, global_off, d_rec,
+                              stream=None, rec_off=0):
+    _check(lib.ug_utf8_validate_shard_async(_at(t_in, offset), n, halo_before, halo_after,
+                                            global_off, _at(d_rec, rec_off), _stream(stream)),
+           "utf8_validate_shard_async")
+
+
+def utf16le_validate_shard_async(t_in, offset, n, halo_before, halo_after, global_off, d_rec,
+                                 stream=None, rec_off=0):
+    _check(lib.ug_utf16le_validate_shard_async(_at(t_in, 2 * offset), n, halo_before,
+                                               halo_after, global_off, _at(d_rec, rec_off),
+                                               _stream(stream)),
+           "utf16le_validate_shard_async")
+
+
+def combine_records_async(d_recs, nranks, rank, total_in, d_result, d_out_offset=None,
+                          stream=None):
+    _check(lib.ug_combine_records_async(_ptr(d_recs), nranks, rank, total_in, _ptr(d_result),
+                                        _ptr(d_out_offset), _stream(stream)),
+           "combine_records_async")
+
+
+def combine_records_host(records: list, rank: int, total_in: int):
+    """records: list of ShardRecord (or 5-tuples).  Returns (Result, out_offset)."""
+    arr = (_CRecord * len(records))()
+    for i, r in enumerate(records):
+        arr[i].count, arr[i].first_err, arr[i].written, arr[i].kind, arr[i].reserved = r
+    off = ctypes.c_uint64()
+    r = lib.ug_combine_records_host(ctypes.cast(arr, ctypes.c_void_p), len(records), rank,
+                                    total_in, ctypes.byref(off))
+    return _res(r), int(off.value)
+
+
+def utf8_cut_backoff(buf: bytes | bytearray, at: int) -> int:
+    """Units to move a nominal cut at index `at` of a HOST buffer back to a char start."""
+    b = (ctypes.c_uint8 * len(buf)).from_buffer_copy(bytes(buf))
+    return int(lib.ug_utf8_cut_backoff(ctypes.c_void_p(ctypes.addressof(b) + at), at))
+
+
+def utf16_cut_backoff(words, at: int) -> int:
+    import numpy as np
+    a = np.ascontiguousarray(words, dtype=np.uint16)
+    return int(lib.ug_utf16_cut_backoff(ctypes.c_void_p(a.ctypes.data + 2 * at), at))
+
+
+# --------------------------------------------------------------------------- host buffers
+def utf8_to_utf16le_host(t_in_host, t_out_host, stream=None) -> Result:
+    """End-to-end: host (pinned) uint8 tensor -> host int16 tensor, H2D + kernel + D2H."""
+    return _res(lib.utf8_to_utf16le_host(_ptr(t_in_host), _units(t_in_host), _ptr(t_out_host),
+                                         _units(t_out_host), _stream(stream)))
+
+
+def utf16le_to_utf8_host(t_in_host, t_out_host, stream=None) -> Result:
+    return _res(lib.utf16le_to_utf8_host(_ptr(t_in_host), _units(t_in_host), _ptr(t_out_host),
+                                         _units(t_out_host), _stream(stream)))

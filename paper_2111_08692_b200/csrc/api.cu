@@ -1,0 +1,495 @@
+// api.cu -- the C-ABI of libunigpu.so (declared, with argument semantics and citations, in
+// include/unigpu.h).  Host-side only: argument checks, the per-(device, stream) workspace,
+// grid sizing, launches.  Every step of the path runs in kernels.cu; there is no CPU fallback:
+// if a launch fails the call returns UG_ERR_CUDA.
+#include <atomic>
+#include <cstdint>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <utility>
+
+#include "../../include/unigpu.h"
+#include "internal.h"
+
+using namespace ug;
+
+static_assert(sizeof(ResultDev) == sizeof(ug_result), "ug_result layout");
+static_assert(sizeof(RecordDev) == sizeof(ug_shard_record), "ug_shard_record layout");
+static_assert(sizeof(ug_shard_record) == 32, "record is 32 bytes");
+
+namespace {
+
+std::atomic<uint64_t> g_launches{0};
+constexpr unsigned long long MAX_N = (1ull << 38) - 1;  // status words carry 38-bit values
+
+struct Workspace {
+  int device = -1;
+  cudaStream_t stream = nullptr;
+  std::mutex mu;
+  uint64_t *status = nullptr;
+  size_t status_cap = 0;
+  Counters *ctr = nullptr;
+  ResultDev *d_res = nullptr;
+  ResultDev *h_res = nullptr;  // pinned
+  unsigned long long *d_len = nullptr;
+  unsigned long long *h_len = nullptr;  // pinned
+  uint32_t epoch = 0;
+  void *d_in = nullptr;
+  size_t d_in_cap = 0;
+  void *d_out = nullptr;
+  size_t d_out_cap = 0;
+};
+
+struct DeviceInfo {
+  int sms = 0;
+  int occ[4] = {0, 0, 0, 0};
+  bool configured = false;
+};
+
+std::mutex g_mu;
+std::map<std::pair<int, uintptr_t>, Workspace *> g_ws;
+std::map<int, DeviceInfo> g_dev;
+
+cudaError_t device_info(int dev, DeviceInfo **out) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  DeviceInfo &d = g_dev[dev];
+  if (!d.configured) {
+    cudaError_t e = cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+    if (e != cudaSuccess) return e;
+    for (int i = 0; i < 4; i++) {
+      e = tile_configure((Op)i);
+      if (e != cudaSuccess) return e;
+      e = tile_occupancy((Op)i, &d.occ[i]);
+      if (e != cudaSuccess) return e;
+      if (d.occ[i] < 1) d.occ[i] = 1;
+    }
+    d.configured = true;
+  }
+  *out = &d;
+  return cudaSuccess;
+}
+
+cudaError_t get_ws(cudaStream_t s, Workspace **out) {
+  int dev;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto key = std::make_pair(dev, (uintptr_t)s);
+  auto it = g_ws.find(key);
+  if (it != g_ws.end()) {
+    *out = it->second;
+    return cudaSuccess;
+  }
+  Workspace *w = new Workspace();
+  w->device = dev;
+  w->stream = s;
+  if ((e = cudaMalloc(&w->ctr, sizeof(Counters))) != cudaSuccess) return e;
+  Counters init;
+  std::memset(&init, 0, sizeof(init));
+  init.err_min = NONE;
+  if ((e = cudaMemcpy(w->ctr, &init, sizeof(init), cudaMemcpyHostToDevice)) != cudaSuccess)
+    return e;
+  if ((e = cudaMalloc(&w->d_res, sizeof(ResultDev))) != cudaSuccess) return e;
+  if ((e = cudaMallocHost(&w->h_res, sizeof(ResultDev))) != cudaSuccess) return e;
+  if ((e = cudaMalloc(&w->d_len, sizeof(unsigned long long))) != cudaSuccess) return e;
+  if ((e = cudaMallocHost(&w->h_len, sizeof(unsigned long long))) != cudaSuccess) return e;
+  g_ws[key] = w;
+  *out = w;
+  return cudaSuccess;
+}
+
+cudaError_t ensure_status(Workspace *w, size_t ntiles) {
+  if (ntiles <= w->status_cap) return cudaSuccess;
+  size_t cap = w->status_cap * 2 > ntiles ? w->status_cap * 2 : ntiles;
+  if (w->status) {
+    cudaError_t e = cudaStreamSynchronize(w->stream);
+    if (e != cudaSuccess) return e;
+    cudaFree(w->status);
+    w->status = nullptr;
+    w->status_cap = 0;
+  }
+  cudaError_t e = cudaMalloc(&w->status, cap * sizeof(uint64_t));
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(w->status, 0, cap * sizeof(uint64_t), w->stream);
+  if (e != cudaSuccess) return e;
+  w->status_cap = cap;
+  return cudaSuccess;
+}
+
+uint32_t next_epoch(Workspace *w) {
+  w->epoch = (w->epoch + 1) & 0xFFFFFFu;
+  if (w->epoch == 0) {  // wrapped: old words could alias the new epoch
+    if (w->status) cudaMemsetAsync(w->status, 0, w->status_cap * sizeof(uint64_t), w->stream);
+    w->epoch = 1;
+  }
+  return w->epoch;
+}
+
+Window make_window(const void *base, unsigned long long nbytes, unsigned long long hb,
+                   unsigned long long ha) {
+  Window w;
+  w.base = reinterpret_cast<const uint8_t *>(base);
+  w.n = (long long)nbytes;
+  w.lo_valid = -(long long)hb;
+  w.hi_valid = (long long)(nbytes + ha);
+  w.lead = (long long)((uintptr_t)base & 15u);
+  w.mem_lo = ((uintptr_t)base - hb) & ~(uintptr_t)15;
+  w.mem_hi = ((uintptr_t)base + nbytes + ha + 15) & ~(uintptr_t)15;
+  return w;
+}
+
+// Enqueue one tile kernel.  Units: n / halos in code units of the input encoding.
+int enqueue_tile(Op op, const void *in, unsigned long long n, unsigned long long hb,
+                 unsigned long long ha, unsigned long long global_off, void *out,
+                 unsigned long long out_cap, ResultDev *d_result, RecordDev *d_rec,
+                 cudaStream_t s) {
+  const bool u16in = (op == Op::U16_VALIDATE || op == Op::U16_TO_U8);
+  const unsigned long long us = u16in ? 2 : 1;
+  if (n > MAX_N) return UG_ERR_ARG;
+  if (n > 0 && in == nullptr) return UG_ERR_ARG;
+  if (u16in && ((uintptr_t)in & 1u)) return UG_ERR_ARG;
+  if (op == Op::U8_TO_U16 && ((uintptr_t)out & 1u)) return UG_ERR_ARG;
+  if ((op == Op::U8_TO_U16 || op == Op::U16_TO_U8) && out == nullptr && out_cap > 0)
+    return UG_ERR_ARG;
+  if (n == 0) {
+    if (d_result && cudaMemsetAsync(d_result, 0, sizeof(ResultDev), s) != cudaSuccess)
+      return UG_ERR_CUDA;
+    if (d_rec) {  // {count 0, first_err NONE, written 0, kind OK}
+      if (cudaMemsetAsync(d_rec, 0, sizeof(RecordDev), s) != cudaSuccess ||
+          cudaMemsetAsync(&d_rec->first_err, 0xFF, sizeof(d_rec->first_err), s) != cudaSuccess)
+        return UG_ERR_CUDA;
+    }
+    return UG_OK;
+  }
+  Workspace *w;
+  if (get_ws(s, &w) != cudaSuccess) return UG_ERR_CUDA;
+  DeviceInfo *di;
+  if (device_info(w->device, &di) != cudaSuccess) return UG_ERR_CUDA;
+  std::lock_guard<std::mutex> lk(w->mu);
+  TileArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.win = make_window(in, n * us, hb * us, ha * us);
+  a.ntiles = (unsigned long long)((a.win.n - 1 + a.win.lead) / TILE + 1);
+  a.out = out;
+  a.out_cap = out ? out_cap : 0;
+  if (op == Op::U8_TO_U16 || op == Op::U16_TO_U8) {
+    if (ensure_status(w, a.ntiles) != cudaSuccess) return UG_ERR_CUDA;
+    a.status = w->status;
+  }
+  a.epoch = next_epoch(w);
+  a.ctr = w->ctr;
+  a.result = d_result;
+  a.rec = d_rec;
+  a.global_off = global_off;
+  unsigned long long maxg = (unsigned long long)di->sms * (unsigned long long)di->occ[(int)op];
+  int grid = (int)(a.ntiles < maxg ? a.ntiles : maxg);
+  if (launch_tile(op, a, grid, s) != cudaSuccess) return UG_ERR_CUDA;
+  g_launches.fetch_add(1);
+  return UG_OK;
+}
+
+ug_result make_result(int err, uint64_t pos, uint64_t wr) {
+  ug_result r;
+  r.error = err;
+  r.reserved = 0;
+  r.position = pos;
+  r.written = wr;
+  return r;
+}
+
+// Run an async tile op into the workspace's result slot and wait for it.
+ug_result run_sync(Op op, const void *in, unsigned long long n, void *out,
+                   unsigned long long out_cap, cudaStream_t s) {
+  if (n == 0) {
+    if (in == nullptr && n > 0) return make_result(UG_ERR_ARG, 0, 0);
+    return make_result(UG_OK, 0, 0);
+  }
+  Workspace *w;
+  if (get_ws(s, &w) != cudaSuccess) return make_result(UG_ERR_CUDA, 0, 0);
+  int rc = enqueue_tile(op, in, n, 0, 0, 0, out, out_cap, w->d_res, nullptr, s);
+  if (rc != UG_OK) return make_result(rc, 0, 0);
+  std::lock_guard<std::mutex> lk(w->mu);
+  if (cudaMemcpyAsync(w->h_res, w->d_res, sizeof(ResultDev), cudaMemcpyDeviceToHost, s) !=
+          cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return make_result(UG_ERR_CUDA, 0, 0);
+  ug_result r;
+  std::memcpy(&r, w->h_res, sizeof(r));
+  return r;
+}
+
+int enqueue_len(bool u16in, const void *in, unsigned long long n, unsigned long long *d_len,
+                cudaStream_t s) {
+  if (d_len == nullptr) return UG_ERR_ARG;
+  if (n > 0 && in == nullptr) return UG_ERR_ARG;
+  if (u16in && ((uintptr_t)in & 1u)) return UG_ERR_ARG;
+  if (n == 0) return cudaMemsetAsync(d_len, 0, sizeof(*d_len), s) == cudaSuccess ? UG_OK
+                                                                                 : UG_ERR_CUDA;
+  Workspace *w;
+  if (get_ws(s, &w) != cudaSuccess) return UG_ERR_CUDA;
+  DeviceInfo *di;
+  if (device_info(w->device, &di) != cudaSuccess) return UG_ERR_CUDA;
+  std::lock_guard<std::mutex> lk(w->mu);
+  unsigned long long per_block = (unsigned long long)NT * 16 * 4;  // bytes per block pass
+  unsigned long long bytes = n * (u16in ? 2 : 1);
+  unsigned long long want = (bytes + per_block - 1) / per_block;
+  unsigned long long maxg = (unsigned long long)di->sms * 4;
+  int grid = (int)(want < maxg ? (want ? want : 1) : maxg);
+  cudaError_t e = u16in ? launch_len16((const uint16_t *)in, n, w->ctr, d_len, grid, s)
+                        : launch_len8((const uint8_t *)in, n, w->ctr, d_len, grid, s);
+  if (e != cudaSuccess) return UG_ERR_CUDA;
+  g_launches.fetch_add(1);
+  return UG_OK;
+}
+
+uint64_t run_len(bool u16in, const void *in, unsigned long long n, cudaStream_t s) {
+  if (n == 0) return 0;
+  Workspace *w;
+  if (get_ws(s, &w) != cudaSuccess) return 0;
+  if (enqueue_len(u16in, in, n, w->d_len, s) != UG_OK) return 0;
+  std::lock_guard<std::mutex> lk(w->mu);
+  if (cudaMemcpyAsync(w->h_len, w->d_len, sizeof(*w->h_len), cudaMemcpyDeviceToHost, s) !=
+          cudaSuccess ||
+      cudaStreamSynchronize(s) != cudaSuccess)
+    return 0;
+  return *w->h_len;
+}
+
+cudaError_t ensure_staging(Workspace *w, size_t in_bytes, size_t out_bytes) {
+  cudaError_t e;
+  if (in_bytes > w->d_in_cap) {
+    if (w->d_in) {
+      cudaStreamSynchronize(w->stream);
+      cudaFree(w->d_in);
+    }
+    w->d_in = nullptr;
+    w->d_in_cap = 0;
+    if ((e = cudaMalloc(&w->d_in, in_bytes)) != cudaSuccess) return e;
+    w->d_in_cap = in_bytes;
+  }
+  if (out_bytes > w->d_out_cap) {
+    if (w->d_out) {
+      cudaStreamSynchronize(w->stream);
+      cudaFree(w->d_out);
+    }
+    w->d_out = nullptr;
+    w->d_out_cap = 0;
+    if ((e = cudaMalloc(&w->d_out, out_bytes)) != cudaSuccess) return e;
+    w->d_out_cap = out_bytes;
+  }
+  return cudaSuccess;
+}
+
+// Host-buffer transcode: H2D, one fused kernel, D2H of out[0..written).
+ug_result run_host(Op op, const void *in_host, unsigned long long n, void *out_host,
+                   unsigned long long out_cap, cudaStream_t s) {
+  const bool u16in = op == Op::U16_TO_U8;
+  const size_t ius = u16in ? 2 : 1, ous = u16in ? 1 : 2;
+  if (n == 0) return make_result(UG_OK, 0, 0);
+  if (in_host == nullptr || (out_host == nullptr && out_cap > 0))
+    return make_result(UG_ERR_ARG, 0, 0);
+  unsigned long long bound = u16in ? 3 * n : n;  // at most this many output units
+  unsigned long long cap = out_cap < bound ? out_cap : bound;
+  Workspace *w;
+  if (get_ws(s, &w) != cudaSuccess) return make_result(UG_ERR_CUDA, 0, 0);
+  {
+    std::lock_guard<std::mutex> lk(w->mu);
+    if (ensure_staging(w, n * ius, (cap ? cap : 1) * ous) != cudaSuccess)
+      return make_result(UG_ERR_CUDA, 0, 0);
+    if (cudaMemcpyAsync(w->d_in, in_host, n * ius, cudaMemcpyHostToDevice, s) != cudaSuccess)
+      return make_result(UG_ERR_CUDA, 0, 0);
+  }
+  ug_result r = run_sync(op, w->d_in, n, w->d_out, cap, s);
+  if (r.error < 0) return r;
+  if (r.written) {
+    std::lock_guard<std::mutex> lk(w->mu);
+    if (cudaMemcpyAsync(out_host, w->d_out, r.written * ous, cudaMemcpyDeviceToHost, s) !=
+            cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+      return make_result(UG_ERR_CUDA, 0, 0);
+  }
+  return r;
+}
+
+}  // namespace
+
+extern "C" {
+
+ug_result utf8_validate(const uint8_t *in, size_t n, void *stream) {
+  if (n > 0 && in == nullptr) return make_result(UG_ERR_ARG, 0, 0);
+  return run_sync(Op::U8_VALIDATE, in, n, nullptr, 0, (cudaStream_t)stream);
+}
+ug_result utf16le_validate(const uint16_t *in, size_t n, void *stream) {
+  if (n > 0 && in == nullptr) return make_result(UG_ERR_ARG, 0, 0);
+  return run_sync(Op::U16_VALIDATE, in, n, nullptr, 0, (cudaStream_t)stream);
+}
+ug_result utf8_to_utf16le(const uint8_t *in, size_t n, uint16_t *out, size_t out_cap,
+                          void *stream) {
+  if (n > 0 && in == nullptr) return make_result(UG_ERR_ARG, 0, 0);
+  return run_sync(Op::U8_TO_U16, in, n, out, out_cap, (cudaStream_t)stream);
+}
+ug_result utf16le_to_utf8(const uint16_t *in, size_t n, uint8_t *out, size_t out_cap,
+                          void *stream) {
+  if (n > 0 && in == nullptr) return make_result(UG_ERR_ARG, 0, 0);
+  return run_sync(Op::U16_TO_U8, in, n, out, out_cap, (cudaStream_t)stream);
+}
+uint64_t utf16_length_from_utf8(const uint8_t *in, size_t n, void *stream) {
+  return run_len(false, in, n, (cudaStream_t)stream);
+}
+uint64_t utf8_length_from_utf16le(const uint16_t *in, size_t n, void *stream) {
+  return run_len(true, in, n, (cudaStream_t)stream);
+}
+
+int ug_utf8_validate_async(const uint8_t *in, size_t n, ug_result *d_result, void *stream) {
+  if (!d_result) return UG_ERR_ARG;
+  return enqueue_tile(Op::U8_VALIDATE, in, n, 0, 0, 0, nullptr, 0, (ResultDev *)d_result,
+                      nullptr, (cudaStream_t)stream);
+}
+int ug_utf16le_validate_async(const uint16_t *in, size_t n, ug_result *d_result, void *stream) {
+  if (!d_result) return UG_ERR_ARG;
+  return enqueue_tile(Op::U16_VALIDATE, in, n, 0, 0, 0, nullptr, 0, (ResultDev *)d_result,
+                      nullptr, (cudaStream_t)stream);
+}
+int ug_utf8_to_utf16le_async(const uint8_t *in, size_t n, uint16_t *out, size_t out_cap,
+                             ug_result *d_result, void *stream) {
+  if (!d_result) return UG_ERR_ARG;
+  return enqueue_tile(Op::U8_TO_U16, in, n, 0, 0, 0, out, out_cap, (ResultDev *)d_result,
+                      nullptr, (cudaStream_t)stream);
+}
+int ug_utf16le_to_utf8_async(const uint16_t *in, size_t n, uint8_t *out, size_t out_cap,
+                             ug_result *d_result, void *stream) {
+  if (!d_result) return UG_ERR_ARG;
+  return enqueue_tile(Op::U16_TO_U8, in, n, 0, 0, 0, out, out_cap, (ResultDev *)d_result,
+                      nullptr, (cudaStream_t)stream);
+}
+int ug_utf16_length_from_utf8_async(const uint8_t *in, size_t n, uint64_t *d_len, void *stream) {
+  return enqueue_len(false, in, n, (unsigned long long *)d_len, (cudaStream_t)stream);
+}
+int ug_utf8_length_from_utf16le_async(const uint16_t *in, size_t n, uint64_t *d_len,
+                                      void *stream) {
+  return enqueue_len(true, in, n, (unsigned long long *)d_len, (cudaStream_t)stream);
+}
+
+static size_t clamp_halo(size_t h, size_t maxh) { return h < maxh ? h : maxh; }
+
+int ug_utf8_to_utf16le_shard_async(const uint8_t *in, size_t n, size_t halo_before,
+                                   size_t halo_after, uint64_t in_global_offset, uint16_t *out,
+                                   size_t out_cap, ug_shard_record *d_rec, void *stream) {
+  if (!d_rec) return UG_ERR_ARG;
+  return enqueue_tile(Op::U8_TO_U16, in, n, clamp_halo(halo_before, 3),
+                      clamp_halo(halo_after, 3), in_global_offset, out, out_cap, nullptr,
+                      (RecordDev *)d_rec, (cudaStream_t)stream);
+}
+int ug_utf16le_to_utf8_shard_async(const uint16_t *in, size_t n, size_t halo_before,
+                                   size_t halo_after, uint64_t in_global_offset, uint8_t *out,
+                                   size_t out_cap, ug_shard_record *d_rec, void *stream) {
+  if (!d_rec) return UG_ERR_ARG;
+  return enqueue_tile(Op::U16_TO_U8, in, n, clamp_halo(halo_before, 1),
+                      clamp_halo(halo_after, 1), in_global_offset, out, out_cap, nullptr,
+                      (RecordDev *)d_rec, (cudaStream_t)stream);
+}
+int ug_utf8_validate_shard_async(const uint8_t *in, size_t n, size_t halo_before,
+                                 size_t halo_after, uint64_t in_global_offset,
+                                 ug_shard_record *d_rec, void *stream) {
+  if (!d_rec) return UG_ERR_ARG;
+  return enqueue_tile(Op::U8_VALIDATE, in, n, clamp_halo(halo_before, 3),
+                      clamp_halo(halo_after, 3), in_global_offset, nullptr, 0, nullptr,
+                      (RecordDev *)d_rec, (cudaStream_t)stream);
+}
+int ug_utf16le_validate_shard_async(const uint16_t *in, size_t n, size_t halo_before,
+                                    size_t halo_after, uint64_t in_global_offset,
+                                    ug_shard_record *d_rec, void *stream) {
+  if (!d_rec) return UG_ERR_ARG;
+  return enqueue_tile(Op::U16_VALIDATE, in, n, clamp_halo(halo_before, 1),
+                      clamp_halo(halo_after, 1), in_global_offset, nullptr, 0, nullptr,
+                      (RecordDev *)d_rec, (cudaStream_t)stream);
+}
+
+int ug_combine_records_async(const ug_shard_record *d_recs, int nranks, int rank,
+                             uint64_t total_in, ug_result *d_result, uint64_t *d_out_offset,
+                             void *stream) {
+  if (!d_recs || nranks < 1 || rank < 0 || rank >= nranks) return UG_ERR_ARG;
+  if (launch_combine((const RecordDev *)d_recs, nranks, rank, total_in, (ResultDev *)d_result,
+                     (unsigned long long *)d_out_offset, (cudaStream_t)stream) != cudaSuccess)
+    return UG_ERR_CUDA;
+  g_launches.fetch_add(1);
+  return UG_OK;
+}
+
+ug_result ug_combine_records_host(const ug_shard_record *recs, int nranks, int rank,
+                                  uint64_t total_in, uint64_t *out_offset) {
+  if (!recs || nranks < 1 || rank < 0 || rank >= nranks) return make_result(UG_ERR_ARG, 0, 0);
+  ResultDev r;
+  unsigned long long off = 0;
+  combine_host((const RecordDev *)recs, nranks, rank, total_in, &r, &off);
+  if (out_offset) *out_offset = off;
+  ug_result o;
+  std::memcpy(&o, &r, sizeof(o));
+  return o;
+}
+
+size_t ug_utf8_cut_backoff(const uint8_t *at, size_t avail_before) {
+  // at[-k] is the candidate cut byte; step back while it is a continuation byte (<= 3 steps)
+  size_t k = 0;
+  while (k < 3 && k < avail_before && (at[-(ptrdiff_t)k] & 0xC0u) == 0x80u) k++;
+  return k;
+}
+size_t ug_utf16_cut_backoff(const uint16_t *at, size_t avail_before) {
+  return ((at[0] & 0xFC00u) == 0xDC00u && avail_before >= 1) ? 1 : 0;
+}
+
+ug_result utf8_to_utf16le_host(const uint8_t *in_host, size_t n, uint16_t *out_host,
+                               size_t out_cap, void *stream) {
+  return run_host(Op::U8_TO_U16, in_host, n, out_host, out_cap, (cudaStream_t)stream);
+}
+ug_result utf16le_to_utf8_host(const uint16_t *in_host, size_t n, uint8_t *out_host,
+                               size_t out_cap, void *stream) {
+  return run_host(Op::U16_TO_U8, in_host, n, out_host, out_cap, (cudaStream_t)stream);
+}
+
+const char *ug_error_name(int err) {
+  switch (err) {
+    case UG_OK: return "OK";
+    case UG_HEADER_BITS: return "HeaderBits";
+    case UG_TOO_SHORT: return "TooShort";
+    case UG_TOO_LONG: return "TooLong";
+    case UG_OVERLONG: return "Overlong";
+    case UG_TOO_LARGE: return "TooLarge";
+    case UG_SURROGATE: return "Surrogate";
+    case UG_ERR_ARG: return "ErrArg";
+    case UG_ERR_CUDA: return "ErrCuda";
+    case UG_ERR_OUTPUT_TOO_SMALL: return "OutputTooSmall";
+  }
+  return "Unknown";
+}
+
+uint64_t ug_launch_count(void) { return g_launches.load(); }
+
+void ug_release_workspaces(void) {
+  int dev;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  std::lock_guard<std::mutex> lk(g_mu);
+  for (auto it = g_ws.begin(); it != g_ws.end();) {
+    if (it->first.first == dev) {
+      Workspace *w = it->second;
+      cudaStreamSynchronize(w->stream);
+      cudaFree(w->status);
+      cudaFree(w->ctr);
+      cudaFree(w->d_res);
+      cudaFreeHost(w->h_res);
+      cudaFree(w->d_len);
+      cudaFreeHost(w->h_len);
+      cudaFree(w->d_in);
+      cudaFree(w->d_out);
+      delete w;
+      it = g_ws.erase(it);
+    } else {
+      ++it;
+    }
+  }
+}
+
+int ug_abi_version(void) { return UNIGPU_ABI_VERSION; }
+
+}  // extern "C"

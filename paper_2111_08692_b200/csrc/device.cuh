@@ -1,0 +1,205 @@
+// device.cuh -- sm_100a device primitives for libunigpu: TMA bulk copies + mbarriers, relaxed
+// global atomics for the decoupled look-back, the epoch-tagged tile status word, the tile
+// loader shared by all tile kernels, and block-level scan helpers.
+//
+// Nothing here computes the method itself; the UTF-8 / UTF-16 arithmetic lives in utf8.cuh /
+// utf16.cuh.  Independent of oracle/ (shares no code with it).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ug {
+
+constexpr uint32_t FULL = 0xffffffffu;
+constexpr uint64_t NONE = ~0ull;
+constexpr int NT = 256;           // threads per CTA for the tile kernels
+constexpr int TILE = 8192;        // input bytes per tile (8192 UTF-8 bytes / 4096 UTF-16 words)
+constexpr int BPT = TILE / NT;    // 32 contiguous input bytes per thread
+constexpr int HALO = 16;          // bytes of context loaded before and after each tile
+constexpr int INBUF = TILE + 2 * HALO;
+
+// ---------------------------------------------------------------- workspace counters
+// One per (device, stream); zero-initialised once, self-resetting at the end of every call
+// (the last CTA to finish resets them), so each API call is a single launch.
+struct Counters {
+  uint32_t ticket;    // dynamic tile tickets (decoupled look-back needs issue order)
+  uint32_t done;      // CTAs finished
+  unsigned long long err_min;  // smallest error position found (NONE = none)
+  unsigned long long accum;    // reduction accumulator (length-from kernels)
+  unsigned long long pad;
+};
+
+// ---------------------------------------------------------------- status words
+// [63:40] call epoch (24 bits) | [39:38] flag | [37:0] value.  A word whose epoch is not the
+// current call's reads as "not ready", so the array never needs clearing between calls.
+constexpr uint32_t FLAG_AGG = 1, FLAG_PREFIX = 2;
+__device__ __forceinline__ uint64_t pack_status(uint32_t epoch, uint32_t flag, uint64_t v) {
+  return ((uint64_t)epoch << 40) | ((uint64_t)flag << 38) | (v & ((1ull << 38) - 1));
+}
+
+// ---------------------------------------------------------------- PTX wrappers
+__device__ __forceinline__ uint32_t smem_addr(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
+}
+__device__ __forceinline__ void fence_mbar_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "UG_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra UG_WAIT_%=;\n}" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D TMA bulk copy global -> shared, completing on an mbarrier (SASS: UBLKCP).
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
+                                         uint64_t *bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar))
+      : "memory");
+}
+// 1-D TMA bulk copy shared -> global (bulk-group completion).
+__device__ __forceinline__ void bulk_s2g(void *dst, const void *src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+               "r"(smem_addr(src)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read_all() {
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_all() {
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+// order generic-proxy shared-memory writes before async-proxy (TMA) reads of them
+__device__ __forceinline__ void fence_proxy_async_smem() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+__device__ __forceinline__ uint64_t ld_relaxed(const uint64_t *p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_relaxed(uint64_t *p, uint64_t v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// ---------------------------------------------------------------- warp / block helpers
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    uint32_t t = __shfl_up_sync(FULL, v, d);
+    if (lane >= d) v += t;
+  }
+  return v;
+}
+__device__ __forceinline__ uint64_t warp_sum64(uint64_t v) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(FULL, v, d);
+  return v;
+}
+
+// Byte-lane mask (0xFF per byte) of the 4 bytes at positions pos..pos+3 inside [lo, hi).
+__device__ __forceinline__ uint32_t range_bytes(long long pos, long long lo, long long hi) {
+  long long a = lo - pos, b = hi - pos;
+  a = a < 0 ? 0 : (a > 4 ? 4 : a);
+  b = b < 0 ? 0 : (b > 4 ? 4 : b);
+  if (b <= a) return 0u;
+  uint64_t m = ((1ull << (8 * b)) - 1) & ~((1ull << (8 * a)) - 1);
+  return (uint32_t)m;
+}
+
+// ---------------------------------------------------------------- tile loader
+// Input window of one call: positions are BYTE offsets from `base` (the first owned byte).
+// Valid bytes are [lo_valid, hi_valid) = [-halo_before, n + halo_after); everything else reads
+// as 0x00 (start / end of stream).  Tile t covers positions [t*TILE - lead, (t+1)*TILE - lead)
+// so that tiles start on 16-byte boundaries in memory; its smem image holds positions
+// [tile_pos - HALO, tile_pos + TILE + HALO).
+struct Window {
+  const uint8_t *base;
+  long long lo_valid, hi_valid;
+  long long lead;          // base % 16
+  uintptr_t mem_lo, mem_hi;  // 16-byte aligned readable address range covering the window
+  long long n;             // owned bytes
+};
+
+__device__ __forceinline__ long long tile_pos(const Window &w, long long t) {
+  return t * TILE - w.lead;
+}
+
+// Issued by ONE thread: bulk-load the smem image of tile t into buf, completing on bar.
+__device__ __forceinline__ void issue_tile_load(const Window &w, long long t, uint8_t *buf,
+                                                uint64_t *bar) {
+  uintptr_t A = (uintptr_t)(w.base + tile_pos(w, t) - HALO);
+  uintptr_t B = A + INBUF;
+  uintptr_t a = A > w.mem_lo ? A : w.mem_lo;
+  uintptr_t b = B < w.mem_hi ? B : w.mem_hi;
+  uint32_t bytes = b > a ? (uint32_t)(b - a) : 0u;
+  mbar_arrive_expect_tx(bar, bytes);
+  if (bytes) bulk_g2s(buf + (a - A), (const void *)a, bytes, bar);
+}
+
+// After the load landed: zero every smem byte whose position lies outside the valid window
+// (only tiles touching the window edges do any work).  Block-wide; caller syncs after.
+__device__ __forceinline__ void fix_tile_edges(const Window &w, long long t, uint8_t *buf) {
+  long long p0 = tile_pos(w, t) - HALO;
+  if (p0 >= w.lo_valid && p0 + INBUF <= w.hi_valid) return;
+  uint32_t *b32 = reinterpret_cast<uint32_t *>(buf);
+  for (int q = threadIdx.x; q < INBUF / 4; q += blockDim.x) {
+    long long pos = p0 + 4 * q;
+    if (pos >= w.lo_valid && pos + 4 <= w.hi_valid) continue;
+    b32[q] &= range_bytes(pos, w.lo_valid, w.hi_valid);
+  }
+}
+
+// ---------------------------------------------------------------- decoupled look-back
+// Called by one full warp for tile t with its aggregate already published (t > 0).  Returns
+// the exclusive prefix (sum of all earlier tiles' aggregates) in every lane.
+__device__ __forceinline__ uint64_t look_back(uint64_t *status, uint32_t epoch, long long t,
+                                              int lane) {
+  uint64_t excl = 0;
+  long long idx = t - 1;
+  while (true) {
+    long long j = idx - lane;
+    uint32_t flag;
+    uint64_t val;
+    if (j < 0) {
+      flag = FLAG_PREFIX;
+      val = 0;
+    } else {
+      uint64_t s;
+      int spins = 0;
+      while (true) {
+        s = ld_relaxed(status + j);
+        if ((uint32_t)(s >> 40) == epoch && ((s >> 38) & 3u) != 0) break;
+        if (++spins > 8) __nanosleep(32);
+      }
+      flag = (uint32_t)((s >> 38) & 3u);
+      val = s & ((1ull << 38) - 1);
+    }
+    uint32_t pm = __ballot_sync(FULL, flag == FLAG_PREFIX);
+    if (pm) {
+      int first = __ffs(pm) - 1;
+      excl += warp_sum64(lane <= first ? val : 0ull);
+      return excl;
+    }
+    excl += warp_sum64(val);
+    idx -= 32;
+  }
+}
+
+}  // namespace ug

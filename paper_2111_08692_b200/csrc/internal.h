@@ -1,0 +1,60 @@
+// internal.h -- declarations shared by kernels.cu (device code + launchers) and api.cu (the
+// C-ABI).  Not part of the public interface (include/unigpu.h is).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "device.cuh"
+
+namespace ug {
+
+// Device-side mirrors of the public structs (identical layout, checked in api.cu).
+struct ResultDev {
+  int32_t error;
+  uint32_t reserved;
+  unsigned long long position;
+  unsigned long long written;
+};
+struct RecordDev {
+  unsigned long long count;
+  unsigned long long first_err;
+  unsigned long long written;
+  int32_t kind;
+  int32_t reserved;  // 1 = this rank's output buffer was too small
+};
+
+constexpr int ERR_OUTPUT_TOO_SMALL = -3;
+
+// Arguments of one tile-kernel launch (passed by value as the kernel parameter).
+struct TileArgs {
+  Window win;                   // byte positions (UTF-16: 2 bytes per word)
+  void *out;                    // output buffer (uint16_t* or uint8_t*), may be null
+  unsigned long long out_cap;   // in output units
+  unsigned long long ntiles;
+  uint64_t *status;             // tile status words (transcoders)
+  uint32_t epoch;
+  Counters *ctr;
+  ResultDev *result;            // non-sharded result slot, or null
+  RecordDev *rec;               // sharded record slot, or null
+  unsigned long long global_off;  // sharded: global offset of position 0 (code units)
+};
+
+enum class Op : int { U8_VALIDATE = 0, U8_TO_U16 = 1, U16_VALIDATE = 2, U16_TO_U8 = 3 };
+
+size_t tile_smem_bytes(Op op);
+cudaError_t tile_configure(Op op);  // set max dynamic smem (idempotent)
+cudaError_t tile_occupancy(Op op, int *blocks_per_sm);
+cudaError_t launch_tile(Op op, const TileArgs &a, int grid, cudaStream_t s);
+
+cudaError_t launch_len8(const uint8_t *in, unsigned long long n, Counters *ctr,
+                        unsigned long long *d_len, int grid, cudaStream_t s);
+cudaError_t launch_len16(const uint16_t *in, unsigned long long n, Counters *ctr,
+                         unsigned long long *d_len, int grid, cudaStream_t s);
+cudaError_t launch_combine(const RecordDev *recs, int nranks, int rank,
+                           unsigned long long total_in, ResultDev *res,
+                           unsigned long long *out_off, cudaStream_t s);
+// host mirror of the combine kernel (same code path semantics)
+void combine_host(const RecordDev *recs, int nranks, int rank, unsigned long long total_in,
+                  ResultDev *res, unsigned long long *out_off);
+
+}  // namespace ug

@@ -200,6 +200,48 @@ def generate(cfg: Config | str, size: int | None = None, chunks: range | None = 
         shm.unlink()
 
 
+def generate_range(cfg: Config | str, lo: int, hi: int, workers: int | None = None) -> np.ndarray:
+    """Bytes [lo, hi) of config `cfg` (byte offsets, clipped to the config size), generating
+    only the chunks that cover them.  Identical to generate(cfg)[lo:hi] (as bytes)."""
+    if isinstance(cfg, str):
+        cfg = CONFIGS[cfg]
+    lo, hi = max(0, lo), min(cfg.size, hi)
+    if hi <= lo:
+        return np.zeros(0, dtype=np.uint8)
+    c0, c1 = lo // CHUNK, (hi - 1) // CHUNK
+    span = (c1 - c0 + 1) * CHUNK
+    sub = Config(cfg.key, cfg.encoding, cfg.size, cfg.seed, cfg.mix, cfg.desc)
+    total = min(cfg.size - c0 * CHUNK, span)
+    shm = shared_memory.SharedMemory(create=True, size=total)
+    try:
+        sel = list(range(c0, c1 + 1))
+        nw = workers or min(len(sel), max(1, (os.cpu_count() or 2) - 1), 32)
+        args = [(shm.name, sub.mix, sub.encoding, cfg.size, cfg.seed, c, c0 * CHUNK) for c in sel]
+        if len(sel) == 1:
+            _worker_off(args[0])
+        else:
+            with ProcessPoolExecutor(nw, mp_context=get_context("fork")) as ex:
+                list(ex.map(_worker_off, args))
+        out = np.empty(hi - lo, dtype=np.uint8)
+        out[:] = np.frombuffer(shm.buf, dtype=np.uint8, count=total)[lo - c0 * CHUNK:hi - c0 * CHUNK]
+        return out
+    finally:
+        shm.close()
+        shm.unlink()
+
+
+def _worker_off(args):
+    name, mix, encoding, total, seed, c, base = args
+    shm = shared_memory.SharedMemory(name=name)
+    try:
+        lo = c * CHUNK
+        nb = min(CHUNK, total - lo)
+        shm.buf[lo - base:lo - base + nb] = gen_chunk(mix, encoding, nb, seed, c)
+    finally:
+        shm.close()
+    return c
+
+
 def digest(a: np.ndarray) -> str:
     return hashlib.sha256(a.view(np.uint8).tobytes()).hexdigest()
 

@@ -1,0 +1,347 @@
+"""GPU parity (tier T1): the CUDA path, called through the C-ABI binding, against the oracle,
+element by element, on seeded inputs.  Bit-exact: output units, result struct (verdict, first
+error offset, written count), length-from values.  Needs a B200 (sm_100a)."""
+import numpy as np
+import pytest
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_2111_08692_b200 as ug  # noqa: E402
+
+DEV = torch.device("cuda:0")
+TILE = 8192
+
+
+# ----------------------------------------------------------------------------- helpers
+def to_dev(a: np.ndarray, pad_before=0, pad_after=0, fill=0xAA):
+    """Upload with guard bytes around it (to catch reads/writes outside the range) and return
+    (big tensor, view of the payload)."""
+    a = np.ascontiguousarray(a)
+    dt = {np.dtype(np.uint8): torch.uint8, np.dtype(np.uint16): torch.int16,
+          np.dtype("<u2"): torch.int16}[a.dtype]
+    big = np.full(pad_before + a.size + pad_after, fill, dtype=a.dtype)
+    big[pad_before:pad_before + a.size] = a
+    t = torch.from_numpy(big.view(np.int16) if a.dtype.itemsize == 2 else big).to(DEV)
+    return t, t[pad_before:pad_before + a.size]
+
+
+def gpu_fwd(a: np.ndarray, cap=None, offset=0):
+    """utf8_to_utf16le on a device copy of `a` placed at byte `offset` of its buffer."""
+    _, t = to_dev(a, pad_before=offset, pad_after=64)
+    cap = a.size if cap is None else cap
+    big_out = torch.full((cap + 64,), 0x5A5A, dtype=torch.int16, device=DEV)
+    out = big_out[:cap] if cap else big_out[:0]
+    r = ug.utf8_to_utf16le(t, out, n=a.size, out_cap=cap)
+    o = big_out.cpu().numpy().view(np.uint16)
+    assert np.all(o[cap:] == 0x5A5A), "wrote past out_cap"
+    return r, o[: r.written if r.error >= 0 else 0]
+
+
+def gpu_rev(u: np.ndarray, cap=None, offset=0):
+    _, t = to_dev(u.astype(np.uint16), pad_before=offset, pad_after=32)
+    cap = 3 * u.size if cap is None else cap
+    big_out = torch.full((cap + 64,), 0x5A, dtype=torch.uint8, device=DEV)
+    out = big_out[:cap]
+    r = ug.utf16le_to_utf8(t, out, n=u.size, out_cap=cap)
+    o = big_out.cpu().numpy()
+    assert np.all(o[cap:] == 0x5A), "wrote past out_cap"
+    return r, o[: r.written if r.error >= 0 else 0]
+
+
+def check_utf8(a: np.ndarray, offset=0, cap=None):
+    ref_r, ref_o = oracle.utf8_to_utf16le(a, out_cap=cap)
+    r, o = gpu_fwd(a, cap=cap, offset=offset)
+    assert tuple(r) == tuple(ref_r), (a[:64].tobytes().hex(), r, ref_r)
+    if r.error >= 0:
+        assert np.array_equal(o, ref_o)
+    _, t = to_dev(a, pad_before=offset)
+    v = ug.utf8_validate(t)
+    rv = oracle.utf8_validate(a)
+    assert tuple(v) == tuple(rv), (v, rv)
+    assert ug.utf16_length_from_utf8(t) == oracle.utf16_length_from_utf8(a)
+    return r
+
+
+def check_utf16(u: np.ndarray, offset=0, cap=None):
+    ref_r, ref_o = oracle.utf16le_to_utf8(u, out_cap=cap)
+    r, o = gpu_rev(u, cap=cap, offset=offset)
+    assert tuple(r) == tuple(ref_r), (r, ref_r)
+    if r.error >= 0:
+        assert np.array_equal(o, ref_o)
+    _, t = to_dev(u.astype(np.uint16), pad_before=offset)
+    v = ug.utf16le_validate(t)
+    assert tuple(v) == tuple(oracle.utf16le_validate(u))
+    assert ug.utf8_length_from_utf16le(t) == oracle.utf8_length_from_utf16le(u)
+    return r
+
+
+def h(s):
+    return np.frombuffer(bytes.fromhex(s), dtype=np.uint8)
+
+
+# ----------------------------------------------------------------------------- worked examples
+def test_spec_examples(golden):
+    for ex in golden["utf8_to_utf16le"]:
+        a = h(ex["in"])
+        r = check_utf8(a)
+        assert r.position == ex["position"]
+    ex = golden["utf8_surrogate_at_1000"]
+    a = np.concatenate([np.full(ex["prefix_ascii"], 0x61, np.uint8), h(ex["bytes"])])
+    r = check_utf8(a)
+    assert (r.error, r.position) == (ug.SURROGATE, 1000)
+    for ex in golden["utf16le_to_utf8"]:
+        u = np.array([int(x, 16) for x in ex["in"]], dtype=np.uint16)
+        r = check_utf16(u)
+        assert r.position == ex["position"]
+
+
+@pytest.mark.parametrize("n", [0, 1, 2, 3, 4, 5, 15, 16, 17, 31, 32, 33, 1023, 1024, 1025,
+                               8191, 8192, 8193, 16384 + 7])
+def test_small_sizes(n):
+    rng = np.random.default_rng(n)
+    a = np.frombuffer(synth.gen_chunk("mixed", "utf8", n, 7, n), dtype=np.uint8) if n else \
+        np.zeros(0, np.uint8)
+    for off in (0, 1, 7, 15):
+        check_utf8(a, offset=off)
+    u = oracle.utf8_to_utf16le(a)[1]
+    for off in (0, 1, 7):
+        check_utf16(u, offset=2 * off)
+    # a random single byte change
+    if n:
+        b = a.copy()
+        b[rng.integers(0, n)] = rng.integers(0, 256)
+        check_utf8(b, offset=3)
+
+
+# ----------------------------------------------------------------------------- phase sweep
+def short_cases():
+    """Short strings: all 1-byte, a stride through 2-byte, class representatives of length 3-4
+    (covering every rule), valid 4-byte characters."""
+    cases = [bytes([b]) for b in range(256)]
+    cases += [bytes([a, b]) for a in range(0x80, 0x100, 3) for b in range(0x00, 0x100, 7)]
+    reps = [0x41, 0x80, 0x9F, 0xA0, 0xBF, 0xC0, 0xC2, 0xDF, 0xE0, 0xE4, 0xED, 0xEF, 0xF0, 0xF4,
+            0xF5, 0xF8, 0xFF]
+    rng = np.random.default_rng(0)
+    for _ in range(600):
+        L = int(rng.integers(3, 5))
+        cases.append(bytes(int(x) for x in rng.choice(reps, L)))
+    cases += ["\U0001F600".encode(), "\U0010FFFF".encode(), "￿".encode(), "߿".encode()]
+    return cases
+
+
+@pytest.mark.parametrize("boundary", [32, 1024, TILE])
+def test_phase_sweep(boundary):
+    """Each short string embedded in ASCII padding so that it straddles a thread (32 B), warp
+    (1 KiB) or tile (8 KiB) boundary at every phase, and at several input alignments."""
+    cases = short_cases()
+    rng = np.random.default_rng(boundary)
+    for i, c in enumerate(cases):
+        c = np.frombuffer(c, dtype=np.uint8)
+        for ph in range(-4, 2):
+            pre = boundary + ph
+            a = np.concatenate([np.full(pre, 0x41, np.uint8), c, np.full(40, 0x42, np.uint8)])
+            check_utf8(a, offset=int(rng.integers(0, 16)) if i % 5 == 0 else 0)
+
+
+def test_valid_text_straddling_every_tile_phase():
+    """Valid 4-byte / 3-byte / 2-byte characters across the 8 KiB tile boundary: S:638."""
+    for ch in ("\U0001F600", "你", "é"):
+        e = ch.encode()
+        for ph in range(0, 8):
+            pre = TILE - ph
+            a = np.frombuffer(b"a" * pre + e * 3 + b"z" * 5, dtype=np.uint8)
+            for off in (0, 5):
+                r = check_utf8(a, offset=off)
+                assert r.error == 0
+            u = oracle.utf8_to_utf16le(a)[1]
+            check_utf16(u)
+
+
+# ----------------------------------------------------------------------------- random fuzz
+def test_fuzz_utf8():
+    rng = np.random.default_rng(1234)
+    reps = np.array([0x00, 0x41, 0x7F, 0x80, 0x8F, 0x90, 0x9F, 0xA0, 0xBF, 0xC0, 0xC1, 0xC2,
+                     0xDF, 0xE0, 0xE1, 0xEC, 0xED, 0xEE, 0xEF, 0xF0, 0xF1, 0xF3, 0xF4, 0xF5,
+                     0xF7, 0xF8, 0xFF], dtype=np.uint8)
+    for k in range(400):
+        n = int(rng.integers(0, 300))
+        if k % 3 == 0:
+            a = reps[rng.integers(0, reps.size, n)]
+        elif k % 3 == 1:
+            a = rng.integers(0, 256, n, dtype=np.uint8)
+        else:
+            a = np.frombuffer(synth.gen_chunk("mixed", "utf8", n, 99, k), dtype=np.uint8).copy()
+            if n:
+                a[rng.integers(0, n)] = rng.integers(0x80, 0x100)
+        check_utf8(a, offset=int(rng.integers(0, 16)))
+
+
+def test_fuzz_utf16():
+    rng = np.random.default_rng(4321)
+    alpha = np.array([0x0041, 0x007F, 0x0080, 0x07FF, 0x0800, 0xD7FF, 0xD800, 0xDBFF, 0xDC00,
+                      0xDFFF, 0xE000, 0xFFFF], dtype=np.uint16)
+    for k in range(400):
+        n = int(rng.integers(0, 200))
+        u = alpha[rng.integers(0, alpha.size, n)] if k % 2 else \
+            rng.integers(0, 65536, n).astype(np.uint16)
+        check_utf16(u, offset=2 * int(rng.integers(0, 8)))
+
+
+# ----------------------------------------------------------------------------- capacity
+def test_capacity():
+    a = np.frombuffer(synth.gen_chunk("mixed", "utf8", 50000, 3, 0), dtype=np.uint8)
+    need = oracle.utf8_to_utf16le(a)[0].written
+    for cap in (0, 1, 7, need // 2, need - 1, need, need + 1):
+        check_utf8(a, cap=cap)
+    u = oracle.utf8_to_utf16le(a)[1]
+    need8 = oracle.utf16le_to_utf8(u)[0].written
+    for cap in (0, 5, need8 - 1, need8):
+        check_utf16(u, cap=cap)
+
+
+# ----------------------------------------------------------------------------- configs
+@pytest.fixture(scope="module")
+def c0():
+    return synth.generate("c0")
+
+
+def test_config0_clean_and_error_copies(c0):
+    r = check_utf8(c0)
+    assert r.error == 0 and r.position == c0.size
+    u = oracle.utf8_to_utf16le(c0)[1]
+    check_utf16(u)
+    rng = np.random.default_rng(np.random.SeedSequence([0, 0xE, 1, 0]))
+    for cls in synth.UTF8_ERROR_CLASSES:
+        for j in range(3):
+            b = c0.copy()
+            p, _ = synth.inject_utf8_error(b, 0, b.size - 8, cls, rng)
+            r = check_utf8(b, offset=j)
+            assert r.position == p and r.error == synth.UTF8_EXPECTED_KIND[cls], (cls, r, p)
+
+
+def test_config3_error_copy():
+    u = synth.generate("c3", size=4 << 20)
+    check_utf16(u)
+    rng = np.random.default_rng(np.random.SeedSequence([4, 0xE, 1, 0]))
+    for j in range(6):
+        v = u.copy()
+        p, _ = synth.inject_utf16_error(v, 0, v.size - 1, rng)
+        r = check_utf16(v)
+        assert (r.error, r.position) == (ug.SURROGATE, p)
+
+
+@pytest.mark.parametrize("key", ["c1", "c2a", "c2b", "c3"])
+def test_configs_reduced(key):
+    """Each config's generator at 8 MiB, both directions, element by element."""
+    x = synth.generate(key, size=8 << 20)
+    if x.dtype == np.uint8:
+        check_utf8(x, offset=3)
+        u = oracle.utf8_to_utf16le(x)[1]
+        check_utf16(u)
+    else:
+        check_utf16(x)
+
+
+# ----------------------------------------------------------------------------- async / host
+def test_async_and_host_variants(c0):
+    t, tin = to_dev(c0)
+    out = torch.zeros(c0.size, dtype=torch.int16, device=DEV)
+    res = ug.result_buffer(DEV, 2)
+    ug.utf8_to_utf16le_async(tin, out, res)
+    ug.utf8_validate_async(tin, res, result_off=ug.RESULT_BYTES)
+    lens = torch.zeros(2, dtype=torch.int64, device=DEV)
+    ug.utf16_length_from_utf8_async(tin, lens)
+    torch.cuda.synchronize()
+    r = ug.decode_results(res)
+    ref = oracle.utf8_to_utf16le(c0)
+    assert tuple(r[0]) == tuple(ref[0])
+    assert tuple(r[1]) == tuple(oracle.utf8_validate(c0))
+    assert int(lens[0]) == ref[0].written
+    assert np.array_equal(out[: ref[0].written].cpu().numpy().view(np.uint16), ref[1])
+    # host buffers (pinned)
+    hin = torch.from_numpy(c0.copy()).pin_memory()
+    hout = torch.zeros(c0.size, dtype=torch.int16).pin_memory()
+    rh = ug.utf8_to_utf16le_host(hin, hout)
+    assert tuple(rh) == tuple(ref[0])
+    assert np.array_equal(hout[: rh.written].numpy().view(np.uint16), ref[1])
+    h8 = torch.zeros(3 * rh.written, dtype=torch.uint8).pin_memory()
+    rr = ug.utf16le_to_utf8_host(hout[: rh.written], h8)
+    assert rr == (0, rh.written, c0.size) and bytes(h8[: rr.written].numpy()) == c0.tobytes()
+
+
+# ----------------------------------------------------------------------------- virtual shards
+def shard_plan(a: np.ndarray, G: int):
+    """Nominal cuts k*floor(n/G) aligned down to 16, backed off to character starts."""
+    n = a.size
+    cuts = [0]
+    for k in range(1, G):
+        c = (k * (n // G)) & ~15
+        cuts.append(c - ug.utf8_cut_backoff(a[max(0, c - 8):c + 8].tobytes(), c - max(0, c - 8)))
+    cuts.append(n)
+    return cuts
+
+
+def run_shards_fwd(a: np.ndarray, G: int):
+    """G logical shards of one device buffer, each through the shard kernel, records combined
+    on the device."""
+    _, t = to_dev(a)
+    cuts = shard_plan(a, G)
+    n = a.size
+    recs = ug.record_buffer(DEV, G)
+    outs = []
+    for k in range(G):
+        lo, hi = cuts[k], cuts[k + 1]
+        out = torch.zeros(max(hi - lo, 1), dtype=torch.int16, device=DEV)
+        ug.utf8_to_utf16le_shard_async(t, lo, hi - lo, min(lo, 3), min(n - hi, 3), lo, out, recs,
+                                       rec_off=k * ug.RECORD_BYTES)
+        outs.append(out)
+    res = ug.result_buffer(DEV, G)
+    offs = torch.zeros(G, dtype=torch.int64, device=DEV)
+    for k in range(G):
+        ug.combine_records_async(recs, G, k, n, res[k * ug.RESULT_BYTES:], offs[k:])
+    torch.cuda.synchronize()
+    results = ug.decode_results(res)
+    assert all(r == results[0] for r in results)
+    records = ug.decode_records(recs)
+    return results[0], records, outs, offs.cpu().tolist(), cuts
+
+
+@pytest.mark.parametrize("G", [2, 3, 8])
+def test_virtual_shards_match_unsharded(c0, G):
+    r, records, outs, offs, cuts = run_shards_fwd(c0, G)
+    ref_r, ref_o = oracle.utf8_to_utf16le(c0)
+    assert tuple(r) == tuple(ref_r)
+    got = np.concatenate([outs[k][: records[k].count].cpu().numpy().view(np.uint16)
+                          for k in range(G)])
+    assert np.array_equal(got, ref_o)
+    assert offs == list(np.cumsum([0] + [rec.count for rec in records[:-1]]))
+    # the reverse direction on each rank's whole-character output, no new cuts
+    for k in range(G):
+        u = outs[k][: records[k].count]
+        out8 = torch.zeros(3 * max(u.numel(), 1), dtype=torch.uint8, device=DEV)
+        rr = ug.utf16le_to_utf8(u, out8)
+        assert rr.error == 0 and bytes(out8[: rr.written].cpu().numpy()) == \
+            c0[cuts[k]:cuts[k + 1]].tobytes()
+
+
+def test_virtual_shards_error_near_cut(c0):
+    """Errors placed within 3 bytes of a shard cut: the global first error, kind and written
+    count are exact (BASELINE config 4's error copies, at 1 MiB)."""
+    G = 4
+    rng = np.random.default_rng(np.random.SeedSequence([5, 0xE, G, 0]))
+    for j in range(16):
+        b = c0.copy()
+        k = int(rng.integers(1, G))
+        c = (k * (b.size // G)) & ~15
+        cls = synth.UTF8_ERROR_CLASSES[j % 5]
+        p, _ = synth.inject_utf8_error(b, c - 3, c + 3, cls, rng)
+        r, *_ = run_shards_fwd(b, G)
+        ref = oracle.utf8_to_utf16le(b)[0]
+        assert tuple(r) == tuple(ref) and r.position == p, (cls, r, ref, p)

@@ -1,0 +1,127 @@
+"""CPU-only checks of the C-ABI library: it loads, exports every symbol include/unigpu.h
+declares, and its host-side logic (cut back-off, record combine, argument checks that return
+before touching the GPU) behaves as specified.  No compute calls need a GPU here."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def ug():
+    import __graft_entry__
+    __graft_entry__.build_library()
+    import paper_2111_08692_b200 as ug
+    return ug
+
+
+def declared_symbols():
+    src = open(os.path.join(ROOT, "include", "unigpu.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"^\s*(?:const\s+)?[A-Za-z_][A-Za-z0-9_]*\s*\*?\s*([A-Za-z_][A-Za-z0-9_]*)\s*\(",
+                       src, flags=re.M)
+    return sorted(set(names))
+
+
+def test_header_declares_the_north_star_names():
+    names = declared_symbols()
+    for n in ("utf8_validate", "utf16le_validate", "utf8_to_utf16le", "utf16le_to_utf8",
+              "utf16_length_from_utf8", "utf8_length_from_utf16le"):
+        assert n in names
+    assert len(names) >= 25
+
+
+def test_library_exports_every_declared_symbol(ug):
+    lib = ctypes.CDLL(ug.LIB_PATH)
+    missing = [n for n in declared_symbols() if not hasattr(lib, n)]
+    assert not missing, missing
+
+
+def test_abi_and_names(ug):
+    assert ug.lib.ug_abi_version() == 1
+    assert ug.error_name(0) == "OK" and ug.error_name(6) == "Surrogate"
+    assert ug.error_name(-3) == "OutputTooSmall"
+
+
+def test_sass_is_sm100a_with_tma(ug):
+    """The kernels are compiled for sm_100a and use TMA bulk copies (UBLKCP)."""
+    import subprocess
+    out = subprocess.run(["cuobjdump", "-sass", ug.LIB_PATH], capture_output=True,
+                         text=True).stdout
+    assert "sm_100a" in out
+    assert "UBLKCP" in out and "PRMT" in out
+
+
+def test_utf8_cut_backoff(ug):
+    """back off over at most 3 continuation bytes."""
+    s = "aé你\U0001F600".encode()  # 61 C3A9 E4BDA0 F09F9880
+    starts = {0, 1, 3, 6}
+    for at in range(len(s)):
+        k = ug.utf8_cut_backoff(s, at)
+        assert at - k in starts and 0 <= k <= 3, (at, k)
+    # never further than 3, even over a run of continuation bytes
+    run = bytes([0x41] + [0x80] * 6)
+    assert ug.utf8_cut_backoff(run, 6) == 3
+    # at the start of the buffer nothing is readable before the cut
+    assert ug.utf8_cut_backoff(bytes([0x80, 0x80]), 0) == 0
+
+
+def test_utf16_cut_backoff(ug):
+    w = [0x41, 0xD83D, 0xDE00, 0x42]
+    assert [ug.utf16_cut_backoff(w, i) for i in range(4)] == [0, 0, 1, 0]
+
+
+def test_combine_records_host(ug):
+    N = ug.NONE
+    # three valid shards: offsets are exclusive prefixes of the counts
+    recs = [(10, N, 0, 0, 0), (7, N, 0, 0, 0), (5, N, 0, 0, 0)]
+    for rank, off in enumerate([0, 10, 17]):
+        r, o = ug.combine_records_host(recs, rank, 100)
+        assert r == (0, 100, 22) and o == off
+    # errors on ranks 1 and 2: the smaller global offset wins; written adds the rank offset
+    recs = [(10, N, 0, 0, 0), (7, 55, 3, 4, 0), (5, 60, 1, 2, 0)]
+    r, o = ug.combine_records_host(recs, 2, 100)
+    assert r == (4, 55, 13) and o == 17
+    # a too-small buffer before the error owner makes the call OutputTooSmall
+    recs = [(10, N, 0, 0, 1), (7, 55, 3, 4, 0)]
+    r, _ = ug.combine_records_host(recs, 0, 100)
+    assert r == (-3, 13, 0)
+    # ... but not after it
+    recs = [(10, 5, 2, 3, 0), (7, N, 0, 0, 1)]
+    r, _ = ug.combine_records_host(recs, 0, 100)
+    assert r == (3, 5, 2)
+
+
+def test_argument_errors_need_no_gpu(ug):
+    """API misuse is rejected on the host before any CUDA call."""
+    null = None
+    r = ug.lib.utf8_validate(ctypes.c_void_p(0), 5, ctypes.c_void_p(0))
+    assert r.error == ug.ERR_ARG
+    r = ug.lib.utf8_to_utf16le(ctypes.c_void_p(0), 5, ctypes.c_void_p(0), 0, ctypes.c_void_p(0))
+    assert r.error == ug.ERR_ARG
+    assert ug.lib.ug_utf8_validate_async(ctypes.c_void_p(16), 4, ctypes.c_void_p(0),
+                                         ctypes.c_void_p(0)) == ug.ERR_ARG
+    # empty input is OK without launching anything
+    r = ug.lib.utf16le_to_utf8(ctypes.c_void_p(0), 0, ctypes.c_void_p(0), 0, ctypes.c_void_p(0))
+    assert (r.error, r.position, r.written) == (0, 0, 0)
+    assert null is None
+
+
+def test_product_does_not_import_oracle():
+    """The product package and the oracle share no code: neither imports / includes the
+    other."""
+    pkg = os.path.join(ROOT, "paper_2111_08692_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h", ".cpp")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert not re.search(r"^\s*(import|from)\s+oracle", txt, re.M), f
+                assert not re.search(r'#include\s+".*oracle', txt), f
+    for f in os.listdir(os.path.join(ROOT, "oracle")):
+        if f.endswith((".c", ".h", ".py")):
+            txt = open(os.path.join(ROOT, "oracle", f)).read()
+            assert not re.search(r"^\s*(import|from)\s+paper_2111_08692_b200", txt, re.M), f
+            assert not re.search(r'#include\s+".*(unigpu|csrc)', txt), f
