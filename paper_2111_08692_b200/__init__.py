@@ -18,7 +18,7 @@ import os
 from typing import NamedTuple
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libunigpu.so")
+LIB_PATH = os.environ.get("UG_LIB_OVERRIDE") or os.path.join(_HERE, "libunigpu.so")
 
 OK, HEADER_BITS, TOO_SHORT, TOO_LONG, OVERLONG, TOO_LARGE, SURROGATE = range(7)
 ERR_ARG, ERR_CUDA, ERR_OUTPUT_TOO_SMALL = -1, -2, -3

@@ -12,9 +12,10 @@ namespace ug {
 
 constexpr uint32_t FULL = 0xffffffffu;
 constexpr uint64_t NONE = ~0ull;
-constexpr int NT = 256;           // threads per CTA for the tile kernels
-constexpr int TILE = 8192;        // input bytes per tile (8192 UTF-8 bytes / 4096 UTF-16 words)
+constexpr int NT = 512;           // threads per CTA for the tile kernels
+constexpr int TILE = 16384;       // input bytes per tile (16 Ki UTF-8 bytes / 8 Ki UTF-16 words)
 constexpr int BPT = TILE / NT;    // 32 contiguous input bytes per thread
+constexpr int LB_PER_LANE = 8;    // look-back window: 32 lanes x 8 status words = 256 tiles
 constexpr int HALO = 16;          // bytes of context loaded before and after each tile
 constexpr int INBUF = TILE + 2 * HALO;
 
@@ -98,6 +99,19 @@ __device__ __forceinline__ void st_relaxed(uint64_t *p, uint64_t v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
+// ---------------------------------------------------------------- named barriers
+// bar.arrive has release and bar.sync acquire semantics for the participating threads' shared
+// memory accesses (producer / consumer hand-off between warp roles).
+// Barrier ids are immediates so ptxas reserves only the ids actually used.
+template <int ID, int N>
+__device__ __forceinline__ void named_sync() {
+  asm volatile("bar.sync %0, %1;" ::"n"(ID), "n"(N) : "memory");
+}
+template <int ID, int N>
+__device__ __forceinline__ void named_arrive() {
+  asm volatile("bar.arrive %0, %1;" ::"n"(ID), "n"(N) : "memory");
+}
+
 // ---------------------------------------------------------------- warp / block helpers
 __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t v, int lane) {
 #pragma unroll
@@ -154,12 +168,14 @@ __device__ __forceinline__ void issue_tile_load(const Window &w, long long t, ui
 }
 
 // After the load landed: zero every smem byte whose position lies outside the valid window
-// (only tiles touching the window edges do any work).  Block-wide; caller syncs after.
-__device__ __forceinline__ void fix_tile_edges(const Window &w, long long t, uint8_t *buf) {
+// (only tiles touching the window edges do any work).  Called by threads 0..nthreads-1; the
+// caller syncs after.
+__device__ __forceinline__ void fix_tile_edges(const Window &w, long long t, uint8_t *buf,
+                                               int nthreads) {
   long long p0 = tile_pos(w, t) - HALO;
   if (p0 >= w.lo_valid && p0 + INBUF <= w.hi_valid) return;
   uint32_t *b32 = reinterpret_cast<uint32_t *>(buf);
-  for (int q = threadIdx.x; q < INBUF / 4; q += blockDim.x) {
+  for (int q = threadIdx.x; q < INBUF / 4; q += nthreads) {
     long long pos = p0 + 4 * q;
     if (pos >= w.lo_valid && pos + 4 <= w.hi_valid) continue;
     b32[q] &= range_bytes(pos, w.lo_valid, w.hi_valid);
@@ -167,38 +183,51 @@ __device__ __forceinline__ void fix_tile_edges(const Window &w, long long t, uin
 }
 
 // ---------------------------------------------------------------- decoupled look-back
-// Called by one full warp for tile t with its aggregate already published (t > 0).  Returns
-// the exclusive prefix (sum of all earlier tiles' aggregates) in every lane.
+// Called by one full warp for tile t whose aggregate is already published (t > 0).  Returns the
+// exclusive prefix (sum of all earlier tiles' aggregates) in every lane.  Each round reads a
+// window of 256 predecessors (8 per lane, nearest first) with independent relaxed loads, so the
+// PREFIX frontier advances 256 tiles per L2 round trip (K2).
 __device__ __forceinline__ uint64_t look_back(uint64_t *status, uint32_t epoch, long long t,
                                               int lane) {
   uint64_t excl = 0;
   long long idx = t - 1;
   while (true) {
-    long long j = idx - lane;
-    uint32_t flag;
-    uint64_t val;
-    if (j < 0) {
-      flag = FLAG_PREFIX;
-      val = 0;
-    } else {
-      uint64_t s;
-      int spins = 0;
-      while (true) {
-        s = ld_relaxed(status + j);
-        if ((uint32_t)(s >> 40) == epoch && ((s >> 38) & 3u) != 0) break;
-        if (++spins > 8) __nanosleep(32);
+    const long long j0 = idx - (long long)LB_PER_LANE * lane;  // nearest tile of this lane
+    uint64_t s[LB_PER_LANE];
+#pragma unroll
+    for (int k = 0; k < LB_PER_LANE; k++) s[k] = (j0 - k >= 0) ? ld_relaxed(status + j0 - k) : 0;
+    // re-poll until every word this lane needs is at least an aggregate
+    int spins = 0;
+    while (true) {
+      bool ready = true;
+#pragma unroll
+      for (int k = 0; k < LB_PER_LANE; k++)
+        if (j0 - k >= 0 && !((uint32_t)(s[k] >> 40) == epoch && ((s[k] >> 38) & 3u) != 0))
+          ready = false;
+      if (ready) break;
+      if (++spins > 4) __nanosleep(20);
+#pragma unroll
+      for (int k = 0; k < LB_PER_LANE; k++)
+        if (j0 - k >= 0 && !((uint32_t)(s[k] >> 40) == epoch && ((s[k] >> 38) & 3u) != 0))
+          s[k] = ld_relaxed(status + j0 - k);
+    }
+    bool has_p = false;
+    uint64_t lane_sum = 0;
+#pragma unroll
+    for (int k = 0; k < LB_PER_LANE; k++) {
+      if (!has_p) {
+        bool pre = (j0 - k < 0) || (((s[k] >> 38) & 3u) == FLAG_PREFIX);
+        lane_sum += (j0 - k < 0) ? 0ull : (s[k] & ((1ull << 38) - 1));
+        has_p = pre;
       }
-      flag = (uint32_t)((s >> 38) & 3u);
-      val = s & ((1ull << 38) - 1);
     }
-    uint32_t pm = __ballot_sync(FULL, flag == FLAG_PREFIX);
+    const uint32_t pm = __ballot_sync(FULL, has_p);
     if (pm) {
-      int first = __ffs(pm) - 1;
-      excl += warp_sum64(lane <= first ? val : 0ull);
-      return excl;
+      const int first = __ffs(pm) - 1;
+      return excl + warp_sum64(lane <= first ? lane_sum : 0ull);
     }
-    excl += warp_sum64(val);
-    idx -= 32;
+    excl += warp_sum64(lane_sum);
+    idx -= (long long)LB_PER_LANE * 32;
   }
 }
 

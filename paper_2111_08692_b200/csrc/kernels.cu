@@ -9,12 +9,14 @@
 // Finalisation (first-error kind, written count, result slot, counter reset) is done by the
 // last CTA to finish (K7), so every API call is one launch.
 //
-// Tile pipeline (all tile kernels): persistent CTAs of 256 threads pull 8 KiB tiles by
+// Tile pipeline (all tile kernels): persistent CTAs of 512 threads pull 16 KiB tiles by
 // atomic ticket (issue order makes the decoupled look-back deadlock-free), bulk-load tile +
 // 16-byte halos into shared memory with TMA (cp.async.bulk + mbarrier, 2 stages: the next
 // tile is in flight while the current one is processed), and each thread owns 32 contiguous
-// input bytes.  Output is staged in shared memory at the global address phase and leaves
-// through one TMA bulk store (cp.async.bulk.global.shared::cta) plus <16 head/tail units.
+// input bytes.  Transcoders: warp 0 publishes the tile aggregate and looks back while the
+// other warps already decode into a shared-memory stage at tile-local offsets; once the
+// tile's global offset is known every thread streams 16-byte output chunks, re-aligned to the
+// global address phase in registers (funnel shifts), with 128-bit stores.
 #include <cstdint>
 
 #include "device.cuh"
@@ -25,8 +27,10 @@
 namespace ug {
 
 constexpr unsigned long long VALMASK = (1ull << 38) - 1;
-constexpr int STAGE8_UNITS = TILE + 16;            // UTF-16 units staged per UTF-8 tile
-constexpr int STAGE16_BYTES = 3 * (TILE / 2) + 32;   // UTF-8 bytes staged per UTF-16 tile
+// named barrier ids (0 is __syncthreads)
+constexpr int BAR_DATA = 1;           // the NT data threads
+constexpr int BAR_C0 = 2, BAR_C1 = 3;  // data -> look-back warp: tile aggregate ready
+constexpr int BAR_P0 = 4, BAR_P1 = 5;  // look-back warp -> data: tile prefix ready
 
 __device__ __forceinline__ uint32_t byte_at(const Window &w, long long pos) {
   return (pos >= w.lo_valid && pos < w.hi_valid) ? (uint32_t)w.base[pos] : 0u;
@@ -38,41 +42,57 @@ __device__ __forceinline__ uint32_t word_at(const Window &w, long long wpos) {
              : 0u;
 }
 
-// Copy staged units [phase, phase + C) to out[P, P + C) (clipped at cap): aligned interior
-// by one TMA bulk store, the < A-unit head and tail by plain stores.  A = units per 16 B.
-template <typename T>
-__device__ __forceinline__ void copy_out(T *out, unsigned long long cap, unsigned long long P,
-                                         uint32_t C, uint32_t phase, const T *stage, int tid) {
-  constexpr unsigned long long A = 16 / sizeof(T);
-  unsigned long long lo = P, hi = P + C;
-  if (hi > cap) hi = cap;
-  if (hi <= lo) return;
-  unsigned long long ua = P - phase;  // stage index k <-> unit ua + k; out + ua is 16B-aligned
-  unsigned long long a_lo = phase ? ua + A : ua;
-  unsigned long long a_hi = ua + ((hi - ua) / A) * A;
-  if (a_lo < a_hi) {
-    if (tid == 0) {
-      fence_proxy_async_smem();
-      bulk_s2g(out + a_lo, stage + (a_lo - ua), (uint32_t)((a_hi - a_lo) * sizeof(T)));
-      bulk_commit();
-    }
-    long long nh = (long long)(a_lo - lo);
-    if (tid < nh) out[lo + tid] = stage[phase + tid];
-    long long nt = (long long)(hi - a_hi);
-    if (tid >= 64 && tid - 64 < nt) out[a_hi + (tid - 64)] = stage[(a_hi - ua) + (tid - 64)];
-  } else {
-    long long m = (long long)(hi - lo);
-    if (tid < m) out[lo + tid] = stage[phase + tid];
+// out[P + k] = stage[k] for k in [0, C), clipped at out[cap).  The 16-byte aligned interior is
+// written with 128-bit stores; each chunk is two 128-bit shared loads re-aligned by a
+// tile-uniform funnel shift.  Head and tail (< 16 bytes each) use scalar stores.
+__device__ __forceinline__ uint4 shift_window(const uint4 &a, const uint4 &b, uint32_t q,
+                                              uint32_t r) {
+  uint4 o;
+  switch (q) {
+    case 0: o = make_uint4(__funnelshift_r(a.x, a.y, r), __funnelshift_r(a.y, a.z, r),
+                           __funnelshift_r(a.z, a.w, r), __funnelshift_r(a.w, b.x, r)); break;
+    case 1: o = make_uint4(__funnelshift_r(a.y, a.z, r), __funnelshift_r(a.z, a.w, r),
+                           __funnelshift_r(a.w, b.x, r), __funnelshift_r(b.x, b.y, r)); break;
+    case 2: o = make_uint4(__funnelshift_r(a.z, a.w, r), __funnelshift_r(a.w, b.x, r),
+                           __funnelshift_r(b.x, b.y, r), __funnelshift_r(b.y, b.z, r)); break;
+    default: o = make_uint4(__funnelshift_r(a.w, b.x, r), __funnelshift_r(b.x, b.y, r),
+                            __funnelshift_r(b.y, b.z, r), __funnelshift_r(b.z, b.w, r)); break;
   }
+  return o;
 }
 
-// Block exclusive scan of per-thread counts: returns the thread's exclusive prefix within the
-// tile and the tile total.  One __syncthreads inside.
+template <typename T>
+__device__ __forceinline__ void copy_out(T *out, unsigned long long cap, unsigned long long P,
+                                         uint32_t C, const T *stage, int tid) {
+  constexpr uint32_t A = 16 / sizeof(T);  // units per 16 bytes
+  unsigned long long hi = P + C;
+  if (hi > cap) hi = cap;
+  if (hi <= P) return;
+  const uint32_t Cc = (uint32_t)(hi - P);
+  const uint32_t mis = (uint32_t)(((uintptr_t)(out + P) & 15u) / sizeof(T));
+  const uint32_t s0 = mis ? A - mis : 0u;  // first stage index landing on a 16B boundary
+  if (s0 >= Cc) {
+    if ((uint32_t)tid < Cc) out[P + tid] = stage[tid];
+    return;
+  }
+  const uint32_t nfull = (Cc - s0) / A;
+  const uint32_t t0 = s0 + nfull * A;
+  if ((uint32_t)tid < s0) out[P + tid] = stage[tid];
+  if (tid >= 64 && (uint32_t)(tid - 64) < Cc - t0) out[P + t0 + (tid - 64)] = stage[t0 + (tid - 64)];
+  const uint32_t sb = s0 * (uint32_t)sizeof(T);  // byte offset of chunk 0 inside stage[0..16)
+  const uint32_t q = sb >> 2, r = (sb & 3u) * 8u;
+  const uint4 *st = reinterpret_cast<const uint4 *>(stage);
+  uint4 *dst = reinterpret_cast<uint4 *>(out + P + s0);
+  for (uint32_t c = tid; c < nfull; c += NT) dst[c] = shift_window(st[c], st[c + 1], q, r);
+}
+
+// Block exclusive scan over the NT data threads: returns the thread's exclusive prefix within
+// the tile and the tile total.  One data-warp barrier inside.
 __device__ __forceinline__ void block_scan(uint32_t cnt, uint32_t *s_wsum, int lane, int warp,
                                            uint32_t *excl, uint32_t *total) {
   uint32_t incl = warp_incl_scan(cnt, lane);
   if (lane == 31) s_wsum[warp] = incl;
-  __syncthreads();
+  named_sync<BAR_DATA, NT>();
   uint32_t wpre = 0, C = 0;
 #pragma unroll
   for (int i = 0; i < NT / 32; i++) {
@@ -84,7 +104,7 @@ __device__ __forceinline__ void block_scan(uint32_t cnt, uint32_t *s_wsum, int l
   *total = C;
 }
 
-// Publish tile t's aggregate, look back, publish its inclusive prefix; warp 0 only.
+// Publish tile t's aggregate, look back, publish its inclusive prefix; one full warp.
 __device__ __forceinline__ unsigned long long tile_prefix(const TileArgs &a, long long t,
                                                           uint32_t C, int lane) {
   unsigned long long P;
@@ -137,24 +157,344 @@ __device__ __forceinline__ void write_outcome(const TileArgs &a, bool xc, int ki
   a.ctr->err_min = NONE;
 }
 
-// ============================================================================ UTF-8 tiles
-template <bool XC>
-__global__ void __launch_bounds__(NT) k_utf8(const TileArgs a) {
+// ============================================================================ UTF-8 policy
+// Positions are bytes.  Thread `tid` owns tile bytes [32 tid, 32 tid + 32).
+struct U8Pol {
+  using Out = uint16_t;
+  static constexpr int UNIT = 1;                      // input bytes per position
+  static constexpr int STAGE = 2 * (TILE + 32);        // stage bytes per buffer
+  struct St {
+    uint32_t w[9];   // own 32 bytes + the next 4
+    uint32_t prev;   // the 4 bytes before
+    uint32_t cm[8];  // width bits (a5)
+    uint32_t err;    // classifier flags (a3)
+    long long pos0;  // position of own byte 0
+    bool wasc, interior;
+  };
+
+  __device__ static __forceinline__ uint32_t analyze(St &s, const uint8_t *buf, int tid,
+                                                     int lane, long long tp, long long n,
+                                                     bool xc) {
+    const uint8_t *my = buf + HALO + BPT * tid;
+    {
+      uint4 q0 = *reinterpret_cast<const uint4 *>(my);
+      uint4 q1 = *reinterpret_cast<const uint4 *>(my + 16);
+      s.w[0] = q0.x; s.w[1] = q0.y; s.w[2] = q0.z; s.w[3] = q0.w;
+      s.w[4] = q1.x; s.w[5] = q1.y; s.w[6] = q1.z; s.w[7] = q1.w;
+    }
+    uint32_t prev = __shfl_up_sync(FULL, s.w[7], 1);
+    uint32_t nxt = __shfl_down_sync(FULL, s.w[0], 1);
+    if (lane == 0) prev = *reinterpret_cast<const uint32_t *>(my - 4);
+    if (lane == 31) nxt = *reinterpret_cast<const uint32_t *>(my + BPT);
+    s.w[8] = nxt;
+    s.prev = prev;
+    s.pos0 = tp + BPT * tid;
+    s.interior = (tp >= 0) && (tp + TILE + 1 <= n);
+    // a2: warp ASCII fast path (no byte >= 0x80 and no pending lead before the warp)
+    uint32_t orv = s.w[0] | s.w[1] | s.w[2] | s.w[3] | s.w[4] | s.w[5] | s.w[6] | s.w[7];
+    bool pend = (prev >= 0xC0000000u) || ((prev & 0x00FF0000u) >= 0x00E00000u) ||
+                ((prev & 0x0000FF00u) >= 0x0000F000u);
+    s.wasc = __all_sync(FULL, ((orv & u8::HI) == 0u) && !pend);
+    s.err = 0;
+    if (s.wasc) {
+#pragma unroll
+      for (int k = 0; k < 8; k++) s.cm[k] = u8::HI;
+    } else {
+      // a3 classification + a5 widths
+      u8::WordMasks pm = u8::masks(prev, true);
+      u8::WordMasks cur = u8::masks(s.w[0], true);
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        u8::WordMasks nx = u8::masks(s.w[k + 1], true);
+        s.err |= u8::classify(pm, cur);
+        s.cm[k] = xc ? u8::width_bits(cur, nx.K) : 0u;
+        pm = cur;
+        cur = nx;
+      }
+      if (tid == NT - 1) s.err |= u8::classify(pm, cur);  // look-ahead positions TILE..TILE+3
+    }
+    uint32_t cnt = 0;
+    if (xc) {
+      if (!s.interior) {
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+          long long pos = s.pos0 + 4 * k;
+          uint32_t own = range_bytes(pos, 0, n) & u8::HI;
+          uint32_t own1 = (range_bytes(pos, 0, n - 1) & u8::HI) >> 1;
+          s.cm[k] &= own | own1;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 8; k++) cnt += __popc(s.cm[k]);
+    }
+    return cnt;
+  }
+
+  __device__ static __forceinline__ bool hint(const St &s) { return s.err != 0; }
+
+  // a4: exact rescan of the owned positions (cold: only in flagged tiles)
+  __device__ static __forceinline__ unsigned long long find_error(const St &s, long long n) {
+    unsigned long long found = NONE;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      const uint32_t wb = k ? s.w[k - 1] : s.prev;
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const long long pos = s.pos0 + 4 * k + j;
+        const uint32_t back = __funnelshift_r(wb, s.w[k], 8 * j);
+        const uint32_t fwd = __funnelshift_r(s.w[k], s.w[k + 1], 8 * j);
+        if (found == NONE && pos >= 0 && pos < n && u8::err_at(back, fwd))
+          found = (unsigned long long)pos;
+      }
+    }
+    return found;
+  }
+
+  // a7: decode the owned characters into stage[o ...] (UTF-16 units)
+  __device__ static __forceinline__ void decode(const St &s, uint16_t *stage, uint32_t o) {
+    if (s.wasc && s.interior) {
+      if ((o & 1u) == 0u) {
+        uint32_t *st32 = reinterpret_cast<uint32_t *>(stage + o);
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+          st32[2 * k] = u8::prmt(s.w[k], 0u, 0x4140u);
+          st32[2 * k + 1] = u8::prmt(s.w[k], 0u, 0x4342u);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 8; k++)
+#pragma unroll
+          for (int j = 0; j < 4; j++) stage[o + 4 * k + j] = (uint16_t)((s.w[k] >> (8 * j)) & 0xFFu);
+      }
+      return;
+    }
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      const uint32_t c = s.cm[k];
+      uint32_t lead = c & u8::HI;
+      while (lead) {
+        const int b = __ffs(lead) - 1;  // 7, 15, 23 or 31
+        lead &= lead - 1u;
+        const uint32_t sh = (uint32_t)(b - 7);
+        const uint32_t x = __funnelshift_r(s.w[k], s.w[k + 1], sh);
+        uint32_t u1;
+        const uint32_t u0 = u8::decode_units(x, &u1);
+        const uint32_t off = o + __popc(c & ((1u << sh) - 1u));
+        stage[off] = (uint16_t)u0;
+        if (c & (1u << (b - 1))) stage[off + 1] = (uint16_t)u1;
+      }
+      o += __popc(c);
+    }
+  }
+
+  // a10 (last CTA, warp 0): kind of the first error and units written before it
+  __device__ static __forceinline__ void finalize(const TileArgs &a, unsigned long long e,
+                                                  bool xc, int lane, int *kind,
+                                                  unsigned long long *wr) {
+    const Window &win = a.win;
+    uint32_t x = 0;
+#pragma unroll
+    for (int j = 0; j < 4; j++) x |= byte_at(win, (long long)e + j) << (8 * j);
+    *kind = u8::decode_kind(x);
+    *wr = 0;
+    if (!xc) return;
+    long long te = ((long long)e + win.lead) / TILE;
+    unsigned long long base = te ? (ld_relaxed(a.status + te - 1) & VALMASK) : 0ull;
+    long long from = te * TILE - win.lead;
+    if (from < 0) from = 0;
+    unsigned long long c = 0;
+    for (long long i = from + lane; i < (long long)e; i += 32) {
+      uint32_t bi = byte_at(win, i), bn = byte_at(win, i + 1);
+      c += ((bi & 0xC0u) != 0x80u) ? 1u : 0u;
+      c += (bi >= 0xF0u && (bn & 0xC0u) == 0x80u && i + 1 < win.n) ? 1u : 0u;
+    }
+    *wr = base + warp_sum64(c);
+  }
+};
+
+// ============================================================================ UTF-16 policy
+// Positions are words.  Thread `tid` owns tile words [16 tid, 16 tid + 16).
+struct U16Pol {
+  using Out = uint8_t;
+  static constexpr int UNIT = 2;
+  static constexpr int STAGE = 3 * (TILE / 2) + 64;
+  struct St {
+    uint32_t w[8];
+    uint32_t prev_word, next_word;
+    unsigned long long first_err;
+    long long pos0;
+    bool wasc, interior, sur;
+  };
+
+  __device__ static __forceinline__ uint32_t analyze(St &s, const uint8_t *buf, int tid,
+                                                     int lane, long long tp_bytes, long long n_bytes,
+                                                     bool xc) {
+    const long long tpw = tp_bytes / 2, nw = n_bytes / 2;
+    const uint8_t *my = buf + HALO + BPT * tid;
+    {
+      uint4 q0 = *reinterpret_cast<const uint4 *>(my);
+      uint4 q1 = *reinterpret_cast<const uint4 *>(my + 16);
+      s.w[0] = q0.x; s.w[1] = q0.y; s.w[2] = q0.z; s.w[3] = q0.w;
+      s.w[4] = q1.x; s.w[5] = q1.y; s.w[6] = q1.z; s.w[7] = q1.w;
+    }
+    uint32_t pv = __shfl_up_sync(FULL, s.w[7], 1);
+    uint32_t nx = __shfl_down_sync(FULL, s.w[0], 1);
+    if (lane == 0) pv = *reinterpret_cast<const uint32_t *>(my - 4);
+    if (lane == 31) nx = *reinterpret_cast<const uint32_t *>(my + BPT);
+    s.prev_word = pv >> 16;
+    s.next_word = nx & 0xFFFFu;
+    s.pos0 = tpw + (BPT / 2) * tid;
+    s.interior = (tpw >= 0) && (tpw + TILE / 2 <= nw);
+    // any surrogate among the thread's words or its two neighbours?  (SWAR on word pairs)
+    uint32_t sur = ((s.prev_word & 0xF800u) == 0xD800u) | ((s.next_word & 0xF800u) == 0xD800u);
+    uint32_t orv = 0;
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      uint32_t x = (s.w[k] & 0xF800F800u) ^ 0xD800D800u;  // zero half <=> surrogate
+      sur |= ((x & 0xFFFFu) == 0u) | ((x >> 16) == 0u);
+      orv |= s.w[k];
+    }
+    s.sur = sur != 0;
+    s.wasc = __all_sync(FULL, (orv & 0xFF80FF80u) == 0u);
+    s.first_err = NONE;
+    uint32_t cnt = 0;
+    if (s.sur) {
+      // a9 pairing predicate (exact) + a5 widths
+      uint32_t p = s.prev_word;
+#pragma unroll
+      for (int i = 0; i < 16; i++) {
+        const uint32_t u = (s.w[i >> 1] >> (16 * (i & 1))) & 0xFFFFu;
+        const uint32_t q = (i < 15) ? ((s.w[(i + 1) >> 1] >> (16 * ((i + 1) & 1))) & 0xFFFFu)
+                                    : s.next_word;
+        const long long pos = s.pos0 + i;
+        if (s.interior || (pos >= 0 && pos < nw)) {
+          if (s.first_err == NONE && u16::err_at(p, u, q)) s.first_err = (unsigned long long)pos;
+          if (xc) cnt += u16::width(u, p);
+        }
+        p = u;
+      }
+    } else if (xc) {
+      // no surrogates: 1 / 2 / 3 bytes by range, two words per register
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        const uint32_t lo = s.w[k] & 0xFFFFu, hi = s.w[k] >> 16;
+        const uint32_t wl = 1u + (lo >= 0x80u) + (lo >= 0x800u);
+        const uint32_t wh = 1u + (hi >= 0x80u) + (hi >= 0x800u);
+        if (s.interior) {
+          cnt += wl + wh;
+        } else {
+          const long long pos = s.pos0 + 2 * k;
+          cnt += ((pos >= 0 && pos < nw) ? wl : 0u) + ((pos + 1 >= 0 && pos + 1 < nw) ? wh : 0u);
+        }
+      }
+    }
+    return cnt;
+  }
+
+  __device__ static __forceinline__ bool hint(const St &s) { return s.first_err != NONE; }
+  __device__ static __forceinline__ unsigned long long find_error(const St &s, long long) {
+    return s.first_err;
+  }
+
+  // a7: encode the owned words into stage[o ...] (UTF-8 bytes)
+  __device__ static __forceinline__ void decode(const St &s, uint8_t *stage, uint32_t o,
+                                                long long nw) {
+    if (s.wasc && s.interior) {
+      if ((o & 3u) == 0u) {
+        uint32_t *st32 = reinterpret_cast<uint32_t *>(stage + o);
+#pragma unroll
+        for (int k = 0; k < 4; k++) st32[k] = u8::prmt(s.w[2 * k], s.w[2 * k + 1], 0x6420u);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; i++) stage[o + i] = (uint8_t)(s.w[i >> 1] >> (16 * (i & 1)));
+      }
+      return;
+    }
+    uint32_t p = s.prev_word;
+#pragma unroll
+    for (int i = 0; i < 16; i++) {
+      const uint32_t u = (s.w[i >> 1] >> (16 * (i & 1))) & 0xFFFFu;
+      const long long pos = s.pos0 + i;
+      if (s.interior || (pos >= 0 && pos < nw)) {
+        const uint32_t wd = u16::width(u, p);
+        const uint32_t v = u16::utf8_bytes(u, p);
+        stage[o] = (uint8_t)v;
+        if (wd > 1) stage[o + 1] = (uint8_t)(v >> 8);
+        if (wd > 2) stage[o + 2] = (uint8_t)(v >> 16);
+        o += wd;
+      }
+      p = u;
+    }
+  }
+
+  __device__ static __forceinline__ void finalize(const TileArgs &a, unsigned long long e,
+                                                  bool xc, int lane, int *kind,
+                                                  unsigned long long *wr) {
+    const Window &win = a.win;
+    *kind = u8::SURROGATE;
+    *wr = 0;
+    if (!xc) return;
+    long long te = (2 * (long long)e + win.lead) / TILE;
+    unsigned long long base = te ? (ld_relaxed(a.status + te - 1) & VALMASK) : 0ull;
+    long long from = (te * TILE - win.lead) / 2;
+    if (from < 0) from = 0;
+    unsigned long long c = 0;
+    for (long long i = from + lane; i < (long long)e; i += 32)
+      c += u16::width(word_at(win, i), word_at(win, i - 1));
+    *wr = base + warp_sum64(c);
+  }
+};
+
+template <class Pol>
+__device__ __forceinline__ void pol_decode(const typename Pol::St &s, typename Pol::Out *stage,
+                                           uint32_t o, long long n_units);
+template <>
+__device__ __forceinline__ void pol_decode<U8Pol>(const U8Pol::St &s, uint16_t *stage,
+                                                  uint32_t o, long long) {
+  U8Pol::decode(s, stage, o);
+}
+template <>
+__device__ __forceinline__ void pol_decode<U16Pol>(const U16Pol::St &s, uint8_t *stage,
+                                                   uint32_t o, long long nw) {
+  U16Pol::decode(s, stage, o, nw);
+}
+
+// Last CTA to finish: outcome + counter reset.  n_units in input code units.
+template <class Pol>
+__device__ __forceinline__ void finish_call(const TileArgs &a, bool xc, int tid, int warp,
+                                            int lane, int *s_last) {
+  if (tid == 0) {
+    __threadfence();
+    *s_last = (atomicAdd(&a.ctr->done, 1u) == gridDim.x - 1) ? 1 : 0;
+  }
+  __syncthreads();
+  if (*s_last && warp == 0) {
+    __threadfence();
+    const unsigned long long e =
+        *reinterpret_cast<volatile unsigned long long *>(&a.ctr->err_min);
+    unsigned long long total = 0, wr = 0;
+    int kind = 0;
+    if (xc && a.ntiles) total = ld_relaxed(a.status + a.ntiles - 1) & VALMASK;
+    if (e != NONE) Pol::finalize(a, e, xc, lane, &kind, &wr);
+    if (lane == 0)
+      write_outcome(a, xc, kind, e, total, wr, (unsigned long long)(a.win.n / Pol::UNIT));
+  }
+}
+
+// ============================================================================ validators
+// K1 / K3: classify (UTF-8: flag, then exact rescan of flagged tiles) or pair-check (UTF-16).
+template <class Pol>
+__global__ void __launch_bounds__(NT, 2) k_validate(const TileArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t *inbuf = smem;
-  uint16_t *stage = reinterpret_cast<uint16_t *>(smem + 2 * INBUF);
   __shared__ uint64_t bar[2];
-  __shared__ uint32_t s_wsum[NT / 32];
   __shared__ long long s_next[2];
-  __shared__ unsigned long long s_excl, s_emin;
+  __shared__ unsigned long long s_emin;
   __shared__ int s_flag, s_last;
-
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const Window &win = a.win;
   const long long ntiles = (long long)a.ntiles;
-  const long long n = win.n;
-  uint16_t *out = reinterpret_cast<uint16_t *>(a.out);
-  const uint32_t out_mis = (uint32_t)(((uintptr_t)out >> 1) & 7u);
+  const long long n_units = win.n / Pol::UNIT;
 
   if (tid == 0) {
     mbar_init(&bar[0], 1);
@@ -168,7 +508,6 @@ __global__ void __launch_bounds__(NT) k_utf8(const TileArgs a) {
   long long t = s_next[0];
   int s = 0;
   uint32_t parity = 0;
-
   while (t < ntiles) {
     if (tid == 0) {
       long long tn = (long long)atomicAdd(&a.ctr->ticket, 1u);
@@ -179,205 +518,54 @@ __global__ void __launch_bounds__(NT) k_utf8(const TileArgs a) {
       }
       s_flag = 0;
       s_emin = NONE;
-      if (XC) bulk_wait_read_all();  // previous tile's bulk store has read `stage`
     }
     mbar_wait(&bar[s], (parity >> s) & 1u);
     parity ^= 1u << s;
     uint8_t *buf = inbuf + s * INBUF;
-    fix_tile_edges(win, t, buf);
+    fix_tile_edges(win, t, buf, NT);
     __syncthreads();
-
-    // ---------------------------------------------------------------- a1: this thread's bytes
-    const long long tp = tile_pos(win, t);
-    const uint8_t *my = buf + HALO + BPT * tid;
-    uint32_t w[9];
-    {
-      uint4 q0 = *reinterpret_cast<const uint4 *>(my);
-      uint4 q1 = *reinterpret_cast<const uint4 *>(my + 16);
-      w[0] = q0.x; w[1] = q0.y; w[2] = q0.z; w[3] = q0.w;
-      w[4] = q1.x; w[5] = q1.y; w[6] = q1.z; w[7] = q1.w;
-    }
-    uint32_t prev = __shfl_up_sync(FULL, w[7], 1);
-    uint32_t nxt = __shfl_down_sync(FULL, w[0], 1);
-    if (lane == 0) prev = *reinterpret_cast<const uint32_t *>(my - 4);
-    if (lane == 31) nxt = *reinterpret_cast<const uint32_t *>(my + BPT);
-    w[8] = nxt;
-    const long long mypos = tp + BPT * tid;
-    const bool interior = (tp >= 0) && (tp + TILE + 1 <= n);
-
-    // ---------------------------------------------------------------- a2: warp ASCII path
-    uint32_t orv = w[0] | w[1] | w[2] | w[3] | w[4] | w[5] | w[6] | w[7];
-    bool pend = (prev >= 0xC0000000u) || ((prev & 0x00FF0000u) >= 0x00E00000u) ||
-                ((prev & 0x0000FF00u) >= 0x0000F000u);
-    const bool wasc = __all_sync(FULL, ((orv & u8::HI) == 0u) && !pend);
-
-    // ---------------------------------------------------------------- a3/a5: classify, widths
-    uint32_t err = 0;
-    uint32_t cm[8];
-    if (wasc) {
-#pragma unroll
-      for (int k = 0; k < 8; k++) cm[k] = u8::HI;
-    } else {
-      u8::WordMasks pm = u8::masks(prev, true);
-      u8::WordMasks cur = u8::masks(w[0], true);
-#pragma unroll
-      for (int k = 0; k < 8; k++) {
-        u8::WordMasks nx = u8::masks(w[k + 1], true);
-        err |= u8::classify(pm, cur);
-        cm[k] = XC ? u8::width_bits(cur, nx.K) : 0u;
-        pm = cur;
-        cur = nx;
-      }
-      if (tid == NT - 1) err |= u8::classify(pm, cur);  // look-ahead: positions TILE..TILE+3
-    }
-    uint32_t cnt = 0;
-    if (XC) {
-      if (!interior) {
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-          long long pos = mypos + 4 * k;
-          uint32_t own = range_bytes(pos, 0, n) & u8::HI;
-          uint32_t own1 = (range_bytes(pos, 0, n - 1) & u8::HI) >> 1;
-          cm[k] &= own | own1;
-        }
-      }
-#pragma unroll
-      for (int k = 0; k < 8; k++) cnt += __popc(cm[k]);
-    }
-    if (err) s_flag = 1;
-
-    // ---------------------------------------------------------------- a6: scan + look-back
-    uint32_t excl_local = 0, C = 0;
-    if (XC) {
-      block_scan(cnt, s_wsum, lane, warp, &excl_local, &C);
-    } else {
-      __syncthreads();
-    }
-    const bool flagged = s_flag != 0;
-    if (XC && warp == 0) {
-      unsigned long long P = tile_prefix(a, t, C, lane);
-      if (lane == 0) s_excl = P;
-    }
-    // ---------------------------------------------------------------- a4: exact rescan (cold)
-    if (flagged) {
-      uint32_t l32[10];
-      const uint8_t *loc = reinterpret_cast<const uint8_t *>(l32);
-      l32[0] = prev;
-#pragma unroll
-      for (int k = 0; k < 9; k++) l32[k + 1] = w[k];
-      for (int i = 0; i < BPT; i++) {
-        long long pos = mypos + i;
-        if (pos < 0 || pos >= n) continue;
-        if (u8::err_at(loc + 4 + i)) {
-          atomicMin(&s_emin, (unsigned long long)pos);
-          break;
-        }
-      }
+    typename Pol::St st;
+    Pol::analyze(st, buf, tid, lane, tile_pos(win, t), win.n, false);
+    if (Pol::hint(st)) s_flag = 1;
+    __syncthreads();
+    if (s_flag) {
+      unsigned long long e = Pol::find_error(st, n_units);
+      if (e != NONE) atomicMin(&s_emin, e);
     }
     __syncthreads();
-    if (flagged && tid == 0 && s_emin != NONE) atomicMin(&a.ctr->err_min, s_emin);
-
-    if (XC) {
-      // -------------------------------------------------------------- a7: decode into stage
-      const unsigned long long P = s_excl;
-      const uint32_t phase = (out_mis + (uint32_t)P) & 7u;
-      uint32_t o = phase + excl_local;
-      if (wasc && interior) {
-        if ((o & 1u) == 0u) {
-          uint32_t *st32 = reinterpret_cast<uint32_t *>(stage + o);
-#pragma unroll
-          for (int k = 0; k < 8; k++) {
-            st32[2 * k] = u8::prmt(w[k], 0u, 0x4140u);
-            st32[2 * k + 1] = u8::prmt(w[k], 0u, 0x4342u);
-          }
-        } else {
-#pragma unroll
-          for (int k = 0; k < 8; k++)
-#pragma unroll
-            for (int j = 0; j < 4; j++) stage[o + 4 * k + j] = (uint16_t)((w[k] >> (8 * j)) & 0xFFu);
-        }
-      } else {
-#pragma unroll
-        for (int k = 0; k < 8; k++) {
-          const uint32_t c = cm[k];
-          uint32_t lead = c & u8::HI;
-          while (lead) {
-            const int b = __ffs(lead) - 1;  // 7, 15, 23 or 31
-            lead &= lead - 1u;
-            const uint32_t sh = (uint32_t)(b - 7);
-            const uint32_t x = __funnelshift_r(w[k], w[k + 1], sh);
-            uint32_t u1;
-            const uint32_t u0 = u8::decode_units(x, &u1);
-            const uint32_t off = o + __popc(c & ((1u << sh) - 1u));
-            stage[off] = (uint16_t)u0;
-            if (c & (1u << (b - 1))) stage[off + 1] = (uint16_t)u1;
-          }
-          o += __popc(c);
-        }
-      }
-      __syncthreads();
-      // -------------------------------------------------------------- a8: store
-      copy_out<uint16_t>(out, a.out_cap, P, C, phase, stage, tid);
-    }
-    __syncthreads();
+    if (tid == 0 && s_emin != NONE) atomicMin(&a.ctr->err_min, s_emin);
     t = s_next[s ^ 1];
     s ^= 1;
   }
-
-  // -------------------------------------------------------------------- a10: finalize
-  if (tid == 0) {
-    if (XC) bulk_wait_all();
-    __threadfence();
-    s_last = (atomicAdd(&a.ctr->done, 1u) == gridDim.x - 1) ? 1 : 0;
-  }
-  __syncthreads();
-  if (s_last && warp == 0) {
-    __threadfence();
-    unsigned long long e = *reinterpret_cast<volatile unsigned long long *>(&a.ctr->err_min);
-    unsigned long long total = 0, wr = 0;
-    int kind = 0;
-    if (XC && a.ntiles) total = ld_relaxed(a.status + a.ntiles - 1) & VALMASK;
-    if (e != NONE) {
-      uint8_t b[4];
-#pragma unroll
-      for (int j = 0; j < 4; j++) b[j] = (uint8_t)byte_at(win, (long long)e + j);
-      kind = u8::decode_kind(b);
-      if (XC) {
-        long long te = ((long long)e + win.lead) / TILE;
-        unsigned long long base = te ? (ld_relaxed(a.status + te - 1) & VALMASK) : 0ull;
-        long long from = te * TILE - win.lead;
-        if (from < 0) from = 0;
-        unsigned long long c = 0;
-        for (long long i = from + lane; i < (long long)e; i += 32) {
-          uint32_t bi = byte_at(win, i), bn = byte_at(win, i + 1);
-          c += ((bi & 0xC0u) != 0x80u) ? 1u : 0u;
-          c += (bi >= 0xF0u && (bn & 0xC0u) == 0x80u && i + 1 < n) ? 1u : 0u;
-        }
-        wr = base + warp_sum64(c);
-      }
-    }
-    if (lane == 0) write_outcome(a, XC, kind, e, total, wr, (unsigned long long)n);
-  }
+  finish_call<Pol>(a, false, tid, warp, lane, &s_last);
 }
 
-// ============================================================================ UTF-16 tiles
-template <bool XC>
-__global__ void __launch_bounds__(NT) k_utf16(const TileArgs a) {
+// ============================================================================ transcoders
+// K2 / K4.  NT data threads + one look-back warp (warp NT/32).  Per tile i the data warps
+// classify, scan, hand (tile, aggregate) to the look-back warp (named barrier BAR_C0+(i&1)),
+// decode into stage[i&1], then copy out tile i-1 once its prefix arrives (BAR_P0+((i-1)&1)):
+// the look-back of a tile overlaps the whole processing of the next one.
+template <class Pol>
+__global__ void __launch_bounds__(NT + 32, 2) k_transcode(const TileArgs a) {
+  using Out = typename Pol::Out;
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t *inbuf = smem;
-  uint8_t *stage = smem + 2 * INBUF;
+  Out *stage0 = reinterpret_cast<Out *>(smem + 2 * INBUF);
+  constexpr int SU = Pol::STAGE / (int)sizeof(Out);  // stage units per buffer
   __shared__ uint64_t bar[2];
   __shared__ uint32_t s_wsum[NT / 32];
   __shared__ long long s_next[2];
-  __shared__ unsigned long long s_excl, s_emin;
-  __shared__ int s_last;
+  __shared__ long long s_tile[2];
+  __shared__ uint32_t s_cnt[2];
+  __shared__ unsigned long long s_pre[2];
+  __shared__ unsigned long long s_emin;
+  __shared__ int s_flag, s_last;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const Window &win = a.win;  // byte positions
+  const Window &win = a.win;
   const long long ntiles = (long long)a.ntiles;
-  const long long nw = win.n / 2;  // owned words
-  uint8_t *out = reinterpret_cast<uint8_t *>(a.out);
-  const uint32_t out_mis = (uint32_t)((uintptr_t)out & 15u);
+  const long long n_units = win.n / Pol::UNIT;
+  Out *out = reinterpret_cast<Out *>(a.out);
 
   if (tid == 0) {
     mbar_init(&bar[0], 1);
@@ -388,154 +576,76 @@ __global__ void __launch_bounds__(NT) k_utf16(const TileArgs a) {
     if (t0 < ntiles) issue_tile_load(win, t0, inbuf, &bar[0]);
   }
   __syncthreads();
-  long long t = s_next[0];
-  int s = 0;
-  uint32_t parity = 0;
 
-  while (t < ntiles) {
-    if (tid == 0) {
-      long long tn = (long long)atomicAdd(&a.ctr->ticket, 1u);
-      s_next[s ^ 1] = tn;
-      if (tn < ntiles) {
-        fence_proxy_async_smem();
-        issue_tile_load(win, tn, inbuf + (s ^ 1) * INBUF, &bar[s ^ 1]);
-      }
-      s_emin = NONE;
-      if (XC) bulk_wait_read_all();
+  if (warp == NT / 32) {
+    // ------------------------------------------------------------ look-back warp (a6)
+    for (int i = 0;; i++) {
+      if (i & 1) named_sync<BAR_C1, NT + 32>(); else named_sync<BAR_C0, NT + 32>();
+      const long long t = s_tile[i & 1];
+      if (t < 0) break;
+      const unsigned long long P = tile_prefix(a, t, s_cnt[i & 1], lane);
+      if (lane == 0) s_pre[i & 1] = P;
+      if (i & 1) named_arrive<BAR_P1, NT + 32>(); else named_arrive<BAR_P0, NT + 32>();
     }
-    mbar_wait(&bar[s], (parity >> s) & 1u);
-    parity ^= 1u << s;
-    uint8_t *buf = inbuf + s * INBUF;
-    fix_tile_edges(win, t, buf);
-    __syncthreads();
-
-    const long long tpw = tile_pos(win, t) / 2;  // word position of the tile's first word
-    const uint8_t *my = buf + HALO + BPT * tid;
-    uint32_t w[8];
-    {
-      uint4 q0 = *reinterpret_cast<const uint4 *>(my);
-      uint4 q1 = *reinterpret_cast<const uint4 *>(my + 16);
-      w[0] = q0.x; w[1] = q0.y; w[2] = q0.z; w[3] = q0.w;
-      w[4] = q1.x; w[5] = q1.y; w[6] = q1.z; w[7] = q1.w;
-    }
-    uint32_t pv = __shfl_up_sync(FULL, w[7], 1);
-    uint32_t nx = __shfl_down_sync(FULL, w[0], 1);
-    if (lane == 0) pv = *reinterpret_cast<const uint32_t *>(my - 4);
-    if (lane == 31) nx = *reinterpret_cast<const uint32_t *>(my + BPT);
-    const uint32_t prev_word = pv >> 16, next_word = nx & 0xFFFFu;
-    const long long mypos = tpw + (BPT / 2) * tid;  // word position of this thread's first word
-    const bool interior = (tpw >= 0) && (tpw + TILE / 2 <= nw);
-
-    // any surrogate among the thread's words and neighbours?  (SWAR on word pairs)
-    uint32_t sur = 0;
-#pragma unroll
-    for (int k = 0; k < 8; k++) {
-      uint32_t x = (w[k] & 0xF800F800u) ^ 0xD800D800u;  // zero half <=> surrogate
-      sur |= ((x & 0xFFFFu) == 0u) | ((x >> 16) == 0u);
-    }
-    uint32_t orv = 0;
-#pragma unroll
-    for (int k = 0; k < 8; k++) orv |= w[k];
-    const bool wasc = __all_sync(FULL, (orv & 0xFF80FF80u) == 0u);
-
-    // ---------------------------------------------------------------- a9 + a5
-    uint32_t cnt = 0;
-    unsigned long long first_err = NONE;
-    if (sur || ((prev_word & 0xF800u) == 0xD800u) || ((next_word & 0xF800u) == 0xD800u) ||
-        XC) {
-      uint32_t p = prev_word;
-#pragma unroll
-      for (int i = 0; i < 16; i++) {
-        uint32_t u = (w[i >> 1] >> (16 * (i & 1))) & 0xFFFFu;
-        uint32_t q = (i < 15) ? ((w[(i + 1) >> 1] >> (16 * ((i + 1) & 1))) & 0xFFFFu) : next_word;
-        long long pos = mypos + i;
-        bool own = interior || (pos >= 0 && pos < nw);
-        if (own) {
-          if (first_err == NONE && u16::err_at(p, u, q)) first_err = (unsigned long long)pos;
-          if (XC) cnt += u16::width(u, p);
+  } else {
+    // ------------------------------------------------------------ data warps
+    long long t = s_next[0];
+    int s = 0, i = 0;
+    uint32_t parity = 0, C_prev = 0;
+    while (t < ntiles) {
+      if (tid == 0) {
+        long long tn = (long long)atomicAdd(&a.ctr->ticket, 1u);
+        s_next[s ^ 1] = tn;
+        if (tn < ntiles) {
+          fence_proxy_async_smem();
+          issue_tile_load(win, tn, inbuf + (s ^ 1) * INBUF, &bar[s ^ 1]);
         }
-        p = u;
+        s_flag = 0;
+        s_emin = NONE;
       }
-    }
-    if (first_err != NONE) atomicMin(&s_emin, first_err);
+      mbar_wait(&bar[s], (parity >> s) & 1u);
+      parity ^= 1u << s;
+      uint8_t *buf = inbuf + s * INBUF;
+      fix_tile_edges(win, t, buf, NT);
+      named_sync<BAR_DATA, NT>();
 
-    uint32_t excl_local = 0, C = 0;
-    if (XC) {
-      block_scan(cnt, s_wsum, lane, warp, &excl_local, &C);
-      if (warp == 0) {
-        unsigned long long P = tile_prefix(a, t, C, lane);
-        if (lane == 0) s_excl = P;
+      typename Pol::St st;
+      const uint32_t cnt = Pol::analyze(st, buf, tid, lane, tile_pos(win, t), win.n, true);
+      if (Pol::hint(st)) s_flag = 1;
+      uint32_t excl = 0, C = 0;
+      block_scan(cnt, s_wsum, lane, warp, &excl, &C);
+      if (tid == 0) {
+        s_tile[i & 1] = t;
+        s_cnt[i & 1] = C;
       }
-    }
-    __syncthreads();
-    if (tid == 0 && s_emin != NONE) atomicMin(&a.ctr->err_min, s_emin * 2);  // byte position
-
-    if (XC) {
-      // -------------------------------------------------------------- a7: encode into stage
-      const unsigned long long P = s_excl;
-      const uint32_t phase = (out_mis + (uint32_t)P) & 15u;
-      uint32_t o = phase + excl_local;
-      if (wasc && interior) {
-        if ((o & 3u) == 0u) {
-          uint32_t *st32 = reinterpret_cast<uint32_t *>(stage + o);
-#pragma unroll
-          for (int k = 0; k < 4; k++) st32[k] = u8::prmt(w[2 * k], w[2 * k + 1], 0x6420u);
-        } else {
-#pragma unroll
-          for (int i = 0; i < 16; i++) stage[o + i] = (uint8_t)(w[i >> 1] >> (16 * (i & 1)));
-        }
-      } else {
-        uint32_t p = prev_word;
-#pragma unroll
-        for (int i = 0; i < 16; i++) {
-          uint32_t u = (w[i >> 1] >> (16 * (i & 1))) & 0xFFFFu;
-          long long pos = mypos + i;
-          bool own = interior || (pos >= 0 && pos < nw);
-          if (own) {
-            uint32_t wd = u16::width(u, p);
-            uint32_t v = u16::utf8_bytes(u, p);
-            stage[o] = (uint8_t)v;
-            if (wd > 1) stage[o + 1] = (uint8_t)(v >> 8);
-            if (wd > 2) stage[o + 2] = (uint8_t)(v >> 16);
-            o += wd;
-          }
-          p = u;
-        }
+      // hand the aggregate to the look-back warp
+      if (i & 1) named_arrive<BAR_C1, NT + 32>(); else named_arrive<BAR_C0, NT + 32>();
+      if (s_flag) {
+        unsigned long long e = Pol::find_error(st, n_units);
+        if (e != NONE) atomicMin(&s_emin, e);
       }
-      __syncthreads();
-      copy_out<uint8_t>(out, a.out_cap, P, C, phase, stage, tid);
+      pol_decode<Pol>(st, stage0 + (i & 1) * SU, excl, n_units);
+      if (i > 0) {  // a8: copy out the previous tile once its prefix is known
+        if ((i - 1) & 1) named_sync<BAR_P1, NT + 32>(); else named_sync<BAR_P0, NT + 32>();
+        copy_out<Out>(out, a.out_cap, s_pre[(i - 1) & 1], C_prev, stage0 + ((i - 1) & 1) * SU,
+                      tid);
+      }
+      named_sync<BAR_DATA, NT>();
+      if (tid == 0 && s_emin != NONE) atomicMin(&a.ctr->err_min, s_emin);
+      C_prev = C;
+      t = s_next[s ^ 1];
+      s ^= 1;
+      i++;
     }
-    __syncthreads();
-    t = s_next[s ^ 1];
-    s ^= 1;
-  }
-
-  if (tid == 0) {
-    if (XC) bulk_wait_all();
-    __threadfence();
-    s_last = (atomicAdd(&a.ctr->done, 1u) == gridDim.x - 1) ? 1 : 0;
+    if (i > 0) {
+      if ((i - 1) & 1) named_sync<BAR_P1, NT + 32>(); else named_sync<BAR_P0, NT + 32>();
+      copy_out<Out>(out, a.out_cap, s_pre[(i - 1) & 1], C_prev, stage0 + ((i - 1) & 1) * SU, tid);
+    }
+    if (tid == 0) s_tile[i & 1] = -1;  // stop the look-back warp
+    if (i & 1) named_arrive<BAR_C1, NT + 32>(); else named_arrive<BAR_C0, NT + 32>();
   }
   __syncthreads();
-  if (s_last && warp == 0) {
-    __threadfence();
-    unsigned long long eb = *reinterpret_cast<volatile unsigned long long *>(&a.ctr->err_min);
-    unsigned long long e = (eb == NONE) ? NONE : eb / 2;  // word position
-    unsigned long long total = 0, wr = 0;
-    if (XC && a.ntiles) total = ld_relaxed(a.status + a.ntiles - 1) & VALMASK;
-    if (e != NONE && XC) {
-      long long te = (2 * (long long)e + win.lead) / TILE;
-      unsigned long long base = te ? (ld_relaxed(a.status + te - 1) & VALMASK) : 0ull;
-      long long from = (te * TILE - win.lead) / 2;
-      if (from < 0) from = 0;
-      unsigned long long c = 0;
-      for (long long i = from + lane; i < (long long)e; i += 32)
-        c += u16::width(word_at(win, i), word_at(win, i - 1));
-      wr = base + warp_sum64(c);
-    }
-    if (lane == 0)
-      write_outcome(a, XC, e == NONE ? 0 : (int)u8::SURROGATE, e, total, wr,
-                    (unsigned long long)nw);
-  }
+  finish_call<Pol>(a, true, tid, warp, lane, &s_last);
 }
 
 // ============================================================================ length-from
@@ -690,18 +800,22 @@ size_t tile_smem_bytes(Op op) {
   switch (op) {
     case Op::U8_VALIDATE:
     case Op::U16_VALIDATE: return 2 * INBUF;
-    case Op::U8_TO_U16: return 2 * INBUF + 2 * STAGE8_UNITS;
-    case Op::U16_TO_U8: return 2 * INBUF + STAGE16_BYTES;
+    case Op::U8_TO_U16: return 2 * INBUF + 2 * U8Pol::STAGE;
+    case Op::U16_TO_U8: return 2 * INBUF + 2 * U16Pol::STAGE;
   }
   return 0;
 }
 
+static int tile_threads(Op op) {
+  return (op == Op::U8_TO_U16 || op == Op::U16_TO_U8) ? NT + 32 : NT;
+}
+
 static const void *tile_fn(Op op) {
   switch (op) {
-    case Op::U8_VALIDATE: return (const void *)k_utf8<false>;
-    case Op::U8_TO_U16: return (const void *)k_utf8<true>;
-    case Op::U16_VALIDATE: return (const void *)k_utf16<false>;
-    case Op::U16_TO_U8: return (const void *)k_utf16<true>;
+    case Op::U8_VALIDATE: return (const void *)k_validate<U8Pol>;
+    case Op::U8_TO_U16: return (const void *)k_transcode<U8Pol>;
+    case Op::U16_VALIDATE: return (const void *)k_validate<U16Pol>;
+    case Op::U16_TO_U8: return (const void *)k_transcode<U16Pol>;
   }
   return nullptr;
 }
@@ -712,17 +826,18 @@ cudaError_t tile_configure(Op op) {
 }
 
 cudaError_t tile_occupancy(Op op, int *blocks_per_sm) {
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, tile_fn(op), NT,
-                                                       tile_smem_bytes(op));
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, tile_fn(op),
+                                                       tile_threads(op), tile_smem_bytes(op));
 }
 
 cudaError_t launch_tile(Op op, const TileArgs &a, int grid, cudaStream_t s) {
   size_t sm = tile_smem_bytes(op);
+  int nt = tile_threads(op);
   switch (op) {
-    case Op::U8_VALIDATE: k_utf8<false><<<grid, NT, sm, s>>>(a); break;
-    case Op::U8_TO_U16: k_utf8<true><<<grid, NT, sm, s>>>(a); break;
-    case Op::U16_VALIDATE: k_utf16<false><<<grid, NT, sm, s>>>(a); break;
-    case Op::U16_TO_U8: k_utf16<true><<<grid, NT, sm, s>>>(a); break;
+    case Op::U8_VALIDATE: k_validate<U8Pol><<<grid, nt, sm, s>>>(a); break;
+    case Op::U8_TO_U16: k_transcode<U8Pol><<<grid, nt, sm, s>>>(a); break;
+    case Op::U16_VALIDATE: k_validate<U16Pol><<<grid, nt, sm, s>>>(a); break;
+    case Op::U16_TO_U8: k_transcode<U16Pol><<<grid, nt, sm, s>>>(a); break;
   }
   return cudaGetLastError();
 }

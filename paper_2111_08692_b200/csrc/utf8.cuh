@@ -127,37 +127,47 @@ __device__ __forceinline__ uint32_t decode_units(uint32_t x, uint32_t *u1) {
 }
 
 // ---------------------------------------------------------------- exact (cold) path
-// Kind of the failure of a sequential decoder at s[0] (rules in the order of DESIGN.md R2);
-// s[1..3] are the following bytes, 0x00 past the end of the input.
-__device__ __forceinline__ int decode_kind(const uint8_t *s) {
-  uint32_t b = s[0];
+// All bytes are passed in registers (little-endian words): no local arrays.
+__device__ __forceinline__ uint32_t byte_of(uint32_t x, int k) { return (x >> (8 * k)) & 0xFFu; }
+
+// Kind of the failure of a sequential decoder whose window is x = s[0..3] (rules in the order
+// of DESIGN.md R2); bytes past the end of the input are 0x00 (not continuation bytes).
+__device__ __forceinline__ int decode_kind(uint32_t x) {
+  uint32_t b = x & 0xFFu;
   if (b < 0x80u) return OK;
   if (b < 0xC0u) return TOO_LONG;
   if (b >= 0xF8u) return HEADER_BITS;
   int L = b < 0xE0u ? 2 : (b < 0xF0u ? 3 : 4);
-  for (int k = 1; k < L; k++)
-    if ((s[k] & 0xC0u) != 0x80u) return TOO_SHORT;
   uint32_t cp = b & (0x7Fu >> L);
-  for (int k = 1; k < L; k++) cp = (cp << 6) | (s[k] & 0x3Fu);
-  const uint32_t minv[5] = {0, 0, 0x80u, 0x800u, 0x10000u};
-  if (cp < minv[L]) return OVERLONG;
+#pragma unroll
+  for (int k = 1; k < 4; k++) {
+    if (k < L) {
+      uint32_t c = byte_of(x, k);
+      if ((c & 0xC0u) != 0x80u) return TOO_SHORT;
+      cp = (cp << 6) | (c & 0x3Fu);
+    }
+  }
+  uint32_t minv = L == 2 ? 0x80u : (L == 3 ? 0x800u : 0x10000u);
+  if (cp < minv) return OVERLONG;
   if (cp > 0x10FFFFu) return TOO_LARGE;
   if (cp >= 0xD800u && cp <= 0xDFFFu) return SURROGATE;
   return OK;
 }
 
-// Exact local predicate at s[0] (s[-3..3] readable): A(i) for a non-continuation byte (the
-// character starting there fails), B(i) for a continuation byte (no lead within the 3
-// previous bytes that declares it).  DESIGN.md D2 / SURVEY.md C.4(i).
-__device__ __forceinline__ bool err_at(const uint8_t *s) {
-  uint32_t c = s[0];
-  if ((c & 0xC0u) != 0x80u) return decode_kind(s) != OK;
+__device__ __forceinline__ int declared_len(uint32_t b) {
+  return b < 0x80u ? 1 : (b < 0xC0u ? 0 : (b < 0xE0u ? 2 : (b < 0xF0u ? 3 : (b < 0xF8u ? 4 : 0))));
+}
+
+// Exact local predicate at position i (D2 / SURVEY.md C.4(i)): back = s[i-4..i-1],
+// fwd = s[i..i+3].  A(i): a non-continuation byte whose character fails to decode.  B(i): a
+// continuation byte with no lead within the 3 previous bytes that declares it.
+__device__ __forceinline__ bool err_at(uint32_t back, uint32_t fwd) {
+  uint32_t c = fwd & 0xFFu;
+  if ((c & 0xC0u) != 0x80u) return decode_kind(fwd) != OK;
+#pragma unroll
   for (int d = 1; d <= 3; d++) {
-    uint32_t b = s[-d];
-    if ((b & 0xC0u) != 0x80u) {
-      int decl = b < 0x80u ? 1 : (b < 0xE0u ? 2 : (b < 0xF0u ? 3 : (b < 0xF8u ? 4 : 0)));
-      return !(decl > d);
-    }
+    uint32_t b = byte_of(back, 4 - d);
+    if ((b & 0xC0u) != 0x80u) return !(declared_len(b) > d);
   }
   return true;
 }

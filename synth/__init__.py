@@ -110,7 +110,16 @@ def _draw_emoji(rng, m):
     return cp, np.where(u, 2, 1).astype(np.int64)
 
 
+def _draw_ascii(rng, m):
+    """Config 1: bytes uniform in 0x20-0x7E, 2% of them replaced by LF."""
+    cp = rng.integers(0x20, 0x7F, m, dtype=np.uint32)
+    cp[rng.random(m, dtype=np.float32) < 0.02] = 0x0A
+    return cp, np.ones(m, dtype=np.uint8)
+
+
 def _draw(mix, rng, m):
+    if mix == "ascii":
+        return _draw_ascii(rng, m)
     if mix == "mixed":
         return _draw_mixed(rng, m)
     if mix == "words2":  # mean 6, 1/15 punctuation in words -> 80% script / 20% ASCII
@@ -122,7 +131,7 @@ def _draw(mix, rng, m):
     raise ValueError(mix)
 
 
-_MEAN_UNITS = {"mixed": 1.6, "words2": 1.8, "words3": 2.8, "emoji": 1.7}
+_MEAN_UNITS = {"ascii": 1.0, "mixed": 1.6, "words2": 1.8, "words3": 2.8, "emoji": 1.7}
 
 
 def _encode(cp: np.ndarray, encoding: str) -> bytes:
