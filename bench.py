@@ -137,26 +137,17 @@ def ncu_traffic():
 
 
 # ------------------------------------------------------------------------------ sharding
-def plan(n: int, G: int):
-    """Nominal cuts k*floor(n/G) aligned down to 16 bytes."""
-    return [0] + [(k * (n // G)) & ~15 for k in range(1, G)] + [n]
-
-
 def load_shard(cfg, rank, G, size):
-    """Generate this rank's bytes [c_k - 16, c_{k+1} + 16) and back the two cuts off to
-    character starts with the library's cut rule.  Returns (host array, lo, hi, base)."""
-    import paper_2111_08692_b200 as ug
-    nom = plan(size, G)
+    """Generate this rank's bytes [c_k - 16, c_{k+1} + 16) (nominal cuts) and back the two cuts
+    off to character starts with the library's cut rule (paper_2111_08692_b200.dist).
+    Returns (host array of bytes [base, ...), lo, hi, base)."""
+    from paper_2111_08692_b200 import dist as ugd
+    nom = ugd.nominal_cuts(size, G)
     c0, c1 = nom[rank], nom[rank + 1]
     base = max(0, c0 - 16)
     buf = synth.generate_range(cfg, base, min(size, c1 + 16))
-
-    def back(c):
-        if c in (0, size):
-            return c
-        i = c - base
-        return c - ug.utf8_cut_backoff(buf[max(0, i - 8):i + 8].tobytes(), i - max(0, i - 8))
-    return buf, back(c0), back(c1), base
+    get = lambda a, b: buf[a - base:b - base].tobytes()  # noqa: E731
+    return buf, ugd.utf8_cut(get, c0, size), ugd.utf8_cut(get, c1, size), base
 
 
 # ------------------------------------------------------------------------------ ours
@@ -178,7 +169,8 @@ def run_ours(args):
     host, lo, hi, base = load_shard(cfg, rank, G, size)
     t_gen = time.time() - t_gen
     n8 = hi - lo
-    hb, ha = min(lo, 3), min(size - hi, 3)
+    from paper_2111_08692_b200 import dist as ugd
+    hb, ha = ugd.halos(lo, hi, size, 3)
     t_all = torch.from_numpy(host).to(dev)                      # bytes [base, ...)
     t_in = t_all[lo - base: hi - base]
     stream = torch.cuda.current_stream()
@@ -210,6 +202,7 @@ def run_ours(args):
 
     def gather_combine(which):
         if G > 1:
+            # one NCCL all-gather of the 32-byte shard records, then the combine kernel
             dist.all_gather_into_tensor(allrec[which * G * R:(which + 1) * G * R],
                                         rec[which * R:(which + 1) * R])
             ug.combine_records_async(allrec[which * G * R:], G, rank,
@@ -318,8 +311,12 @@ def run_ours(args):
                        "gen_seconds": round(t_gen, 1)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
                          "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
-                         "kernel": "k_utf8<true> (utf8_to_utf16le)",
+                         "traffic": (round(traffic["dram_bytes_per_input_byte"] * n8)
+                                     if traffic else None),
+                         "traffic_source": (traffic["capture"] + " (" + traffic["config"] +
+                                            "), DRAM bytes per input byte x this launch's input"
+                                            if traffic else None),
+                         "kernel": "k_transcode<U8Pol> (utf8_to_utf16le)",
                          "algorithmic_bytes_per_launch": fwd_bytes,
                          "avg_launch_ms": round(fwd_ms, 4), "peak_source": peak_src},
             "clocks": clk,

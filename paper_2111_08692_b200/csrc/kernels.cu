@@ -189,7 +189,7 @@ struct U8Pol {
     s.w[8] = nxt;
     s.prev = prev;
     s.pos0 = tp + BPT * tid;
-    s.interior = (tp >= 0) && (tp + TILE + 1 <= n);
+    s.interior = (tp >= 0) && (tp + TILE <= n);
     // a2: warp ASCII fast path (no byte >= 0x80 and no pending lead before the warp)
     uint32_t orv = s.w[0] | s.w[1] | s.w[2] | s.w[3] | s.w[4] | s.w[5] | s.w[6] | s.w[7];
     bool pend = (prev >= 0xC0000000u) || ((prev & 0x00FF0000u) >= 0x00E00000u) ||
@@ -207,7 +207,7 @@ struct U8Pol {
       for (int k = 0; k < 8; k++) {
         u8::WordMasks nx = u8::masks(s.w[k + 1], true);
         s.err |= u8::classify(pm, cur);
-        s.cm[k] = xc ? u8::width_bits(cur, nx.K) : 0u;
+        s.cm[k] = xc ? u8::emit_bits(pm, cur) : 0u;
         pm = cur;
         cur = nx;
       }
@@ -217,12 +217,7 @@ struct U8Pol {
     if (xc) {
       if (!s.interior) {
 #pragma unroll
-        for (int k = 0; k < 8; k++) {
-          long long pos = s.pos0 + 4 * k;
-          uint32_t own = range_bytes(pos, 0, n) & u8::HI;
-          uint32_t own1 = (range_bytes(pos, 0, n - 1) & u8::HI) >> 1;
-          s.cm[k] &= own | own1;
-        }
+        for (int k = 0; k < 8; k++) s.cm[k] &= range_bytes(s.pos0 + 4 * k, 0, n) & u8::HI;
       }
 #pragma unroll
       for (int k = 0; k < 8; k++) cnt += __popc(s.cm[k]);
@@ -251,7 +246,8 @@ struct U8Pol {
   }
 
   // a7: decode the owned characters into stage[o ...] (UTF-16 units)
-  __device__ static __forceinline__ void decode(const St &s, uint16_t *stage, uint32_t o) {
+  __device__ static __forceinline__ void decode(const St &s, uint16_t *stage, uint32_t o,
+                                                uint32_t lim) {
     if (s.wasc && s.interior) {
       if ((o & 1u) == 0u) {
         uint32_t *st32 = reinterpret_cast<uint32_t *>(stage + o);
@@ -268,22 +264,48 @@ struct U8Pol {
       }
       return;
     }
+    // SWAR decode: one candidate unit per position (two per op).  Every position stores its
+    // unit at its exclusive-prefix slot; a non-emitting position's store lands on the slot of
+    // the next emitting one and is overwritten by it (program order).  Only the last word
+    // predicates, so nothing spills into the next thread's first slot.
+    uint32_t cc = s.w[0] & 0x3F3F3F3Fu;
+    uint32_t cn = s.w[1] & 0x3F3F3F3Fu;
+    uint32_t pe = u8::payload_even(cc);
+    uint32_t po = u8::payload_odd(cc, cn);
+    uint32_t fprev = s.prev & (s.prev << 1) & (s.prev << 2) & (s.prev << 3) & u8::HI;
 #pragma unroll
     for (int k = 0; k < 8; k++) {
-      const uint32_t c = s.cm[k];
-      uint32_t lead = c & u8::HI;
-      while (lead) {
-        const int b = __ffs(lead) - 1;  // 7, 15, 23 or 31
-        lead &= lead - 1u;
-        const uint32_t sh = (uint32_t)(b - 7);
-        const uint32_t x = __funnelshift_r(s.w[k], s.w[k + 1], sh);
-        uint32_t u1;
-        const uint32_t u0 = u8::decode_units(x, &u1);
-        const uint32_t off = o + __popc(c & ((1u << sh) - 1u));
-        stage[off] = (uint16_t)u0;
-        if (c & (1u << (b - 1))) stage[off + 1] = (uint16_t)u1;
+      const uint32_t x = s.w[k];
+      const uint32_t cnn = (k < 7) ? (s.w[k + 2] & 0x3F3F3F3Fu) : 0u;
+      const uint32_t pe_n = u8::payload_even(cn);
+      const uint32_t pe2 = u8::prmt(pe, pe_n, 0x5432u);
+      const uint32_t s1 = x << 1;
+      const uint32_t K = x & ~s1 & u8::HI;
+      const uint32_t L = x & s1 & u8::HI;
+      const uint32_t E = L & (x << 2);
+      const uint32_t F = E & (x << 3);
+      const uint32_t LO = K & __funnelshift_l(fprev, F, 8);
+      uint32_t ue, uo;
+      u8::units4(x, pe, po, pe2, L, E, F, LO, &ue, &uo);
+      const uint32_t em = s.cm[k];
+      const uint32_t pre = ((em >> 7) & 0x01010101u) * 0x01010100u;  // exclusive prefix bytes
+      uint16_t *st = stage + o;
+      if (k < 7) {
+        st[0] = (uint16_t)ue;
+        st[(pre >> 8) & 0xFFu] = (uint16_t)uo;
+        st[(pre >> 16) & 0xFFu] = (uint16_t)(ue >> 16);
+        st[pre >> 24] = (uint16_t)(uo >> 16);
+      } else {
+        if (em & 0x00000080u) st[0] = (uint16_t)ue;
+        if (em & 0x00008000u) st[(pre >> 8) & 0xFFu] = (uint16_t)uo;
+        if (em & 0x00800000u) st[(pre >> 16) & 0xFFu] = (uint16_t)(ue >> 16);
+        if (em & 0x80000000u) st[pre >> 24] = (uint16_t)(uo >> 16);
       }
-      o += __popc(c);
+      o += __popc(em);
+      fprev = F;
+      pe = pe_n;
+      po = u8::payload_odd(cn, cnn);
+      cn = cnn;
     }
   }
 
@@ -304,9 +326,8 @@ struct U8Pol {
     if (from < 0) from = 0;
     unsigned long long c = 0;
     for (long long i = from + lane; i < (long long)e; i += 32) {
-      uint32_t bi = byte_at(win, i), bn = byte_at(win, i + 1);
-      c += ((bi & 0xC0u) != 0x80u) ? 1u : 0u;
-      c += (bi >= 0xF0u && (bn & 0xC0u) == 0x80u && i + 1 < win.n) ? 1u : 0u;
+      uint32_t bi = byte_at(win, i), bp = byte_at(win, i - 1);
+      c += ((bi & 0xC0u) != 0x80u || bp >= 0xF0u) ? 1u : 0u;
     }
     *wr = base + warp_sum64(c);
   }
@@ -398,7 +419,7 @@ struct U16Pol {
 
   // a7: encode the owned words into stage[o ...] (UTF-8 bytes)
   __device__ static __forceinline__ void decode(const St &s, uint8_t *stage, uint32_t o,
-                                                long long nw) {
+                                                uint32_t lim, long long nw) {
     if (s.wasc && s.interior) {
       if ((o & 3u) == 0u) {
         uint32_t *st32 = reinterpret_cast<uint32_t *>(stage + o);
@@ -410,19 +431,23 @@ struct U16Pol {
       }
       return;
     }
+    // branch-free: every word stores up to 3 bytes at its offset; bytes past its width are
+    // overwritten by the following words (program order).  Stores are clipped at the thread's
+    // end slot `lim` so nothing spills into the next thread's bytes.
     uint32_t p = s.prev_word;
 #pragma unroll
     for (int i = 0; i < 16; i++) {
       const uint32_t u = (s.w[i >> 1] >> (16 * (i & 1))) & 0xFFFFu;
-      const long long pos = s.pos0 + i;
-      if (s.interior || (pos >= 0 && pos < nw)) {
-        const uint32_t wd = u16::width(u, p);
-        const uint32_t v = u16::utf8_bytes(u, p);
-        stage[o] = (uint8_t)v;
-        if (wd > 1) stage[o + 1] = (uint8_t)(v >> 8);
-        if (wd > 2) stage[o + 2] = (uint8_t)(v >> 16);
-        o += wd;
+      uint32_t wd = u16::width(u, p);
+      if (!s.interior) {
+        const long long pos = s.pos0 + i;
+        wd = (pos >= 0 && pos < nw) ? wd : 0u;
       }
+      const uint32_t v = u16::utf8_bytes(u, p);
+      if (o < lim) stage[o] = (uint8_t)v;
+      if (o + 1 < lim) stage[o + 1] = (uint8_t)(v >> 8);
+      if (o + 2 < lim) stage[o + 2] = (uint8_t)(v >> 16);
+      o += wd;
       p = u;
     }
   }
@@ -447,16 +472,16 @@ struct U16Pol {
 
 template <class Pol>
 __device__ __forceinline__ void pol_decode(const typename Pol::St &s, typename Pol::Out *stage,
-                                           uint32_t o, long long n_units);
+                                           uint32_t o, uint32_t lim, long long n_units);
 template <>
 __device__ __forceinline__ void pol_decode<U8Pol>(const U8Pol::St &s, uint16_t *stage,
-                                                  uint32_t o, long long) {
-  U8Pol::decode(s, stage, o);
+                                                  uint32_t o, uint32_t lim, long long) {
+  U8Pol::decode(s, stage, o, lim);
 }
 template <>
 __device__ __forceinline__ void pol_decode<U16Pol>(const U16Pol::St &s, uint8_t *stage,
-                                                   uint32_t o, long long nw) {
-  U16Pol::decode(s, stage, o, nw);
+                                                   uint32_t o, uint32_t lim, long long nw) {
+  U16Pol::decode(s, stage, o, lim, nw);
 }
 
 // Last CTA to finish: outcome + counter reset.  n_units in input code units.
@@ -624,7 +649,7 @@ __global__ void __launch_bounds__(NT + 32, 2) k_transcode(const TileArgs a) {
         unsigned long long e = Pol::find_error(st, n_units);
         if (e != NONE) atomicMin(&s_emin, e);
       }
-      pol_decode<Pol>(st, stage0 + (i & 1) * SU, excl, n_units);
+      pol_decode<Pol>(st, stage0 + (i & 1) * SU, excl, excl + cnt, n_units);
       if (i > 0) {  // a8: copy out the previous tile once its prefix is known
         if ((i - 1) & 1) named_sync<BAR_P1, NT + 32>(); else named_sync<BAR_P0, NT + 32>();
         copy_out<Out>(out, a.out_cap, s_pre[(i - 1) & 1], C_prev, stage0 + ((i - 1) & 1) * SU,

@@ -19,9 +19,8 @@ __device__ __forceinline__ bool is_high(uint32_t u) { return (u & 0xFC00u) == 0x
 __device__ __forceinline__ bool is_low(uint32_t u) { return (u & 0xFC00u) == 0xDC00u; }
 
 __device__ __forceinline__ uint32_t width(uint32_t u, uint32_t prev) {
-  if (u < 0x80u) return 1u;
-  if (u < 0x800u || is_high(u) || (is_low(u) && is_high(prev))) return 2u;
-  return 3u;
+  const bool two = u < 0x800u || is_high(u) || (is_low(u) && is_high(prev));
+  return 1u + (u >= 0x80u ? 1u : 0u) + (two ? 0u : 1u);
 }
 
 __device__ __forceinline__ bool err_at(uint32_t prev, uint32_t u, uint32_t next) {
@@ -29,17 +28,21 @@ __device__ __forceinline__ bool err_at(uint32_t prev, uint32_t u, uint32_t next)
 }
 
 // UTF-8 bytes of word u (little-endian packed, width(u, prev) of them are meaningful).
+// Branch-free: all candidates computed, then selected.
 __device__ __forceinline__ uint32_t utf8_bytes(uint32_t u, uint32_t prev) {
-  if (u < 0x80u) return u;
-  if (u < 0x800u) return (0xC0u | (u >> 6)) | ((0x80u | (u & 0x3Fu)) << 8);
-  if (is_high(u)) {
-    uint32_t h10 = (u & 0x3FFu) + 0x40u;  // cp >> 10
-    return (0xF0u | (h10 >> 8)) | ((0x80u | ((h10 >> 2) & 0x3Fu)) << 8);
-  }
-  if (is_low(u) && is_high(prev))
-    return (0x80u | ((prev & 3u) << 4) | ((u >> 6) & 0xFu)) | ((0x80u | (u & 0x3Fu)) << 8);
-  return (0xE0u | (u >> 12)) | ((0x80u | ((u >> 6) & 0x3Fu)) << 8) |
-         ((0x80u | (u & 0x3Fu)) << 16);
+  const uint32_t t6 = 0x80u | (u & 0x3Fu);         // last continuation byte
+  const uint32_t m6 = 0x80u | ((u >> 6) & 0x3Fu);  // middle continuation byte
+  const uint32_t b2 = (0xC0u | (u >> 6)) | (t6 << 8);
+  const uint32_t b3 = (0xE0u | (u >> 12)) | (m6 << 8) | (t6 << 16);
+  const uint32_t h10 = (u & 0x3FFu) + 0x40u;       // cp >> 10 of a pair
+  const uint32_t bh = (0xF0u | (h10 >> 8)) | ((0x80u | ((h10 >> 2) & 0x3Fu)) << 8);
+  const uint32_t bl = (0x80u | ((prev & 3u) << 4) | ((u >> 6) & 0xFu)) | (t6 << 8);
+  uint32_t v = b3;
+  v = (is_low(u) && is_high(prev)) ? bl : v;
+  v = is_high(u) ? bh : v;
+  v = (u < 0x800u) ? b2 : v;
+  v = (u < 0x80u) ? u : v;
+  return v;
 }
 
 }  // namespace u16

@@ -10,9 +10,9 @@
 //    tests/test_derivations.py.  A position flags iff the input is invalid, and the first
 //    flagged position r satisfies e <= r <= e+3 for the first error e.
 //  * widths: units a position emits in UTF-16: 1 per non-continuation
-//    byte, +1 for a lead >= F0 followed by a continuation byte (the surrogate pair's second
-//    unit, attributed to the lead so a character never splits across tiles).  At most one
-//    unit per input byte on ANY input, so out_cap = n is always safe.
+//    byte, and 1 for a continuation byte that directly follows a byte >= F0 (it emits the
+//    surrogate pair's second unit).  Exactly 0 or 1 unit per input byte on ANY input, so
+//    out_cap = n is always safe, and every position is a fixed-size slot.
 //  * decode(): code point assembly, and the UTF-16 encoding of PAPER.md:87.
 //  * err_at(): the exact local first-error predicate (D2), used only to rescan
 //    flagged tiles.
@@ -66,6 +66,7 @@ struct WordMasks {
   uint32_t F;   // >= F0
   uint32_t t1;  // T1[hi(byte)]
   uint32_t t2;  // T2[lo(byte)]
+  uint32_t t3;  // T3[hi(byte)]
 };
 
 __device__ __forceinline__ WordMasks masks(uint32_t x, bool tables) {
@@ -80,9 +81,10 @@ __device__ __forceinline__ WordMasks masks(uint32_t x, bool tables) {
     uint32_t sh = sel_hi(x) ^ 0x8888u;
     uint32_t sl = sel_lo(x);
     m.t1 = prmt(T1_A, T1_B, sh);
+    m.t3 = prmt(T3_A, T3_B, sh);
     m.t2 = prmt(T2_0, T2_1, sl) | prmt(T2_2, T2_3, sl ^ 0x8888u);
   } else {
-    m.t1 = m.t2 = 0;
+    m.t1 = m.t2 = m.t3 = 0;
   }
   return m;
 }
@@ -102,15 +104,14 @@ __device__ __forceinline__ uint32_t classify(const WordMasks &p, const WordMasks
   // value rules: T1[hi(prev1)] & T2[lo(prev1)] & T3[hi(cur)]
   uint32_t t1 = __funnelshift_l(p.t1, c.t1, 8);
   uint32_t t2 = __funnelshift_l(p.t2, c.t2, 8);
-  uint32_t t3 = prmt(T3_A, T3_B, sel_hi(c.x) ^ 0x8888u);
-  return structural | count | (t1 & t2 & t3);
+  return structural | count | (t1 & t2 & c.t3);
 }
 
-// Width bits of word c (next word n for the look-ahead): msb of byte j = non-continuation
-// byte (1 unit); bit 6 of byte j = lead >= F0 followed by a continuation (2nd unit).
-__device__ __forceinline__ uint32_t width_bits(const WordMasks &c, uint32_t Knext) {
-  uint32_t Kn1 = __funnelshift_r(c.K, Knext, 8);  // continuation flag of byte j+1
-  return (~c.K & HI) | ((c.F & Kn1) >> 1);
+// Emit bits of word c (previous word p): msb of byte j set iff position j emits a UTF-16 unit
+// (a non-continuation byte, or a continuation byte right after a byte >= F0).
+__device__ __forceinline__ uint32_t emit_bits(const WordMasks &p, const WordMasks &c) {
+  uint32_t Fp1 = __funnelshift_l(p.F, c.F, 8);  // byte j-1 >= F0
+  return (~c.K & HI) | (c.K & Fp1);
 }
 
 // Decode the character whose lead is the low byte of x (bytes b0..b3 = x, little endian) and
@@ -124,6 +125,53 @@ __device__ __forceinline__ uint32_t decode_units(uint32_t x, uint32_t *u1) {
   *u1 = 0xDC00u | (cp & 0x3FFu);
   uint32_t hi = 0xD7C0u + (cp >> 10);
   return b0 < 0x80u ? b0 : (b0 < 0xE0u ? v2 : (b0 < 0xF0u ? v3 : hi));
+}
+
+// ---------------------------------------------------------------- SWAR decode (a7)
+// Code-unit candidates for the 4 positions of word x (bytes b0..b3; b4.. from xn), two
+// positions per 32-bit op in 16-bit lanes: "even" lanes hold positions 0 and 2, "odd" lanes
+// positions 1 and 3.  With c_j = b_j & 0x3F and P(j) = c_j << 6 | c_{j+1}:
+//   ASCII      u = b_j
+//   2-byte     u = P(j)                                  (b_j & 0x3F has bit 5 clear)
+//   3-byte     u = (b_j & 0xF) << 12 | P(j+1)
+//   4-byte     hi = 0xD7C0 + ((b_j & 7) << 8 | P(j+1) >> 4),  lo = 0xDC00 | P(j+2)
+// Pe / Po are P at the even / odd positions of this word; Pe2 / Po2 the same two positions
+// later (they need the next word's P).
+__device__ __forceinline__ uint32_t pair_payload(uint32_t s) {
+  // s holds, per 16-bit lane, [c_{j+1}, c_j]; returns c_j << 6 | c_{j+1} per lane
+  return (s & 0x003F003Fu) | ((s >> 2) & 0x0FC00FC0u);
+}
+__device__ __forceinline__ uint32_t payload_even(uint32_t c) { return pair_payload(prmt(c, 0u, 0x2301u)); }
+__device__ __forceinline__ uint32_t payload_odd(uint32_t c, uint32_t cn) {
+  return pair_payload(prmt(c, cn, 0x3412u));
+}
+// per-16-bit-lane masks (0xFFFF) from per-byte top-bit masks, even / odd positions
+__device__ __forceinline__ uint32_t lanes_even(uint32_t m) { return prmt(m, 0u, 0xAA88u); }
+__device__ __forceinline__ uint32_t lanes_odd(uint32_t m) { return prmt(m, 0u, 0xBB99u); }
+__device__ __forceinline__ uint32_t mux(uint32_t m, uint32_t a, uint32_t b) {
+  return (a & m) | (b & ~m);
+}
+
+// The unit emitted at each of the 4 positions (ue: positions 0 and 2, uo: 1 and 3).  A
+// continuation byte right after a 4-byte lead emits the low surrogate 0xDC00 | P(i+1).
+// x: bytes of this word; Pe, Po: P at even / odd positions; Pe2: P at positions 2 and 4;
+// L/E/F: >= C0 / E0 / F0 top-bit masks; LO: continuation-after-F0 top-bit mask.
+__device__ __forceinline__ void units4(uint32_t x, uint32_t Pe, uint32_t Po, uint32_t Pe2,
+                                       uint32_t L, uint32_t E, uint32_t F, uint32_t LO,
+                                       uint32_t *ue, uint32_t *uo) {
+  const uint32_t asc_e = prmt(x, 0u, 0x4240u), asc_o = prmt(x, 0u, 0x4341u);
+  const uint32_t u3_e = ((x << 12) & 0xF000F000u) | Po;
+  const uint32_t u3_o = ((x << 4) & 0xF000F000u) | Pe2;
+  const uint32_t hi_e = (((x << 8) & 0x07000700u) | ((Po >> 4) & 0x00FF00FFu)) + 0xD7C0D7C0u;
+  const uint32_t hi_o = ((x & 0x07000700u) | ((Pe2 >> 4) & 0x00FF00FFu)) + 0xD7C0D7C0u;
+  uint32_t e = mux(lanes_even(L), Pe, asc_e);
+  e = mux(lanes_even(E), u3_e, e);
+  e = mux(lanes_even(F), hi_e, e);
+  *ue = mux(lanes_even(LO), Po | 0xDC00DC00u, e);  // 0xDC00 has bits 10-11 set
+  uint32_t o = mux(lanes_odd(L), Po, asc_o);
+  o = mux(lanes_odd(E), u3_o, o);
+  o = mux(lanes_odd(F), hi_o, o);
+  *uo = mux(lanes_odd(LO), Pe2 | 0xDC00DC00u, o);
 }
 
 // ---------------------------------------------------------------- exact (cold) path

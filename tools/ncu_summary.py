@@ -33,8 +33,14 @@ if raw:
                  "dram__throughput.avg.pct_of_peak_sustained_elapsed"):
             print(f"{k:<55} {v}")
 sass = list(csv.reader(io.StringIO(run(["--page", "source", "--csv", "--print-source", "sass"]))))
+# the page holds one section per profiled kernel: take the first
 h = sass[1]
-data = sass[2:]
+data = []
+for r in sass[2:]:
+    if r and r[0] == "Kernel Name":
+        break
+    if len(r) == len(h):
+        data.append(r)
 ix = {k: i for i, k in enumerate(h)}
 S = "Warp Stall Sampling (All Samples)"
 tot = sum(float(r[ix[S]] or 0) for r in data)
