@@ -334,7 +334,7 @@ struct U8Pol {
 };
 
 // ============================================================================ UTF-16 policy
-// Positions are words.  Thread `tid` owns tile words [16 tid, 16 tid + 16).
+// Positions are words.  Thread `tid` owns tile words [16 tid, 16 tid + 16), two per register.
 struct U16Pol {
   using Out = uint8_t;
   static constexpr int UNIT = 2;
@@ -342,9 +342,10 @@ struct U16Pol {
   struct St {
     uint32_t w[8];
     uint32_t prev_word, next_word;
+    uint32_t own[8];                 // owned lanes (top bits), all set in interior tiles
     unsigned long long first_err;
     long long pos0;
-    bool wasc, interior, sur;
+    bool wasc, interior;
   };
 
   __device__ static __forceinline__ uint32_t analyze(St &s, const uint8_t *buf, int tid,
@@ -366,47 +367,44 @@ struct U16Pol {
     s.next_word = nx & 0xFFFFu;
     s.pos0 = tpw + (BPT / 2) * tid;
     s.interior = (tpw >= 0) && (tpw + TILE / 2 <= nw);
-    // any surrogate among the thread's words or its two neighbours?  (SWAR on word pairs)
-    uint32_t sur = ((s.prev_word & 0xF800u) == 0xD800u) | ((s.next_word & 0xF800u) == 0xD800u);
     uint32_t orv = 0;
 #pragma unroll
     for (int k = 0; k < 8; k++) {
-      uint32_t x = (s.w[k] & 0xF800F800u) ^ 0xD800D800u;  // zero half <=> surrogate
-      sur |= ((x & 0xFFFFu) == 0u) | ((x >> 16) == 0u);
       orv |= s.w[k];
-    }
-    s.sur = sur != 0;
-    s.wasc = __all_sync(FULL, (orv & 0xFF80FF80u) == 0u);
-    s.first_err = NONE;
-    uint32_t cnt = 0;
-    if (s.sur) {
-      // a9 pairing predicate (exact) + a5 widths
-      uint32_t p = s.prev_word;
-#pragma unroll
-      for (int i = 0; i < 16; i++) {
-        const uint32_t u = (s.w[i >> 1] >> (16 * (i & 1))) & 0xFFFFu;
-        const uint32_t q = (i < 15) ? ((s.w[(i + 1) >> 1] >> (16 * ((i + 1) & 1))) & 0xFFFFu)
-                                    : s.next_word;
-        const long long pos = s.pos0 + i;
-        if (s.interior || (pos >= 0 && pos < nw)) {
-          if (s.first_err == NONE && u16::err_at(p, u, q)) s.first_err = (unsigned long long)pos;
-          if (xc) cnt += u16::width(u, p);
-        }
-        p = u;
+      if (s.interior) {
+        s.own[k] = u16::LANE_TOP;
+      } else {
+        const long long pos = s.pos0 + 2 * k;
+        s.own[k] = ((pos >= 0 && pos < nw) ? 0x8000u : 0u) |
+                   ((pos + 1 >= 0 && pos + 1 < nw) ? 0x80000000u : 0u);
       }
-    } else if (xc) {
-      // no surrogates: 1 / 2 / 3 bytes by range, two words per register
+    }
+    s.wasc = __all_sync(FULL, (orv & 0xFF80FF80u) == 0u);
+    // a9 pairing predicate (exact) and a5 widths, two words per op
+    uint32_t cnt = 0, anyerr = 0;
+    uint32_t Hprev = (s.prev_word & 0xFC00u) == 0xD800u ? 0x80000000u : 0u;  // as a lane-1 bit
+    u16::Cls2 c = u16::classes2(s.w[0]);
+    uint32_t errm[8];
 #pragma unroll
-      for (int k = 0; k < 8; k++) {
-        const uint32_t lo = s.w[k] & 0xFFFFu, hi = s.w[k] >> 16;
-        const uint32_t wl = 1u + (lo >= 0x80u) + (lo >= 0x800u);
-        const uint32_t wh = 1u + (hi >= 0x80u) + (hi >= 0x800u);
-        if (s.interior) {
-          cnt += wl + wh;
-        } else {
-          const long long pos = s.pos0 + 2 * k;
-          cnt += ((pos >= 0 && pos < nw) ? wl : 0u) + ((pos + 1 >= 0 && pos + 1 < nw) ? wh : 0u);
-        }
+    for (int k = 0; k < 8; k++) {
+      const u16::Cls2 cn = (k < 7) ? u16::classes2(s.w[k + 1])
+                                   : u16::classes2(s.next_word & 0xFFFFu);
+      const uint32_t Hp = __funnelshift_l(Hprev, c.H, 16);   // previous word is high
+      const uint32_t Ln = __funnelshift_r(c.L, cn.L, 16);     // next word is low
+      errm[k] = ((c.H & ~Ln) | (c.L & ~Hp)) & s.own[k];
+      anyerr |= errm[k];
+      if (xc) {
+        const uint32_t nA = ~c.A & u16::LANE_TOP;
+        cnt += __popc(s.own[k]) + __popc(nA & s.own[k]) + __popc(u16::three2(c, Hp) & s.own[k]);
+      }
+      Hprev = c.H;
+      c = cn;
+    }
+    s.first_err = NONE;
+    if (anyerr) {  // cold: first erroneous lane
+#pragma unroll
+      for (int k = 7; k >= 0; k--) {
+        if (errm[k]) s.first_err = (unsigned long long)(s.pos0 + 2 * k + ((errm[k] & 0x8000u) ? 0 : 1));
       }
     }
     return cnt;
@@ -417,9 +415,11 @@ struct U16Pol {
     return s.first_err;
   }
 
-  // a7: encode the owned words into stage[o ...] (UTF-8 bytes)
+  // a7: encode the owned words into stage[o ...] (UTF-8 bytes).  Every word stores 3 bytes at
+  // its offset; bytes past its width are overwritten by the following words (program order);
+  // stores are clipped at the thread's end slot `lim`.
   __device__ static __forceinline__ void decode(const St &s, uint8_t *stage, uint32_t o,
-                                                uint32_t lim, long long nw) {
+                                                uint32_t lim, long long) {
     if (s.wasc && s.interior) {
       if ((o & 3u) == 0u) {
         uint32_t *st32 = reinterpret_cast<uint32_t *>(stage + o);
@@ -431,24 +431,39 @@ struct U16Pol {
       }
       return;
     }
-    // branch-free: every word stores up to 3 bytes at its offset; bytes past its width are
-    // overwritten by the following words (program order).  Stores are clipped at the thread's
-    // end slot `lim` so nothing spills into the next thread's bytes.
-    uint32_t p = s.prev_word;
+    uint32_t prevreg = s.prev_word << 16;
+    uint32_t Hprev = (s.prev_word & 0xFC00u) == 0xD800u ? 0x80000000u : 0u;
 #pragma unroll
-    for (int i = 0; i < 16; i++) {
-      const uint32_t u = (s.w[i >> 1] >> (16 * (i & 1))) & 0xFFFFu;
-      uint32_t wd = u16::width(u, p);
-      if (!s.interior) {
-        const long long pos = s.pos0 + i;
-        wd = (pos >= 0 && pos < nw) ? wd : 0u;
+    for (int k = 0; k < 8; k++) {
+      const uint32_t r = s.w[k];
+      const u16::Cls2 c = u16::classes2(r);
+      const uint32_t Hp = __funnelshift_l(Hprev, c.H, 16);
+      const uint32_t pl = __funnelshift_l(prevreg, r, 16);
+      uint32_t B0, B1, B2;
+      u16::encode2(r, pl, c, Hp, &B0, &B1, &B2);
+      const uint32_t three = u16::three2(c, Hp);
+      const uint32_t nA = ~c.A & u16::LANE_TOP;
+      const uint32_t wa = (s.own[k] & 0x8000u) ? 1u + ((nA >> 15) & 1u) + ((three >> 15) & 1u) : 0u;
+      const uint32_t wb = (s.own[k] & 0x80000000u) ? 1u + (nA >> 31) + (three >> 31) : 0u;
+      const uint32_t ob = o + wa;
+      if (k < 7) {  // spill past a word is covered by the >= 2 owned words that follow it
+        stage[o] = (uint8_t)B0;
+        stage[o + 1] = (uint8_t)B1;
+        stage[o + 2] = (uint8_t)B2;
+        stage[ob] = (uint8_t)(B0 >> 16);
+        stage[ob + 1] = (uint8_t)(B1 >> 16);
+        stage[ob + 2] = (uint8_t)(B2 >> 16);
+      } else {      // the thread's last two words: clip at its end slot
+        if (o < lim) stage[o] = (uint8_t)B0;
+        if (o + 1 < lim) stage[o + 1] = (uint8_t)B1;
+        if (o + 2 < lim) stage[o + 2] = (uint8_t)B2;
+        if (ob < lim) stage[ob] = (uint8_t)(B0 >> 16);
+        if (ob + 1 < lim) stage[ob + 1] = (uint8_t)(B1 >> 16);
+        if (ob + 2 < lim) stage[ob + 2] = (uint8_t)(B2 >> 16);
       }
-      const uint32_t v = u16::utf8_bytes(u, p);
-      if (o < lim) stage[o] = (uint8_t)v;
-      if (o + 1 < lim) stage[o + 1] = (uint8_t)(v >> 8);
-      if (o + 2 < lim) stage[o + 2] = (uint8_t)(v >> 16);
-      o += wd;
-      p = u;
+      o = ob + wb;
+      Hprev = c.H;
+      prevreg = r;
     }
   }
 
