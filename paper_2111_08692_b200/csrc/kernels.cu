@@ -93,15 +93,16 @@ __device__ __forceinline__ void block_scan(uint32_t cnt, uint32_t *s_wsum, int l
   uint32_t incl = warp_incl_scan(cnt, lane);
   if (lane == 31) s_wsum[warp] = incl;
   named_sync<BAR_DATA, NT>();
-  uint32_t wpre = 0, C = 0;
+  // every warp scans the NT/32 warp totals with shuffles (lane l holds warp l's total)
+  uint32_t v = (lane < NT / 32) ? s_wsum[lane] : 0u;
 #pragma unroll
-  for (int i = 0; i < NT / 32; i++) {
-    uint32_t v = s_wsum[i];
-    wpre += (i < warp) ? v : 0u;
-    C += v;
+  for (int d = 1; d < NT / 32; d <<= 1) {
+    uint32_t t = __shfl_up_sync(FULL, v, d);
+    if (lane >= d) v += t;
   }
-  *excl = wpre + incl - cnt;
-  *total = C;
+  const uint32_t wincl = __shfl_sync(FULL, v, warp);
+  *total = __shfl_sync(FULL, v, NT / 32 - 1);
+  *excl = wincl - __shfl_sync(FULL, incl, 31) + incl - cnt;
 }
 
 // Publish tile t's aggregate, look back, publish its inclusive prefix; one full warp.
@@ -219,8 +220,11 @@ struct U8Pol {
 #pragma unroll
         for (int k = 0; k < 8; k++) s.cm[k] &= range_bytes(s.pos0 + 4 * k, 0, n) & u8::HI;
       }
+      // emit bits are byte msbs: sum the 8 words bytewise (<= 8 per byte), then fold the bytes
+      uint32_t acc = 0;
 #pragma unroll
-      for (int k = 0; k < 8; k++) cnt += __popc(s.cm[k]);
+      for (int k = 0; k < 8; k++) acc += s.cm[k] >> 7;
+      cnt = (acc * 0x01010101u) >> 24;
     }
     return cnt;
   }
@@ -288,20 +292,20 @@ struct U8Pol {
       uint32_t ue, uo;
       u8::units4(x, pe, po, pe2, L, E, F, LO, &ue, &uo);
       const uint32_t em = s.cm[k];
-      const uint32_t pre = ((em >> 7) & 0x01010101u) * 0x01010100u;  // exclusive prefix bytes
+      const uint32_t inc = (em >> 7) * 0x01010101u;  // byte j: units emitted by positions <= j
       uint16_t *st = stage + o;
       if (k < 7) {
         st[0] = (uint16_t)ue;
-        st[(pre >> 8) & 0xFFu] = (uint16_t)uo;
-        st[(pre >> 16) & 0xFFu] = (uint16_t)(ue >> 16);
-        st[pre >> 24] = (uint16_t)(uo >> 16);
+        st[inc & 0xFFu] = (uint16_t)uo;
+        st[(inc >> 8) & 0xFFu] = (uint16_t)(ue >> 16);
+        st[(inc >> 16) & 0xFFu] = (uint16_t)(uo >> 16);
       } else {
         if (em & 0x00000080u) st[0] = (uint16_t)ue;
-        if (em & 0x00008000u) st[(pre >> 8) & 0xFFu] = (uint16_t)uo;
-        if (em & 0x00800000u) st[(pre >> 16) & 0xFFu] = (uint16_t)(ue >> 16);
-        if (em & 0x80000000u) st[pre >> 24] = (uint16_t)(uo >> 16);
+        if (em & 0x00008000u) st[inc & 0xFFu] = (uint16_t)uo;
+        if (em & 0x00800000u) st[(inc >> 8) & 0xFFu] = (uint16_t)(ue >> 16);
+        if (em & 0x80000000u) st[(inc >> 16) & 0xFFu] = (uint16_t)(uo >> 16);
       }
-      o += __popc(em);
+      o += inc >> 24;
       fprev = F;
       pe = pe_n;
       po = u8::payload_odd(cn, cnn);
@@ -380,8 +384,9 @@ struct U16Pol {
       }
     }
     s.wasc = __all_sync(FULL, (orv & 0xFF80FF80u) == 0u);
-    // a9 pairing predicate (exact) and a5 widths, two words per op
-    uint32_t cnt = 0, anyerr = 0;
+    // a9 pairing predicate (exact) and a5 widths, two words per op.  Widths are summed per
+    // 16-bit lane (1 + [u >= 0x80] + [three-byte]) and folded once.
+    uint32_t lanes = 0, anyerr = 0;
     uint32_t Hprev = (s.prev_word & 0xFC00u) == 0xD800u ? 0x80000000u : 0u;  // as a lane-1 bit
     u16::Cls2 c = u16::classes2(s.w[0]);
     uint32_t errm[8];
@@ -391,15 +396,19 @@ struct U16Pol {
                                    : u16::classes2(s.next_word & 0xFFFFu);
       const uint32_t Hp = __funnelshift_l(Hprev, c.H, 16);   // previous word is high
       const uint32_t Ln = __funnelshift_r(c.L, cn.L, 16);     // next word is low
-      errm[k] = ((c.H & ~Ln) | (c.L & ~Hp)) & s.own[k];
-      anyerr |= errm[k];
+      uint32_t e = (c.H & ~Ln) | (c.L & ~Hp);
       if (xc) {
-        const uint32_t nA = ~c.A & u16::LANE_TOP;
-        cnt += __popc(s.own[k]) + __popc(nA & s.own[k]) + __popc(u16::three2(c, Hp) & s.own[k]);
+        uint32_t wl = 0x00010001u + ((~c.A & u16::LANE_TOP) >> 15) + (u16::three2(c, Hp) >> 15);
+        if (!s.interior) wl &= (s.own[k] >> 15) * 0xFFFFu;
+        lanes += wl;
       }
+      if (!s.interior) e &= s.own[k];
+      errm[k] = e;
+      anyerr |= e;
       Hprev = c.H;
       c = cn;
     }
+    const uint32_t cnt = (lanes & 0xFFFFu) + (lanes >> 16);
     s.first_err = NONE;
     if (anyerr) {  // cold: first erroneous lane
 #pragma unroll
@@ -407,7 +416,7 @@ struct U16Pol {
         if (errm[k]) s.first_err = (unsigned long long)(s.pos0 + 2 * k + ((errm[k] & 0x8000u) ? 0 : 1));
       }
     }
-    return cnt;
+    return xc ? cnt : 0u;
   }
 
   __device__ static __forceinline__ bool hint(const St &s) { return s.first_err != NONE; }
@@ -441,10 +450,9 @@ struct U16Pol {
       const uint32_t pl = __funnelshift_l(prevreg, r, 16);
       uint32_t B0, B1, B2;
       u16::encode2(r, pl, c, Hp, &B0, &B1, &B2);
-      const uint32_t three = u16::three2(c, Hp);
-      const uint32_t nA = ~c.A & u16::LANE_TOP;
-      const uint32_t wa = (s.own[k] & 0x8000u) ? 1u + ((nA >> 15) & 1u) + ((three >> 15) & 1u) : 0u;
-      const uint32_t wb = (s.own[k] & 0x80000000u) ? 1u + (nA >> 31) + (three >> 31) : 0u;
+      uint32_t wl = 0x00010001u + ((~c.A & u16::LANE_TOP) >> 15) + (u16::three2(c, Hp) >> 15);
+      if (!s.interior) wl &= (s.own[k] >> 15) * 0xFFFFu;
+      const uint32_t wa = wl & 0xFFFFu, wb = wl >> 16;
       const uint32_t ob = o + wa;
       if (k < 7) {  // spill past a word is covered by the >= 2 owned words that follow it
         stage[o] = (uint8_t)B0;
