@@ -51,6 +51,7 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=2)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-per-op", action="store_true")
     p.add_argument("--out", default="")
     return p.parse_args()
 
@@ -145,7 +146,8 @@ def load_shard(cfg, rank, G, size):
     nom = ugd.nominal_cuts(size, G)
     c0, c1 = nom[rank], nom[rank + 1]
     base = max(0, c0 - 16)
-    buf = synth.generate_range(cfg, base, min(size, c1 + 16))
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    buf = synth.generate_range(cfg, base, min(size, c1 + 16), workers=max(1, (cores or 2) // G))
     get = lambda a, b: buf[a - base:b - base].tobytes()  # noqa: E731
     return buf, ugd.utf8_cut(get, c0, size), ugd.utf8_cut(get, c1, size), base
 
@@ -193,10 +195,13 @@ def run_ours(args):
     u16 = out16[:n16]
     # code points of this rank (reporting only): non-continuation bytes
     nchar = int(((t_in & 0xC0) != 0x80).sum())
-    tot16 = torch.tensor([n16], dtype=torch.int64, device=dev)
+    # global UTF-16 offset of this rank's output (exclusive prefix of the counts), untimed
+    cnts = torch.zeros(G, dtype=torch.int64, device=dev)
+    cnts[rank] = n16
     if G > 1:
-        dist.all_reduce(tot16)
-    N16_global = int(tot16[0])
+        dist.all_reduce(cnts)
+    N16_global = int(cnts.sum())
+    off16 = int(cnts[:rank].sum())
 
     ev_f = []  # (start, end) events around each forward launch
 
@@ -221,7 +226,7 @@ def run_ours(args):
             ev_f.append((e0, e1))
         gather_combine(0)
         ug.utf8_length_from_utf16le_async(u16, lens, len_off=8)
-        ug.utf16le_to_utf8_shard_async(u16, 0, n16, 0, 0, 0, out8, rec, rec_off=R)
+        ug.utf16le_to_utf8_shard_async(u16, 0, n16, 0, 0, off16, out8, rec, rec_off=R)
         gather_combine(1)
 
     for _ in range(args.warmup):
@@ -287,6 +292,10 @@ def run_ours(args):
     if not args.no_e2e:
         e2e = run_e2e(args, ug, host[lo - base: hi - base], n16, G, rank, dev, dist)
 
+    per_op = None
+    if not args.no_per_op:
+        per_op = measure_per_op(ug, t_all, lo - base, n8, hb, ha, out16, u16, out8, dev, peak)
+
     cpu = None
     if rank == 0 and G == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, size)
@@ -319,6 +328,7 @@ def run_ours(args):
                          "kernel": "k_transcode<U8Pol> (utf8_to_utf16le)",
                          "algorithmic_bytes_per_launch": fwd_bytes,
                          "avg_launch_ms": round(fwd_ms, 4), "peak_source": peak_src},
+            "per_op": per_op,
             "clocks": clk,
             "gpu_launches": int(launches),
             "e2e": e2e,
@@ -332,6 +342,45 @@ def run_ours(args):
     if G > 1:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def measure_per_op(ug, t_all, off, n8, hb, ha, out16, u16, out8, dev, peak, reps=5):
+    """Each hot-path op alone on this rank's shard (after the timed step; same buffers):
+    mean CUDA-event time over `reps`, input GB/s, algorithmic HBM GB/s and its fraction of the
+    measured copy peak.  Rows a1-a11 of SURVEY 8(a) individually."""
+    import torch
+    stream = torch.cuda.current_stream()
+    t_in = t_all[off:off + n8]
+    n16 = u16.numel()
+    res = ug.result_buffer(dev, 1)
+    lens = torch.zeros(1, dtype=torch.int64, device=dev)
+    rec = ug.record_buffer(dev, 1)
+    ops = {
+        "utf8_validate": (lambda: ug.utf8_validate_async(t_in, res), n8, n8),
+        "utf8_to_utf16le": (lambda: ug.utf8_to_utf16le_shard_async(
+            t_all, off, n8, hb, ha, 0, out16, rec), n8, n8 + 2 * n16),
+        "utf16_length_from_utf8": (lambda: ug.utf16_length_from_utf8_async(t_in, lens), n8, n8),
+        "utf16le_validate": (lambda: ug.utf16le_validate_async(u16, res), 2 * n16, 2 * n16),
+        "utf16le_to_utf8": (lambda: ug.utf16le_to_utf8_shard_async(
+            u16, 0, n16, 0, 0, 0, out8, rec), 2 * n16, 2 * n16 + n8),
+        "utf8_length_from_utf16le": (lambda: ug.utf8_length_from_utf16le_async(u16, lens),
+                                     2 * n16, 2 * n16),
+    }
+    out = {}
+    for name, (fn, in_bytes, hbm_bytes) in ops.items():
+        fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(reps):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / reps
+        out[name] = {"ms": round(ms, 4), "input_gbs": round(in_bytes / ms / 1e6, 1),
+                     "hbm_gbs": round(hbm_bytes / ms / 1e6, 1),
+                     "frac_of_peak": round(hbm_bytes / ms / 1e6 / peak, 4)}
+    return out
 
 
 def run_e2e(args, ug, host_shard, n16, G, rank, dev, dist):

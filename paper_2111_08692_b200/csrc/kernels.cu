@@ -173,6 +173,7 @@ struct U8Pol {
     bool wasc, interior;
   };
 
+  template <bool IN>  // IN: the whole tile is owned (tile-uniform)
   __device__ static __forceinline__ uint32_t analyze(St &s, const uint8_t *buf, int tid,
                                                      int lane, long long tp, long long n,
                                                      bool xc) {
@@ -190,7 +191,7 @@ struct U8Pol {
     s.w[8] = nxt;
     s.prev = prev;
     s.pos0 = tp + BPT * tid;
-    s.interior = (tp >= 0) && (tp + TILE <= n);
+    s.interior = IN;
     // a2: warp ASCII fast path (no byte >= 0x80 and no pending lead before the warp)
     uint32_t orv = s.w[0] | s.w[1] | s.w[2] | s.w[3] | s.w[4] | s.w[5] | s.w[6] | s.w[7];
     bool pend = (prev >= 0xC0000000u) || ((prev & 0x00FF0000u) >= 0x00E00000u) ||
@@ -216,7 +217,7 @@ struct U8Pol {
     }
     uint32_t cnt = 0;
     if (xc) {
-      if (!s.interior) {
+      if (!IN) {
 #pragma unroll
         for (int k = 0; k < 8; k++) s.cm[k] &= range_bytes(s.pos0 + 4 * k, 0, n) & u8::HI;
       }
@@ -339,6 +340,17 @@ struct U8Pol {
 
 // ============================================================================ UTF-16 policy
 // Positions are words.  Thread `tid` owns tile words [16 tid, 16 tid + 16), two per register.
+// Position of the first set lane bit among 8 registers of lane masks (cold path).
+__device__ __noinline__ unsigned long long first_error_lane(uint32_t e0, uint32_t e1, uint32_t e2,
+                                                            uint32_t e3, uint32_t e4, uint32_t e5,
+                                                            uint32_t e6, uint32_t e7,
+                                                            long long pos0) {
+  const uint32_t e[8] = {e0, e1, e2, e3, e4, e5, e6, e7};
+  for (int k = 0; k < 8; k++)
+    if (e[k]) return (unsigned long long)(pos0 + 2 * k + ((e[k] & 0x8000u) ? 0 : 1));
+  return NONE;
+}
+
 struct U16Pol {
   using Out = uint8_t;
   static constexpr int UNIT = 2;
@@ -352,6 +364,7 @@ struct U16Pol {
     bool wasc, interior;
   };
 
+  template <bool IN>  // IN: the whole tile is owned (tile-uniform)
   __device__ static __forceinline__ uint32_t analyze(St &s, const uint8_t *buf, int tid,
                                                      int lane, long long tp_bytes, long long n_bytes,
                                                      bool xc) {
@@ -370,12 +383,12 @@ struct U16Pol {
     s.prev_word = pv >> 16;
     s.next_word = nx & 0xFFFFu;
     s.pos0 = tpw + (BPT / 2) * tid;
-    s.interior = (tpw >= 0) && (tpw + TILE / 2 <= nw);
+    s.interior = IN;
     uint32_t orv = 0;
 #pragma unroll
     for (int k = 0; k < 8; k++) {
       orv |= s.w[k];
-      if (s.interior) {
+      if (IN) {
         s.own[k] = u16::LANE_TOP;
       } else {
         const long long pos = s.pos0 + 2 * k;
@@ -399,10 +412,10 @@ struct U16Pol {
       uint32_t e = (c.H & ~Ln) | (c.L & ~Hp);
       if (xc) {
         uint32_t wl = 0x00010001u + ((~c.A & u16::LANE_TOP) >> 15) + (u16::three2(c, Hp) >> 15);
-        if (!s.interior) wl &= (s.own[k] >> 15) * 0xFFFFu;
+        if (!IN) wl &= (s.own[k] >> 15) * 0xFFFFu;
         lanes += wl;
       }
-      if (!s.interior) e &= s.own[k];
+      if (!IN) e &= s.own[k];
       errm[k] = e;
       anyerr |= e;
       Hprev = c.H;
@@ -410,12 +423,9 @@ struct U16Pol {
     }
     const uint32_t cnt = (lanes & 0xFFFFu) + (lanes >> 16);
     s.first_err = NONE;
-    if (anyerr) {  // cold: first erroneous lane
-#pragma unroll
-      for (int k = 7; k >= 0; k--) {
-        if (errm[k]) s.first_err = (unsigned long long)(s.pos0 + 2 * k + ((errm[k] & 0x8000u) ? 0 : 1));
-      }
-    }
+    if (anyerr)  // cold
+      s.first_err = first_error_lane(errm[0], errm[1], errm[2], errm[3], errm[4], errm[5],
+                                     errm[6], errm[7], s.pos0);
     return xc ? cnt : 0u;
   }
 
@@ -573,7 +583,11 @@ __global__ void __launch_bounds__(NT, 2) k_validate(const TileArgs a) {
     fix_tile_edges(win, t, buf, NT);
     __syncthreads();
     typename Pol::St st;
-    Pol::analyze(st, buf, tid, lane, tile_pos(win, t), win.n, false);
+    const long long tp = tile_pos(win, t);
+    if (tp >= 0 && tp + TILE <= win.n)
+      Pol::template analyze<true>(st, buf, tid, lane, tp, win.n, false);
+    else
+      Pol::template analyze<false>(st, buf, tid, lane, tp, win.n, false);
     if (Pol::hint(st)) s_flag = 1;
     __syncthreads();
     if (s_flag) {
@@ -658,7 +672,10 @@ __global__ void __launch_bounds__(NT + 32, 2) k_transcode(const TileArgs a) {
       named_sync<BAR_DATA, NT>();
 
       typename Pol::St st;
-      const uint32_t cnt = Pol::analyze(st, buf, tid, lane, tile_pos(win, t), win.n, true);
+      const long long tp = tile_pos(win, t);
+      const uint32_t cnt = (tp >= 0 && tp + TILE <= win.n)
+                               ? Pol::template analyze<true>(st, buf, tid, lane, tp, win.n, true)
+                               : Pol::template analyze<false>(st, buf, tid, lane, tp, win.n, true);
       if (Pol::hint(st)) s_flag = 1;
       uint32_t excl = 0, C = 0;
       block_scan(cnt, s_wsum, lane, warp, &excl, &C);
@@ -763,6 +780,16 @@ __global__ void __launch_bounds__(NT) k_len8(const uint8_t *in, unsigned long lo
   finish_reduction(sum, ctr, d_len);
 }
 
+// Two words per op: per 16-bit lane 1 + [u >= 0x80] + [u >= 0x800 and not a surrogate] (a
+// surrogate counts 2, so a pair counts 4), accumulated per lane and folded per uint4.
+__device__ __forceinline__ uint32_t len16_lanes(uint32_t r) {
+  const uint32_t lo15 = r & 0x7FFF7FFFu;
+  const uint32_t ge80 = ((lo15 + 0x7F807F80u) | r) & u16::LANE_TOP;
+  const uint32_t ge800 = ((lo15 + 0x78007800u) | r) & u16::LANE_TOP;
+  const uint32_t sur = u16::zero_lanes((r & 0xF800F800u) ^ 0xD800D800u);
+  return ((ge80 >> 15) + ((ge800 & ~sur) >> 15));  // per lane 0..2 (bits 0-1, 16-17)
+}
+
 __global__ void __launch_bounds__(NT) k_len16(const uint16_t *in, unsigned long long n,
                                               Counters *ctr, unsigned long long *d_len) {
   const uintptr_t addr = (uintptr_t)in;
@@ -772,19 +799,19 @@ __global__ void __launch_bounds__(NT) k_len16(const uint16_t *in, unsigned long 
   const unsigned long long nb = (n - head) / 8;
   const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
   unsigned long long sum = 0;
-  auto pair = [](uint32_t x) { return len16_word(x & 0xFFFFu) + len16_word(x >> 16); };
+  auto quad = [](const uint4 &v) {
+    const uint32_t l = len16_lanes(v.x) + len16_lanes(v.y) + len16_lanes(v.z) + len16_lanes(v.w);
+    return 8u + (l & 0xFFFFu) + (l >> 16);
+  };
   unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
   for (; i + 3 * stride < nb; i += 4 * stride) {
     uint4 v[4];
 #pragma unroll
     for (int j = 0; j < 4; j++) v[j] = __ldcs(body + i + j * stride);
 #pragma unroll
-    for (int j = 0; j < 4; j++) sum += pair(v[j].x) + pair(v[j].y) + pair(v[j].z) + pair(v[j].w);
+    for (int j = 0; j < 4; j++) sum += quad(v[j]);
   }
-  for (; i < nb; i += stride) {
-    uint4 v = __ldcs(body + i);
-    sum += pair(v.x) + pair(v.y) + pair(v.z) + pair(v.w);
-  }
+  for (; i < nb; i += stride) sum += quad(__ldcs(body + i));
   if (blockIdx.x == 0) {
     for (unsigned long long j = threadIdx.x; j < head; j += blockDim.x) sum += len16_word(in[j]);
     for (unsigned long long j = head + nb * 8 + threadIdx.x; j < n; j += blockDim.x)
