@@ -492,4 +492,8 @@ void ug_release_workspaces(void) {
 
 int ug_abi_version(void) { return UNIGPU_ABI_VERSION; }
 
+#ifdef UG_TRACE
+cudaError_t ug_trace_read_impl(void *host, size_t bytes);
+int ug_debug_trace(void *host, size_t bytes) { return (int)ug::trace_read(host, bytes); }
+#endif
 }  // extern "C"

@@ -15,7 +15,10 @@ constexpr uint64_t NONE = ~0ull;
 constexpr int NT = 512;           // threads per CTA for the tile kernels
 constexpr int TILE = 16384;       // input bytes per tile (16 Ki UTF-8 bytes / 8 Ki UTF-16 words)
 constexpr int BPT = TILE / NT;    // 32 contiguous input bytes per thread
-constexpr int LB_PER_LANE = 8;    // look-back window: 32 lanes x 8 status words = 256 tiles
+#ifndef UG_LB_PER_LANE
+#define UG_LB_PER_LANE 8
+#endif
+constexpr int LB_PER_LANE = UG_LB_PER_LANE;  // look-back window: 32 lanes x 8 = 256 tiles
 constexpr int HALO = 16;          // bytes of context loaded before and after each tile
 constexpr int INBUF = TILE + 2 * HALO;
 
@@ -187,11 +190,15 @@ __device__ __forceinline__ void fix_tile_edges(const Window &w, long long t, uin
 // exclusive prefix (sum of all earlier tiles' aggregates) in every lane.  Each round reads a
 // window of 256 predecessors (8 per lane, nearest first) with independent relaxed loads, so the
 // PREFIX frontier advances 256 tiles per L2 round trip (K2).
+#ifdef UG_TRACE
+__device__ int g_rounds_dummy;
+#endif
 __device__ __forceinline__ uint64_t look_back(uint64_t *status, uint32_t epoch, long long t,
-                                              int lane) {
+                                              int lane, int *rounds = nullptr) {
   uint64_t excl = 0;
   long long idx = t - 1;
   while (true) {
+    if (rounds) ++*rounds;
     const long long j0 = idx - (long long)LB_PER_LANE * lane;  // nearest tile of this lane
     uint64_t s[LB_PER_LANE];
 #pragma unroll

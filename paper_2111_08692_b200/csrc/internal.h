@@ -57,4 +57,7 @@ cudaError_t launch_combine(const RecordDev *recs, int nranks, int rank,
 void combine_host(const RecordDev *recs, int nranks, int rank, unsigned long long total_in,
                   ResultDev *res, unsigned long long *out_off);
 
+#ifdef UG_TRACE
+cudaError_t trace_read(void *host, size_t bytes);
+#endif
 }  // namespace ug

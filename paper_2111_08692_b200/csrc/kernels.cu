@@ -26,6 +26,17 @@
 
 namespace ug {
 
+#ifdef UG_TRACE
+// Debug trace (tools only): per CTA, per iteration: [tile, lb_start, lb_end, rounds, pwait_start, pwait_end]
+constexpr int TR_IT = 64;
+__device__ unsigned long long g_trace[1024][TR_IT][6];
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#endif
+
 constexpr unsigned long long VALMASK = (1ull << 38) - 1;
 // named barrier ids (0 is __syncthreads)
 constexpr int BAR_DATA = 1;           // the NT data threads
@@ -105,18 +116,14 @@ __device__ __forceinline__ void block_scan(uint32_t cnt, uint32_t *s_wsum, int l
   *excl = wincl - __shfl_sync(FULL, incl, 31) + incl - cnt;
 }
 
-// Publish tile t's aggregate, look back, publish its inclusive prefix; one full warp.
+// Look back for tile t (its aggregate C already published by the data warps) and publish its
+// inclusive prefix; one full warp.  Returns the exclusive prefix.
 __device__ __forceinline__ unsigned long long tile_prefix(const TileArgs &a, long long t,
-                                                          uint32_t C, int lane) {
-  unsigned long long P;
-  if (t == 0) {
-    P = 0;
-    if (lane == 0) st_relaxed(a.status, pack_status(a.epoch, FLAG_PREFIX, C));
-  } else {
-    if (lane == 0) st_relaxed(a.status + t, pack_status(a.epoch, FLAG_AGG, C));
-    P = look_back(a.status, a.epoch, t, lane);
-    if (lane == 0) st_relaxed(a.status + t, pack_status(a.epoch, FLAG_PREFIX, P + C));
-  }
+                                                          uint32_t C, int lane,
+                                                          int *rounds = nullptr) {
+  if (t == 0) return 0;  // tile 0 published its prefix with its aggregate
+  const unsigned long long P = look_back(a.status, a.epoch, t, lane, rounds);
+  if (lane == 0) st_relaxed(a.status + t, pack_status(a.epoch, FLAG_PREFIX, P + C));
   return P;
 }
 
@@ -160,16 +167,28 @@ __device__ __forceinline__ void write_outcome(const TileArgs &a, bool xc, int ki
 
 // ============================================================================ UTF-8 policy
 // Positions are bytes.  Thread `tid` owns tile bytes [32 tid, 32 tid + 32).
+// Bit i of a chunk mask = position pos0 + i.
+__device__ __forceinline__ uint32_t bit_range(long long pos0, long long lo, long long hi) {
+  long long a = lo - pos0, b = hi - pos0;
+  a = a < 0 ? 0 : (a > 32 ? 32 : a);
+  b = b < 0 ? 0 : (b > 32 ? 32 : b);
+  if (b <= a) return 0u;
+  const uint32_t mb = b == 32 ? 0xFFFFFFFFu : ((1u << b) - 1u);
+  const uint32_t ma = a == 32 ? 0xFFFFFFFFu : ((1u << a) - 1u);
+  return mb & ~ma;
+}
+
 struct U8Pol {
   using Out = uint16_t;
   static constexpr int UNIT = 1;                      // input bytes per position
   static constexpr int STAGE = 2 * (TILE + 32);        // stage bytes per buffer
   struct St {
-    uint32_t w[9];   // own 32 bytes + the next 4
+    uint32_t w[8];   // own 32 bytes
     uint32_t prev;   // the 4 bytes before
-    uint32_t cm[8];  // width bits (a5)
+    uint32_t nxt;    // the 4 bytes after
     uint32_t err;    // classifier flags (a3)
     long long pos0;  // position of own byte 0
+    long long n;
     bool wasc, interior;
   };
 
@@ -188,46 +207,22 @@ struct U8Pol {
     uint32_t nxt = __shfl_down_sync(FULL, s.w[0], 1);
     if (lane == 0) prev = *reinterpret_cast<const uint32_t *>(my - 4);
     if (lane == 31) nxt = *reinterpret_cast<const uint32_t *>(my + BPT);
-    s.w[8] = nxt;
     s.prev = prev;
+    s.nxt = nxt;
     s.pos0 = tp + BPT * tid;
+    s.n = n;
     s.interior = IN;
     // a2: warp ASCII fast path (no byte >= 0x80 and no pending lead before the warp)
     uint32_t orv = s.w[0] | s.w[1] | s.w[2] | s.w[3] | s.w[4] | s.w[5] | s.w[6] | s.w[7];
     bool pend = (prev >= 0xC0000000u) || ((prev & 0x00FF0000u) >= 0x00E00000u) ||
                 ((prev & 0x0000FF00u) >= 0x0000F000u);
-    s.wasc = __all_sync(FULL, ((orv & u8::HI) == 0u) && !pend);
+    s.wasc = __all_sync(FULL, ((orv & HI) == 0u) && !pend);
+    uint32_t emit = 0xFFFFFFFFu;
     s.err = 0;
-    if (s.wasc) {
-#pragma unroll
-      for (int k = 0; k < 8; k++) s.cm[k] = u8::HI;
-    } else {
-      // a3 classification + a5 widths
-      u8::WordMasks pm = u8::masks(prev, true);
-      u8::WordMasks cur = u8::masks(s.w[0], true);
-#pragma unroll
-      for (int k = 0; k < 8; k++) {
-        u8::WordMasks nx = u8::masks(s.w[k + 1], true);
-        s.err |= u8::classify(pm, cur);
-        s.cm[k] = xc ? u8::emit_bits(pm, cur) : 0u;
-        pm = cur;
-        cur = nx;
-      }
-      if (tid == NT - 1) s.err |= u8::classify(pm, cur);  // look-ahead positions TILE..TILE+3
-    }
-    uint32_t cnt = 0;
-    if (xc) {
-      if (!IN) {
-#pragma unroll
-        for (int k = 0; k < 8; k++) s.cm[k] &= range_bytes(s.pos0 + 4 * k, 0, n) & u8::HI;
-      }
-      // emit bits are byte msbs: sum the 8 words bytewise (<= 8 per byte), then fold the bytes
-      uint32_t acc = 0;
-#pragma unroll
-      for (int k = 0; k < 8; k++) acc += s.cm[k] >> 7;
-      cnt = (acc * 0x01010101u) >> 24;
-    }
-    return cnt;
+    if (!s.wasc) s.err = u8::analyze32(s.w, prev, nxt, tid == NT - 1, &emit);  // a3, a5
+    if (!xc) return 0u;
+    if (!IN) emit &= bit_range(s.pos0, 0, n);
+    return popc(emit);
   }
 
   __device__ static __forceinline__ bool hint(const St &s) { return s.err != 0; }
@@ -238,11 +233,12 @@ struct U8Pol {
 #pragma unroll
     for (int k = 0; k < 8; k++) {
       const uint32_t wb = k ? s.w[k - 1] : s.prev;
+      const uint32_t wn = k < 7 ? s.w[k + 1] : s.nxt;
 #pragma unroll
       for (int j = 0; j < 4; j++) {
         const long long pos = s.pos0 + 4 * k + j;
-        const uint32_t back = __funnelshift_r(wb, s.w[k], 8 * j);
-        const uint32_t fwd = __funnelshift_r(s.w[k], s.w[k + 1], 8 * j);
+        const uint32_t back = fsr(wb, s.w[k], 8 * j);
+        const uint32_t fwd = fsr(s.w[k], wn, 8 * j);
         if (found == NONE && pos >= 0 && pos < n && u8::err_at(back, fwd))
           found = (unsigned long long)pos;
       }
@@ -250,16 +246,21 @@ struct U8Pol {
     return found;
   }
 
-  // a7: decode the owned characters into stage[o ...] (UTF-16 units)
+  // a7: decode the owned characters into stage[o ...] (UTF-16 units).  Every position stores
+  // its unit at its exclusive-prefix slot; a non-emitting position's store lands on the slot of
+  // the next emitting one and is overwritten by it (program order).  Only the last word
+  // predicates, so nothing spills into the next thread's first slot (a character ends at most
+  // 3 positions after a non-emitting position of it).
+  template <bool IN>
   __device__ static __forceinline__ void decode(const St &s, uint16_t *stage, uint32_t o,
-                                                uint32_t lim) {
-    if (s.wasc && s.interior) {
+                                                uint32_t, long long) {
+    if (IN && s.wasc) {
       if ((o & 1u) == 0u) {
         uint32_t *st32 = reinterpret_cast<uint32_t *>(stage + o);
 #pragma unroll
         for (int k = 0; k < 8; k++) {
-          st32[2 * k] = u8::prmt(s.w[k], 0u, 0x4140u);
-          st32[2 * k + 1] = u8::prmt(s.w[k], 0u, 0x4342u);
+          st32[2 * k] = prmt(s.w[k], 0u, 0x4140u);
+          st32[2 * k + 1] = prmt(s.w[k], 0u, 0x4342u);
         }
       } else {
 #pragma unroll
@@ -269,48 +270,26 @@ struct U8Pol {
       }
       return;
     }
-    // SWAR decode: one candidate unit per position (two per op).  Every position stores its
-    // unit at its exclusive-prefix slot; a non-emitting position's store lands on the slot of
-    // the next emitting one and is overwritten by it (program order).  Only the last word
-    // predicates, so nothing spills into the next thread's first slot.
-    uint32_t cc = s.w[0] & 0x3F3F3F3Fu;
-    uint32_t cn = s.w[1] & 0x3F3F3F3Fu;
-    uint32_t pe = u8::payload_even(cc);
-    uint32_t po = u8::payload_odd(cc, cn);
-    uint32_t fprev = s.prev & (s.prev << 1) & (s.prev << 2) & (s.prev << 3) & u8::HI;
+    u8::Carry cy = u8::carry_of(s.prev);
+    uint16_t *st = stage + o;
 #pragma unroll
     for (int k = 0; k < 8; k++) {
-      const uint32_t x = s.w[k];
-      const uint32_t cnn = (k < 7) ? (s.w[k + 2] & 0x3F3F3F3Fu) : 0u;
-      const uint32_t pe_n = u8::payload_even(cn);
-      const uint32_t pe2 = u8::prmt(pe, pe_n, 0x5432u);
-      const uint32_t s1 = x << 1;
-      const uint32_t K = x & ~s1 & u8::HI;
-      const uint32_t L = x & s1 & u8::HI;
-      const uint32_t E = L & (x << 2);
-      const uint32_t F = E & (x << 3);
-      const uint32_t LO = K & __funnelshift_l(fprev, F, 8);
-      uint32_t ue, uo;
-      u8::units4(x, pe, po, pe2, L, E, F, LO, &ue, &uo);
-      const uint32_t em = s.cm[k];
+      uint32_t u01, u23;
+      uint32_t em = u8::units4(s.w[k], cy, &u01, &u23);
+      if (!IN) em &= range_bytes(s.pos0 + 4 * k, 0, s.n) & HI;
       const uint32_t inc = (em >> 7) * 0x01010101u;  // byte j: units emitted by positions <= j
-      uint16_t *st = stage + o;
       if (k < 7) {
-        st[0] = (uint16_t)ue;
-        st[inc & 0xFFu] = (uint16_t)uo;
-        st[(inc >> 8) & 0xFFu] = (uint16_t)(ue >> 16);
-        st[(inc >> 16) & 0xFFu] = (uint16_t)(uo >> 16);
+        st[0] = (uint16_t)u01;
+        st[inc & 0xFFu] = (uint16_t)(u01 >> 16);
+        st[(inc >> 8) & 0xFFu] = (uint16_t)u23;
+        st[(inc >> 16) & 0xFFu] = (uint16_t)(u23 >> 16);
       } else {
-        if (em & 0x00000080u) st[0] = (uint16_t)ue;
-        if (em & 0x00008000u) st[inc & 0xFFu] = (uint16_t)uo;
-        if (em & 0x00800000u) st[(inc >> 8) & 0xFFu] = (uint16_t)(ue >> 16);
-        if (em & 0x80000000u) st[(inc >> 16) & 0xFFu] = (uint16_t)(uo >> 16);
+        if (em & 0x00000080u) st[0] = (uint16_t)u01;
+        if (em & 0x00008000u) st[inc & 0xFFu] = (uint16_t)(u01 >> 16);
+        if (em & 0x00800000u) st[(inc >> 8) & 0xFFu] = (uint16_t)u23;
+        if (em & 0x80000000u) st[(inc >> 16) & 0xFFu] = (uint16_t)(u23 >> 16);
       }
-      o += inc >> 24;
-      fprev = F;
-      pe = pe_n;
-      po = u8::payload_odd(cn, cnn);
-      cn = cnn;
+      st += inc >> 24;
     }
   }
 
@@ -330,10 +309,9 @@ struct U8Pol {
     long long from = te * TILE - win.lead;
     if (from < 0) from = 0;
     unsigned long long c = 0;
-    for (long long i = from + lane; i < (long long)e; i += 32) {
-      uint32_t bi = byte_at(win, i), bp = byte_at(win, i - 1);
-      c += ((bi & 0xC0u) != 0x80u || bp >= 0xF0u) ? 1u : 0u;
-    }
+    for (long long i = from + lane; i < (long long)e; i += 32)
+      c += u8::emits_at(byte_at(win, i), byte_at(win, i - 1), byte_at(win, i - 2),
+                        byte_at(win, i - 3));
     *wr = base + warp_sum64(c);
   }
 };
@@ -437,13 +415,14 @@ struct U16Pol {
   // a7: encode the owned words into stage[o ...] (UTF-8 bytes).  Every word stores 3 bytes at
   // its offset; bytes past its width are overwritten by the following words (program order);
   // stores are clipped at the thread's end slot `lim`.
+  template <bool IN>
   __device__ static __forceinline__ void decode(const St &s, uint8_t *stage, uint32_t o,
                                                 uint32_t lim, long long) {
-    if (s.wasc && s.interior) {
+    if (IN && s.wasc) {
       if ((o & 3u) == 0u) {
         uint32_t *st32 = reinterpret_cast<uint32_t *>(stage + o);
 #pragma unroll
-        for (int k = 0; k < 4; k++) st32[k] = u8::prmt(s.w[2 * k], s.w[2 * k + 1], 0x6420u);
+        for (int k = 0; k < 4; k++) st32[k] = prmt(s.w[2 * k], s.w[2 * k + 1], 0x6420u);
       } else {
 #pragma unroll
         for (int i = 0; i < 16; i++) stage[o + i] = (uint8_t)(s.w[i >> 1] >> (16 * (i & 1)));
@@ -461,7 +440,7 @@ struct U16Pol {
       uint32_t B0, B1, B2;
       u16::encode2(r, pl, c, Hp, &B0, &B1, &B2);
       uint32_t wl = 0x00010001u + ((~c.A & u16::LANE_TOP) >> 15) + (u16::three2(c, Hp) >> 15);
-      if (!s.interior) wl &= (s.own[k] >> 15) * 0xFFFFu;
+      if (!IN) wl &= (s.own[k] >> 15) * 0xFFFFu;
       const uint32_t wa = wl & 0xFFFFu, wb = wl >> 16;
       const uint32_t ob = o + wa;
       if (k < 7) {  // spill past a word is covered by the >= 2 owned words that follow it
@@ -502,20 +481,6 @@ struct U16Pol {
     *wr = base + warp_sum64(c);
   }
 };
-
-template <class Pol>
-__device__ __forceinline__ void pol_decode(const typename Pol::St &s, typename Pol::Out *stage,
-                                           uint32_t o, uint32_t lim, long long n_units);
-template <>
-__device__ __forceinline__ void pol_decode<U8Pol>(const U8Pol::St &s, uint16_t *stage,
-                                                  uint32_t o, uint32_t lim, long long) {
-  U8Pol::decode(s, stage, o, lim);
-}
-template <>
-__device__ __forceinline__ void pol_decode<U16Pol>(const U16Pol::St &s, uint8_t *stage,
-                                                   uint32_t o, uint32_t lim, long long nw) {
-  U16Pol::decode(s, stage, o, lim, nw);
-}
 
 // Last CTA to finish: outcome + counter reset.  n_units in input code units.
 template <class Pol>
@@ -645,7 +610,21 @@ __global__ void __launch_bounds__(NT + 32, 2) k_transcode(const TileArgs a) {
       if (i & 1) named_sync<BAR_C1, NT + 32>(); else named_sync<BAR_C0, NT + 32>();
       const long long t = s_tile[i & 1];
       if (t < 0) break;
+#ifdef UG_TRACE
+      unsigned long long t0 = gtime();
+      int rounds = 0;
+      const unsigned long long P = tile_prefix(a, t, s_cnt[i & 1], lane, &rounds);
+      if (lane == 0 && i < TR_IT && blockIdx.x < 1024) g_trace[blockIdx.x][i][3] = rounds;
+#else
       const unsigned long long P = tile_prefix(a, t, s_cnt[i & 1], lane);
+#endif
+#ifdef UG_TRACE
+      if (lane == 0 && i < TR_IT && blockIdx.x < 1024) {
+        g_trace[blockIdx.x][i][0] = t;
+        g_trace[blockIdx.x][i][1] = t0;
+        g_trace[blockIdx.x][i][2] = gtime();
+      }
+#endif
       if (lane == 0) s_pre[i & 1] = P;
       if (i & 1) named_arrive<BAR_P1, NT + 32>(); else named_arrive<BAR_P0, NT + 32>();
     }
@@ -673,13 +652,17 @@ __global__ void __launch_bounds__(NT + 32, 2) k_transcode(const TileArgs a) {
 
       typename Pol::St st;
       const long long tp = tile_pos(win, t);
-      const uint32_t cnt = (tp >= 0 && tp + TILE <= win.n)
+      const bool inner = tp >= 0 && tp + TILE <= win.n;  // tile-uniform
+      const uint32_t cnt = inner
                                ? Pol::template analyze<true>(st, buf, tid, lane, tp, win.n, true)
                                : Pol::template analyze<false>(st, buf, tid, lane, tp, win.n, true);
       if (Pol::hint(st)) s_flag = 1;
       uint32_t excl = 0, C = 0;
       block_scan(cnt, s_wsum, lane, warp, &excl, &C);
       if (tid == 0) {
+        // publish the tile aggregate at once (a6): successors' look-backs must not wait for
+        // this CTA's look-back warp to reach this tile
+        st_relaxed(a.status + t, pack_status(a.epoch, t == 0 ? FLAG_PREFIX : FLAG_AGG, C));
         s_tile[i & 1] = t;
         s_cnt[i & 1] = C;
       }
@@ -689,9 +672,21 @@ __global__ void __launch_bounds__(NT + 32, 2) k_transcode(const TileArgs a) {
         unsigned long long e = Pol::find_error(st, n_units);
         if (e != NONE) atomicMin(&s_emin, e);
       }
-      pol_decode<Pol>(st, stage0 + (i & 1) * SU, excl, excl + cnt, n_units);
+      if (inner)
+        Pol::template decode<true>(st, stage0 + (i & 1) * SU, excl, excl + cnt, n_units);
+      else
+        Pol::template decode<false>(st, stage0 + (i & 1) * SU, excl, excl + cnt, n_units);
       if (i > 0) {  // a8: copy out the previous tile once its prefix is known
+#ifdef UG_TRACE
+        unsigned long long w0 = gtime();
+#endif
         if ((i - 1) & 1) named_sync<BAR_P1, NT + 32>(); else named_sync<BAR_P0, NT + 32>();
+#ifdef UG_TRACE
+        if (tid == 0 && i - 1 < TR_IT && blockIdx.x < 1024) {
+          g_trace[blockIdx.x][i - 1][4] = w0;
+          g_trace[blockIdx.x][i - 1][5] = gtime();
+        }
+#endif
         copy_out<Out>(out, a.out_cap, s_pre[(i - 1) & 1], C_prev, stage0 + ((i - 1) & 1) * SU,
                       tid);
       }
@@ -716,8 +711,8 @@ __global__ void __launch_bounds__(NT + 32, 2) k_transcode(const TileArgs a) {
 // ============================================================================ length-from
 __device__ __forceinline__ uint32_t len8_word(uint32_t x) {
   uint32_t s1 = x << 1;
-  uint32_t cont = x & ~s1 & u8::HI;
-  uint32_t f0 = x & s1 & (x << 2) & (x << 3) & u8::HI;
+  uint32_t cont = x & ~s1 & HI;
+  uint32_t f0 = x & s1 & (x << 2) & (x << 3) & HI;
   return 4u - __popc(cont) + __popc(f0);
 }
 __device__ __forceinline__ uint32_t len8_byte(uint32_t b) {
@@ -871,6 +866,11 @@ void combine_host(const RecordDev *recs, int nranks, int rank, unsigned long lon
 }
 
 // ============================================================================ launchers
+#ifdef UG_TRACE
+cudaError_t trace_read(void *host, size_t bytes) {
+  return cudaMemcpyFromSymbol(host, g_trace, bytes < sizeof(g_trace) ? bytes : sizeof(g_trace));
+}
+#endif
 size_t tile_smem_bytes(Op op) {
   switch (op) {
     case Op::U8_VALIDATE:

@@ -1,193 +1,168 @@
-// utf8.cuh -- UTF-8 arithmetic of the hot path, SWAR over 32-bit words (4 bytes per op).
+// utf8.cuh -- UTF-8 arithmetic of the hot path (host-compilable: tools/emu_u8.cpp).
 //
-//  * classify(): the validation classifier.  Six value rules (plus the C0/C1
-//    and F5..FF leads that can only fail them) come from three 16-entry nibble tables keyed by
-//    hi(prev1), lo(prev1), hi(cur) and AND-ed (the "three-nibble lookup-table classification"
-//    of BASELINE north_star; PAPER.md:98 cites Keiser-Lemire for it).  The tables live in
-//    REGISTERS and are read with PRMT (one byte permute = four 8-entry lookups).  The
-//    structural rules (too short, too long) and the continuation-count check
-//    are plain LOP3 bit logic.  Derivation and its brute-force check: DESIGN.md D3,
-//    tests/test_derivations.py.  A position flags iff the input is invalid, and the first
-//    flagged position r satisfies e <= r <= e+3 for the first error e.
-//  * widths: units a position emits in UTF-16: 1 per non-continuation
-//    byte, and 1 for a continuation byte that directly follows a byte >= F0 (it emits the
-//    surrogate pair's second unit).  Exactly 0 or 1 unit per input byte on ANY input, so
-//    out_cap = n is always safe, and every position is a fixed-size slot.
-//  * decode(): code point assembly, and the UTF-16 encoding of PAPER.md:87.
-//  * err_at(): the exact local first-error predicate (D2), used only to rescan
-//    flagged tiles.
+// Two representations, each used where it is cheapest (D3/D4):
+//
+//  * VALIDATION on BIT PLANES.  A thread's 32 bytes are transposed (PRMT 4x4 byte transposes +
+//    three delta swaps) into eight 32-bit planes, P[b] bit i = bit b of byte i.  Every rule is
+//    then one LOP3/SHF per 32 positions:
+//      - structure (rules 2 and 3, plus the continuation count): with
+//        L = lead >= C0, E = lead >= E0, F = lead >= F0 and K = continuation byte, the bytes
+//        that must be continuations are R = S1(L) | S2(E) | S3(F) (Sd = shift by d positions,
+//        carrying the 3 bytes before the chunk); any position where R != K is in error;
+//      - value (rules 4-6 and the C0/C1, F5..FF leads): the lead bytes E0, F0
+//        need a second byte >= A0 / >= 90, ED, F4 need one < A0 / < 90, and C0, C1, F5..FF
+//        are always wrong; flagged at the lead, looking one byte ahead.
+//    A position flags iff the input is invalid there, and the first flagged position r obeys
+//    e <= r <= e + 3 for the first error e (e is the start of the offending sequence, DESIGN
+//    R1), so a tile that flags rescans its own positions with the exact predicate err_at().
+//  * TRANSCODING in BYTE-SWAR at END positions (4 positions per 32-bit op).  Each character
+//    emits its UTF-16 unit at its LAST byte e (a 4-byte character emits its high surrogate at
+//    its third byte and its low surrogate at its fourth), so every emitted unit is a function
+//    of bytes e-2..e only, and its low byte always has the same form:
+//      lb = (b[e-1] << 6 | b[e] & 0x3F) & 0xFF        (ASCII: b[e])
+//      hb = (b[e-1] & 0x3F) >> 2  |  (b[e-2] & 0xF) << 4 if b[e-2] >= E0   (ASCII: 0)
+//    (the code point is the concatenation of the payload bits, the
+//    surrogate pair).  The low surrogate is 0xDC00 | (G & 0x3FF) and the high surrogate
+//    0xD800 | ((G >> 4) - 0x40) of the same G = hb:lb.  Each position emits 0 or 1 unit on ANY
+//    input, so out_cap = n always suffices.
 #pragma once
 #include <cstdint>
 
+#include "swar.cuh"
+
 namespace ug {
 namespace u8 {
-
-constexpr uint32_t HI = 0x80808080u;
 
 // Kinds (same numbering as include/unigpu.h).
 enum { OK = 0, HEADER_BITS = 1, TOO_SHORT = 2, TOO_LONG = 3, OVERLONG = 4, TOO_LARGE = 5,
        SURROGATE = 6 };
 
-// Class bits: 0 overlong-2 (C0/C1 + cont), 1 overlong-3 (E0 80..9F), 2 surrogate (ED A0..BF),
-// 3 overlong-4 (F0 80..8F), 4 too-large (F4 90..BF), 5 too-large lead (F5..FF + cont).
-// T1 / T3 are indexed by (hi nibble ^ 8): 8..F -> entries 0..7, ASCII nibbles 0..7 -> PRMT
-// sign mode on bytes whose msb is 0 -> 0x00.  T2 (lo nibble) needs all 16 entries: two PRMTs,
-// the second with the selector's bit 3 flipped, OR-ed (each contributes 0x00 in sign mode).
-constexpr uint32_t T1_A = 0x00000000u;  // hi(prev1) 8,9,A,B
-constexpr uint32_t T1_B = 0x38060001u;  // hi(prev1) C,D,E,F
-constexpr uint32_t T2_0 = 0x0000010Bu;  // lo(prev1) 0..3
-constexpr uint32_t T2_1 = 0x20202010u;  // lo(prev1) 4..7
-constexpr uint32_t T2_2 = 0x20202020u;  // lo(prev1) 8..B
-constexpr uint32_t T2_3 = 0x20202420u;  // lo(prev1) C..F
-constexpr uint32_t T3_A = 0x3535332Bu;  // hi(cur) 8,9,A,B
-constexpr uint32_t T3_B = 0x00000000u;  // hi(cur) C..F
-
-__device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
-  uint32_t d;
-  asm("prmt.b32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(sel));
-  return d;
+// ---------------------------------------------------------------- bit planes
+// t_j = byte j of a, b, c, d (a 4x4 byte transpose, 8 PRMT).
+UG_HD void tr4(uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t &t0, uint32_t &t1,
+               uint32_t &t2, uint32_t &t3) {
+  const uint32_t ab0 = prmt(a, b, 0x5140u), ab1 = prmt(a, b, 0x7362u);
+  const uint32_t cd0 = prmt(c, d, 0x5140u), cd1 = prmt(c, d, 0x7362u);
+  t0 = prmt(ab0, cd0, 0x5410u);
+  t1 = prmt(ab0, cd0, 0x7632u);
+  t2 = prmt(ab1, cd1, 0x5410u);
+  t3 = prmt(ab1, cd1, 0x7632u);
 }
-// byte k of x -> nibble k of the result (low 16 bits), for the hi / lo nibbles of each byte
-__device__ __forceinline__ uint32_t sel_hi(uint32_t x) {
-  uint32_t z = (x >> 4) & 0x0F0F0F0Fu;
-  return prmt(z | (z >> 4), 0u, 0x4420u);
+// Exchange bit b (b & D set) of every byte of a with bit b - D of the same byte of c.
+template <int D>
+UG_HD void dswap(uint32_t &a, uint32_t &c) {
+  constexpr uint32_t M = D == 1 ? 0x55555555u : (D == 2 ? 0x33333333u : 0x0F0F0F0Fu);
+  const uint32_t t = ((a >> D) ^ c) & M;
+  c ^= t;
+  a ^= t << D;
 }
-__device__ __forceinline__ uint32_t sel_lo(uint32_t x) {
-  uint32_t z = x & 0x0F0F0F0Fu;
-  return prmt(z | (z >> 4), 0u, 0x4420u);
+// w[0..7] = 32 bytes (position 4r + k = byte k of w[r]) -> P[b] bit i = bit b of byte i.
+// R[r] gathers positions r, 8+r, 16+r, 24+r; the delta swaps then transpose every byte lane's
+// 8x8 (register, bit) matrix, so bit 8k + r of P[b] is bit b of position 8k + r.
+UG_HD void planes32(const uint32_t w[8], uint32_t P[8]) {
+  tr4(w[0], w[2], w[4], w[6], P[0], P[1], P[2], P[3]);
+  tr4(w[1], w[3], w[5], w[7], P[4], P[5], P[6], P[7]);
+  dswap<1>(P[0], P[1]); dswap<1>(P[2], P[3]); dswap<1>(P[4], P[5]); dswap<1>(P[6], P[7]);
+  dswap<2>(P[0], P[2]); dswap<2>(P[1], P[3]); dswap<2>(P[4], P[6]); dswap<2>(P[5], P[7]);
+  dswap<4>(P[0], P[4]); dswap<4>(P[1], P[5]); dswap<4>(P[2], P[6]); dswap<4>(P[3], P[7]);
 }
 
-// Per-word quantities carried from one word to the next.
-struct WordMasks {
-  uint32_t x;   // the bytes
-  uint32_t K;   // continuation bytes (10xxxxxx), msb per byte
-  uint32_t L;   // >= C0
-  uint32_t E;   // >= E0
-  uint32_t F;   // >= F0
-  uint32_t t1;  // T1[hi(byte)]
-  uint32_t t2;  // T2[lo(byte)]
-  uint32_t t3;  // T3[hi(byte)]
-};
+// msb-per-byte masks of a word: lead >= C0, >= E0, >= F0.
+UG_HD uint32_t lead_c0(uint32_t x) { return x & (x << 1) & HI; }
 
-__device__ __forceinline__ WordMasks masks(uint32_t x, bool tables) {
-  WordMasks m;
-  uint32_t s1 = x << 1, s2 = x << 2, s3 = x << 3;
-  m.x = x;
-  m.K = x & ~s1 & HI;
-  m.L = x & s1 & HI;
-  m.E = m.L & s2;
-  m.F = m.E & s3;
-  if (tables) {
-    uint32_t sh = sel_hi(x) ^ 0x8888u;
-    uint32_t sl = sel_lo(x);
-    m.t1 = prmt(T1_A, T1_B, sh);
-    m.t3 = prmt(T3_A, T3_B, sh);
-    m.t2 = prmt(T2_0, T2_1, sl) | prmt(T2_2, T2_3, sl ^ 0x8888u);
-  } else {
-    m.t1 = m.t2 = m.t3 = 0;
+// Carry words for the bit-plane shifts: bits 31, 30, 29 = the mask at positions -1, -2, -3
+// (bytes 3, 2, 1 of `prev`), from msb-per-byte form by one multiply (bit 23 -> 30, 15 -> 29).
+UG_HD uint32_t carry3(uint32_t msb_mask) { return msb_mask * 0x4081u; }
+
+// Validation of one 32-byte chunk (a3) and its emit mask (a5).
+//   w: the 32 bytes; prev: the 4 bytes before (byte 3 = position -1); nxt: the 4 bytes after.
+//   Returns the error flags (bit i = position i; nonzero iff some position flags).
+//   *emit: bit i set iff position i emits a UTF-16 unit (end-position rule above).
+//   tail: also flag continuation bytes missing at positions 32..34 (the last chunk of a tile).
+UG_HD uint32_t analyze32(const uint32_t w[8], uint32_t prev, uint32_t nxt, bool tail,
+                         uint32_t *emit) {
+  uint32_t P[8];
+  planes32(w, P);
+  const uint32_t L = P[7] & P[6], E = L & P[5], F = E & P[4];
+  const uint32_t K = P[7] & ~P[6];
+  const uint32_t pL = lead_c0(prev), pE = pL & (prev << 2), pF = pE & (prev << 3);
+  const uint32_t cL = carry3(pL), cE = carry3(pE), cF = carry3(pF);
+  const uint32_t S2E = fsl(cE, E, 2), S3F = fsl(cF, F, 3);
+  // structure: required continuations == continuation bytes
+  uint32_t err = (fsl(cL, L, 1) | S2E | S3F) ^ K;
+  // values, at the lead, against the next byte's bits 5 and 4 (Q: next >= A0 after an E lead,
+  // next >= 90 after an F lead)
+  const uint32_t E3 = E & ~P[4], F3 = F & ~P[3];
+  const uint32_t Z3 = ~(P[3] | P[2] | P[1]);
+  const uint32_t T0 = Z3 & ~P[0] & (E3 | F3);                    // E0, F0: need Q
+  const uint32_t T1 = (P[3] & P[2] & ~P[1] & P[0] & E3) |         // ED
+                      (P[2] & ~P[1] & ~P[0] & F3);                // F4: need !Q
+  const uint32_t AE = (P[2] & (P[1] | P[0]) & F3) | (F & P[3]) |  // F5..F7, F8..FF
+                      (L & ~P[5] & ~P[4] & Z3);                   // C0, C1
+  const uint32_t N5 = fsr(P[5], nxt >> 5, 1), N4 = fsr(P[4], nxt >> 4, 1);
+  const uint32_t Q = N5 | (N4 & F);
+  err |= (T0 & ~Q) | (T1 & Q) | AE;
+  if (tail) {
+    // leads at positions 29..31 whose continuations (positions 32..34) are missing
+    const uint32_t Rt = (L >> 31) | (E >> 30) | (F >> 29);
+    const uint32_t Kn = nxt & ~(nxt << 1) & 0x00808080u;
+    const uint32_t Knb = ((Kn >> 7) & 1u) | ((Kn >> 14) & 2u) | ((Kn >> 21) & 4u);
+    if (Rt & ~Knb) err |= 0x80000000u;
   }
-  return m;
+  *emit = ~P[7] | fsl(cL & ~cE, L & ~E, 1) | S2E | S3F;
+  return err;
 }
 
-// Error bits (nonzero iff some position of word `c` flags) given the previous word `p`.
-__device__ __forceinline__ uint32_t classify(const WordMasks &p, const WordMasks &c) {
-  uint32_t p1 = __funnelshift_l(p.x, c.x, 8);     // byte i-1 for each byte i
-  uint32_t Kp1 = __funnelshift_l(p.K, c.K, 8);
-  uint32_t Lp1 = __funnelshift_l(p.L, c.L, 8);
-  uint32_t Ep2 = __funnelshift_l(p.E, c.E, 16);
-  uint32_t Fp3 = __funnelshift_l(p.F, c.F, 24);
-  // rule 2 (lead then non-continuation) | rule 3 (ASCII then continuation)
-  uint32_t structural = (Lp1 & ~c.K) | (c.K & ~p1);
-  // continuation-count check: the 2nd continuation of a 3/4-byte lead must follow exactly
-  // when prev2 >= E0 or prev3 >= F0
-  uint32_t count = (Kp1 & c.K) ^ (Ep2 | Fp3);
-  // value rules: T1[hi(prev1)] & T2[lo(prev1)] & T3[hi(cur)]
-  uint32_t t1 = __funnelshift_l(p.t1, c.t1, 8);
-  uint32_t t2 = __funnelshift_l(p.t2, c.t2, 8);
-  return structural | count | (t1 & t2 & c.t3);
+// ---------------------------------------------------------------- transcoding (a5, a7)
+// Carried from one word to the next: the previous word and its lead masks.
+struct Carry {
+  uint32_t x, L2, E, F;  // bytes; 2-byte leads (C0..DF); >= E0; >= F0  (msb per byte)
+};
+UG_HD Carry carry_of(uint32_t x) {
+  const uint32_t L = lead_c0(x), E = L & (x << 2);
+  return Carry{x, L & ~E, E, E & (x << 3)};
 }
 
-// Emit bits of word c (previous word p): msb of byte j set iff position j emits a UTF-16 unit
-// (a non-continuation byte, or a continuation byte right after a byte >= F0).
-__device__ __forceinline__ uint32_t emit_bits(const WordMasks &p, const WordMasks &c) {
-  uint32_t Fp1 = __funnelshift_l(p.F, c.F, 8);  // byte j-1 >= F0
-  return (~c.K & HI) | (c.K & Fp1);
-}
-
-// Decode the character whose lead is the low byte of x (bytes b0..b3 = x, little endian) and
-// encode it as UTF-16.  Returns the first unit; *u1 = second unit.
-__device__ __forceinline__ uint32_t decode_units(uint32_t x, uint32_t *u1) {
-  uint32_t b0 = x & 0xFFu;
-  uint32_t v2 = ((b0 & 0x1Fu) << 6) | ((x >> 8) & 0x3Fu);
-  uint32_t v3 = ((b0 & 0x0Fu) << 12) | ((x >> 2) & 0x0FC0u) | ((x >> 16) & 0x3Fu);
-  uint32_t cp = ((b0 & 0x07u) << 18) | ((x << 4) & 0x3F000u) | ((x >> 10) & 0x0FC0u) |
-                ((x >> 24) & 0x3Fu);
-  *u1 = 0xDC00u | (cp & 0x3FFu);
-  uint32_t hi = 0xD7C0u + (cp >> 10);
-  return b0 < 0x80u ? b0 : (b0 < 0xE0u ? v2 : (b0 < 0xF0u ? v3 : hi));
-}
-
-// ---------------------------------------------------------------- SWAR decode (a7)
-// Code-unit candidates for the 4 positions of word x (bytes b0..b3; b4.. from xn), two
-// positions per 32-bit op in 16-bit lanes: "even" lanes hold positions 0 and 2, "odd" lanes
-// positions 1 and 3.  With c_j = b_j & 0x3F and P(j) = c_j << 6 | c_{j+1}:
-//   ASCII      u = b_j
-//   2-byte     u = P(j)                                  (b_j & 0x3F has bit 5 clear)
-//   3-byte     u = (b_j & 0xF) << 12 | P(j+1)
-//   4-byte     hi = 0xD7C0 + ((b_j & 7) << 8 | P(j+1) >> 4),  lo = 0xDC00 | P(j+2)
-// Pe / Po are P at the even / odd positions of this word; Pe2 / Po2 the same two positions
-// later (they need the next word's P).
-__device__ __forceinline__ uint32_t pair_payload(uint32_t s) {
-  // s holds, per 16-bit lane, [c_{j+1}, c_j]; returns c_j << 6 | c_{j+1} per lane
-  return (s & 0x003F003Fu) | ((s >> 2) & 0x0FC00FC0u);
-}
-__device__ __forceinline__ uint32_t payload_even(uint32_t c) { return pair_payload(prmt(c, 0u, 0x2301u)); }
-__device__ __forceinline__ uint32_t payload_odd(uint32_t c, uint32_t cn) {
-  return pair_payload(prmt(c, cn, 0x3412u));
-}
-// per-16-bit-lane masks (0xFFFF) from per-byte top-bit masks, even / odd positions
-__device__ __forceinline__ uint32_t lanes_even(uint32_t m) { return prmt(m, 0u, 0xAA88u); }
-__device__ __forceinline__ uint32_t lanes_odd(uint32_t m) { return prmt(m, 0u, 0xBB99u); }
-__device__ __forceinline__ uint32_t mux(uint32_t m, uint32_t a, uint32_t b) {
-  return (a & m) | (b & ~m);
-}
-
-// The unit emitted at each of the 4 positions (ue: positions 0 and 2, uo: 1 and 3).  A
-// continuation byte right after a 4-byte lead emits the low surrogate 0xDC00 | P(i+1).
-// x: bytes of this word; Pe, Po: P at even / odd positions; Pe2: P at positions 2 and 4;
-// L/E/F: >= C0 / E0 / F0 top-bit masks; LO: continuation-after-F0 top-bit mask.
-__device__ __forceinline__ void units4(uint32_t x, uint32_t Pe, uint32_t Po, uint32_t Pe2,
-                                       uint32_t L, uint32_t E, uint32_t F, uint32_t LO,
-                                       uint32_t *ue, uint32_t *uo) {
-  const uint32_t asc_e = prmt(x, 0u, 0x4240u), asc_o = prmt(x, 0u, 0x4341u);
-  const uint32_t u3_e = ((x << 12) & 0xF000F000u) | Po;
-  const uint32_t u3_o = ((x << 4) & 0xF000F000u) | Pe2;
-  const uint32_t hi_e = (((x << 8) & 0x07000700u) | ((Po >> 4) & 0x00FF00FFu)) + 0xD7C0D7C0u;
-  const uint32_t hi_o = ((x & 0x07000700u) | ((Pe2 >> 4) & 0x00FF00FFu)) + 0xD7C0D7C0u;
-  uint32_t e = mux(lanes_even(L), Pe, asc_e);
-  e = mux(lanes_even(E), u3_e, e);
-  e = mux(lanes_even(F), hi_e, e);
-  *ue = mux(lanes_even(LO), Po | 0xDC00DC00u, e);  // 0xDC00 has bits 10-11 set
-  uint32_t o = mux(lanes_odd(L), Po, asc_o);
-  o = mux(lanes_odd(E), u3_o, o);
-  o = mux(lanes_odd(F), hi_o, o);
-  *uo = mux(lanes_odd(LO), Pe2 | 0xDC00DC00u, o);
+// The 4 positions of word x (previous word in c, updated): units of positions 0 / 1 in the
+// low / high half of *u01, positions 2 / 3 in *u23.  Returns the emit mask (msb per byte).
+// Units at non-emitting positions are garbage.
+UG_HD uint32_t units4(uint32_t x, Carry &c, uint32_t *u01, uint32_t *u23) {
+  const Carry n = carry_of(x);
+  const uint32_t bp1 = fsl(c.x, x, 8), bp2 = fsl(c.x, x, 16);  // bytes e-1, e-2
+  const uint32_t S1L2 = fsl(c.L2, n.L2, 8);                    // end of a 2-byte character
+  const uint32_t S2E = fsl(c.E, n.E, 16);                      // end of 3-byte / high surrogate
+  const uint32_t S2F = fsl(c.F, n.F, 16);                      // high surrogate
+  const uint32_t S3F = fsl(c.F, n.F, 24);                      // low surrogate
+  c = n;
+  const uint32_t em = (~x & HI) | S1L2 | S2E | S3F;
+  const uint32_t n7 = (x & HI) >> 7;   // 1 in every non-ASCII byte
+  const uint32_t f7 = S3F >> 7;        // 1 at low surrogates
+  uint32_t lb = mux(n7 * 0xC0u, bp1 << 6, x);
+  const uint32_t A1 = n7 * 15u - f7 * 12u;          // 0x0F, or 0x03 at a low surrogate
+  const uint32_t A2 = (S2E >> 7) * 0xF0u;
+  uint32_t hb = ((bp1 >> 2) & A1) | (f7 * 0xDCu) | ((bp2 << 4) & A2);
+  // high surrogate: G = hb:lb = cp >> 6, unit = 0xD800 | ((G >> 4) - 0x40)
+  const uint32_t Mh = (S2F >> 7) * 0xFFu;
+  const uint32_t hbm = (hb | HI) - 0x04040404u;     // per byte 0x80 + hb - 4, no borrows
+  lb = mux(Mh, mux(0xF0F0F0F0u, hbm << 4, lb >> 4), lb);
+  hb = mux(Mh, ((hbm >> 4) & 0x03030303u) | 0xD8D8D8D8u, hb);
+  *u01 = prmt(lb, hb, 0x5140u);
+  *u23 = prmt(lb, hb, 0x7362u);
+  return em;
 }
 
 // ---------------------------------------------------------------- exact (cold) path
-// All bytes are passed in registers (little-endian words): no local arrays.
-__device__ __forceinline__ uint32_t byte_of(uint32_t x, int k) { return (x >> (8 * k)) & 0xFFu; }
+UG_HD uint32_t byte_of(uint32_t x, int k) { return (x >> (8 * k)) & 0xFFu; }
 
 // Kind of the failure of a sequential decoder whose window is x = s[0..3] (rules in the order
 // of DESIGN.md R2); bytes past the end of the input are 0x00 (not continuation bytes).
-__device__ __forceinline__ int decode_kind(uint32_t x) {
+UG_HD int decode_kind(uint32_t x) {
   uint32_t b = x & 0xFFu;
   if (b < 0x80u) return OK;
   if (b < 0xC0u) return TOO_LONG;
   if (b >= 0xF8u) return HEADER_BITS;
   int L = b < 0xE0u ? 2 : (b < 0xF0u ? 3 : 4);
   uint32_t cp = b & (0x7Fu >> L);
-#pragma unroll
   for (int k = 1; k < 4; k++) {
     if (k < L) {
       uint32_t c = byte_of(x, k);
@@ -202,22 +177,27 @@ __device__ __forceinline__ int decode_kind(uint32_t x) {
   return OK;
 }
 
-__device__ __forceinline__ int declared_len(uint32_t b) {
+UG_HD int declared_len(uint32_t b) {
   return b < 0x80u ? 1 : (b < 0xC0u ? 0 : (b < 0xE0u ? 2 : (b < 0xF0u ? 3 : (b < 0xF8u ? 4 : 0))));
 }
 
 // Exact local predicate at position i (D2 / SURVEY.md C.4(i)): back = s[i-4..i-1],
 // fwd = s[i..i+3].  A(i): a non-continuation byte whose character fails to decode.  B(i): a
 // continuation byte with no lead within the 3 previous bytes that declares it.
-__device__ __forceinline__ bool err_at(uint32_t back, uint32_t fwd) {
+UG_HD bool err_at(uint32_t back, uint32_t fwd) {
   uint32_t c = fwd & 0xFFu;
   if ((c & 0xC0u) != 0x80u) return decode_kind(fwd) != OK;
-#pragma unroll
   for (int d = 1; d <= 3; d++) {
     uint32_t b = byte_of(back, 4 - d);
     if ((b & 0xC0u) != 0x80u) return !(declared_len(b) > d);
   }
   return true;
+}
+
+// Emission rule at position i from bytes i-3..i (the cold finalize count, same rule as units4).
+UG_HD uint32_t emits_at(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) {
+  // b0 = s[i], b1 = s[i-1], b2 = s[i-2], b3 = s[i-3]
+  return (b0 < 0x80u || (b1 >= 0xC0u && b1 < 0xE0u) || b2 >= 0xE0u || b3 >= 0xF0u) ? 1u : 0u;
 }
 
 }  // namespace u8

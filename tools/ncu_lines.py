@@ -12,6 +12,7 @@ import sys
 import tempfile
 
 rep, ksub, sidx, nbytes = sys.argv[1], sys.argv[2], int(sys.argv[3]), float(sys.argv[4])
+COL = os.environ.get("COL", "Instructions Executed")  # e.g. COL=stall_barrier
 lib = sys.argv[5] if len(sys.argv) > 5 else "paper_2111_08692_b200/libunigpu.so"
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=tmp, capture_output=True)
@@ -49,7 +50,7 @@ base = int(data[0][ix["Address"]], 16)
 agg = collections.Counter()
 tot = 0
 for r in data:
-    ex = float(r[ix["Instructions Executed"]] or 0)
+    ex = float(r[ix[COL]] or 0)
     tot += ex
     agg[lines.get(int(r[ix["Address"]], 16) - base, "?")] += ex
 src_cache = {}
