@@ -12,8 +12,8 @@ namespace ug {
 
 constexpr uint32_t FULL = 0xffffffffu;
 constexpr uint64_t NONE = ~0ull;
-constexpr int NT = 512;           // threads per CTA for the tile kernels
-constexpr int TILE = 16384;       // input bytes per tile (16 Ki UTF-8 bytes / 8 Ki UTF-16 words)
+constexpr int NT = 256;           // data threads per CTA for the tile kernels
+constexpr int TILE = 8192;        // input bytes per tile (8 Ki UTF-8 bytes / 4 Ki UTF-16 words)
 constexpr int BPT = TILE / NT;    // 32 contiguous input bytes per thread
 #ifndef UG_LB_PER_LANE
 #define UG_LB_PER_LANE 8
@@ -55,6 +55,9 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)),
                "r"(bytes)
                : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   asm volatile(
@@ -100,6 +103,10 @@ __device__ __forceinline__ uint64_t ld_relaxed(const uint64_t *p) {
 }
 __device__ __forceinline__ void st_relaxed(uint64_t *p, uint64_t v) {
   asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ void sts16(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((unsigned short)v) : "memory");
 }
 
 // ---------------------------------------------------------------- named barriers
@@ -170,6 +177,12 @@ __device__ __forceinline__ void issue_tile_load(const Window &w, long long t, ui
   if (bytes) bulk_g2s(buf + (a - A), (const void *)a, bytes, bar);
 }
 
+// Does tile t's smem image reach outside the valid window (needs fix_tile_edges)?
+__device__ __forceinline__ bool tile_at_edge(const Window &w, long long t) {
+  const long long p0 = tile_pos(w, t) - HALO;
+  return !(p0 >= w.lo_valid && p0 + INBUF <= w.hi_valid);
+}
+
 // After the load landed: zero every smem byte whose position lies outside the valid window
 // (only tiles touching the window edges do any work).  Called by threads 0..nthreads-1; the
 // caller syncs after.
@@ -190,50 +203,87 @@ __device__ __forceinline__ void fix_tile_edges(const Window &w, long long t, uin
 // exclusive prefix (sum of all earlier tiles' aggregates) in every lane.  Each round reads a
 // window of 256 predecessors (8 per lane, nearest first) with independent relaxed loads, so the
 // PREFIX frontier advances 256 tiles per L2 round trip (K2).
-#ifdef UG_TRACE
-__device__ int g_rounds_dummy;
-#endif
-__device__ __forceinline__ uint64_t look_back(uint64_t *status, uint32_t epoch, long long t,
-                                              int lane, int *rounds = nullptr) {
-  uint64_t excl = 0;
-  long long idx = t - 1;
+// One look-back round over K status words per lane: lane l examines tiles
+// idx - K*l, ..., idx - K*l - K + 1 (nearest first).  Waits (re-polling only the words that
+// are not yet published, with a back-off) until every word up to this lane's first inclusive
+// prefix is published; returns true and the prefix if some lane saw one, else adds the whole
+// window's aggregates to *excl.
+template <int K>
+__device__ __forceinline__ bool look_back_round(uint64_t *status, uint32_t epoch, long long idx,
+                                                int lane, uint64_t *excl, int *polls) {
+  const long long j0 = idx - (long long)K * lane;
+  uint64_t s[K];
+#pragma unroll
+  for (int k = 0; k < K; k++) s[k] = (j0 - k >= 0) ? ld_relaxed(status + j0 - k) : 0;
+  int spins = 0;
   while (true) {
-    if (rounds) ++*rounds;
-    const long long j0 = idx - (long long)LB_PER_LANE * lane;  // nearest tile of this lane
-    uint64_t s[LB_PER_LANE];
+    // ready: every word up to (and including) this lane's first PREFIX is published
+    bool ready = true, stop = false;
 #pragma unroll
-    for (int k = 0; k < LB_PER_LANE; k++) s[k] = (j0 - k >= 0) ? ld_relaxed(status + j0 - k) : 0;
-    // re-poll until every word this lane needs is at least an aggregate
-    int spins = 0;
-    while (true) {
-      bool ready = true;
-#pragma unroll
-      for (int k = 0; k < LB_PER_LANE; k++)
-        if (j0 - k >= 0 && !((uint32_t)(s[k] >> 40) == epoch && ((s[k] >> 38) & 3u) != 0))
-          ready = false;
-      if (ready) break;
-      if (++spins > 4) __nanosleep(20);
-#pragma unroll
-      for (int k = 0; k < LB_PER_LANE; k++)
-        if (j0 - k >= 0 && !((uint32_t)(s[k] >> 40) == epoch && ((s[k] >> 38) & 3u) != 0))
-          s[k] = ld_relaxed(status + j0 - k);
-    }
-    bool has_p = false;
-    uint64_t lane_sum = 0;
-#pragma unroll
-    for (int k = 0; k < LB_PER_LANE; k++) {
-      if (!has_p) {
-        bool pre = (j0 - k < 0) || (((s[k] >> 38) & 3u) == FLAG_PREFIX);
-        lane_sum += (j0 - k < 0) ? 0ull : (s[k] & ((1ull << 38) - 1));
-        has_p = pre;
+    for (int k = 0; k < K; k++) {
+      if (!stop && j0 - k >= 0) {
+        const bool pub = (uint32_t)(s[k] >> 40) == epoch && ((s[k] >> 38) & 3u) != 0;
+        if (!pub) ready = false;
+        if (pub && ((s[k] >> 38) & 3u) == FLAG_PREFIX) stop = true;
       }
     }
-    const uint32_t pm = __ballot_sync(FULL, has_p);
-    if (pm) {
-      const int first = __ffs(pm) - 1;
-      return excl + warp_sum64(lane <= first ? lane_sum : 0ull);
+    if (polls) ++*polls;
+    if (__all_sync(FULL, ready)) break;
+    __nanosleep(spins < 2 ? 64 : 256);
+    ++spins;
+    bool stop2 = false;
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+      if (!stop2 && j0 - k >= 0) {
+        const bool pub = (uint32_t)(s[k] >> 40) == epoch && ((s[k] >> 38) & 3u) != 0;
+        if (!pub) s[k] = ld_relaxed(status + j0 - k);
+        else if (((s[k] >> 38) & 3u) == FLAG_PREFIX) stop2 = true;
+      }
     }
-    excl += warp_sum64(lane_sum);
+  }
+  bool has_p = false;
+  uint64_t lane_sum = 0;
+#pragma unroll
+  for (int k = 0; k < K; k++) {
+    if (!has_p) {
+      bool pre = (j0 - k < 0) || (((s[k] >> 38) & 3u) == FLAG_PREFIX);
+      lane_sum += (j0 - k < 0) ? 0ull : (s[k] & ((1ull << 38) - 1));
+      has_p = pre;
+    }
+  }
+  const uint32_t pm = __ballot_sync(FULL, has_p);
+  if (pm) {
+    const int first = __ffs(pm) - 1;
+    *excl += warp_sum64(lane <= first ? lane_sum : 0ull);
+    return true;
+  }
+  *excl += warp_sum64(lane_sum);
+  return false;
+}
+
+// Exclusive prefix of tile t (t > 0): the sum of all earlier tiles' aggregates, from the
+// nearest inclusive prefix.  A first round probes only the 32 nearest predecessors (one
+// status word per lane), later rounds LB_PER_LANE per lane: the look-backs of all CTAs poll
+// L2 concurrently, so each round's request volume matters.
+__device__ __forceinline__ uint64_t look_back(uint64_t *status, uint32_t epoch, long long t,
+                                              int lane, int *rounds = nullptr,
+                                              unsigned long long *t_first = nullptr,
+                                              int *polls = nullptr) {
+  uint64_t excl = 0;
+  long long idx = t - 1;
+  if (rounds) ++*rounds;
+  if (look_back_round<1>(status, epoch, idx, lane, &excl, polls)) return excl;
+#ifdef UG_TRACE
+  if (t_first && *t_first == 0) {
+    unsigned long long tt;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tt));
+    *t_first = tt;
+  }
+#endif
+  idx -= 32;
+  while (true) {
+    if (rounds) ++*rounds;
+    if (look_back_round<LB_PER_LANE>(status, epoch, idx, lane, &excl, polls)) return excl;
     idx -= (long long)LB_PER_LANE * 32;
   }
 }

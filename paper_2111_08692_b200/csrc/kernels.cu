@@ -29,7 +29,7 @@ namespace ug {
 #ifdef UG_TRACE
 // Debug trace (tools only): per CTA, per iteration: [tile, lb_start, lb_end, rounds, pwait_start, pwait_end]
 constexpr int TR_IT = 64;
-__device__ unsigned long long g_trace[1024][TR_IT][6];
+__device__ unsigned long long g_trace[1024][TR_IT][8];
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -97,6 +97,35 @@ __device__ __forceinline__ void copy_out(T *out, unsigned long long cap, unsigne
   for (uint32_t c = tid; c < nfull; c += NT) dst[c] = shift_window(st[c], st[c + 1], q, r);
 }
 
+// One warp copies stage[lo, lo + cnt) to out[G, G + cnt), clipped at out[cap): 128-bit stores
+// for the 16-byte aligned interior (two 128-bit shared loads re-aligned by funnel shifts),
+// scalar head and tail.
+template <typename T>
+__device__ __forceinline__ void copy_out_warp(T *out, unsigned long long cap,
+                                              unsigned long long G, uint32_t lo, uint32_t cnt,
+                                              const T *stage, int lane) {
+  constexpr uint32_t A = 16 / sizeof(T);  // units per 16 bytes
+  unsigned long long hi = G + cnt;
+  if (hi > cap) hi = cap;
+  if (hi <= G) return;
+  const uint32_t Cc = (uint32_t)(hi - G);
+  const uint32_t mis = (uint32_t)(((uintptr_t)(out + G) & 15u) / sizeof(T));
+  const uint32_t s0 = mis ? A - mis : 0u;  // first unit landing on a 16-byte boundary
+  if (s0 >= Cc) {
+    if ((uint32_t)lane < Cc) out[G + lane] = stage[lo + lane];
+    return;
+  }
+  const uint32_t nfull = (Cc - s0) / A;
+  const uint32_t t0 = s0 + nfull * A;
+  if ((uint32_t)lane < s0) out[G + lane] = stage[lo + lane];
+  if ((uint32_t)lane < Cc - t0) out[G + t0 + lane] = stage[lo + t0 + lane];
+  const uint32_t sb = (lo + s0) * (uint32_t)sizeof(T);  // stage byte offset of chunk 0
+  const uint32_t q = (sb & 15u) >> 2, r = (sb & 3u) * 8u;
+  const uint4 *st = reinterpret_cast<const uint4 *>(stage) + (sb >> 4);
+  uint4 *dst = reinterpret_cast<uint4 *>(out + G + s0);
+  for (uint32_t c = lane; c < nfull; c += 32) dst[c] = shift_window(st[c], st[c + 1], q, r);
+}
+
 // Block exclusive scan over the NT data threads: returns the thread's exclusive prefix within
 // the tile and the tile total.  One data-warp barrier inside.
 __device__ __forceinline__ void block_scan(uint32_t cnt, uint32_t *s_wsum, int lane, int warp,
@@ -116,15 +145,14 @@ __device__ __forceinline__ void block_scan(uint32_t cnt, uint32_t *s_wsum, int l
   *excl = wincl - __shfl_sync(FULL, incl, 31) + incl - cnt;
 }
 
-// Look back for tile t (its aggregate C already published by the data warps) and publish its
-// inclusive prefix; one full warp.  Returns the exclusive prefix.
-__device__ __forceinline__ unsigned long long tile_prefix(const TileArgs &a, long long t,
-                                                          uint32_t C, int lane,
-                                                          int *rounds = nullptr) {
-  if (t == 0) return 0;  // tile 0 published its prefix with its aggregate
-  const unsigned long long P = look_back(a.status, a.epoch, t, lane, rounds);
-  if (lane == 0) st_relaxed(a.status + t, pack_status(a.epoch, FLAG_PREFIX, P + C));
-  return P;
+// Exclusive prefix of tile t (sum of all earlier tiles' aggregates); one full warp.  Needs only
+// the predecessors, so it runs while tile t itself is still being loaded and classified.
+__device__ __forceinline__ unsigned long long tile_excl_prefix(const TileArgs &a, long long t,
+                                                               int lane, int *rounds = nullptr,
+                                                               unsigned long long *t_first = nullptr,
+                                                               int *polls = nullptr) {
+  if (t == 0) return 0;
+  return look_back(a.status, a.epoch, t, lane, rounds, t_first, polls);
 }
 
 // Write the call's outcome (last CTA, lane 0) and reset the per-call counters.
@@ -189,13 +217,14 @@ struct U8Pol {
     uint32_t err;    // classifier flags (a3)
     long long pos0;  // position of own byte 0
     long long n;
-    bool wasc, interior;
+    bool wasc;
   };
 
-  template <bool IN>  // IN: the whole tile is owned (tile-uniform)
-  __device__ static __forceinline__ uint32_t analyze(St &s, const uint8_t *buf, int tid,
-                                                     int lane, long long tp, long long n,
-                                                     bool xc) {
+  // Thread tid's 32 bytes of the tile image in `buf` (plus the 4 before and after), its
+  // position, and the warp-uniform ASCII verdict (a2).
+  template <bool IN>
+  __device__ static __forceinline__ void load(St &s, const uint8_t *buf, int tid, int lane,
+                                              long long tp, long long n) {
     const uint8_t *my = buf + HALO + BPT * tid;
     {
       uint4 q0 = *reinterpret_cast<const uint4 *>(my);
@@ -211,17 +240,21 @@ struct U8Pol {
     s.nxt = nxt;
     s.pos0 = tp + BPT * tid;
     s.n = n;
-    s.interior = IN;
     // a2: warp ASCII fast path (no byte >= 0x80 and no pending lead before the warp)
     uint32_t orv = s.w[0] | s.w[1] | s.w[2] | s.w[3] | s.w[4] | s.w[5] | s.w[6] | s.w[7];
     bool pend = (prev >= 0xC0000000u) || ((prev & 0x00FF0000u) >= 0x00E00000u) ||
                 ((prev & 0x0000FF00u) >= 0x0000F000u);
     s.wasc = __all_sync(FULL, ((orv & HI) == 0u) && !pend);
+  }
+
+  // a3 classification (flags into s.err) and, if xc, the number of units the thread emits.
+  template <bool IN>  // IN: the whole tile is owned (tile-uniform)
+  __device__ static __forceinline__ uint32_t analyze(St &s, int tid, bool xc) {
     uint32_t emit = 0xFFFFFFFFu;
     s.err = 0;
-    if (!s.wasc) s.err = u8::analyze32(s.w, prev, nxt, tid == NT - 1, &emit);  // a3, a5
+    if (!s.wasc) s.err = u8::analyze32(s.w, s.prev, s.nxt, tid == NT - 1, &emit);  // a3, a5
     if (!xc) return 0u;
-    if (!IN) emit &= bit_range(s.pos0, 0, n);
+    if (!IN) emit &= bit_range(s.pos0, 0, s.n);
     return popc(emit);
   }
 
@@ -271,25 +304,29 @@ struct U8Pol {
       return;
     }
     u8::Carry cy = u8::carry_of(s.prev);
-    uint16_t *st = stage + o;
+    uint32_t p = smem_addr(stage + o);  // shared-window byte address of this thread's slot
 #pragma unroll
     for (int k = 0; k < 8; k++) {
       uint32_t u01, u23;
       uint32_t em = u8::units4(s.w[k], cy, &u01, &u23);
-      if (!IN) em &= range_bytes(s.pos0 + 4 * k, 0, s.n) & HI;
-      const uint32_t inc = (em >> 7) * 0x01010101u;  // byte j: units emitted by positions <= j
+      if (!IN) em &= range_bytes(s.pos0 + 4 * k, 0, s.n) & 0x01010101u;
+      const uint32_t inc2 = em * 0x02020202u;  // byte j: 2 x units emitted by positions <= j
+      const uint32_t a1 = mad(prmt(inc2, 0u, 0x4440u), 1u, p);
+      const uint32_t a2 = mad(prmt(inc2, 0u, 0x4441u), 1u, p);
+      const uint32_t a3 = mad(prmt(inc2, 0u, 0x4442u), 1u, p);
+      const uint32_t u1 = u01 >> 16, u3 = u23 >> 16;
       if (k < 7) {
-        st[0] = (uint16_t)u01;
-        st[inc & 0xFFu] = (uint16_t)(u01 >> 16);
-        st[(inc >> 8) & 0xFFu] = (uint16_t)u23;
-        st[(inc >> 16) & 0xFFu] = (uint16_t)(u23 >> 16);
+        sts16(p, u01);
+        sts16(a1, u1);
+        sts16(a2, u23);
+        sts16(a3, u3);
       } else {
-        if (em & 0x00000080u) st[0] = (uint16_t)u01;
-        if (em & 0x00008000u) st[inc & 0xFFu] = (uint16_t)(u01 >> 16);
-        if (em & 0x00800000u) st[(inc >> 8) & 0xFFu] = (uint16_t)u23;
-        if (em & 0x80000000u) st[(inc >> 16) & 0xFFu] = (uint16_t)(u23 >> 16);
+        if (em & 0x00000001u) sts16(p, u01);
+        if (em & 0x00000100u) sts16(a1, u1);
+        if (em & 0x00010000u) sts16(a2, u23);
+        if (em & 0x01000000u) sts16(a3, u3);
       }
-      st += inc >> 24;
+      p += inc2 >> 24;
     }
   }
 
@@ -339,13 +376,12 @@ struct U16Pol {
     uint32_t own[8];                 // owned lanes (top bits), all set in interior tiles
     unsigned long long first_err;
     long long pos0;
-    bool wasc, interior;
+    bool wasc;
   };
 
   template <bool IN>  // IN: the whole tile is owned (tile-uniform)
-  __device__ static __forceinline__ uint32_t analyze(St &s, const uint8_t *buf, int tid,
-                                                     int lane, long long tp_bytes, long long n_bytes,
-                                                     bool xc) {
+  __device__ static __forceinline__ void load(St &s, const uint8_t *buf, int tid, int lane,
+                                              long long tp_bytes, long long n_bytes) {
     const long long tpw = tp_bytes / 2, nw = n_bytes / 2;
     const uint8_t *my = buf + HALO + BPT * tid;
     {
@@ -361,7 +397,6 @@ struct U16Pol {
     s.prev_word = pv >> 16;
     s.next_word = nx & 0xFFFFu;
     s.pos0 = tpw + (BPT / 2) * tid;
-    s.interior = IN;
     uint32_t orv = 0;
 #pragma unroll
     for (int k = 0; k < 8; k++) {
@@ -375,6 +410,10 @@ struct U16Pol {
       }
     }
     s.wasc = __all_sync(FULL, (orv & 0xFF80FF80u) == 0u);
+  }
+
+  template <bool IN>  // IN: the whole tile is owned (tile-uniform)
+  __device__ static __forceinline__ uint32_t analyze(St &s, int, bool xc) {
     // a9 pairing predicate (exact) and a5 widths, two words per op.  Widths are summed per
     // 16-bit lane (1 + [u >= 0x80] + [three-byte]) and folded once.
     uint32_t lanes = 0, anyerr = 0;
@@ -507,7 +546,7 @@ __device__ __forceinline__ void finish_call(const TileArgs &a, bool xc, int tid,
 // ============================================================================ validators
 // K1 / K3: classify (UTF-8: flag, then exact rescan of flagged tiles) or pair-check (UTF-16).
 template <class Pol>
-__global__ void __launch_bounds__(NT, 2) k_validate(const TileArgs a) {
+__global__ void __launch_bounds__(NT, 4) k_validate(const TileArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t *inbuf = smem;
   __shared__ uint64_t bar[2];
@@ -549,10 +588,13 @@ __global__ void __launch_bounds__(NT, 2) k_validate(const TileArgs a) {
     __syncthreads();
     typename Pol::St st;
     const long long tp = tile_pos(win, t);
-    if (tp >= 0 && tp + TILE <= win.n)
-      Pol::template analyze<true>(st, buf, tid, lane, tp, win.n, false);
-    else
-      Pol::template analyze<false>(st, buf, tid, lane, tp, win.n, false);
+    if (tp >= 0 && tp + TILE <= win.n) {
+      Pol::template load<true>(st, buf, tid, lane, tp, win.n);
+      Pol::template analyze<true>(st, tid, false);
+    } else {
+      Pol::template load<false>(st, buf, tid, lane, tp, win.n);
+      Pol::template analyze<false>(st, tid, false);
+    }
     if (Pol::hint(st)) s_flag = 1;
     __syncthreads();
     if (s_flag) {
@@ -568,141 +610,240 @@ __global__ void __launch_bounds__(NT, 2) k_validate(const TileArgs a) {
 }
 
 // ============================================================================ transcoders
-// K2 / K4.  NT data threads + one look-back warp (warp NT/32).  Per tile i the data warps
-// classify, scan, hand (tile, aggregate) to the look-back warp (named barrier BAR_C0+(i&1)),
-// decode into stage[i&1], then copy out tile i-1 once its prefix arrives (BAR_P0+((i-1)&1)):
-// the look-back of a tile overlaps the whole processing of the next one.
+// K2 / K4.  NT data threads + one look-back warp (warp NT/32); several CTAs per SM.
+// Per tile the data warps take a ticket and bulk-load the tile (TMA), classify, block-scan,
+// publish the tile aggregate and hand it to the look-back warp (named barrier BAR_C), decode
+// into the stage at tile-local offsets while the look-back runs, wait for the prefix (BAR_P,
+// which also orders every warp's stage writes before the copy-out) and copy the stage out.
+// A ticket is taken only when its tile is about to be processed, so a tile's aggregate is
+// published one load + classify after its ticket (the look-back of every later tile waits
+// for it); the load latency is hidden by the other CTAs on the SM instead of by prefetching.
+constexpr int RING = 4;  // input tile slots: loading, classifying, two awaiting their prefix
+#ifndef UG_NLB
+#define UG_NLB 1
+#endif
+constexpr int NLB = UG_NLB;  // look-back warps per CTA (alternating tiles)
+
+// Decode tile j (ring slot js, prefix P, aggregate C; this thread's offset excl / count cnt)
+// into the stage at the tile's global 16-byte phase, then store it: the 16-byte aligned
+// interior by one TMA bulk store (thread 0), the head and tail by scalar stores.  Ends with
+// the stage still being read by the bulk copy (the caller waits before the next decode).
 template <class Pol>
-__global__ void __launch_bounds__(NT + 32, 2) k_transcode(const TileArgs a) {
+__device__ __forceinline__ void emit_tile(const TileArgs &a, const uint8_t *img, long long t,
+                                          unsigned long long P, uint32_t C, uint32_t excl,
+                                          uint32_t cnt, typename Pol::Out *stage, int tid,
+                                          int lane) {
+  using Out = typename Pol::Out;
+  constexpr uint32_t A = 16 / sizeof(Out);  // units per 16 bytes
+  const Window &win = a.win;
+  const long long tp = tile_pos(win, t);
+  Out *out = reinterpret_cast<Out *>(a.out);
+  // phase: unit index of global unit P inside its 16-byte granule
+  const uint32_t ph = (uint32_t)((((uintptr_t)(out + P)) & 15u) / sizeof(Out));
+  typename Pol::St st;
+  if (tp >= 0 && tp + TILE <= win.n) {  // tile-uniform
+    Pol::template load<true>(st, img, tid, lane, tp, win.n);
+    Pol::template decode<true>(st, stage, ph + excl, ph + excl + cnt, win.n / Pol::UNIT);
+  } else {
+    Pol::template load<false>(st, img, tid, lane, tp, win.n);
+    Pol::template decode<false>(st, stage, ph + excl, ph + excl + cnt, win.n / Pol::UNIT);
+  }
+  named_sync<BAR_DATA, NT>();  // the whole tile is in the stage
+  unsigned long long hi = P + C;
+  if (hi > a.out_cap) hi = a.out_cap;
+  if (hi <= P) return;
+  const uint32_t Cc = (uint32_t)(hi - P);
+  const uint32_t h = ph ? A - ph : 0u;  // head units (before the first 16-byte boundary)
+  if (h >= Cc) {
+    if ((uint32_t)tid < Cc) out[P + tid] = stage[ph + tid];
+    return;
+  }
+  const uint32_t nb = (Cc - h) / A;  // whole 16-byte granules
+  const uint32_t tl = h + nb * A;    // first tail unit
+  if ((uint32_t)tid < h) out[P + tid] = stage[ph + tid];
+  if ((uint32_t)tid < Cc - tl) out[P + tl + tid] = stage[ph + tl + tid];
+  if (tid == 0 && nb) {
+    fence_proxy_async_smem();  // the stage writes above (generic proxy) before the TMA read
+    bulk_s2g(out + P + h, stage + ph + h, nb * 16u);
+    bulk_commit();
+  }
+}
+
+// K2 / K4.  NT data threads + one look-back warp (warp NT/32); up to 4 CTAs per SM.
+//  * Tiles are taken by atomic ticket (issue order keeps the decoupled look-back
+//    deadlock-free) and bulk-loaded (TMA) into a ring of RING input slots, one tile ahead.
+//  * Tile i is classified, block-scanned (the one CTA barrier of the classify stage) and its
+//    aggregate published at once; the look-back warp computes its exclusive prefix P
+//    starting at the ticket (it needs only the predecessors) and publishes P + C when the
+//    aggregate arrives.
+//  * Tile i - 2 - whose prefix had two tiles of time to arrive - is then decoded from its
+//    still-resident input image straight into the stage at its global 16-byte phase and
+//    shipped by one TMA bulk store.
+template <class Pol>
+__global__ void __launch_bounds__(NT + 32 * NLB, 4) k_transcode(const TileArgs a) {
   using Out = typename Pol::Out;
   extern __shared__ __align__(128) uint8_t smem[];
-  uint8_t *inbuf = smem;
-  Out *stage0 = reinterpret_cast<Out *>(smem + 2 * INBUF);
-  constexpr int SU = Pol::STAGE / (int)sizeof(Out);  // stage units per buffer
-  __shared__ uint64_t bar[2];
-  __shared__ uint32_t s_wsum[NT / 32];
-  __shared__ long long s_next[2];
-  __shared__ long long s_tile[2];
-  __shared__ uint32_t s_cnt[2];
-  __shared__ unsigned long long s_pre[2];
-  __shared__ unsigned long long s_emin;
-  __shared__ int s_flag, s_last;
+  uint8_t *ring = smem;                                         // RING input tile images
+  Out *stage = reinterpret_cast<Out *>(smem + RING * INBUF);   // output stage (global phase)
+  __shared__ uint64_t mb_load[RING];  // tile load landed (TMA tx) / no tile (plain arrive)
+  __shared__ uint64_t mb_tick[RING];  // thread 0 -> look-back warp: ticket of slot taken
+  __shared__ uint64_t mb_agg[RING];   // thread 0 -> look-back warp: aggregate of slot
+  __shared__ uint64_t mb_pre[RING];   // look-back warp -> data warps: prefix of slot
+  __shared__ uint32_t s_wsum[2][NT / 32];
+  __shared__ long long s_t[RING];
+  __shared__ uint32_t s_cnt[RING];
+  __shared__ unsigned long long s_pre[RING];
+  __shared__ int s_flag[2], s_last;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const Window &win = a.win;
   const long long ntiles = (long long)a.ntiles;
   const long long n_units = win.n / Pol::UNIT;
-  Out *out = reinterpret_cast<Out *>(a.out);
+
+  // Thread 0: take the next ticket and start loading it into ring slot `slot`.
+  auto next_tile = [&](int slot) {
+    const long long tn = (long long)atomicAdd(&a.ctr->ticket, 1u);
+    s_t[slot] = tn;
+    mbar_arrive(&mb_tick[slot]);  // the look-back of tile tn can start now
+    if (tn < ntiles) {
+      fence_proxy_async_smem();
+      issue_tile_load(win, tn, ring + slot * INBUF, &mb_load[slot]);
+    } else {
+      mbar_arrive(&mb_load[slot]);
+    }
+  };
 
   if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+#pragma unroll
+    for (int j = 0; j < RING; j++) {
+      mbar_init(&mb_load[j], 1);
+      mbar_init(&mb_tick[j], 1);
+      mbar_init(&mb_agg[j], 1);
+      mbar_init(&mb_pre[j], 1);
+    }
+    s_flag[0] = s_flag[1] = 0;
     fence_mbar_init();
-    long long t0 = (long long)atomicAdd(&a.ctr->ticket, 1u);
-    s_next[0] = t0;
-    if (t0 < ntiles) issue_tile_load(win, t0, inbuf, &bar[0]);
+    next_tile(0);
   }
   __syncthreads();
 
-  if (warp == NT / 32) {
-    // ------------------------------------------------------------ look-back warp (a6)
-    for (int i = 0;; i++) {
-      if (i & 1) named_sync<BAR_C1, NT + 32>(); else named_sync<BAR_C0, NT + 32>();
-      const long long t = s_tile[i & 1];
-      if (t < 0) break;
+  if (warp >= NT / 32) {
+    // ------------------------------------------------------------ look-back warps (a6)
+    // Warp NT/32 + a handles the tiles i = a (mod NLB): a look-back is mostly waiting for
+    // predecessors, so two agents keep one tile's wait from queueing behind the previous one.
+    for (int i = warp - NT / 32;; i += NLB) {
+      const int sl = i % RING;
+      const uint32_t ph = (i / RING) & 1;
+      mbar_wait(&mb_tick[sl], ph);
+      const long long t = s_t[sl];
+      if (t >= ntiles) break;
 #ifdef UG_TRACE
       unsigned long long t0 = gtime();
-      int rounds = 0;
-      const unsigned long long P = tile_prefix(a, t, s_cnt[i & 1], lane, &rounds);
-      if (lane == 0 && i < TR_IT && blockIdx.x < 1024) g_trace[blockIdx.x][i][3] = rounds;
-#else
-      const unsigned long long P = tile_prefix(a, t, s_cnt[i & 1], lane);
-#endif
-#ifdef UG_TRACE
+      int rounds = 0, polls = 0;
+      unsigned long long tf = 0;
+      const unsigned long long P = tile_excl_prefix(a, t, lane, &rounds, &tf, &polls);
       if (lane == 0 && i < TR_IT && blockIdx.x < 1024) {
         g_trace[blockIdx.x][i][0] = t;
         g_trace[blockIdx.x][i][1] = t0;
         g_trace[blockIdx.x][i][2] = gtime();
+        g_trace[blockIdx.x][i][3] = rounds;
+        g_trace[blockIdx.x][i][6] = tf;
+        g_trace[blockIdx.x][i][7] = polls;
       }
+#else
+      const unsigned long long P = tile_excl_prefix(a, t, lane);
 #endif
-      if (lane == 0) s_pre[i & 1] = P;
-      if (i & 1) named_arrive<BAR_P1, NT + 32>(); else named_arrive<BAR_P0, NT + 32>();
+      mbar_wait(&mb_agg[sl], ph);
+      if (lane == 0) {
+        if (t != 0) st_relaxed(a.status + t, pack_status(a.epoch, FLAG_PREFIX, P + s_cnt[sl]));
+        s_pre[sl] = P;
+        mbar_arrive(&mb_pre[sl]);
+      }
     }
   } else {
     // ------------------------------------------------------------ data warps
-    long long t = s_next[0];
-    int s = 0, i = 0;
-    uint32_t parity = 0, C_prev = 0;
-    while (t < ntiles) {
-      if (tid == 0) {
-        long long tn = (long long)atomicAdd(&a.ctr->ticket, 1u);
-        s_next[s ^ 1] = tn;
-        if (tn < ntiles) {
-          fence_proxy_async_smem();
-          issue_tile_load(win, tn, inbuf + (s ^ 1) * INBUF, &bar[s ^ 1]);
-        }
-        s_flag = 0;
-        s_emin = NONE;
+    uint32_t ex[2] = {0u, 0u}, cn[2] = {0u, 0u};  // this thread's offset / count, tiles i-1, i-2
+    int i = 0;
+    auto emit = [&](int j) {  // decode + store tile j (all data threads)
+      const int js = j % RING;
+#ifdef UG_TRACE
+      unsigned long long w0 = gtime();
+#endif
+      mbar_wait(&mb_pre[js], (j / RING) & 1);
+#ifdef UG_TRACE
+      if (tid == 0 && j < TR_IT && blockIdx.x < 1024) {
+        g_trace[blockIdx.x][j][4] = w0;
+        g_trace[blockIdx.x][j][5] = gtime();
       }
-      mbar_wait(&bar[s], (parity >> s) & 1u);
-      parity ^= 1u << s;
-      uint8_t *buf = inbuf + s * INBUF;
-      fix_tile_edges(win, t, buf, NT);
-      named_sync<BAR_DATA, NT>();
-
+#endif
+      emit_tile<Pol>(a, ring + js * INBUF, s_t[js], s_pre[js], s_cnt[js], ex[j & 1], cn[j & 1],
+                     stage, tid, lane);
+    };
+    while (true) {
+      const int sl = i % RING;
+#if !defined(UG_LATE_TICKET) && !defined(UG_MID_TICKET)
+      if (tid == 0) {
+        bulk_wait_read_all();  // the previous bulk store has read the stage (barrier below)
+        next_tile((i + 1) % RING);  // its slot held tile i - 3, emitted last iteration
+      }
+#else
+      if (tid == 0) bulk_wait_read_all();  // the previous bulk store has read the stage
+#endif
+      mbar_wait(&mb_load[sl], (i / RING) & 1);
+      const long long t = s_t[sl];
+      if (t >= ntiles) break;
+      uint8_t *img = ring + sl * INBUF;
+      if (tile_at_edge(win, t)) {  // tile-uniform
+        fix_tile_edges(win, t, img, NT);
+        named_sync<BAR_DATA, NT>();
+      }
       typename Pol::St st;
       const long long tp = tile_pos(win, t);
-      const bool inner = tp >= 0 && tp + TILE <= win.n;  // tile-uniform
-      const uint32_t cnt = inner
-                               ? Pol::template analyze<true>(st, buf, tid, lane, tp, win.n, true)
-                               : Pol::template analyze<false>(st, buf, tid, lane, tp, win.n, true);
-      if (Pol::hint(st)) s_flag = 1;
+      uint32_t cnt;
+      if (tp >= 0 && tp + TILE <= win.n) {  // tile-uniform
+        Pol::template load<true>(st, img, tid, lane, tp, win.n);
+        cnt = Pol::template analyze<true>(st, tid, true);
+      } else {
+        Pol::template load<false>(st, img, tid, lane, tp, win.n);
+        cnt = Pol::template analyze<false>(st, tid, true);
+      }
+      if (Pol::hint(st)) s_flag[i & 1] = 1;
       uint32_t excl = 0, C = 0;
-      block_scan(cnt, s_wsum, lane, warp, &excl, &C);
+      block_scan(cnt, s_wsum[i & 1], lane, warp, &excl, &C);
       if (tid == 0) {
-        // publish the tile aggregate at once (a6): successors' look-backs must not wait for
-        // this CTA's look-back warp to reach this tile
+        // publish the tile aggregate at once (a6): successors' look-backs need it
         st_relaxed(a.status + t, pack_status(a.epoch, t == 0 ? FLAG_PREFIX : FLAG_AGG, C));
-        s_tile[i & 1] = t;
-        s_cnt[i & 1] = C;
+        s_cnt[sl] = C;
+        mbar_arrive(&mb_agg[sl]);
+        // s_flag[(i + 1) & 1] was last read after the block scan of i - 1; it is next set
+        // after the load of tile i + 1 lands
+        s_flag[(i + 1) & 1] = 0;
+#ifdef UG_MID_TICKET
+        // the next tile: its load overlaps the emit of tile i - 2 below
+        next_tile((i + 1) % RING);
+#endif
       }
-      // hand the aggregate to the look-back warp
-      if (i & 1) named_arrive<BAR_C1, NT + 32>(); else named_arrive<BAR_C0, NT + 32>();
-      if (s_flag) {
+      if (s_flag[i & 1]) {  // a4 (cold): straight to the call's minimum
         unsigned long long e = Pol::find_error(st, n_units);
-        if (e != NONE) atomicMin(&s_emin, e);
+        if (e != NONE) atomicMin(&a.ctr->err_min, e);
       }
-      if (inner)
-        Pol::template decode<true>(st, stage0 + (i & 1) * SU, excl, excl + cnt, n_units);
-      else
-        Pol::template decode<false>(st, stage0 + (i & 1) * SU, excl, excl + cnt, n_units);
-      if (i > 0) {  // a8: copy out the previous tile once its prefix is known
-#ifdef UG_TRACE
-        unsigned long long w0 = gtime();
+      if (i >= 2) emit(i - 2);  // a7, a8
+      ex[i & 1] = excl;  // tile i - 2's slot is free now
+      cn[i & 1] = cnt;
+#ifdef UG_LATE_TICKET
+      // take the next ticket only now: between a ticket and its tile's aggregate there is
+      // no wait on other CTAs (the load latency is covered by the other CTAs on the SM)
+      if (tid == 0) next_tile((i + 1) % RING);
 #endif
-        if ((i - 1) & 1) named_sync<BAR_P1, NT + 32>(); else named_sync<BAR_P0, NT + 32>();
-#ifdef UG_TRACE
-        if (tid == 0 && i - 1 < TR_IT && blockIdx.x < 1024) {
-          g_trace[blockIdx.x][i - 1][4] = w0;
-          g_trace[blockIdx.x][i - 1][5] = gtime();
-        }
-#endif
-        copy_out<Out>(out, a.out_cap, s_pre[(i - 1) & 1], C_prev, stage0 + ((i - 1) & 1) * SU,
-                      tid);
-      }
-      named_sync<BAR_DATA, NT>();
-      if (tid == 0 && s_emin != NONE) atomicMin(&a.ctr->err_min, s_emin);
-      C_prev = C;
-      t = s_next[s ^ 1];
-      s ^= 1;
       i++;
     }
-    if (i > 0) {
-      if ((i - 1) & 1) named_sync<BAR_P1, NT + 32>(); else named_sync<BAR_P0, NT + 32>();
-      copy_out<Out>(out, a.out_cap, s_pre[(i - 1) & 1], C_prev, stage0 + ((i - 1) & 1) * SU, tid);
+    // drain: tiles i - 2 and i - 1
+    for (int j = (i >= 2 ? i - 2 : 0); j < i; j++) {
+      if (tid == 0) bulk_wait_read_all();
+      named_sync<BAR_DATA, NT>();  // the stage is free again
+      emit(j);
     }
-    if (tid == 0) s_tile[i & 1] = -1;  // stop the look-back warp
-    if (i & 1) named_arrive<BAR_C1, NT + 32>(); else named_arrive<BAR_C0, NT + 32>();
+    if (tid == 0) bulk_wait_all();  // all output written before the CTA retires
   }
   __syncthreads();
   finish_call<Pol>(a, true, tid, warp, lane, &s_last);
@@ -875,14 +1016,14 @@ size_t tile_smem_bytes(Op op) {
   switch (op) {
     case Op::U8_VALIDATE:
     case Op::U16_VALIDATE: return 2 * INBUF;
-    case Op::U8_TO_U16: return 2 * INBUF + 2 * U8Pol::STAGE;
-    case Op::U16_TO_U8: return 2 * INBUF + 2 * U16Pol::STAGE;
+    case Op::U8_TO_U16: return RING * INBUF + U8Pol::STAGE;
+    case Op::U16_TO_U8: return RING * INBUF + U16Pol::STAGE;
   }
   return 0;
 }
 
 static int tile_threads(Op op) {
-  return (op == Op::U8_TO_U16 || op == Op::U16_TO_U8) ? NT + 32 : NT;
+  return (op == Op::U8_TO_U16 || op == Op::U16_TO_U8) ? NT + 32 * NLB : NT;
 }
 
 static const void *tile_fn(Op op) {
@@ -910,8 +1051,8 @@ cudaError_t launch_tile(Op op, const TileArgs &a, int grid, cudaStream_t s) {
   int nt = tile_threads(op);
   switch (op) {
     case Op::U8_VALIDATE: k_validate<U8Pol><<<grid, nt, sm, s>>>(a); break;
-    case Op::U8_TO_U16: k_transcode<U8Pol><<<grid, nt, sm, s>>>(a); break;
     case Op::U16_VALIDATE: k_validate<U16Pol><<<grid, nt, sm, s>>>(a); break;
+    case Op::U8_TO_U16: k_transcode<U8Pol><<<grid, nt, sm, s>>>(a); break;
     case Op::U16_TO_U8: k_transcode<U16Pol><<<grid, nt, sm, s>>>(a); break;
   }
   return cudaGetLastError();

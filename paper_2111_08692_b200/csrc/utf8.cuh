@@ -124,26 +124,26 @@ UG_HD Carry carry_of(uint32_t x) {
 }
 
 // The 4 positions of word x (previous word in c, updated): units of positions 0 / 1 in the
-// low / high half of *u01, positions 2 / 3 in *u23.  Returns the emit mask (msb per byte).
-// Units at non-emitting positions are garbage.
+// low / high half of *u01, positions 2 / 3 in *u23.  Returns the emit mask, 1 in the lsb of
+// every emitting byte.  Units at non-emitting positions are garbage.
+// The class masks are taken in lsb-per-byte form straight from a funnel shift by 8d + 1
+// (d = distance to the lead), so every per-byte constant is one multiply (FMA pipe).
 UG_HD uint32_t units4(uint32_t x, Carry &c, uint32_t *u01, uint32_t *u23) {
   const Carry n = carry_of(x);
   const uint32_t bp1 = fsl(c.x, x, 8), bp2 = fsl(c.x, x, 16);  // bytes e-1, e-2
-  const uint32_t S1L2 = fsl(c.L2, n.L2, 8);                    // end of a 2-byte character
-  const uint32_t S2E = fsl(c.E, n.E, 16);                      // end of 3-byte / high surrogate
-  const uint32_t S2F = fsl(c.F, n.F, 16);                      // high surrogate
-  const uint32_t S3F = fsl(c.F, n.F, 24);                      // low surrogate
+  const uint32_t s1l2 = fsl(c.L2, n.L2, 1);                    // end of a 2-byte character
+  const uint32_t s2e = fsl(c.E, n.E, 9);                       // end of 3-byte / high surrogate
+  const uint32_t s2f = fsl(c.F, n.F, 9);                       // high surrogate
+  const uint32_t s3f = fsl(c.F, n.F, 17);                      // low surrogate
   c = n;
-  const uint32_t em = (~x & HI) | S1L2 | S2E | S3F;
-  const uint32_t n7 = (x & HI) >> 7;   // 1 in every non-ASCII byte
-  const uint32_t f7 = S3F >> 7;        // 1 at low surrogates
+  const uint32_t n7 = (x >> 7) & 0x01010101u;  // 1 in every non-ASCII byte
+  const uint32_t em = ((n7 ^ 0x01010101u) | s1l2 | s2e | s3f);
   uint32_t lb = mux(n7 * 0xC0u, bp1 << 6, x);
-  const uint32_t A1 = n7 * 15u - f7 * 12u;          // 0x0F, or 0x03 at a low surrogate
-  const uint32_t A2 = (S2E >> 7) * 0xF0u;
-  uint32_t hb = ((bp1 >> 2) & A1) | (f7 * 0xDCu) | ((bp2 << 4) & A2);
+  const uint32_t A1 = mad(s3f, 0xFFFFFFF4u, n7 * 15u);  // 0x0F, or 0x03 at a low surrogate
+  uint32_t hb = ((bp1 >> 2) & A1) | (s3f * 0xDCu) | ((bp2 << 4) & (s2e * 0xF0u));
   // high surrogate: G = hb:lb = cp >> 6, unit = 0xD800 | ((G >> 4) - 0x40)
-  const uint32_t Mh = (S2F >> 7) * 0xFFu;
-  const uint32_t hbm = (hb | HI) - 0x04040404u;     // per byte 0x80 + hb - 4, no borrows
+  const uint32_t Mh = s2f * 0xFFu;
+  const uint32_t hbm = (hb | HI) - 0x04040404u;  // per byte 0x80 + hb - 4, no borrows
   lb = mux(Mh, mux(0xF0F0F0F0u, hbm << 4, lb >> 4), lb);
   hb = mux(Mh, ((hbm >> 4) & 0x03030303u) | 0xD8D8D8D8u, hb);
   *u01 = prmt(lb, hb, 0x5140u);

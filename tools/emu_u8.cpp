@@ -96,23 +96,23 @@ static void run(const std::vector<uint8_t> &s, const char *name) {
       // ownership clip (positions >= n) as the kernel does for partial tiles
       uint32_t ownb = 0;
       for (int j = 0; j < 4; j++)
-        if (c * CH + 4 * k + j < n) ownb |= 0xFFu << (8 * j);
+        if (c * CH + 4 * k + j < n) ownb |= 0x01u << (8 * j);
       em &= ownb;
       // the msb-form emit mask must equal the bit-plane one
       uint32_t nib = (em_bits >> (4 * k)) & 0xFu;
-      uint32_t msb = ((em >> 7) & 1u) | ((em >> 14) & 2u) | ((em >> 21) & 4u) | ((em >> 28) & 8u);
+      uint32_t msb = (em & 1u) | ((em >> 7) & 2u) | ((em >> 14) & 4u) | ((em >> 21) & 8u);
       CHECK(nib == msb, "%s: emit mismatch chunk %lld word %d: %x vs %x", name, c, k, nib, msb);
-      const uint32_t inc = (em >> 7) * 0x01010101u;
+      const uint32_t inc = em * 0x01010101u;
       if (k < 7) {
         st[so] = (uint16_t)u01;
         st[so + (inc & 0xFFu)] = (uint16_t)(u01 >> 16);
         st[so + ((inc >> 8) & 0xFFu)] = (uint16_t)u23;
         st[so + ((inc >> 16) & 0xFFu)] = (uint16_t)(u23 >> 16);
       } else {
-        if (em & 0x80u) st[so] = (uint16_t)u01;
-        if (em & 0x8000u) st[so + (inc & 0xFFu)] = (uint16_t)(u01 >> 16);
-        if (em & 0x800000u) st[so + ((inc >> 8) & 0xFFu)] = (uint16_t)u23;
-        if (em & 0x80000000u) st[so + ((inc >> 16) & 0xFFu)] = (uint16_t)(u23 >> 16);
+        if (em & 0x1u) st[so] = (uint16_t)u01;
+        if (em & 0x100u) st[so + (inc & 0xFFu)] = (uint16_t)(u01 >> 16);
+        if (em & 0x10000u) st[so + ((inc >> 8) & 0xFFu)] = (uint16_t)u23;
+        if (em & 0x1000000u) st[so + ((inc >> 16) & 0xFFu)] = (uint16_t)(u23 >> 16);
       }
       so += inc >> 24;
     }

@@ -1,0 +1,5 @@
+mkdir -p gpurun_out
+timeout -s KILL 600 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/pytest_e6.log 2>&1; echo "pytest=$?" > gpurun_out/exp6.log; tail -2 gpurun_out/pytest_e6.log >> gpurun_out/exp6.log
+UG_LIB_OVERRIDE=build_variants/libunigpu_trace.so timeout 300 python tools/trace_lb.py 1024 >> gpurun_out/exp6.log 2>&1
+timeout 300 python tools/opbench.py c4 1024 10 >> gpurun_out/exp6.log 2>&1
+./tools/ubench >> gpurun_out/exp6.log 2>&1

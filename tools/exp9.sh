@@ -1,0 +1,2 @@
+mkdir -p gpurun_out
+UG_LIB_OVERRIDE=build_variants/libunigpu_trace.so timeout 300 python tools/trace_lb.py 1024 > gpurun_out/exp9.log 2>&1

@@ -13,7 +13,7 @@ for _ in range(3):
     ug.utf8_to_utf16le(t8, o16)
 torch.cuda.synchronize()
 L = ctypes.CDLL(os.environ["UG_LIB_OVERRIDE"])
-buf = np.zeros((1024, 64, 6), dtype=np.uint64)
+buf = np.zeros((1024, 64, 8), dtype=np.uint64)
 L.ug_debug_trace.argtypes = [ctypes.c_void_p, ctypes.c_size_t]
 rc = L.ug_debug_trace(buf.ctypes.data, buf.nbytes)
 nb = int((buf[:, 0, 1] > 0).sum())
@@ -25,6 +25,9 @@ pw = (b[:, :, 5] - b[:, :, 4]) / 1000.0
 valid = b[:, :, 1] > 0
 print("ctas", nb, "rc", rc)
 print("lookback us: mean %.2f p50 %.2f p90 %.2f max %.2f" % (lb[valid].mean(), np.median(lb[valid]), np.percentile(lb[valid], 90), lb[valid].max()))
+ft = (b[:, :, 6] - b[:, :, 1]) / 1000.0
+print("first poll done after us: mean %.2f p50 %.2f p90 %.2f" % (ft[valid].mean(), np.median(ft[valid]), np.percentile(ft[valid], 90)))
+print("polls: mean %.1f p50 %.1f p90 %.1f" % (b[:, :, 7][valid].mean(), np.median(b[:, :, 7][valid]), np.percentile(b[:, :, 7][valid], 90)))
 print("rounds: mean %.2f max %d hist %s" % (rounds[valid].mean(), rounds[valid].max(), np.bincount(rounds[valid].astype(int))[:10]))
 v2 = b[:, :, 4] > 0
 print("prefix wait us: mean %.2f p50 %.2f p90 %.2f" % (pw[v2].mean(), np.median(pw[v2]), np.percentile(pw[v2], 90)))
