@@ -231,7 +231,7 @@ int enqueue_len(bool u16in, const void *in, unsigned long long n, unsigned long 
   DeviceInfo *di;
   if (device_info(w->device, &di) != cudaSuccess) return UG_ERR_CUDA;
   std::lock_guard<std::mutex> lk(w->mu);
-  unsigned long long per_block = (unsigned long long)NT * 16 * 4;  // bytes per block pass
+  unsigned long long per_block = (unsigned long long)LNT * 16 * 4;  // bytes per block pass
   unsigned long long bytes = n * (u16in ? 2 : 1);
   unsigned long long want = (bytes + per_block - 1) / per_block;
   unsigned long long maxg = (unsigned long long)di->sms * 4;

@@ -13,6 +13,7 @@ namespace ug {
 constexpr uint32_t FULL = 0xffffffffu;
 constexpr uint64_t NONE = ~0ull;
 constexpr int NT = 256;           // data threads per CTA for the tile kernels
+constexpr int LNT = 512;          // threads per CTA for the length reductions
 constexpr int TILE = 8192;        // input bytes per tile (8 Ki UTF-8 bytes / 4 Ki UTF-16 words)
 constexpr int BPT = TILE / NT;    // 32 contiguous input bytes per thread
 #ifndef UG_LB_PER_LANE
@@ -229,7 +230,7 @@ __device__ __forceinline__ bool look_back_round(uint64_t *status, uint32_t epoch
     }
     if (polls) ++*polls;
     if (__all_sync(FULL, ready)) break;
-    __nanosleep(spins < 2 ? 64 : 256);
+    __nanosleep(spins < 2 ? 128 : 512);
     ++spins;
     bool stop2 = false;
 #pragma unroll

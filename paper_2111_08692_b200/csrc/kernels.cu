@@ -252,7 +252,7 @@ struct U8Pol {
   __device__ static __forceinline__ uint32_t analyze(St &s, int tid, bool xc) {
     uint32_t emit = 0xFFFFFFFFu;
     s.err = 0;
-    if (!s.wasc) s.err = u8::analyze32(s.w, s.prev, s.nxt, tid == NT - 1, &emit);  // a3, a5
+    if (!s.wasc) s.err = u8::analyze32(s.w, s.prev, s.nxt, (tid & 31) == 31, &emit);  // a3, a5
     if (!xc) return 0u;
     if (!IN) emit &= bit_range(s.pos0, 0, s.n);
     return popc(emit);
@@ -544,48 +544,58 @@ __device__ __forceinline__ void finish_call(const TileArgs &a, bool xc, int tid,
 }
 
 // ============================================================================ validators
-// K1 / K3: classify (UTF-8: flag, then exact rescan of flagged tiles) or pair-check (UTF-16).
+// K1 / K3: classify (UTF-8: flag, then exact rescan) or pair-check (UTF-16).  No inter-CTA
+// dependence, so tiles go in static order (CTA c: c, c + G, ...) through a ring of VRING TMA
+// slots kept VRING - 1 tiles ahead.  No CTA barrier per tile: each warp arrives on the slot's
+// "empty" mbarrier when done with the image and thread 0 refills the slot once all have.  A
+// warp that flags rescans its own 1 KiB (every warp's last lane checks the 3-byte look-ahead,
+// so a flag never has to be resolved by another warp).
+constexpr int VRING = 4;
+
 template <class Pol>
 __global__ void __launch_bounds__(NT, 4) k_validate(const TileArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
-  uint8_t *inbuf = smem;
-  __shared__ uint64_t bar[2];
-  __shared__ long long s_next[2];
-  __shared__ unsigned long long s_emin;
-  __shared__ int s_flag, s_last;
+  __shared__ uint64_t mb_full[VRING], mb_empty[VRING];
+  __shared__ int s_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const Window &win = a.win;
   const long long ntiles = (long long)a.ntiles;
   const long long n_units = win.n / Pol::UNIT;
+  const long long G = gridDim.x;
 
   if (tid == 0) {
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
+#pragma unroll
+    for (int j = 0; j < VRING; j++) {
+      mbar_init(&mb_full[j], 1);
+      mbar_init(&mb_empty[j], NT / 32);
+    }
     fence_mbar_init();
-    long long t0 = (long long)atomicAdd(&a.ctr->ticket, 1u);
-    s_next[0] = t0;
-    if (t0 < ntiles) issue_tile_load(win, t0, inbuf, &bar[0]);
+#pragma unroll
+    for (int j = 0; j < VRING - 1; j++) {
+      const long long t = blockIdx.x + j * G;
+      if (t < ntiles) issue_tile_load(win, t, smem + j * INBUF, &mb_full[j]);
+    }
   }
   __syncthreads();
-  long long t = s_next[0];
-  int s = 0;
-  uint32_t parity = 0;
-  while (t < ntiles) {
-    if (tid == 0) {
-      long long tn = (long long)atomicAdd(&a.ctr->ticket, 1u);
-      s_next[s ^ 1] = tn;
+  int k = 0;
+  for (long long t = blockIdx.x; t < ntiles; t += G, k++) {
+    const int sl = k % VRING;
+    if (tid == 0) {  // refill the slot freed by tile k - 1 with tile k + VRING - 1
+      const long long tn = t + (VRING - 1) * G;
+      const int sn = (k + VRING - 1) % VRING;
       if (tn < ntiles) {
+        if (k >= 1) mbar_wait(&mb_empty[sn], ((k - 1) / VRING) & 1);
         fence_proxy_async_smem();
-        issue_tile_load(win, tn, inbuf + (s ^ 1) * INBUF, &bar[s ^ 1]);
+        issue_tile_load(win, tn, smem + sn * INBUF, &mb_full[sn]);
       }
-      s_flag = 0;
-      s_emin = NONE;
     }
-    mbar_wait(&bar[s], (parity >> s) & 1u);
-    parity ^= 1u << s;
-    uint8_t *buf = inbuf + s * INBUF;
-    fix_tile_edges(win, t, buf, NT);
-    __syncthreads();
+    uint8_t *buf = smem + sl * INBUF;
+    mbar_wait(&mb_full[sl], (k / VRING) & 1);
+    if (tile_at_edge(win, t)) {  // tile-uniform
+      named_sync<BAR_DATA, NT>();  // everyone has waited for the load
+      fix_tile_edges(win, t, buf, NT);
+      named_sync<BAR_DATA, NT>();
+    }
     typename Pol::St st;
     const long long tp = tile_pos(win, t);
     if (tp >= 0 && tp + TILE <= win.n) {
@@ -595,17 +605,14 @@ __global__ void __launch_bounds__(NT, 4) k_validate(const TileArgs a) {
       Pol::template load<false>(st, buf, tid, lane, tp, win.n);
       Pol::template analyze<false>(st, tid, false);
     }
-    if (Pol::hint(st)) s_flag = 1;
-    __syncthreads();
-    if (s_flag) {
-      unsigned long long e = Pol::find_error(st, n_units);
-      if (e != NONE) atomicMin(&s_emin, e);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&mb_empty[sl]);  // this warp is done with the image
+    if (__any_sync(FULL, Pol::hint(st))) {       // a4 (cold)
+      const unsigned long long e = Pol::find_error(st, n_units);
+      if (e != NONE) atomicMin(&a.ctr->err_min, e);
     }
-    __syncthreads();
-    if (tid == 0 && s_emin != NONE) atomicMin(&a.ctr->err_min, s_emin);
-    t = s_next[s ^ 1];
-    s ^= 1;
   }
+  __syncthreads();
   finish_call<Pol>(a, false, tid, warp, lane, &s_last);
 }
 
@@ -737,6 +744,11 @@ __global__ void __launch_bounds__(NT + 32 * NLB, 4) k_transcode(const TileArgs a
       mbar_wait(&mb_tick[sl], ph);
       const long long t = s_t[sl];
       if (t >= ntiles) break;
+#ifndef UG_LB_AT_TICKET
+      // start when the tile itself is classified: its predecessors were ticketed earlier and
+      // are classified around the same time, so an earlier start would only poll L2 longer
+      mbar_wait(&mb_agg[sl], ph);
+#endif
 #ifdef UG_TRACE
       unsigned long long t0 = gtime();
       int rounds = 0, polls = 0;
@@ -753,7 +765,9 @@ __global__ void __launch_bounds__(NT + 32 * NLB, 4) k_transcode(const TileArgs a
 #else
       const unsigned long long P = tile_excl_prefix(a, t, lane);
 #endif
+#ifdef UG_LB_AT_TICKET
       mbar_wait(&mb_agg[sl], ph);
+#endif
       if (lane == 0) {
         if (t != 0) st_relaxed(a.status + t, pack_status(a.epoch, FLAG_PREFIX, P + s_cnt[sl]));
         s_pre[sl] = P;
@@ -865,7 +879,7 @@ __device__ __forceinline__ uint32_t len16_word(uint32_t u) {
 
 __device__ __forceinline__ void finish_reduction(unsigned long long sum, Counters *ctr,
                                                  unsigned long long *d_len) {
-  __shared__ unsigned long long s_part[NT / 32];
+  __shared__ unsigned long long s_part[LNT / 32];
   __shared__ int s_last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   sum = warp_sum64(sum);
@@ -886,7 +900,7 @@ __device__ __forceinline__ void finish_reduction(unsigned long long sum, Counter
   }
 }
 
-__global__ void __launch_bounds__(NT) k_len8(const uint8_t *in, unsigned long long n,
+__global__ void __launch_bounds__(LNT) k_len8(const uint8_t *in, unsigned long long n,
                                              Counters *ctr, unsigned long long *d_len) {
   const uintptr_t addr = (uintptr_t)in;
   unsigned long long head = (16u - (addr & 15u)) & 15u;
@@ -926,7 +940,7 @@ __device__ __forceinline__ uint32_t len16_lanes(uint32_t r) {
   return ((ge80 >> 15) + ((ge800 & ~sur) >> 15));  // per lane 0..2 (bits 0-1, 16-17)
 }
 
-__global__ void __launch_bounds__(NT) k_len16(const uint16_t *in, unsigned long long n,
+__global__ void __launch_bounds__(LNT) k_len16(const uint16_t *in, unsigned long long n,
                                               Counters *ctr, unsigned long long *d_len) {
   const uintptr_t addr = (uintptr_t)in;
   unsigned long long head = ((16u - (addr & 15u)) & 15u) / 2;
@@ -1015,7 +1029,7 @@ cudaError_t trace_read(void *host, size_t bytes) {
 size_t tile_smem_bytes(Op op) {
   switch (op) {
     case Op::U8_VALIDATE:
-    case Op::U16_VALIDATE: return 2 * INBUF;
+    case Op::U16_VALIDATE: return VRING * INBUF;
     case Op::U8_TO_U16: return RING * INBUF + U8Pol::STAGE;
     case Op::U16_TO_U8: return RING * INBUF + U16Pol::STAGE;
   }
@@ -1060,12 +1074,12 @@ cudaError_t launch_tile(Op op, const TileArgs &a, int grid, cudaStream_t s) {
 
 cudaError_t launch_len8(const uint8_t *in, unsigned long long n, Counters *ctr,
                         unsigned long long *d_len, int grid, cudaStream_t s) {
-  k_len8<<<grid, NT, 0, s>>>(in, n, ctr, d_len);
+  k_len8<<<grid, LNT, 0, s>>>(in, n, ctr, d_len);
   return cudaGetLastError();
 }
 cudaError_t launch_len16(const uint16_t *in, unsigned long long n, Counters *ctr,
                          unsigned long long *d_len, int grid, cudaStream_t s) {
-  k_len16<<<grid, NT, 0, s>>>(in, n, ctr, d_len);
+  k_len16<<<grid, LNT, 0, s>>>(in, n, ctr, d_len);
   return cudaGetLastError();
 }
 cudaError_t launch_combine(const RecordDev *recs, int nranks, int rank,

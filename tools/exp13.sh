@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+UG_LIB_OVERRIDE=build_variants/libunigpu_atagg.so timeout -s KILL 600 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/pytest_e13.log 2>&1; echo "pytest=$?" > gpurun_out/exp13.log; tail -1 gpurun_out/pytest_e13.log >> gpurun_out/exp13.log
+UG_LIB_OVERRIDE=build_variants/libunigpu_ataggtrace.so timeout 300 python tools/trace_lb.py 1024 >> gpurun_out/exp13.log 2>&1
+for v in atagg ataggl; do UG_LIB_OVERRIDE=build_variants/libunigpu_$v.so OPS=utf8_to_utf16le,utf16le_to_utf8 timeout 300 python tools/opbench.py c4 1024 10 >> gpurun_out/exp13.log 2>&1; done
