@@ -371,13 +371,17 @@ struct U16Pol {
   static constexpr int UNIT = 2;
   static constexpr int STAGE = 3 * (TILE / 2) + 64;
   struct St {
-    uint32_t w[8];
+    uint32_t w[8];                   // words 2k (low half), 2k + 1 (high half) of w[k]
     uint32_t prev_word, next_word;
-    uint32_t own[8];                 // owned lanes (top bits), all set in interior tiles
+    uint32_t own;                    // bit i: word i owned (all set in interior tiles)
     unsigned long long first_err;
     long long pos0;
     bool wasc;
   };
+  // msb-per-byte ownership of words 4g..4g+3
+  __device__ static __forceinline__ uint32_t own4(const St &s, int g) {
+    return ((((s.own >> (4 * g)) & 0xFu) * 0x00204081u) & 0x01010101u) << 7;
+  }
 
   template <bool IN>  // IN: the whole tile is owned (tile-uniform)
   __device__ static __forceinline__ void load(St &s, const uint8_t *buf, int tid, int lane,
@@ -397,53 +401,49 @@ struct U16Pol {
     s.prev_word = pv >> 16;
     s.next_word = nx & 0xFFFFu;
     s.pos0 = tpw + (BPT / 2) * tid;
-    uint32_t orv = 0;
-#pragma unroll
-    for (int k = 0; k < 8; k++) {
-      orv |= s.w[k];
-      if (IN) {
-        s.own[k] = u16::LANE_TOP;
-      } else {
-        const long long pos = s.pos0 + 2 * k;
-        s.own[k] = ((pos >= 0 && pos < nw) ? 0x8000u : 0u) |
-                   ((pos + 1 >= 0 && pos + 1 < nw) ? 0x80000000u : 0u);
-      }
-    }
+    s.own = IN ? 0xFFFFu : (bit_range(s.pos0, 0, nw) & 0xFFFFu);
+    const uint32_t orv = s.w[0] | s.w[1] | s.w[2] | s.w[3] | s.w[4] | s.w[5] | s.w[6] | s.w[7];
     s.wasc = __all_sync(FULL, (orv & 0xFF80FF80u) == 0u);
   }
 
-  template <bool IN>  // IN: the whole tile is owned (tile-uniform)
+  // a9 pairing predicate (exact) and a5 widths, byte-SWAR over 4 words.
+  template <bool IN>
   __device__ static __forceinline__ uint32_t analyze(St &s, int, bool xc) {
-    // a9 pairing predicate (exact) and a5 widths, two words per op.  Widths are summed per
-    // 16-bit lane (1 + [u >= 0x80] + [three-byte]) and folded once.
-    uint32_t lanes = 0, anyerr = 0;
-    uint32_t Hprev = (s.prev_word & 0xFC00u) == 0xD800u ? 0x80000000u : 0u;  // as a lane-1 bit
-    u16::Cls2 c = u16::classes2(s.w[0]);
-    uint32_t errm[8];
+    uint32_t Hprev = u16::is_high(s.prev_word) ? 0x80000000u : 0u;  // byte 3 = word -1
+    u16::Cls4 c = u16::classes4(s.w[0], s.w[1]);
+    uint32_t acc = 0, anyerr = 0, errm[4];
 #pragma unroll
-    for (int k = 0; k < 8; k++) {
-      const u16::Cls2 cn = (k < 7) ? u16::classes2(s.w[k + 1])
-                                   : u16::classes2(s.next_word & 0xFFFFu);
-      const uint32_t Hp = __funnelshift_l(Hprev, c.H, 16);   // previous word is high
-      const uint32_t Ln = __funnelshift_r(c.L, cn.L, 16);     // next word is low
-      uint32_t e = (c.H & ~Ln) | (c.L & ~Hp);
-      if (xc) {
-        uint32_t wl = 0x00010001u + ((~c.A & u16::LANE_TOP) >> 15) + (u16::three2(c, Hp) >> 15);
-        if (!IN) wl &= (s.own[k] >> 15) * 0xFFFFu;
-        lanes += wl;
+    for (int g = 0; g < 4; g++) {
+      u16::Cls4 cn;
+      uint32_t Lnext;
+      if (g < 3) {
+        cn = u16::classes4(s.w[2 * g + 2], s.w[2 * g + 3]);
+        Lnext = cn.L;
+      } else {
+        Lnext = u16::is_low(s.next_word) ? 0x80u : 0u;
       }
-      if (!IN) e &= s.own[k];
-      errm[k] = e;
+      const uint32_t Hp = fsl(Hprev, c.H, 8), Ln = fsr(c.L, Lnext, 8);
+      uint32_t e = (c.H & ~Ln) | (c.L & ~Hp);
+      uint32_t d = u16::wm1(c) + 0x01010101u;  // widths
+      if (!IN) {
+        const uint32_t o4 = own4(s, g);
+        e &= o4;
+        d &= (o4 >> 7) * 0xFFu;
+      }
+      acc += d;
+      errm[g] = e;
       anyerr |= e;
       Hprev = c.H;
-      c = cn;
+      if (g < 3) c = cn;
     }
-    const uint32_t cnt = (lanes & 0xFFFFu) + (lanes >> 16);
     s.first_err = NONE;
-    if (anyerr)  // cold
-      s.first_err = first_error_lane(errm[0], errm[1], errm[2], errm[3], errm[4], errm[5],
-                                     errm[6], errm[7], s.pos0);
-    return xc ? cnt : 0u;
+    if (anyerr) {  // cold
+#pragma unroll
+      for (int g = 3; g >= 0; g--)
+        if (errm[g])
+          s.first_err = (unsigned long long)(s.pos0 + 4 * g + (__ffs(errm[g]) - 8) / 8);
+    }
+    return xc ? (acc * 0x01010101u) >> 24 : 0u;
   }
 
   __device__ static __forceinline__ bool hint(const St &s) { return s.first_err != NONE; }
@@ -453,7 +453,7 @@ struct U16Pol {
 
   // a7: encode the owned words into stage[o ...] (UTF-8 bytes).  Every word stores 3 bytes at
   // its offset; bytes past its width are overwritten by the following words (program order);
-  // stores are clipped at the thread's end slot `lim`.
+  // the thread's last 4 words clip at its end slot `lim`.
   template <bool IN>
   __device__ static __forceinline__ void decode(const St &s, uint8_t *stage, uint32_t o,
                                                 uint32_t lim, long long) {
@@ -468,38 +468,37 @@ struct U16Pol {
       }
       return;
     }
-    uint32_t prevreg = s.prev_word << 16;
-    uint32_t Hprev = (s.prev_word & 0xFC00u) == 0xD800u ? 0x80000000u : 0u;
+    uint32_t p = smem_addr(stage + o);
+    const uint32_t pend = smem_addr(stage + lim);
+    uint32_t lprev = (s.prev_word & 0xFFu) << 24;
 #pragma unroll
-    for (int k = 0; k < 8; k++) {
-      const uint32_t r = s.w[k];
-      const u16::Cls2 c = u16::classes2(r);
-      const uint32_t Hp = __funnelshift_l(Hprev, c.H, 16);
-      const uint32_t pl = __funnelshift_l(prevreg, r, 16);
-      uint32_t B0, B1, B2;
-      u16::encode2(r, pl, c, Hp, &B0, &B1, &B2);
-      uint32_t wl = 0x00010001u + ((~c.A & u16::LANE_TOP) >> 15) + (u16::three2(c, Hp) >> 15);
-      if (!IN) wl &= (s.own[k] >> 15) * 0xFFFFu;
-      const uint32_t wa = wl & 0xFFFFu, wb = wl >> 16;
-      const uint32_t ob = o + wa;
-      if (k < 7) {  // spill past a word is covered by the >= 2 owned words that follow it
-        stage[o] = (uint8_t)B0;
-        stage[o + 1] = (uint8_t)B1;
-        stage[o + 2] = (uint8_t)B2;
-        stage[ob] = (uint8_t)(B0 >> 16);
-        stage[ob + 1] = (uint8_t)(B1 >> 16);
-        stage[ob + 2] = (uint8_t)(B2 >> 16);
-      } else {      // the thread's last two words: clip at its end slot
-        if (o < lim) stage[o] = (uint8_t)B0;
-        if (o + 1 < lim) stage[o + 1] = (uint8_t)B1;
-        if (o + 2 < lim) stage[o + 2] = (uint8_t)B2;
-        if (ob < lim) stage[ob] = (uint8_t)(B0 >> 16);
-        if (ob + 1 < lim) stage[ob + 1] = (uint8_t)(B1 >> 16);
-        if (ob + 2 < lim) stage[ob + 2] = (uint8_t)(B2 >> 16);
+    for (int g = 0; g < 4; g++) {
+      const u16::Cls4 c = u16::classes4(s.w[2 * g], s.w[2 * g + 1]);
+      const uint32_t lp = fsl(lprev, c.lo, 8);
+      lprev = c.lo;
+      uint32_t O0, O1, O2;
+      u16::encode4(c, lp, &O0, &O1, &O2);
+      uint32_t d = u16::wm1(c) + 0x01010101u;
+      if (!IN) d &= (own4(s, g) >> 7) * 0xFFu;
+      const uint32_t inc = d * 0x01010101u;  // byte j: bytes emitted by words <= j
+      const uint32_t a1 = p + prmt(inc, 0u, 0x4440u);
+      const uint32_t a2 = p + prmt(inc, 0u, 0x4441u);
+      const uint32_t a3 = p + prmt(inc, 0u, 0x4442u);
+      const uint32_t A[4] = {p, a1, a2, a3};
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const uint32_t b0 = O0 >> (8 * j), b1 = O1 >> (8 * j), b2 = O2 >> (8 * j);
+        if (g < 3) {
+          sts8(A[j], b0);
+          sts8(A[j] + 1, b1);
+          sts8(A[j] + 2, b2);
+        } else {
+          if (A[j] < pend) sts8(A[j], b0);
+          if (A[j] + 1 < pend) sts8(A[j] + 1, b1);
+          if (A[j] + 2 < pend) sts8(A[j] + 2, b2);
+        }
       }
-      o = ob + wb;
-      Hprev = c.H;
-      prevreg = r;
+      p += inc >> 24;
     }
   }
 

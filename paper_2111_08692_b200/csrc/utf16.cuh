@@ -12,24 +12,26 @@
 #pragma once
 #include <cstdint>
 
+#include "swar.cuh"
+
 namespace ug {
 namespace u16 {
 
-__device__ __forceinline__ bool is_high(uint32_t u) { return (u & 0xFC00u) == 0xD800u; }
-__device__ __forceinline__ bool is_low(uint32_t u) { return (u & 0xFC00u) == 0xDC00u; }
+UG_HD bool is_high(uint32_t u) { return (u & 0xFC00u) == 0xD800u; }
+UG_HD bool is_low(uint32_t u) { return (u & 0xFC00u) == 0xDC00u; }
 
-__device__ __forceinline__ uint32_t width(uint32_t u, uint32_t prev) {
+UG_HD uint32_t width(uint32_t u, uint32_t prev) {
   const bool two = u < 0x800u || is_high(u) || (is_low(u) && is_high(prev));
   return 1u + (u >= 0x80u ? 1u : 0u) + (two ? 0u : 1u);
 }
 
-__device__ __forceinline__ bool err_at(uint32_t prev, uint32_t u, uint32_t next) {
+UG_HD bool err_at(uint32_t prev, uint32_t u, uint32_t next) {
   return (is_high(u) && !is_low(next)) || (is_low(u) && !is_high(prev));
 }
 
 // UTF-8 bytes of word u (little-endian packed, width(u, prev) of them are meaningful).
 // Branch-free: all candidates computed, then selected.
-__device__ __forceinline__ uint32_t utf8_bytes(uint32_t u, uint32_t prev) {
+UG_HD uint32_t utf8_bytes(uint32_t u, uint32_t prev) {
   const uint32_t t6 = 0x80u | (u & 0x3Fu);         // last continuation byte
   const uint32_t m6 = 0x80u | ((u >> 6) & 0x3Fu);  // middle continuation byte
   const uint32_t b2 = (0xC0u | (u >> 6)) | (t6 << 8);
@@ -45,6 +47,7 @@ __device__ __forceinline__ uint32_t utf8_bytes(uint32_t u, uint32_t prev) {
   return v;
 }
 
+#if defined(__CUDACC__)
 // ---------------------------------------------------------------- SWAR (two words per op)
 // Masks carry one bit per 16-bit lane, at bit 15 (low word) and bit 31 (high word).
 constexpr uint32_t LANE_TOP = 0x80008000u;
@@ -107,6 +110,72 @@ __device__ __forceinline__ void encode2(uint32_t r, uint32_t pl, const Cls2 &c, 
   uint32_t b1 = (t6 & mT) | (m6 & ~mT);
   *B1 = (hm & mH) | (b1 & ~mH);
   *B2 = t6;
+}
+
+
+#endif  // __CUDACC__
+
+// ---------------------------------------------------------------- byte-SWAR, 4 words per op
+// The 4 words of two registers (wa = words 0, 1; wb = words 2, 3) are split into their low
+// and high bytes (2 PRMT), so every class test, width and output byte below is one byte lane
+// per word.  Masks are msb-per-byte.
+//  * widths (a5): w = 1 + [u >= 0x80] + [u >= 0x800 and u not a surrogate]: a surrogate
+//    emits 2 bytes, so a pair emits its 4 and every word at most 3 on ANY input
+//    (SPEC.md S:175).  The same rule gives utf8_length_from_utf16le.
+//  * output (a7), first / second / third byte of each word:
+//      u < 0x80     : u
+//      u < 0x800    : C0 | u >> 6,          80 | u & 3F
+//      other BMP    : E0 | u >> 12,         80 | (u >> 6) & 3F,   80 | u & 3F
+//      high h (pair): F0 | h' >> 8,         80 | (h' >> 2) & 3F            h' = (h & 3FF) + 40
+//      low l (pair) : 80 | (h & 3) << 4 | (l >> 6) & F,   80 | l & 3F      (h: previous word)
+struct Cls4 {
+  uint32_t lo, hi;              // low / high bytes of the 4 words
+  uint32_t ge80, ge800, S, H;   // u >= 0x80, u >= 0x800, surrogate, high surrogate
+  uint32_t L;                   // low surrogate
+};
+UG_HD Cls4 classes4(uint32_t wa, uint32_t wb) {
+  Cls4 c;
+  c.lo = prmt(wa, wb, 0x6420u);
+  c.hi = prmt(wa, wb, 0x7531u);
+  const uint32_t h7 = c.hi & 0x7F7F7F7Fu;
+  c.ge800 = ((h7 + 0x78787878u) | c.hi) & HI;         // hi >= 8 (no carries: 7-bit adds)
+  c.ge80 = ((h7 + 0x7F7F7F7Fu) | c.hi | c.lo) & HI;    // hi != 0 or lo >= 0x80
+  const uint32_t z = (c.hi & 0xF8F8F8F8u) ^ 0xD8D8D8D8u;
+  c.S = ~(((z & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | z) & HI;  // hi in D8..DF
+  const uint32_t b2 = c.hi << 5;                        // bit 2 of hi: DC..DF
+  c.L = c.S & b2;
+  c.H = c.S & ~b2;
+  return c;
+}
+// width - 1 per byte lane (0..2)
+UG_HD uint32_t wm1(const Cls4 &c) { return (c.ge80 >> 7) + ((c.ge800 & ~c.S) >> 7); }
+// byte mask (0xFF per lane) from an msb-per-byte mask
+UG_HD uint32_t bmask(uint32_t m) { return prmt(m, 0u, 0xBA98u); }
+
+// Output byte planes of the 4 words: byte j of *O0 / *O1 / *O2 = first / second / third
+// output byte of word j (meaningful up to its width).  lp: low byte of the previous word
+// in each lane (the high surrogate's low bits for a low surrogate).
+UG_HD void encode4(const Cls4 &c, uint32_t lp, uint32_t *O0, uint32_t *O1, uint32_t *O2) {
+  const uint32_t U6 = mux(0xFCFCFCFCu, c.hi << 2, c.lo >> 6);   // (u >> 6) & 0xFF
+  const uint32_t T = (c.lo & 0x3F3F3F3Fu) | HI;                 // 80 | u & 3F
+  // first byte
+  const uint32_t vB = U6 | 0xC0C0C0C0u;
+  const uint32_t vC = ((c.hi >> 4) & 0x0F0F0F0Fu) | 0xE0E0E0E0u;
+  const uint32_t cy = (c.lo & (c.lo << 1) & HI) >> 7;           // lo >= 0xC0: h' carries
+  const uint32_t vH = ((c.hi & 0x03030303u) + cy) | 0xF0F0F0F0u;
+  const uint32_t vL = ((lp << 4) & 0x30303030u) | (U6 & 0x0F0F0F0Fu) | HI;
+  const uint32_t mS = bmask(c.S), mH = bmask(c.H);
+  const uint32_t mB = bmask(c.ge80 & ~c.ge800), mA = bmask(~c.ge80 & HI);
+  uint32_t x = mux(mH, vH, vL);
+  x = mux(mS, x, vC);
+  x = mux(mB, vB, x);
+  *O0 = mux(mA, c.lo, x);
+  // second byte
+  const uint32_t vH1 = ((((c.lo >> 2) & 0x3F3F3F3Fu) + 0x10101010u) & 0x3F3F3F3Fu) | HI;
+  const uint32_t mC = bmask(c.ge800 & ~c.S);
+  *O1 = mux(mC, (U6 & 0x3F3F3F3Fu) | HI, mux(mH, vH1, T));
+  // third byte
+  *O2 = T;
 }
 
 }  // namespace u16
