@@ -495,5 +495,6 @@ int ug_abi_version(void) { return UNIGPU_ABI_VERSION; }
 #ifdef UG_TRACE
 cudaError_t ug_trace_read_impl(void *host, size_t bytes);
 int ug_debug_trace(void *host, size_t bytes) { return (int)ug::trace_read(host, bytes); }
+int ug_debug_counters(void *host) { return (int)ug::dbg_read(host); }
 #endif
 }  // extern "C"

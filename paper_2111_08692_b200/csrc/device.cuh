@@ -12,9 +12,13 @@ namespace ug {
 
 constexpr uint32_t FULL = 0xffffffffu;
 constexpr uint64_t NONE = ~0ull;
-constexpr int NT = 256;           // data threads per CTA for the tile kernels
+#ifndef UG_NT
+#define UG_NT 512
+#endif
+constexpr int NT = UG_NT;         // data threads per CTA for the tile kernels
 constexpr int LNT = 512;          // threads per CTA for the length reductions
-constexpr int TILE = 8192;        // input bytes per tile (8 Ki UTF-8 bytes / 4 Ki UTF-16 words)
+constexpr int TILE = NT * 32;     // input bytes per tile (32 per data thread)
+constexpr int CTAS_PER_SM = 1024 / NT;  // transcoder CTAs per SM (register budget)
 constexpr int BPT = TILE / NT;    // 32 contiguous input bytes per thread
 #ifndef UG_LB_PER_LANE
 #define UG_LB_PER_LANE 8
@@ -108,6 +112,10 @@ __device__ __forceinline__ void st_relaxed(uint64_t *p, uint64_t v) {
 
 __device__ __forceinline__ void sts8(uint32_t addr, uint32_t v) {
   asm volatile("st.shared.u8 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+template <int OFF>  // st.shared.u8 [addr + OFF] with the offset as an immediate
+__device__ __forceinline__ void sts8o(uint32_t addr, uint32_t v) {
+  asm volatile("st.shared.u8 [%0+%2], %1;" ::"r"(addr), "r"(v), "n"(OFF) : "memory");
 }
 __device__ __forceinline__ void sts16(uint32_t addr, uint32_t v) {
   asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((unsigned short)v) : "memory");

@@ -59,5 +59,6 @@ void combine_host(const RecordDev *recs, int nranks, int rank, unsigned long lon
 
 #ifdef UG_TRACE
 cudaError_t trace_read(void *host, size_t bytes);
+cudaError_t dbg_read(void *host);
 #endif
 }  // namespace ug

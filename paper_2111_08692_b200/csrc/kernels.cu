@@ -29,7 +29,8 @@ namespace ug {
 #ifdef UG_TRACE
 // Debug trace (tools only): per CTA, per iteration: [tile, lb_start, lb_end, rounds, pwait_start, pwait_end]
 constexpr int TR_IT = 64;
-__device__ unsigned long long g_trace[1024][TR_IT][8];
+__device__ unsigned long long g_trace[1024][TR_IT][12];
+__device__ unsigned long long g_dbg[8];  // [0] warps rescanned (validate), [1] tiles rescanned (transcode)
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
@@ -40,8 +41,6 @@ __device__ __forceinline__ unsigned long long gtime() {
 constexpr unsigned long long VALMASK = (1ull << 38) - 1;
 // named barrier ids (0 is __syncthreads)
 constexpr int BAR_DATA = 1;           // the NT data threads
-constexpr int BAR_C0 = 2, BAR_C1 = 3;  // data -> look-back warp: tile aggregate ready
-constexpr int BAR_P0 = 4, BAR_P1 = 5;  // look-back warp -> data: tile prefix ready
 
 __device__ __forceinline__ uint32_t byte_at(const Window &w, long long pos) {
   return (pos >= w.lo_valid && pos < w.hi_valid) ? (uint32_t)w.base[pos] : 0u;
@@ -217,6 +216,7 @@ struct U8Pol {
     uint32_t err;    // classifier flags (a3)
     long long pos0;  // position of own byte 0
     long long n;
+    const uint8_t *img;  // own bytes in the smem tile image
     bool wasc;
   };
 
@@ -226,6 +226,7 @@ struct U8Pol {
   __device__ static __forceinline__ void load(St &s, const uint8_t *buf, int tid, int lane,
                                               long long tp, long long n) {
     const uint8_t *my = buf + HALO + BPT * tid;
+    s.img = my;
     {
       uint4 q0 = *reinterpret_cast<const uint4 *>(my);
       uint4 q1 = *reinterpret_cast<const uint4 *>(my + 16);
@@ -288,18 +289,35 @@ struct U8Pol {
   __device__ static __forceinline__ void decode(const St &s, uint16_t *stage, uint32_t o,
                                                 uint32_t, long long) {
     if (IN && s.wasc) {
-      if ((o & 1u) == 0u) {
-        uint32_t *st32 = reinterpret_cast<uint32_t *>(stage + o);
+      // a2: the warp's 1 KiB is ASCII and its 1024 units are contiguous from lane 0's slot.
+      // Written cooperatively: lane l zero-extends warp words l, l + 32, ... (read back from
+      // the tile image), so each store instruction covers consecutive 8-byte chunks.
+      const int lane = threadIdx.x & 31;
+      const uint32_t *wb = reinterpret_cast<const uint32_t *>(s.img - BPT * lane) + lane;
+      const uint32_t o0 = __shfl_sync(FULL, o, 0);
+      uint16_t *sb = stage + o0 + 4 * lane;
+      if ((o0 & 3u) == 0u) {  // warp-uniform
 #pragma unroll
-        for (int k = 0; k < 8; k++) {
-          st32[2 * k] = prmt(s.w[k], 0u, 0x4140u);
-          st32[2 * k + 1] = prmt(s.w[k], 0u, 0x4342u);
+        for (int j = 0; j < 8; j++) {
+          const uint32_t x = wb[32 * j];
+          *reinterpret_cast<uint2 *>(sb + 128 * j) =
+              make_uint2(prmt(x, 0u, 0x4140u), prmt(x, 0u, 0x4342u));
+        }
+      } else if ((o0 & 1u) == 0u) {
+#pragma unroll
+        for (int j = 0; j < 8; j++) {
+          const uint32_t x = wb[32 * j];
+          uint32_t *d = reinterpret_cast<uint32_t *>(sb + 128 * j);
+          d[0] = prmt(x, 0u, 0x4140u);
+          d[1] = prmt(x, 0u, 0x4342u);
         }
       } else {
 #pragma unroll
-        for (int k = 0; k < 8; k++)
+        for (int j = 0; j < 8; j++) {
+          const uint32_t x = wb[32 * j];
 #pragma unroll
-          for (int j = 0; j < 4; j++) stage[o + 4 * k + j] = (uint16_t)((s.w[k] >> (8 * j)) & 0xFFu);
+          for (int q = 0; q < 4; q++) sb[128 * j + q] = (uint16_t)((x >> (8 * q)) & 0xFFu);
+        }
       }
       return;
     }
@@ -372,6 +390,7 @@ struct U16Pol {
   static constexpr int STAGE = 3 * (TILE / 2) + 64;
   struct St {
     uint32_t w[8];                   // words 2k (low half), 2k + 1 (high half) of w[k]
+    const uint8_t *img;              // own words in the smem tile image
     uint32_t prev_word, next_word;
     uint32_t own;                    // bit i: word i owned (all set in interior tiles)
     unsigned long long first_err;
@@ -388,6 +407,7 @@ struct U16Pol {
                                               long long tp_bytes, long long n_bytes) {
     const long long tpw = tp_bytes / 2, nw = n_bytes / 2;
     const uint8_t *my = buf + HALO + BPT * tid;
+    s.img = my;
     {
       uint4 q0 = *reinterpret_cast<const uint4 *>(my);
       uint4 q1 = *reinterpret_cast<const uint4 *>(my + 16);
@@ -458,13 +478,26 @@ struct U16Pol {
   __device__ static __forceinline__ void decode(const St &s, uint8_t *stage, uint32_t o,
                                                 uint32_t lim, long long) {
     if (IN && s.wasc) {
-      if ((o & 3u) == 0u) {
-        uint32_t *st32 = reinterpret_cast<uint32_t *>(stage + o);
+      // a2: the warp's 512 words are ASCII, its 512 output bytes contiguous from lane 0's
+      // slot; lane l narrows warp word quads l, l + 32, ... so stores cover consecutive bytes.
+      const int lane = threadIdx.x & 31;
+      const uint2 *wb = reinterpret_cast<const uint2 *>(s.img - BPT * lane) + lane;
+      const uint32_t o0 = __shfl_sync(FULL, o, 0);
+      uint8_t *sb = stage + o0 + 4 * lane;
+      if ((o0 & 3u) == 0u) {  // warp-uniform
 #pragma unroll
-        for (int k = 0; k < 4; k++) st32[k] = prmt(s.w[2 * k], s.w[2 * k + 1], 0x6420u);
+        for (int j = 0; j < 4; j++) {
+          const uint2 x = wb[32 * j];
+          *reinterpret_cast<uint32_t *>(sb + 128 * j) = prmt(x.x, x.y, 0x6420u);
+        }
       } else {
 #pragma unroll
-        for (int i = 0; i < 16; i++) stage[o + i] = (uint8_t)(s.w[i >> 1] >> (16 * (i & 1)));
+        for (int j = 0; j < 4; j++) {
+          const uint2 x = wb[32 * j];
+          const uint32_t v = prmt(x.x, x.y, 0x6420u);
+#pragma unroll
+          for (int q = 0; q < 4; q++) sb[128 * j + q] = (uint8_t)(v >> (8 * q));
+        }
       }
       return;
     }
@@ -489,13 +522,13 @@ struct U16Pol {
       for (int j = 0; j < 4; j++) {
         const uint32_t b0 = O0 >> (8 * j), b1 = O1 >> (8 * j), b2 = O2 >> (8 * j);
         if (g < 3) {
-          sts8(A[j], b0);
-          sts8(A[j] + 1, b1);
-          sts8(A[j] + 2, b2);
+          sts8o<0>(A[j], b0);
+          sts8o<1>(A[j], b1);
+          sts8o<2>(A[j], b2);
         } else {
-          if (A[j] < pend) sts8(A[j], b0);
-          if (A[j] + 1 < pend) sts8(A[j] + 1, b1);
-          if (A[j] + 2 < pend) sts8(A[j] + 2, b2);
+          if (A[j] < pend) sts8o<0>(A[j], b0);
+          if (A[j] + 1 < pend) sts8o<1>(A[j], b1);
+          if (A[j] + 2 < pend) sts8o<2>(A[j], b2);
         }
       }
       p += inc >> 24;
@@ -552,7 +585,7 @@ __device__ __forceinline__ void finish_call(const TileArgs &a, bool xc, int tid,
 constexpr int VRING = 4;
 
 template <class Pol>
-__global__ void __launch_bounds__(NT, 4) k_validate(const TileArgs a) {
+__global__ void __launch_bounds__(NT, CTAS_PER_SM) k_validate(const TileArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t mb_full[VRING], mb_empty[VRING];
   __shared__ int s_last;
@@ -607,6 +640,10 @@ __global__ void __launch_bounds__(NT, 4) k_validate(const TileArgs a) {
     __syncwarp();
     if (lane == 0) mbar_arrive(&mb_empty[sl]);  // this warp is done with the image
     if (__any_sync(FULL, Pol::hint(st))) {       // a4 (cold)
+#ifdef UG_TRACE
+      if (lane == 0) atomicAdd(&g_dbg[0], 1ull);
+      if (lane == 0 && g_dbg[2] == 0) { g_dbg[2] = 1; g_dbg[3] = (unsigned long long)t; g_dbg[4] = warp; }
+#endif
       const unsigned long long e = Pol::find_error(st, n_units);
       if (e != NONE) atomicMin(&a.ctr->err_min, e);
     }
@@ -686,7 +723,7 @@ __device__ __forceinline__ void emit_tile(const TileArgs &a, const uint8_t *img,
 //    still-resident input image straight into the stage at its global 16-byte phase and
 //    shipped by one TMA bulk store.
 template <class Pol>
-__global__ void __launch_bounds__(NT + 32 * NLB, 4) k_transcode(const TileArgs a) {
+__global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const TileArgs a) {
   using Out = typename Pol::Out;
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t *ring = smem;                                         // RING input tile images
@@ -706,9 +743,8 @@ __global__ void __launch_bounds__(NT + 32 * NLB, 4) k_transcode(const TileArgs a
   const long long ntiles = (long long)a.ntiles;
   const long long n_units = win.n / Pol::UNIT;
 
-  // Thread 0: take the next ticket and start loading it into ring slot `slot`.
-  auto next_tile = [&](int slot) {
-    const long long tn = (long long)atomicAdd(&a.ctr->ticket, 1u);
+  // Thread 0: publish ticket tn for ring slot `slot` and start loading its tile.
+  auto start_tile = [&](int slot, long long tn) {
     s_t[slot] = tn;
     mbar_arrive(&mb_tick[slot]);  // the look-back of tile tn can start now
     if (tn < ntiles) {
@@ -729,7 +765,7 @@ __global__ void __launch_bounds__(NT + 32 * NLB, 4) k_transcode(const TileArgs a
     }
     s_flag[0] = s_flag[1] = 0;
     fence_mbar_init();
-    next_tile(0);
+    start_tile(0, (long long)atomicAdd(&a.ctr->ticket, 1u));
   }
   __syncthreads();
 
@@ -789,20 +825,28 @@ __global__ void __launch_bounds__(NT + 32 * NLB, 4) k_transcode(const TileArgs a
         g_trace[blockIdx.x][j][5] = gtime();
       }
 #endif
+      if (tid == 0) bulk_wait_read_all();  // the previous bulk store has read the stage
+      named_sync<BAR_DATA, NT>();
       emit_tile<Pol>(a, ring + js * INBUF, s_t[js], s_pre[js], s_cnt[js], ex[j & 1], cn[j & 1],
                      stage, tid, lane);
     };
     while (true) {
       const int sl = i % RING;
-#if !defined(UG_LATE_TICKET) && !defined(UG_MID_TICKET)
-      if (tid == 0) {
-        bulk_wait_read_all();  // the previous bulk store has read the stage (barrier below)
-        next_tile((i + 1) % RING);  // its slot held tile i - 3, emitted last iteration
-      }
-#else
-      if (tid == 0) bulk_wait_read_all();  // the previous bulk store has read the stage
+      // The next ticket: the atomic is issued now and its result used only after this
+      // thread's share of the classification, so its L2 round trip is off the critical path
+      // (every warp waits for warp 0 at the block scan).
+      long long tn = 0;
+      if (tid == 0) tn = (long long)atomicAdd(&a.ctr->ticket, 1u);
+#ifdef UG_TRACE
+      const unsigned long long lw0 = gtime();
 #endif
       mbar_wait(&mb_load[sl], (i / RING) & 1);
+#ifdef UG_TRACE
+      if (tid == 0 && i < TR_IT && blockIdx.x < 1024) {
+        g_trace[blockIdx.x][i][8] = lw0;
+        g_trace[blockIdx.x][i][9] = gtime();
+      }
+#endif
       const long long t = s_t[sl];
       if (t >= ntiles) break;
       uint8_t *img = ring + sl * INBUF;
@@ -821,6 +865,8 @@ __global__ void __launch_bounds__(NT + 32 * NLB, 4) k_transcode(const TileArgs a
         cnt = Pol::template analyze<false>(st, tid, true);
       }
       if (Pol::hint(st)) s_flag[i & 1] = 1;
+      // ring slot (i + 1) % RING held tile i - 3, emitted last iteration
+      if (tid == 0) start_tile((i + 1) % RING, tn);
       uint32_t excl = 0, C = 0;
       block_scan(cnt, s_wsum[i & 1], lane, warp, &excl, &C);
       if (tid == 0) {
@@ -831,31 +877,28 @@ __global__ void __launch_bounds__(NT + 32 * NLB, 4) k_transcode(const TileArgs a
         // s_flag[(i + 1) & 1] was last read after the block scan of i - 1; it is next set
         // after the load of tile i + 1 lands
         s_flag[(i + 1) & 1] = 0;
-#ifdef UG_MID_TICKET
-        // the next tile: its load overlaps the emit of tile i - 2 below
-        next_tile((i + 1) % RING);
-#endif
       }
       if (s_flag[i & 1]) {  // a4 (cold): straight to the call's minimum
+#ifdef UG_TRACE
+        if (tid == 0) atomicAdd(&g_dbg[1], 1ull);
+        if (Pol::hint(st) && g_dbg[5] == 0) { g_dbg[5] = 1; g_dbg[6] = (unsigned long long)t; g_dbg[7] = tid; }
+#endif
         unsigned long long e = Pol::find_error(st, n_units);
         if (e != NONE) atomicMin(&a.ctr->err_min, e);
       }
+#ifdef UG_TRACE
+      if (tid == 0 && i < TR_IT && blockIdx.x < 1024) g_trace[blockIdx.x][i][10] = gtime();  // AGG
+#endif
       if (i >= 2) emit(i - 2);  // a7, a8
+#ifdef UG_TRACE
+      if (tid == 0 && i < TR_IT && blockIdx.x < 1024) g_trace[blockIdx.x][i][11] = gtime();  // end
+#endif
       ex[i & 1] = excl;  // tile i - 2's slot is free now
       cn[i & 1] = cnt;
-#ifdef UG_LATE_TICKET
-      // take the next ticket only now: between a ticket and its tile's aggregate there is
-      // no wait on other CTAs (the load latency is covered by the other CTAs on the SM)
-      if (tid == 0) next_tile((i + 1) % RING);
-#endif
       i++;
     }
     // drain: tiles i - 2 and i - 1
-    for (int j = (i >= 2 ? i - 2 : 0); j < i; j++) {
-      if (tid == 0) bulk_wait_read_all();
-      named_sync<BAR_DATA, NT>();  // the stage is free again
-      emit(j);
-    }
+    for (int j = (i >= 2 ? i - 2 : 0); j < i; j++) emit(j);
     if (tid == 0) bulk_wait_all();  // all output written before the CTA retires
   }
   __syncthreads();
@@ -1021,6 +1064,7 @@ void combine_host(const RecordDev *recs, int nranks, int rank, unsigned long lon
 
 // ============================================================================ launchers
 #ifdef UG_TRACE
+cudaError_t dbg_read(void *host) { return cudaMemcpyFromSymbol(host, g_dbg, sizeof(g_dbg)); }
 cudaError_t trace_read(void *host, size_t bytes) {
   return cudaMemcpyFromSymbol(host, g_trace, bytes < sizeof(g_trace) ? bytes : sizeof(g_trace));
 }

@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+timeout -s KILL 600 python -m pytest tests/test_gpu_parity.py -x -q 2>&1 | tail -1 > gpurun_out/exp18.log
+for c in "c1 1024" "c4 1024"; do set -- $c; OPS=utf8_to_utf16le,utf16le_to_utf8 timeout 300 python tools/opbench.py $1 $2 10 >> gpurun_out/exp18.log 2>&1; done
+UG_LIB_OVERRIDE=build_variants/libunigpu_trace.so timeout 300 python tools/trace2.py c1 1024 >> gpurun_out/exp18.log 2>&1
