@@ -253,7 +253,11 @@ struct U8Pol {
   __device__ static __forceinline__ uint32_t analyze(St &s, int tid, bool xc) {
     uint32_t emit = 0xFFFFFFFFu;
     s.err = 0;
+#ifdef UG_ABL_NOVAL
+    emit = ~s.w[0] & 0x80808080u;
+#else
     if (!s.wasc) s.err = u8::analyze32(s.w, s.prev, s.nxt, (tid & 31) == 31, &emit);  // a3, a5
+#endif
     if (!xc) return 0u;
     if (!IN) emit &= bit_range(s.pos0, 0, s.n);
     return popc(emit);
@@ -321,6 +325,19 @@ struct U8Pol {
       }
       return;
     }
+#ifdef UG_ABL_NODECODE
+    {
+      uint32_t p = smem_addr(stage + o);
+#pragma unroll
+      for (int k = 0; k < 8; k++) {
+        uint32_t em = (~s.w[k] >> 7) & 0x01010101u;
+        const uint32_t inc2 = em * 0x02020202u;
+        sts16(p, s.w[k]);
+        p += inc2 >> 24;
+      }
+      return;
+    }
+#endif
     u8::Carry cy = u8::carry_of(s.prev);
     uint32_t p = smem_addr(stage + o);  // shared-window byte address of this thread's slot
 #pragma unroll
@@ -332,7 +349,7 @@ struct U8Pol {
       const uint32_t a1 = mad(prmt(inc2, 0u, 0x4440u), 1u, p);
       const uint32_t a2 = mad(prmt(inc2, 0u, 0x4441u), 1u, p);
       const uint32_t a3 = mad(prmt(inc2, 0u, 0x4442u), 1u, p);
-      const uint32_t u1 = u01 >> 16, u3 = u23 >> 16;
+      const uint32_t u1 = shr_fma<16>(u01), u3 = shr_fma<16>(u23);
       if (k < 7) {
         sts16(p, u01);
         sts16(a1, u1);
@@ -344,7 +361,7 @@ struct U8Pol {
         if (em & 0x00010000u) sts16(a2, u23);
         if (em & 0x01000000u) sts16(a3, u3);
       }
-      p += inc2 >> 24;
+      p += shr_fma<24>(inc2);
     }
   }
 
@@ -736,7 +753,7 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
   __shared__ long long s_t[RING];
   __shared__ uint32_t s_cnt[RING];
   __shared__ unsigned long long s_pre[RING];
-  __shared__ int s_flag[2], s_last;
+  __shared__ int s_flag[3], s_last;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const Window &win = a.win;
@@ -763,7 +780,7 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
       mbar_init(&mb_agg[j], 1);
       mbar_init(&mb_pre[j], 1);
     }
-    s_flag[0] = s_flag[1] = 0;
+    s_flag[0] = s_flag[1] = s_flag[2] = 0;
     fence_mbar_init();
     start_tile(0, (long long)atomicAdd(&a.ctr->ticket, 1u));
   }
@@ -798,7 +815,11 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
         g_trace[blockIdx.x][i][7] = polls;
       }
 #else
+#ifdef UG_ABL_NOLB
+      const unsigned long long P = (unsigned long long)t * (TILE / 2);
+#else
       const unsigned long long P = tile_excl_prefix(a, t, lane);
+#endif
 #endif
 #ifdef UG_LB_AT_TICKET
       mbar_wait(&mb_agg[sl], ph);
@@ -864,9 +885,14 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
         Pol::template load<false>(st, img, tid, lane, tp, win.n);
         cnt = Pol::template analyze<false>(st, tid, true);
       }
-      if (Pol::hint(st)) s_flag[i & 1] = 1;
-      // ring slot (i + 1) % RING held tile i - 3, emitted last iteration
-      if (tid == 0) start_tile((i + 1) % RING, tn);
+      if (Pol::hint(st)) s_flag[i % 3] = 1;
+      if (tid == 0) {
+        // ring slot (i + 1) % RING held tile i - 3, emitted last iteration
+        start_tile((i + 1) % RING, tn);
+        // flag slot of tile i + 1: last read after the block scan of i - 2 (every thread has
+        // passed the block scan of i - 1 since), next written after the block scan of i
+        s_flag[(i + 1) % 3] = 0;
+      }
       uint32_t excl = 0, C = 0;
       block_scan(cnt, s_wsum[i & 1], lane, warp, &excl, &C);
       if (tid == 0) {
@@ -874,11 +900,8 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
         st_relaxed(a.status + t, pack_status(a.epoch, t == 0 ? FLAG_PREFIX : FLAG_AGG, C));
         s_cnt[sl] = C;
         mbar_arrive(&mb_agg[sl]);
-        // s_flag[(i + 1) & 1] was last read after the block scan of i - 1; it is next set
-        // after the load of tile i + 1 lands
-        s_flag[(i + 1) & 1] = 0;
       }
-      if (s_flag[i & 1]) {  // a4 (cold): straight to the call's minimum
+      if (s_flag[i % 3]) {  // a4 (cold): straight to the call's minimum
 #ifdef UG_TRACE
         if (tid == 0) atomicAdd(&g_dbg[1], 1ull);
         if (Pol::hint(st) && g_dbg[5] == 0) { g_dbg[5] = 1; g_dbg[6] = (unsigned long long)t; g_dbg[7] = tid; }

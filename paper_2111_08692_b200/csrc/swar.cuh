@@ -69,6 +69,17 @@ UG_HD uint32_t umulhi(uint32_t a, uint32_t b) {
   return (uint32_t)(((uint64_t)a * b) >> 32);
 #endif
 }
+// x >> S as IMAD.HI (FMA pipe, half rate): for code whose ALU pipe is the bottleneck.
+template <int S>
+UG_HD uint32_t shr_fma(uint32_t x) {
+#if defined(__CUDA_ARCH__)
+  uint32_t d;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(d) : "r"(x), "n"(1u << (32 - S)));
+  return d;
+#else
+  return x >> S;
+#endif
+}
 // a * b + c on the FMA pipe (IMAD).
 UG_HD uint32_t mad(uint32_t a, uint32_t b, uint32_t c) {
 #if defined(__CUDA_ARCH__)
