@@ -18,7 +18,10 @@ constexpr uint64_t NONE = ~0ull;
 constexpr int NT = UG_NT;         // data threads per CTA for the tile kernels
 constexpr int LNT = 512;          // threads per CTA for the length reductions
 constexpr int TILE = NT * 32;     // input bytes per tile (32 per data thread)
-constexpr int CTAS_PER_SM = 1024 / NT;  // transcoder CTAs per SM (register budget)
+#ifndef UG_CPS
+#define UG_CPS (1024 / UG_NT)
+#endif
+constexpr int CTAS_PER_SM = UG_CPS;  // transcoder CTAs per SM (register budget)
 constexpr int BPT = TILE / NT;    // 32 contiguous input bytes per thread
 #ifndef UG_LB_PER_LANE
 #define UG_LB_PER_LANE 8
@@ -241,7 +244,11 @@ __device__ __forceinline__ bool look_back_round(uint64_t *status, uint32_t epoch
     }
     if (polls) ++*polls;
     if (__all_sync(FULL, ready)) break;
-    __nanosleep(spins < 2 ? 128 : 512);
+#ifndef UG_SLEEP0
+#define UG_SLEEP0 128
+#define UG_SLEEP1 512
+#endif
+    __nanosleep(spins < 2 ? UG_SLEEP0 : UG_SLEEP1);
     ++spins;
     bool stop2 = false;
 #pragma unroll
@@ -271,6 +278,29 @@ __device__ __forceinline__ bool look_back_round(uint64_t *status, uint32_t epoch
   }
   *excl += warp_sum64(lane_sum);
   return false;
+}
+
+// Push-forward (after tile t's inclusive prefix `incl` is known): publish the inclusive
+// prefixes of the run of successors t+1, t+2, ... (up to 32) whose aggregates are already
+// published.  An inclusive prefix is unique, so a push racing with the tile's own look-back (or
+// another push) writes the same value.  Keeps the published-prefix frontier close behind the
+// aggregate frontier, so look-backs resolve in their first, 32-wide probe.
+__device__ __forceinline__ void push_forward(uint64_t *status, uint32_t epoch, long long t,
+                                             long long ntiles, uint64_t incl, int lane) {
+  const long long j = t + 1 + lane;
+  uint64_t w = (j < ntiles) ? ld_relaxed(status + j) : 0ull;
+  const uint32_t fl = ((uint32_t)(w >> 40) == epoch) ? (uint32_t)((w >> 38) & 3u) : 0u;
+  // the run: lanes below the first lane that is unpublished or already an inclusive prefix
+  const uint32_t stop = __ballot_sync(FULL, fl != FLAG_AGG);
+  const int run = stop ? __ffs(stop) - 1 : 32;
+  uint64_t v = (lane < run) ? (w & ((1ull << 38) - 1)) : 0ull;
+  // inclusive scan of the aggregates over the run
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint64_t o = __shfl_up_sync(FULL, v, d);
+    if (lane >= d) v += o;
+  }
+  if (lane < run) st_relaxed(status + j, pack_status(epoch, FLAG_PREFIX, incl + v));
 }
 
 // Exclusive prefix of tile t (t > 0): the sum of all earlier tiles' aggregates, from the

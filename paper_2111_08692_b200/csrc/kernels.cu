@@ -446,6 +446,10 @@ struct U16Pol {
   // a9 pairing predicate (exact) and a5 widths, byte-SWAR over 4 words.
   template <bool IN>
   __device__ static __forceinline__ uint32_t analyze(St &s, int, bool xc) {
+#ifdef UG_ABL_NOVAL
+    s.first_err = NONE;
+    return xc ? 16u : 0u;
+#endif
     uint32_t Hprev = u16::is_high(s.prev_word) ? 0x80000000u : 0u;  // byte 3 = word -1
     u16::Cls4 c = u16::classes4(s.w[0], s.w[1]);
     uint32_t acc = 0, anyerr = 0, errm[4];
@@ -518,6 +522,14 @@ struct U16Pol {
       }
       return;
     }
+#ifdef UG_ABL_NODECODE
+    {
+      uint8_t *q = stage + o;
+#pragma unroll
+      for (int k = 0; k < 8; k++) q[k] = (uint8_t)s.w[k];
+      return;
+    }
+#endif
     uint32_t p = smem_addr(stage + o);
     const uint32_t pend = smem_addr(stage + lim);
     uint32_t lprev = (s.prev_word & 0xFFu) << 24;
@@ -824,11 +836,15 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
 #ifdef UG_LB_AT_TICKET
       mbar_wait(&mb_agg[sl], ph);
 #endif
+      const unsigned long long incl = P + s_cnt[sl];
       if (lane == 0) {
-        if (t != 0) st_relaxed(a.status + t, pack_status(a.epoch, FLAG_PREFIX, P + s_cnt[sl]));
+        if (t != 0) st_relaxed(a.status + t, pack_status(a.epoch, FLAG_PREFIX, incl));
         s_pre[sl] = P;
         mbar_arrive(&mb_pre[sl]);
       }
+#ifndef UG_NO_PUSH
+      push_forward(a.status, a.epoch, t, ntiles, incl, lane);
+#endif
     }
   } else {
     // ------------------------------------------------------------ data warps
@@ -919,6 +935,15 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
       ex[i & 1] = excl;  // tile i - 2's slot is free now
       cn[i & 1] = cnt;
       i++;
+    }
+    // every look-back agent must see a past-the-end ticket to stop: the one owning tile i has;
+    // post the same for the others (their slots are free: tiles i - 3.. were emitted)
+    if (tid == 0) {
+#pragma unroll
+      for (int k = 1; k < NLB; k++) {
+        s_t[(i + k) % RING] = ntiles;
+        mbar_arrive(&mb_tick[(i + k) % RING]);
+      }
     }
     // drain: tiles i - 2 and i - 1
     for (int j = (i >= 2 ? i - 2 : 0); j < i; j++) emit(j);

@@ -31,7 +31,7 @@ else:
     n16 = ug.utf16_length_from_utf8(t8)
     u16 = torch.empty(n16, dtype=torch.int16, device=dev)
     r = ug.utf8_to_utf16le(t8, u16)
-    assert r.error == 0 or os.environ.get("UG_LIB_OVERRIDE", "").find("_no") >= 0 or os.environ.get("UG_LIB_OVERRIDE", "").find("_both") >= 0 or os.environ.get("UG_LIB_OVERRIDE", "").find("nolb") >= 0, r
+    assert r.error == 0 or os.environ.get("UG_LIB_OVERRIDE", "").find("_no") >= 0 or os.environ.get("UG_LIB_OVERRIDE", "").find("_both") >= 0 or os.environ.get("UG_LIB_OVERRIDE", "").find("nolb") >= 0 or os.environ.get("UG_LIB_OVERRIDE", "").find("bothp") >= 0 or os.environ.get("UG_LIB_OVERRIDE", "").find("both") >= 0 or os.environ.get("UG_LIB_OVERRIDE", "").find("slong") >= 0 or os.environ.get("UG_LIB_OVERRIDE", "").find("sshort") >= 0, r
 n8, n16 = t8.numel(), u16.numel()
 o16 = torch.empty(n8, dtype=torch.int16, device=dev)
 o8 = torch.empty(3 * n16, dtype=torch.uint8, device=dev)
