@@ -8,6 +8,10 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#ifndef UG_MBAR_SUSPEND_NS
+#define UG_MBAR_SUSPEND_NS 20000
+#endif
+
 namespace ug {
 
 constexpr uint32_t FULL = 0xffffffffu;
@@ -68,12 +72,14 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  // try_wait with a suspend-time hint: the warp sleeps until the phase completes (or the hint
+  // expires) instead of spinning on the issue slots the other warps need
   asm volatile(
       "{\n\t.reg .pred p;\n"
       "UG_WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra UG_WAIT_%=;\n}" ::"r"(smem_addr(bar)),
-      "r"(parity)
+      "r"(parity), "n"(UG_MBAR_SUSPEND_NS)
       : "memory");
 }
 // 1-D TMA bulk copy global -> shared, completing on an mbarrier (SASS: UBLKCP).

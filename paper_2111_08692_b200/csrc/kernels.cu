@@ -611,7 +611,10 @@ __device__ __forceinline__ void finish_call(const TileArgs &a, bool xc, int tid,
 // "empty" mbarrier when done with the image and thread 0 refills the slot once all have.  A
 // warp that flags rescans its own 1 KiB (every warp's last lane checks the 3-byte look-ahead,
 // so a flag never has to be resolved by another warp).
-constexpr int VRING = 4;
+#ifndef UG_VRING
+#define UG_VRING 4
+#endif
+constexpr int VRING = UG_VRING;
 
 template <class Pol>
 __global__ void __launch_bounds__(NT, CTAS_PER_SM) k_validate(const TileArgs a) {
