@@ -182,13 +182,24 @@ size_t ug_utf8_cut_backoff(const uint8_t *at, size_t avail_before);
 size_t ug_utf16_cut_backoff(const uint16_t *at, size_t avail_before);
 
 /* ------------------------------------------------------------------ host buffers
- * End-to-end variants on HOST memory (pinned memory gives DMA-speed copies): copy the input
- * to the device, run the fused kernel, copy out[0..written) back, synchronise.  Uses a
- * library-owned device staging area per (device, stream), grown on demand. */
+ * End-to-end variants on HOST memory (pinned memory gives DMA-speed copies in both
+ * directions at once).  Same result as the device functions on the same data.  The input is
+ * processed as a pipeline of chunks of ug_set_host_chunk() input units cut at character starts
+ * (DESIGN.md f2): chunk i is copied in on one copy stream, transcoded as a shard (the sharded
+ * kernel is exact at any cut, D2) on `stream`, and its output copied out on a second
+ * copy stream as soon as its 32-byte record has fixed its output offset, so host->device
+ * copies, kernels and device->host copies overlap.  Uses library-owned device staging (input
+ * + worst-case output) per (device, stream), grown on demand; synchronous (returns when the
+ * output is in out_host).  out_host[0..written) is exact; nothing at or beyond
+ * out_host[out_cap] is written. */
 ug_result utf8_to_utf16le_host(const uint8_t *in_host, size_t n, uint16_t *out_host,
                                size_t out_cap, void *stream);
 ug_result utf16le_to_utf8_host(const uint16_t *in_host, size_t n, uint8_t *out_host,
                                size_t out_cap, void *stream);
+
+/* Chunk size of the host-buffer pipeline, in input code units (default 32 Mi units); returns
+ * the previous value.  0 restores the default.  Process-wide. */
+size_t ug_set_host_chunk(size_t units);
 
 /* ------------------------------------------------------------------ misc */
 /* Human-readable name of a ug_error value (static string). */

@@ -84,6 +84,7 @@ def _load():
         "ug_utf16_cut_backoff": ([P, S], S),
         "utf8_to_utf16le_host": ([P, S, P, S, P], _CResult),
         "utf16le_to_utf8_host": ([P, S, P, S, P], _CResult),
+        "ug_set_host_chunk": ([S], S),
         "ug_error_name": ([I], ctypes.c_char_p),
         "ug_launch_count": ([], U64),
         "ug_release_workspaces": ([], None),
@@ -316,8 +317,14 @@ def utf16_cut_backoff(words, at: int) -> int:
 
 
 # --------------------------------------------------------------------------- host buffers
+def set_host_chunk(units: int) -> int:
+    """Chunk size (input units) of the pipelined host-buffer path; returns the previous one."""
+    return int(lib.ug_set_host_chunk(units))
+
+
 def utf8_to_utf16le_host(t_in_host, t_out_host, stream=None) -> Result:
-    """End-to-end: host (pinned) uint8 tensor -> host int16 tensor, H2D + kernel + D2H."""
+    """End-to-end: host (pinned) uint8 tensor -> host int16 tensor; chunked pipeline of
+    H2D / kernel / D2H on overlapping streams."""
     return _res(lib.utf8_to_utf16le_host(_ptr(t_in_host), _units(t_in_host), _ptr(t_out_host),
                                          _units(t_out_host), _stream(stream)))
 

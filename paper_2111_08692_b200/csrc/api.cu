@@ -8,6 +8,7 @@
 #include <map>
 #include <mutex>
 #include <utility>
+#include <vector>
 
 #include "../../include/unigpu.h"
 #include "internal.h"
@@ -21,6 +22,8 @@ static_assert(sizeof(ug_shard_record) == 32, "record is 32 bytes");
 namespace {
 
 std::atomic<uint64_t> g_launches{0};
+constexpr size_t HOST_CHUNK_DEFAULT = 32ull << 20;  // input units per pipelined host chunk
+std::atomic<size_t> g_host_chunk{HOST_CHUNK_DEFAULT};
 constexpr unsigned long long MAX_N = (1ull << 38) - 1;  // status words carry 38-bit values
 
 struct Workspace {
@@ -39,6 +42,13 @@ struct Workspace {
   size_t d_in_cap = 0;
   void *d_out = nullptr;
   size_t d_out_cap = 0;
+  // host-buffer pipeline (run_host): copy streams, per-chunk events and shard records
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  cudaEvent_t ev_start = nullptr;
+  std::vector<cudaEvent_t> ev_in, ev_done;
+  RecordDev *d_recs = nullptr;
+  RecordDev *h_recs = nullptr;  // pinned
+  size_t rec_cap = 0;
 };
 
 struct DeviceInfo {
@@ -281,35 +291,137 @@ cudaError_t ensure_staging(Workspace *w, size_t in_bytes, size_t out_bytes) {
   return cudaSuccess;
 }
 
-// Host-buffer transcode: H2D, one fused kernel, D2H of out[0..written).
+// Per-chunk resources of the host pipeline: two copy streams, an input-landed and a
+// kernel-done event per chunk, one shard record per chunk (device + pinned copy).
+cudaError_t ensure_pipeline(Workspace *w, size_t nchunks) {
+  cudaError_t e;
+  if (!w->h2d) {
+    if ((e = cudaStreamCreateWithFlags(&w->h2d, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaStreamCreateWithFlags(&w->d2h, cudaStreamNonBlocking)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&w->ev_start, cudaEventDisableTiming)) != cudaSuccess)
+      return e;
+  }
+  while (w->ev_in.size() < nchunks) {
+    cudaEvent_t a, b;
+    if ((e = cudaEventCreateWithFlags(&a, cudaEventDisableTiming)) != cudaSuccess) return e;
+    if ((e = cudaEventCreateWithFlags(&b, cudaEventDisableTiming)) != cudaSuccess) return e;
+    w->ev_in.push_back(a);
+    w->ev_done.push_back(b);
+  }
+  if (nchunks > w->rec_cap) {
+    cudaFree(w->d_recs);
+    cudaFreeHost(w->h_recs);
+    w->d_recs = nullptr;
+    w->h_recs = nullptr;
+    w->rec_cap = 0;
+    if ((e = cudaMalloc(&w->d_recs, nchunks * sizeof(RecordDev))) != cudaSuccess) return e;
+    if ((e = cudaMallocHost(&w->h_recs, nchunks * sizeof(RecordDev))) != cudaSuccess) return e;
+    w->rec_cap = nchunks;
+  }
+  return cudaSuccess;
+}
+
+// Host-buffer transcode as a three-stage pipeline over chunks of the input (DESIGN.md f2):
+//   h2d stream:  copy chunk i into the device staging input (all chunks enqueued up front);
+//   `s`:         once chunks i and i+1 have landed (i+1 holds the after-halo), the fused kernel
+//                transcodes chunk i as a shard (exact at any cut, D2) into the
+//                staging output at an upper-bound offset, and its 32-byte record is copied to
+//                pinned memory;
+//   d2h stream:  the host waits for record i, which fixes chunk i's output offset (the prefix
+//                of the earlier chunks' counts), and enqueues the copy of its output units.
+// Copies in both directions and the kernels overlap; the result is combined from the records
+// exactly as the unsharded kernel states it (first error, written, output too small).
 ug_result run_host(Op op, const void *in_host, unsigned long long n, void *out_host,
                    unsigned long long out_cap, cudaStream_t s) {
   const bool u16in = op == Op::U16_TO_U8;
   const size_t ius = u16in ? 2 : 1, ous = u16in ? 1 : 2;
+  const unsigned long long ub = u16in ? 3 : 1;  // output units per input unit, at most
+  const unsigned long long halo = u16in ? 1 : 3;
   if (n == 0) return make_result(UG_OK, 0, 0);
   if (in_host == nullptr || (out_host == nullptr && out_cap > 0))
     return make_result(UG_ERR_ARG, 0, 0);
-  unsigned long long bound = u16in ? 3 * n : n;  // at most this many output units
-  unsigned long long cap = out_cap < bound ? out_cap : bound;
+  if (n > MAX_N) return make_result(UG_ERR_ARG, 0, 0);
   Workspace *w;
   if (get_ws(s, &w) != cudaSuccess) return make_result(UG_ERR_CUDA, 0, 0);
+  // chunk cuts at character starts (the kernel is exact at any cut; this keeps chunks whole)
+  const unsigned long long C = g_host_chunk.load() ? g_host_chunk.load() : HOST_CHUNK_DEFAULT;
+  std::vector<unsigned long long> cut;
+  cut.push_back(0);
+  for (unsigned long long c = C; c < n; c += C) {
+    unsigned long long k = u16in ? ug_utf16_cut_backoff((const uint16_t *)in_host + c, c)
+                                 : ug_utf8_cut_backoff((const uint8_t *)in_host + c, c);
+    if (c - k > cut.back()) cut.push_back(c - k);
+  }
+  cut.push_back(n);
+  const size_t nch = cut.size() - 1;
   {
     std::lock_guard<std::mutex> lk(w->mu);
-    if (ensure_staging(w, n * ius, (cap ? cap : 1) * ous) != cudaSuccess)
-      return make_result(UG_ERR_CUDA, 0, 0);
-    if (cudaMemcpyAsync(w->d_in, in_host, n * ius, cudaMemcpyHostToDevice, s) != cudaSuccess)
-      return make_result(UG_ERR_CUDA, 0, 0);
-  }
-  ug_result r = run_sync(op, w->d_in, n, w->d_out, cap, s);
-  if (r.error < 0) return r;
-  if (r.written) {
-    std::lock_guard<std::mutex> lk(w->mu);
-    if (cudaMemcpyAsync(out_host, w->d_out, r.written * ous, cudaMemcpyDeviceToHost, s) !=
-            cudaSuccess ||
-        cudaStreamSynchronize(s) != cudaSuccess)
+    if (ensure_staging(w, n * ius, n * ub * ous) != cudaSuccess ||
+        ensure_pipeline(w, nch) != cudaSuccess)
       return make_result(UG_ERR_CUDA, 0, 0);
   }
-  return r;
+  const uint8_t *hin = (const uint8_t *)in_host;
+  uint8_t *din = (uint8_t *)w->d_in, *dout = (uint8_t *)w->d_out;
+  // stage 1: all input copies, ordered after earlier work on the caller's stream
+  if (cudaEventRecord(w->ev_start, s) != cudaSuccess ||
+      cudaStreamWaitEvent(w->h2d, w->ev_start, 0) != cudaSuccess)
+    return make_result(UG_ERR_CUDA, 0, 0);
+  for (size_t i = 0; i < nch; i++) {
+    if (cudaMemcpyAsync(din + cut[i] * ius, hin + cut[i] * ius, (cut[i + 1] - cut[i]) * ius,
+                        cudaMemcpyHostToDevice, w->h2d) != cudaSuccess ||
+        cudaEventRecord(w->ev_in[i], w->h2d) != cudaSuccess)
+      return make_result(UG_ERR_CUDA, 0, 0);
+  }
+  // stage 2: one shard kernel per chunk + its record to pinned memory
+  for (size_t i = 0; i < nch; i++) {
+    const unsigned long long lo = cut[i], hi = cut[i + 1];
+    const unsigned long long hb = lo < halo ? lo : halo, ha = n - hi < halo ? n - hi : halo;
+    if (cudaStreamWaitEvent(s, w->ev_in[i + 1 < nch ? i + 1 : i], 0) != cudaSuccess)
+      return make_result(UG_ERR_CUDA, 0, 0);
+    int rc = enqueue_tile(op, din + lo * ius, hi - lo, hb, ha, lo, dout + lo * ub * ous,
+                          (hi - lo) * ub, nullptr, w->d_recs + i, s);
+    if (rc != UG_OK) return make_result(rc, 0, 0);
+    if (cudaMemcpyAsync(w->h_recs + i, w->d_recs + i, sizeof(RecordDev), cudaMemcpyDeviceToHost,
+                        s) != cudaSuccess ||
+        cudaEventRecord(w->ev_done[i], s) != cudaSuccess)
+      return make_result(UG_ERR_CUDA, 0, 0);
+  }
+  // stage 3: as each record lands, place the chunk's output
+  unsigned long long prefix = 0, e = NONE, wr = 0;
+  int kind = 0;
+  bool fits = true, failed = false;
+  for (size_t i = 0; i < nch && !failed; i++) {
+    if (cudaEventSynchronize(w->ev_done[i]) != cudaSuccess) {
+      failed = true;
+      break;
+    }
+    const RecordDev &r = w->h_recs[i];
+    const unsigned long long units = r.first_err == NONE ? r.count : r.written;
+    if (fits && prefix + units > out_cap) fits = false;
+    if (fits && units) {
+      if (cudaStreamWaitEvent(w->d2h, w->ev_done[i], 0) != cudaSuccess ||
+          cudaMemcpyAsync((uint8_t *)out_host + prefix * ous, dout + cut[i] * ub * ous,
+                          units * ous, cudaMemcpyDeviceToHost, w->d2h) != cudaSuccess) {
+        failed = true;
+        break;
+      }
+    }
+    if (r.first_err != NONE) {
+      e = r.first_err;
+      wr = prefix + r.written;
+      kind = r.kind;
+      break;
+    }
+    prefix += r.count;
+  }
+  // every stage drained before the staging buffers can be reused
+  if (cudaStreamSynchronize(w->d2h) != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess ||
+      cudaStreamSynchronize(w->h2d) != cudaSuccess || failed)
+    return make_result(UG_ERR_CUDA, 0, 0);
+  const unsigned long long required = e == NONE ? prefix : wr;
+  if (required > out_cap) return make_result(UG_ERR_OUTPUT_TOO_SMALL, required, 0);
+  if (e == NONE) return make_result(UG_OK, n, prefix);
+  return make_result(kind, e, wr);
 }
 
 }  // namespace
@@ -448,6 +560,11 @@ ug_result utf16le_to_utf8_host(const uint16_t *in_host, size_t n, uint8_t *out_h
   return run_host(Op::U16_TO_U8, in_host, n, out_host, out_cap, (cudaStream_t)stream);
 }
 
+size_t ug_set_host_chunk(size_t units) {
+  size_t prev = g_host_chunk.exchange(units ? units : HOST_CHUNK_DEFAULT);
+  return prev;
+}
+
 const char *ug_error_name(int err) {
   switch (err) {
     case UG_OK: return "OK";
@@ -482,6 +599,17 @@ void ug_release_workspaces(void) {
       cudaFreeHost(w->h_len);
       cudaFree(w->d_in);
       cudaFree(w->d_out);
+      if (w->h2d) {
+        cudaStreamSynchronize(w->h2d);
+        cudaStreamSynchronize(w->d2h);
+        cudaStreamDestroy(w->h2d);
+        cudaStreamDestroy(w->d2h);
+        cudaEventDestroy(w->ev_start);
+      }
+      for (cudaEvent_t ev : w->ev_in) cudaEventDestroy(ev);
+      for (cudaEvent_t ev : w->ev_done) cudaEventDestroy(ev);
+      cudaFree(w->d_recs);
+      cudaFreeHost(w->h_recs);
       delete w;
       it = g_ws.erase(it);
     } else {

@@ -345,3 +345,86 @@ def test_virtual_shards_error_near_cut(c0):
         r, *_ = run_shards_fwd(b, G)
         ref = oracle.utf8_to_utf16le(b)[0]
         assert tuple(r) == tuple(ref) and r.position == p, (cls, r, ref, p)
+
+
+# ----------------------------------------------------------------------------- host pipeline
+def host_run(x: np.ndarray, chunk: int, cap=None):
+    """*_host on pinned copies of `x` with the pipeline's chunk size set to `chunk` units;
+    guards after out_host[cap] catch writes past the capacity."""
+    fwd = x.dtype == np.uint8
+    cap = (x.size if fwd else 3 * x.size) if cap is None else cap
+    prev = ug.set_host_chunk(chunk)
+    try:
+        hin = torch.from_numpy(x.copy() if fwd else x.astype(np.uint16).view(np.int16)).pin_memory()
+        if fwd:
+            hout = torch.full((cap + 16,), 0x5A5A, dtype=torch.int16).pin_memory()
+            r = ug.utf8_to_utf16le_host(hin, hout[:cap])
+            o = hout.numpy().view(np.uint16)
+            guard = 0x5A5A
+        else:
+            hout = torch.full((cap + 16,), 0x5A, dtype=torch.uint8).pin_memory()
+            r = ug.utf16le_to_utf8_host(hin, hout[:cap])
+            o = hout.numpy()
+            guard = 0x5A
+    finally:
+        ug.set_host_chunk(prev)
+    assert np.all(o[cap:] == guard), "wrote past out_cap"
+    return r, o[: r.written if r.error >= 0 else 0]
+
+
+def check_host(x: np.ndarray, chunk: int, cap=None):
+    fwd = x.dtype == np.uint8
+    ref_r, ref_o = (oracle.utf8_to_utf16le(x, out_cap=cap) if fwd
+                    else oracle.utf16le_to_utf8(x, out_cap=cap))
+    r, o = host_run(x, chunk, cap)
+    assert tuple(r) == tuple(ref_r), (chunk, cap, r, ref_r)
+    if r.error >= 0:
+        assert np.array_equal(o, ref_o)
+    return r
+
+
+@pytest.mark.parametrize("chunk", [1, 7, 1000, 4099, 65536, 0])
+def test_host_pipeline_chunks(c0, chunk):
+    """The pipelined host path (chunks cut at character starts, one shard kernel each, outputs
+    placed by the records' prefix) equals the oracle at any chunk size, both directions."""
+    a = c0[: 3000] if chunk < 1000 else c0
+    r = check_host(a, chunk)
+    assert r.error == 0
+    u = oracle.utf8_to_utf16le(a)[1]
+    check_host(u, chunk)
+
+
+def test_host_pipeline_errors_at_chunk_cuts(c0):
+    """First errors injected within a few units of chunk cuts; data verdicts, positions and
+    written counts match the oracle, and only the prefix before the error is delivered."""
+    chunk = 4099
+    rng = np.random.default_rng(np.random.SeedSequence([0, 0xF2, 1, 0]))
+    for k, cls in enumerate(synth.UTF8_ERROR_CLASSES):
+        for cut in (chunk * (3 + k), chunk * (40 + 7 * k)):
+            b = c0.copy()
+            p, _ = synth.inject_utf8_error(b, cut - 4, cut + 4, cls, rng)
+            r = check_host(b, chunk)
+            assert (r.error, r.position) == (synth.UTF8_EXPECTED_KIND[cls], p), (cls, r, p)
+    u = synth.generate("c3", size=1 << 20)
+    for cut in (3001 * 5, 3001 * 77):
+        v = u.copy()
+        p, _ = synth.inject_utf16_error(v, cut - 2, cut + 2, rng)
+        r = check_host(v, 3001)
+        assert (r.error, r.position) == (ug.SURROGATE, p)
+
+
+def test_host_pipeline_capacity(c0):
+    a = c0[: 300000]
+    need = oracle.utf8_to_utf16le(a)[0].written
+    for cap in (0, 1, need // 2, need - 1, need):
+        check_host(a, 5000, cap=cap)
+    b = a.copy()
+    rng = np.random.default_rng(7)
+    synth.inject_utf8_error(b, 150000, 160000, "stray_continuation", rng)
+    wr = oracle.utf8_to_utf16le(b)[0].written
+    for cap in (wr - 1, wr, wr + 1):
+        check_host(b, 5000, cap=cap)
+    u = oracle.utf8_to_utf16le(a)[1]
+    need8 = oracle.utf16le_to_utf8(u)[0].written
+    for cap in (0, need8 - 1, need8):
+        check_host(u, 3333, cap=cap)
