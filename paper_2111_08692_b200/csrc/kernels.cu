@@ -450,6 +450,10 @@ struct U16Pol {
     s.first_err = NONE;
     return xc ? 16u : 0u;
 #endif
+    if (IN && s.wasc) {  // a2: the warp's words are all below 0x80: one byte each, no surrogate
+      s.first_err = NONE;
+      return xc ? 16u : 0u;
+    }
     uint32_t Hprev = u16::is_high(s.prev_word) ? 0x80000000u : 0u;  // byte 3 = word -1
     u16::Cls4 c = u16::classes4(s.w[0], s.w[1]);
     uint32_t acc = 0, anyerr = 0, errm[4];
@@ -547,13 +551,29 @@ struct U16Pol {
       const uint32_t a2 = p + prmt(inc, 0u, 0x4441u);
       const uint32_t a3 = p + prmt(inc, 0u, 0x4442u);
       const uint32_t A[4] = {p, a1, a2, a3};
+#ifdef UG_U16_SHR_ALU
+      const uint32_t B0[4] = {O0, O0 >> 8, O0 >> 16, O0 >> 24};
+      const uint32_t B1[4] = {O1, O1 >> 8, O1 >> 16, O1 >> 24};
+      const uint32_t B2[4] = {O2, O2 >> 8, O2 >> 16, O2 >> 24};
+#else
+      // byte j to the low byte on the FMA pipe (the ALU pipe is the busy one here)
+      const uint32_t B0[4] = {O0, shr_fma<8>(O0), shr_fma<16>(O0), shr_fma<24>(O0)};
+      const uint32_t B1[4] = {O1, shr_fma<8>(O1), shr_fma<16>(O1), shr_fma<24>(O1)};
+      const uint32_t B2[4] = {O2, shr_fma<8>(O2), shr_fma<16>(O2), shr_fma<24>(O2)};
+#endif
 #pragma unroll
       for (int j = 0; j < 4; j++) {
-        const uint32_t b0 = O0 >> (8 * j), b1 = O1 >> (8 * j), b2 = O2 >> (8 * j);
+        const uint32_t b0 = B0[j], b1 = B1[j], b2 = B2[j];
         if (g < 3) {
           sts8o<0>(A[j], b0);
           sts8o<1>(A[j], b1);
           sts8o<2>(A[j], b2);
+        } else if (IN) {
+          // every word owned (width >= 1): only word 3's second and third bytes and word 2's
+          // third byte can pass the thread's end
+          sts8o<0>(A[j], b0);
+          if (j < 3 || A[j] + 1 < pend) sts8o<1>(A[j], b1);
+          if (j < 2 || A[j] + 2 < pend) sts8o<2>(A[j], b2);
         } else {
           if (A[j] < pend) sts8o<0>(A[j], b0);
           if (A[j] + 1 < pend) sts8o<1>(A[j], b1);
@@ -693,11 +713,16 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM) k_validate(const TileArgs a) 
 // A ticket is taken only when its tile is about to be processed, so a tile's aggregate is
 // published one load + classify after its ticket (the look-back of every later tile waits
 // for it); the load latency is hidden by the other CTAs on the SM instead of by prefetching.
-constexpr int RING = 4;  // input tile slots: loading, classifying, two awaiting their prefix
+#ifndef UG_PF
+#define UG_PF 1
+#endif
+constexpr int PF = UG_PF;        // tiles loading ahead of the one being classified
+constexpr int RING = PF + 3;     // input tile slots: PF loading, classifying, two awaiting prefix
 #ifndef UG_NLB
 #define UG_NLB 1
 #endif
 constexpr int NLB = UG_NLB;  // look-back warps per CTA (alternating tiles)
+static_assert(NLB == 1 || PF == 1, "termination ticks assume one look-back agent when PF > 1");
 
 // Decode tile j (ring slot js, prefix P, aggregate C; this thread's offset excl / count cnt)
 // into the stage at the tile's global 16-byte phase, then store it: the 16-byte aligned
@@ -797,7 +822,8 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
     }
     s_flag[0] = s_flag[1] = s_flag[2] = 0;
     fence_mbar_init();
-    start_tile(0, (long long)atomicAdd(&a.ctr->ticket, 1u));
+#pragma unroll
+    for (int j = 0; j < PF; j++) start_tile(j, (long long)atomicAdd(&a.ctr->ticket, 1u));
   }
   __syncthreads();
 
@@ -906,8 +932,8 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
       }
       if (Pol::hint(st)) s_flag[i % 3] = 1;
       if (tid == 0) {
-        // ring slot (i + 1) % RING held tile i - 3, emitted last iteration
-        start_tile((i + 1) % RING, tn);
+        // ring slot (i + PF) % RING held tile i - 3, emitted last iteration
+        start_tile((i + PF) % RING, tn);
         // flag slot of tile i + 1: last read after the block scan of i - 2 (every thread has
         // passed the block scan of i - 1 since), next written after the block scan of i
         s_flag[(i + 1) % 3] = 0;
