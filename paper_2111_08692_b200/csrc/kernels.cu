@@ -1049,15 +1049,21 @@ __global__ void __launch_bounds__(LNT) k_len8(const uint8_t *in, unsigned long l
   finish_reduction(sum, ctr, d_len);
 }
 
-// Two words per op: per 16-bit lane 1 + [u >= 0x80] + [u >= 0x800 and not a surrogate] (a
-// surrogate counts 2, so a pair counts 4), accumulated per lane and folded per uint4.
-__device__ __forceinline__ uint32_t len16_lanes(uint32_t r) {
-  const uint32_t lo15 = r & 0x7FFF7FFFu;
-  const uint32_t ge80 = ((lo15 + 0x7F807F80u) | r) & u16::LANE_TOP;
-  const uint32_t ge800 = ((lo15 + 0x78007800u) | r) & u16::LANE_TOP;
-  const uint32_t sur = u16::zero_lanes((r & 0xF800F800u) ^ 0xD800D800u);
-  return ((ge80 >> 15) + ((ge800 & ~sur) >> 15));  // per lane 0..2 (bits 0-1, 16-17)
+// Four words per op (byte lanes: low / high bytes split by two PRMT, as u16::classes4): per word
+// [u >= 0x80] + [u >= 0x800 and not a surrogate] (the width minus 1; a surrogate counts 2, so a
+// pair counts 4), added into a byte-lane accumulator by IMAD.HI (FMA pipe; the compares use the
+// ALU pipe).  Lane sums stay below 256 for up to 127 calls.
+__device__ __forceinline__ uint32_t len16_acc4(uint32_t a, uint32_t b, uint32_t acc) {
+  const uint32_t lo = prmt(a, b, 0x6420u), hi = prmt(a, b, 0x7531u);
+  const uint32_t h7 = hi & 0x7F7F7F7Fu;
+  const uint32_t ge80 = (mad(h7, 1u, 0x7F7F7F7Fu) | hi | lo) & HI;   // hi != 0 or lo >= 0x80
+  const uint32_t ge800 = (mad(h7, 1u, 0x78787878u) | hi) & HI;       // hi >= 8
+  const uint32_t z = (hi & 0xF8F8F8F8u) ^ 0xD8D8D8D8u;               // 0 iff hi in D8..DF
+  const uint32_t S = ~(mad(z & 0x7F7F7F7Fu, 1u, 0x7F7F7F7Fu) | z) & HI;
+  acc = mad_hi(ge80, 1u << 25, acc);          // + ge80 >> 7
+  return mad_hi(ge800 & ~S, 1u << 25, acc);   // + (ge800 and not S) >> 7
 }
+__device__ __forceinline__ uint32_t lane_sum(uint32_t acc) { return (acc * 0x01010101u) >> 24; }
 
 __global__ void __launch_bounds__(LNT) k_len16(const uint16_t *in, unsigned long long n,
                                               Counters *ctr, unsigned long long *d_len) {
@@ -1068,17 +1074,18 @@ __global__ void __launch_bounds__(LNT) k_len16(const uint16_t *in, unsigned long
   const unsigned long long nb = (n - head) / 8;
   const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
   unsigned long long sum = 0;
-  auto quad = [](const uint4 &v) {
-    const uint32_t l = len16_lanes(v.x) + len16_lanes(v.y) + len16_lanes(v.z) + len16_lanes(v.w);
-    return 8u + (l & 0xFFFFu) + (l >> 16);
+  auto quad = [](const uint4 &v) {  // 8 words
+    return 8u + lane_sum(len16_acc4(v.z, v.w, len16_acc4(v.x, v.y, 0u)));
   };
   unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
   for (; i + 3 * stride < nb; i += 4 * stride) {
     uint4 v[4];
 #pragma unroll
     for (int j = 0; j < 4; j++) v[j] = __ldcs(body + i + j * stride);
+    uint32_t acc = 0;
 #pragma unroll
-    for (int j = 0; j < 4; j++) sum += quad(v[j]);
+    for (int j = 0; j < 4; j++) acc = len16_acc4(v[j].z, v[j].w, len16_acc4(v[j].x, v[j].y, acc));
+    sum += 32u + lane_sum(acc);
   }
   for (; i < nb; i += stride) sum += quad(__ldcs(body + i));
   if (blockIdx.x == 0) {

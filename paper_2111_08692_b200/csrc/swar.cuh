@@ -90,6 +90,16 @@ UG_HD uint32_t mad(uint32_t a, uint32_t b, uint32_t c) {
   return a * b + c;
 #endif
 }
+// (a * b >> 32) + c on the FMA pipe (IMAD.HI with accumulate).
+UG_HD uint32_t mad_hi(uint32_t a, uint32_t b, uint32_t c) {
+#if defined(__CUDA_ARCH__)
+  uint32_t d;
+  asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+#else
+  return (uint32_t)(((uint64_t)a * b) >> 32) + c;
+#endif
+}
 // (a & m) | (b & ~m): one LOP3.
 UG_HD uint32_t mux(uint32_t m, uint32_t a, uint32_t b) { return (a & m) | (b & ~m); }
 

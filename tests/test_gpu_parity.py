@@ -428,3 +428,21 @@ def test_host_pipeline_capacity(c0):
     need8 = oracle.utf16le_to_utf8(u)[0].written
     for cap in (0, need8 - 1, need8):
         check_host(u, 3333, cap=cap)
+
+
+# ----------------------------------------------------------------------------- length reductions
+@pytest.mark.parametrize("kind", ["uniform", "alphabet"])
+def test_length_from_large_random(kind):
+    """Both length reductions on inputs large enough for their unrolled grid-stride loops
+    (> 3 x grid x 512 vectors), against the oracle, at an odd offset."""
+    rng = np.random.default_rng(np.random.SeedSequence([0x1E, 16, len(kind)]))
+    n = (64 << 20) + 13
+    alpha = np.array([0x41, 0x7F, 0x80, 0x7FF, 0x800, 0xD7FF, 0xD800, 0xDBFF, 0xDC00, 0xDFFF,
+                      0xE000, 0xFFFF], dtype=np.uint16)
+    u = (rng.integers(0, 65536, n).astype(np.uint16) if kind == "uniform"
+         else alpha[rng.integers(0, alpha.size, n)])
+    _, t = to_dev(u, pad_before=3)
+    assert ug.utf8_length_from_utf16le(t) == oracle.utf8_length_from_utf16le(u)
+    b = u.view(np.uint8)
+    _, t8 = to_dev(b, pad_before=5)
+    assert ug.utf16_length_from_utf8(t8) == oracle.utf16_length_from_utf8(b)
