@@ -204,6 +204,7 @@ def run_ours(args):
     off16 = int(cnts[:rank].sum())
 
     ev_f = []  # (start, end) events around each forward launch
+    ev_r = []  # ... and each reverse launch
 
     def gather_combine(which):
         if G > 1:
@@ -226,7 +227,13 @@ def run_ours(args):
             ev_f.append((e0, e1))
         gather_combine(0)
         ug.utf8_length_from_utf16le_async(u16, lens, len_off=8)
+        if record_events:
+            e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e2.record(stream)
         ug.utf16le_to_utf8_shard_async(u16, 0, n16, 0, 0, off16, out8, rec, rec_off=R)
+        if record_events:
+            e3.record(stream)
+            ev_r.append((e2, e3))
         gather_combine(1)
 
     for _ in range(args.warmup):
@@ -253,6 +260,7 @@ def run_ours(args):
     clk = clocks.stop()
     ms = t0.elapsed_time(t1)
     fwd_ms = statistics.mean(a.elapsed_time(b) for a, b in ev_f)
+    rev_ms = statistics.mean(a.elapsed_time(b) for a, b in ev_r)
 
     # ---- verification (untimed): results, lengths, round trip on the device
     r = ug.decode_records(rec)
@@ -266,14 +274,14 @@ def run_ours(args):
         assert glob[0].error == 0 and glob[1].error == 0, glob
 
     # ---- aggregate over ranks: max time, total units
-    tot = torch.tensor([ms, fwd_ms, float(n8), float(n16), float(nchar)], dtype=torch.float64,
-                       device=dev)
+    tot = torch.tensor([ms, fwd_ms, rev_ms, float(n8), float(n16), float(nchar)],
+                       dtype=torch.float64, device=dev)
     if G > 1:
-        mx = tot[:2].clone()
+        mx = tot[:3].clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
-        sm = tot[2:].clone()
+        sm = tot[3:].clone()
         dist.all_reduce(sm, op=dist.ReduceOp.SUM)
-        ms, fwd_ms = float(mx[0]), float(mx[1])
+        ms, fwd_ms, rev_ms = float(mx[0]), float(mx[1]), float(mx[2])
         N8, N16, NCH = int(sm[0]), int(sm[1]), int(sm[2])
     else:
         N8, N16, NCH = n8, n16, nchar
@@ -283,9 +291,19 @@ def run_ours(args):
     value = in_bytes / (ms_step * 1e-3) / 1e9
     gchar = 2 * NCH / (ms_step * 1e-3) / 1e9     # code points transcoded per step (both ways)
     peak, peak_src = hbm_peak()
-    fwd_bytes = n8 + 2 * n16                     # algorithmic bytes of one forward launch
-    achieved = fwd_bytes / (fwd_ms * 1e-3) / 1e9
-    traffic = ncu_traffic()
+    # roofline of the dominant kernel of the step (the longer transcoder launch); both
+    # transcoders move n8 + 2 n16 algorithmic bytes per launch (read one side, write the other)
+    alg_bytes = n8 + 2 * n16
+    kern = {"k_transcode<U8Pol>": {"op": "utf8_to_utf16le", "ms": fwd_ms, "input": n8},
+            "k_transcode<U16Pol>": {"op": "utf16le_to_utf8", "ms": rev_ms, "input": 2 * n16}}
+    traffic = ncu_traffic() or {}
+    for k, d in kern.items():
+        d["achieved"] = alg_bytes / (d["ms"] * 1e-3) / 1e9
+        d["frac"] = d["achieved"] / peak
+        t = traffic.get(k)
+        d["traffic"] = round(t["dram_bytes_per_input_byte"] * d["input"]) if t else None
+    dom = max(kern, key=lambda k: kern[k]["ms"])
+    D = kern[dom]
 
     # ---- end to end through the host-buffer API (pinned host memory, copies timed)
     e2e = None
@@ -318,16 +336,19 @@ def run_ours(args):
                        "chars": NCH,
                        "forward_input_gbs": round(N8 / (fwd_ms * 1e-3) / 1e9 * 1, 2),
                        "gen_seconds": round(t_gen, 1)},
-            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak,
-                         "unit": "GB/s", "frac": round(achieved / peak, 4),
-                         "traffic": (round(traffic["dram_bytes_per_input_byte"] * n8)
-                                     if traffic else None),
+            "roofline": {"bound": "hbm", "achieved": round(D["achieved"], 1), "peak": peak,
+                         "unit": "GB/s", "frac": round(D["frac"], 4),
+                         "traffic": D["traffic"],
                          "traffic_source": (traffic["capture"] + " (" + traffic["config"] +
                                             "), DRAM bytes per input byte x this launch's input"
-                                            if traffic else None),
-                         "kernel": "k_transcode<U8Pol> (utf8_to_utf16le)",
-                         "algorithmic_bytes_per_launch": fwd_bytes,
-                         "avg_launch_ms": round(fwd_ms, 4), "peak_source": peak_src},
+                                            if D["traffic"] is not None else None),
+                         "kernel": f"{dom} ({D['op']}), the longest launch of the step",
+                         "algorithmic_bytes_per_launch": alg_bytes,
+                         "avg_launch_ms": round(D["ms"], 4), "peak_source": peak_src,
+                         "kernels": {k: {"op": d["op"], "avg_launch_ms": round(d["ms"], 4),
+                                         "achieved": round(d["achieved"], 1),
+                                         "frac": round(d["frac"], 4), "traffic": d["traffic"]}
+                                     for k, d in kern.items()}},
             "per_op": per_op,
             "clocks": clk,
             "gpu_launches": int(launches),

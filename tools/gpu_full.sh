@@ -12,3 +12,4 @@ timeout -s KILL 900 ncu --metrics gpu__time_duration.sum --clock-control none -k
 CMD2="python bench.py --size-mib 1024 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"
 timeout -s KILL 600 $CMD2 > gpurun_out/plain2_$TAG.log 2>&1 && \
 timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:k_transcode -s 2 -c 2 -o gpurun_out/full_$TAG $CMD2 > gpurun_out/ncu_full_$TAG.log 2>&1; echo "full=$?"
+cp paper_2111_08692_b200/libunigpu.so gpurun_out/lib_$TAG.so
