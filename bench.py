@@ -295,7 +295,7 @@ def run_ours(args):
     # transcoders move n8 + 2 n16 algorithmic bytes per launch (read one side, write the other)
     alg_bytes = n8 + 2 * n16
     kern = {"k_transcode<U8Pol>": {"op": "utf8_to_utf16le", "ms": fwd_ms, "input": n8},
-            "k_transcode<U16Pol>": {"op": "utf16le_to_utf8", "ms": rev_ms, "input": 2 * n16}}
+            "k_transcode16": {"op": "utf16le_to_utf8", "ms": rev_ms, "input": 2 * n16}}
     traffic = ncu_traffic() or {}
     for k, d in kern.items():
         d["achieved"] = alg_bytes / (d["ms"] * 1e-3) / 1e9

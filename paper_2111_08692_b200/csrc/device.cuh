@@ -208,11 +208,11 @@ __device__ __forceinline__ bool tile_at_edge(const Window &w, long long t) {
 // (only tiles touching the window edges do any work).  Called by threads 0..nthreads-1; the
 // caller syncs after.
 __device__ __forceinline__ void fix_tile_edges(const Window &w, long long t, uint8_t *buf,
-                                               int nthreads) {
+                                               int nthreads, int first = -1) {
   long long p0 = tile_pos(w, t) - HALO;
   if (p0 >= w.lo_valid && p0 + INBUF <= w.hi_valid) return;
   uint32_t *b32 = reinterpret_cast<uint32_t *>(buf);
-  for (int q = threadIdx.x; q < INBUF / 4; q += nthreads) {
+  for (int q = first >= 0 ? first : (int)threadIdx.x; q < INBUF / 4; q += nthreads) {
     long long pos = p0 + 4 * q;
     if (pos >= w.lo_valid && pos + 4 <= w.hi_valid) continue;
     b32[q] &= range_bytes(pos, w.lo_valid, w.hi_valid);

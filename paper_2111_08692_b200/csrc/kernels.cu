@@ -584,6 +584,82 @@ struct U16Pol {
     }
   }
 
+  // a7 + a9 fused (count-first kernel): encode the owned words into stage[o ...] exactly as
+  // decode() does and check the pairing predicate on the same classes (computed once, one
+  // group ahead for the low-surrogate look-ahead).  Returns the first error position or NONE.
+  template <bool IN>
+  __device__ static __forceinline__ unsigned long long decode_validate(const St &s,
+                                                                       uint8_t *stage,
+                                                                       uint32_t o, uint32_t lim) {
+    if (IN && s.wasc) {  // a2: no surrogate, one byte per word
+      decode<true>(s, stage, o, lim, 0);
+      return NONE;
+    }
+    uint32_t p = smem_addr(stage + o);
+    const uint32_t pend = smem_addr(stage + lim);
+    uint32_t lprev = (s.prev_word & 0xFFu) << 24;
+    uint32_t Hprev = u16::is_high(s.prev_word) ? 0x80000000u : 0u;
+    uint32_t errm[4];
+    uint32_t anyerr = 0;
+    u16::Cls4 c = u16::classes4(s.w[0], s.w[1]);
+#pragma unroll
+    for (int g = 0; g < 4; g++) {
+      u16::Cls4 cn;
+      uint32_t Lnext;
+      if (g < 3) {
+        cn = u16::classes4(s.w[2 * g + 2], s.w[2 * g + 3]);
+        Lnext = cn.L;
+      } else {
+        Lnext = u16::is_low(s.next_word) ? 0x80u : 0u;
+      }
+      // a9: high not followed by low, low not preceded by high
+      uint32_t e = (c.H & ~fsr(c.L, Lnext, 8)) | (c.L & ~fsl(Hprev, c.H, 8));
+      const uint32_t lp = fsl(lprev, c.lo, 8);
+      uint32_t O0, O1, O2;
+      u16::encode4(c, lp, &O0, &O1, &O2);
+      uint32_t d = u16::wm1(c) + 0x01010101u;
+      if (!IN) {
+        const uint32_t o4 = own4(s, g);
+        e &= o4;
+        d &= (o4 >> 7) * 0xFFu;
+      }
+      errm[g] = e;
+      anyerr |= e;
+      const uint32_t inc = d * 0x01010101u;  // byte j: bytes emitted by words <= j
+      const uint32_t A[4] = {p, p + prmt(inc, 0u, 0x4440u), p + prmt(inc, 0u, 0x4441u),
+                             p + prmt(inc, 0u, 0x4442u)};
+      const uint32_t B0[4] = {O0, shr_fma<8>(O0), shr_fma<16>(O0), shr_fma<24>(O0)};
+      const uint32_t B1[4] = {O1, shr_fma<8>(O1), shr_fma<16>(O1), shr_fma<24>(O1)};
+      const uint32_t B2[4] = {O2, shr_fma<8>(O2), shr_fma<16>(O2), shr_fma<24>(O2)};
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        if (g < 3) {
+          sts8o<0>(A[j], B0[j]);
+          sts8o<1>(A[j], B1[j]);
+          sts8o<2>(A[j], B2[j]);
+        } else if (IN) {
+          sts8o<0>(A[j], B0[j]);
+          if (j < 3 || A[j] + 1 < pend) sts8o<1>(A[j], B1[j]);
+          if (j < 2 || A[j] + 2 < pend) sts8o<2>(A[j], B2[j]);
+        } else {
+          if (A[j] < pend) sts8o<0>(A[j], B0[j]);
+          if (A[j] + 1 < pend) sts8o<1>(A[j], B1[j]);
+          if (A[j] + 2 < pend) sts8o<2>(A[j], B2[j]);
+        }
+      }
+      p += inc >> 24;
+      Hprev = c.H;
+      lprev = c.lo;
+      if (g < 3) c = cn;
+    }
+    if (!anyerr) return NONE;
+    unsigned long long f = NONE;  // cold
+#pragma unroll
+    for (int g = 3; g >= 0; g--)
+      if (errm[g]) f = (unsigned long long)(s.pos0 + 4 * g + (__ffs(errm[g]) - 8) / 8);
+    return f;
+  }
+
   __device__ static __forceinline__ void finalize(const TileArgs &a, unsigned long long e,
                                                   bool xc, int lane, int *kind,
                                                   unsigned long long *wr) {
@@ -1096,6 +1172,227 @@ __global__ void __launch_bounds__(LNT) k_len16(const uint16_t *in, unsigned long
   finish_reduction(sum, ctr, d_len);
 }
 
+// ============================================================================ count-first K4
+// UTF-16LE -> UTF-8 with validation moved off the look-back's critical path.  A word's UTF-8
+// width depends on the word alone (u16::wm1: 1 + [u >= 0x80] + [u >= 0x800, not a surrogate]),
+// so a tile's output count - and every thread's offset inside it - is a plain width sum, exact
+// on ANY input: validity decides only the error report, never an offset.  So per tile:
+//  * data warps: count only (byte-lane width sums, 4 words per op), an in-warp scan, and the
+//    warp total added to a shared 64-bit (arrivals | sum) word; the warp that completes it
+//    publishes the tile aggregate at once.  No CTA barrier between the load and the publish.
+//  * look-back warp: exclusive prefix (a6) in ticket order, per-warp offsets, push-forward.
+//  * data warps, D16 tiles later: decode + pairing check in one pass (classes computed once,
+//    a7 + a9), stage, TMA bulk store (a8).
+// Against k_transcode<U16Pol> (classify + block scan before the publish) this shortens the
+// ticket -> aggregate latency that every successor's look-back waits on.
+#ifndef UG_RING16
+#define UG_RING16 5  // measured best: 5 slots, one load ahead, emit deferred 3 tiles
+#endif
+constexpr int RING16 = UG_RING16;
+#ifndef UG_PF16
+#define UG_PF16 1
+#endif
+constexpr int PF16 = UG_PF16;  // tiles loading ahead of the one being counted
+constexpr int D16 = RING16 - PF16 - 1;  // tiles awaiting their prefix (emit deferral)
+static_assert(PF16 >= 1 && D16 >= 1, "ring: loads in flight + the tile counted + deferral");
+constexpr int T16_THREADS = NT + 32;
+
+__device__ __forceinline__ void emit_tile16(const TileArgs &a, const uint8_t *img, long long t,
+                                            unsigned long long P, uint32_t C, uint32_t excl,
+                                            uint32_t cnt, uint8_t *stage, int tid, int lane) {
+  constexpr uint32_t A = 16;
+  const Window &win = a.win;
+  const long long tp = tile_pos(win, t);
+  uint8_t *out = reinterpret_cast<uint8_t *>(a.out);
+  const uint32_t ph = (uint32_t)(((uintptr_t)(out + P)) & 15u);
+  U16Pol::St st;
+  unsigned long long f;
+  if (tp >= 0 && tp + TILE <= win.n) {  // tile-uniform
+    U16Pol::load<true>(st, img, tid, lane, tp, win.n);
+    f = U16Pol::decode_validate<true>(st, stage, ph + excl, ph + excl + cnt);
+  } else {
+    U16Pol::load<false>(st, img, tid, lane, tp, win.n);
+    f = U16Pol::decode_validate<false>(st, stage, ph + excl, ph + excl + cnt);
+  }
+  if (f != NONE) atomicMin(&a.ctr->err_min, f);  // a4 (cold)
+  named_sync<BAR_DATA, NT>();  // the whole tile is in the stage
+  unsigned long long hi = P + C;
+  if (hi > a.out_cap) hi = a.out_cap;
+  if (hi <= P) return;
+  const uint32_t Cc = (uint32_t)(hi - P);
+  const uint32_t h = ph ? A - ph : 0u;
+  if (h >= Cc) {
+    if ((uint32_t)tid < Cc) out[P + tid] = stage[ph + tid];
+    return;
+  }
+  const uint32_t nb = (Cc - h) / A;
+  const uint32_t tl = h + nb * A;
+  if ((uint32_t)tid < h) out[P + tid] = stage[ph + tid];
+  if ((uint32_t)tid < Cc - tl) out[P + tl + tid] = stage[ph + tl + tid];
+  if (tid == 0 && nb) {
+    fence_proxy_async_smem();
+    bulk_s2g(out + P + h, stage + ph + h, nb * 16u);
+    bulk_commit();
+  }
+}
+
+__global__ void __launch_bounds__(T16_THREADS, CTAS_PER_SM) k_transcode16(const TileArgs a) {
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t *ring = smem;
+  uint8_t *stage = smem + RING16 * INBUF;
+  __shared__ uint64_t mb_load[RING16];  // tile landed (TMA tx) / no tile
+  __shared__ uint64_t mb_tick[RING16];  // thread 0 -> look-back warp: ticket of the slot
+  __shared__ uint64_t mb_agg[RING16];   // data warps (one arrival each) -> look-back warp
+  __shared__ uint64_t mb_pre[RING16];   // look-back warp -> data warps: prefix known
+  __shared__ long long s_t[RING16];
+  __shared__ uint32_t s_wsum[RING16][NT / 32];  // warp totals, then exclusive warp offsets
+  __shared__ unsigned long long s_acc[RING16];   // arrivals << 32 | running sum of warp totals
+  __shared__ uint32_t s_cnt[RING16];
+  __shared__ unsigned long long s_pre[RING16];
+  __shared__ int s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const Window &win = a.win;
+  const long long ntiles = (long long)a.ntiles;
+
+  auto start_tile = [&](int slot, long long tn) {  // thread 0
+    s_t[slot] = tn;
+    mbar_arrive(&mb_tick[slot]);
+    if (tn < ntiles) {
+      fence_proxy_async_smem();
+      issue_tile_load(win, tn, ring + slot * INBUF, &mb_load[slot]);
+    } else {
+      mbar_arrive(&mb_load[slot]);
+    }
+  };
+  if (tid == 0) {
+#pragma unroll
+    for (int j = 0; j < RING16; j++) {
+      mbar_init(&mb_load[j], 1);
+      mbar_init(&mb_tick[j], 1);
+      mbar_init(&mb_agg[j], NT / 32);
+      mbar_init(&mb_pre[j], 1);
+      s_acc[j] = 0ull;
+    }
+    fence_mbar_init();
+#pragma unroll 1
+    for (int j = 0; j < PF16; j++) start_tile(j, (long long)atomicAdd(&a.ctr->ticket, 1u));
+  }
+  __syncthreads();
+
+  if (warp == NT / 32) {
+    // ------------------------------------------------------------ look-back warp (a6)
+#pragma unroll 1
+    for (int k = 0;; k++) {
+      const int sl = k % RING16;
+      const uint32_t ph = (k / RING16) & 1;
+      mbar_wait(&mb_tick[sl], ph);
+      const long long t = s_t[sl];
+      if (t >= ntiles) break;
+      mbar_wait(&mb_agg[sl], ph);
+      // tile aggregate from the 16 warp totals; exclusive warp offsets back into s_wsum
+      const uint32_t wv = lane < NT / 32 ? s_wsum[sl][lane] : 0u;
+      uint32_t sc = wv;
+#pragma unroll
+      for (int d = 1; d < NT / 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, sc, d);
+        if (lane >= d) sc += y;
+      }
+      const uint32_t C = __shfl_sync(FULL, sc, NT / 32 - 1);  // (published by the last warp)
+      if (lane < NT / 32) s_wsum[sl][lane] = sc - wv;
+      const unsigned long long P = tile_excl_prefix(a, t, lane);
+      const unsigned long long incl = P + C;
+      __syncwarp();
+      if (lane == 0) {
+        if (t != 0) st_relaxed(a.status + t, pack_status(a.epoch, FLAG_PREFIX, incl));
+        s_cnt[sl] = C;
+        s_pre[sl] = P;
+        mbar_arrive(&mb_pre[sl]);  // release: offsets, count, prefix
+      }
+      push_forward(a.status, a.epoch, t, ntiles, incl, lane);
+    }
+  } else {
+    // ------------------------------------------------------------ data warps
+    // this thread's in-warp offset << 8 | count for the D16 + 1 tiles between count and emit
+    uint32_t oc[D16 + 1];
+#pragma unroll
+    for (int j = 0; j <= D16; j++) oc[j] = 0u;
+    auto emit = [&](int j) {
+      const int js = j % RING16;
+      mbar_wait(&mb_pre[js], (j / RING16) & 1);
+      if (tid == 0) bulk_wait_read_all();  // the previous bulk store has read the stage
+      named_sync<BAR_DATA, NT>();
+      uint32_t v = 0;
+#pragma unroll
+      for (int q = 0; q <= D16; q++)
+        if (q == j % (D16 + 1)) v = oc[q];
+      emit_tile16(a, ring + js * INBUF, s_t[js], s_pre[js], s_cnt[js],
+                  s_wsum[js][warp] + (v >> 8), v & 0xFFu, stage, tid, lane);
+    };
+    int i = 0;
+#pragma unroll 1
+    while (true) {
+      const int sl = i % RING16;
+      long long tn = 0;
+      if (tid == 0) tn = (long long)atomicAdd(&a.ctr->ticket, 1u);
+      mbar_wait(&mb_load[sl], (i / RING16) & 1);
+      const long long t = s_t[sl];
+      if (t >= ntiles) break;
+      uint8_t *img = ring + sl * INBUF;
+      if (tile_at_edge(win, t)) {  // tile-uniform
+        fix_tile_edges(win, t, img, NT);
+        named_sync<BAR_DATA, NT>();
+      }
+      // a5: this thread's output bytes (width sum of its 16 words; owned words only)
+      const long long tp = tile_pos(win, t);
+      const uint4 *my = reinterpret_cast<const uint4 *>(img + HALO + BPT * tid);
+      const uint4 q0 = my[0], q1 = my[1];
+      uint32_t cnt;
+      if (tp >= 0 && tp + TILE <= win.n) {
+        cnt = 16u + lane_sum(len16_acc4(q1.z, q1.w, len16_acc4(q1.x, q1.y,
+                             len16_acc4(q0.z, q0.w, len16_acc4(q0.x, q0.y, 0u)))));
+      } else {
+        const uint32_t q[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+        const long long w0 = (tp + BPT * tid) / 2, nw = win.n / 2;
+        cnt = 0;
+#pragma unroll
+        for (int k = 0; k < 16; k++)
+          if (w0 + k >= 0 && w0 + k < nw) cnt += len16_word((q[k >> 1] >> (16 * (k & 1))) & 0xFFFFu);
+      }
+      uint32_t sc = cnt;  // in-warp inclusive scan
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, sc, d);
+        if (lane >= d) sc += y;
+      }
+      if (lane == 31) {
+        s_wsum[sl][warp] = sc;
+        // the last warp to add its total publishes the tile aggregate at once (a6): the
+        // look-back warp may still be busy with the previous tile, and every successor's
+        // look-back waits for this word
+        const unsigned long long old = atomicAdd(&s_acc[sl], (1ull << 32) | sc);
+        if ((old >> 32) == NT / 32 - 1) {
+          st_relaxed(a.status + t,
+                     pack_status(a.epoch, t == 0 ? FLAG_PREFIX : FLAG_AGG, (uint32_t)old + sc));
+          s_acc[sl] = 0ull;  // next use of the slot is RING16 tiles later
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&mb_agg[sl]);
+#pragma unroll
+      for (int q = 0; q <= D16; q++)
+        if (q == i % (D16 + 1)) oc[q] = ((sc - cnt) << 8) | cnt;  // count <= 48, offset < 2^11
+      // slot of tile i + PF16 held tile i + PF16 - RING16 = i - D - 1, emitted last iteration
+      if (tid == 0) start_tile((i + PF16) % RING16, tn);
+      if (i >= D16) emit(i - D16);  // a7-a9, a8
+      i++;
+    }
+    for (int j = (i >= D16 ? i - D16 : 0); j < i; j++) emit(j);
+    if (tid == 0) bulk_wait_all();
+  }
+  __syncthreads();
+  finish_call<U16Pol>(a, true, tid, warp, lane, &s_last);
+}
+
 // ============================================================================ combine
 __host__ __device__ inline void combine_impl(const RecordDev *recs, int nranks, int rank,
                                              unsigned long long total_in, ResultDev *res,
@@ -1158,12 +1455,20 @@ size_t tile_smem_bytes(Op op) {
     case Op::U8_VALIDATE:
     case Op::U16_VALIDATE: return VRING * INBUF;
     case Op::U8_TO_U16: return RING * INBUF + U8Pol::STAGE;
-    case Op::U16_TO_U8: return RING * INBUF + U16Pol::STAGE;
+    case Op::U16_TO_U8:
+#ifndef UG_U16_TILE_SCAN
+      return RING16 * INBUF + U16Pol::STAGE;
+#else
+      return RING * INBUF + U16Pol::STAGE;
+#endif
   }
   return 0;
 }
 
 static int tile_threads(Op op) {
+#ifndef UG_U16_TILE_SCAN
+  if (op == Op::U16_TO_U8) return T16_THREADS;
+#endif
   return (op == Op::U8_TO_U16 || op == Op::U16_TO_U8) ? NT + 32 * NLB : NT;
 }
 
@@ -1172,7 +1477,12 @@ static const void *tile_fn(Op op) {
     case Op::U8_VALIDATE: return (const void *)k_validate<U8Pol>;
     case Op::U8_TO_U16: return (const void *)k_transcode<U8Pol>;
     case Op::U16_VALIDATE: return (const void *)k_validate<U16Pol>;
-    case Op::U16_TO_U8: return (const void *)k_transcode<U16Pol>;
+    case Op::U16_TO_U8:
+#ifndef UG_U16_TILE_SCAN
+      return (const void *)k_transcode16;
+#else
+      return (const void *)k_transcode<U16Pol>;
+#endif
   }
   return nullptr;
 }
@@ -1194,7 +1504,13 @@ cudaError_t launch_tile(Op op, const TileArgs &a, int grid, cudaStream_t s) {
     case Op::U8_VALIDATE: k_validate<U8Pol><<<grid, nt, sm, s>>>(a); break;
     case Op::U16_VALIDATE: k_validate<U16Pol><<<grid, nt, sm, s>>>(a); break;
     case Op::U8_TO_U16: k_transcode<U8Pol><<<grid, nt, sm, s>>>(a); break;
-    case Op::U16_TO_U8: k_transcode<U16Pol><<<grid, nt, sm, s>>>(a); break;
+    case Op::U16_TO_U8:
+#ifndef UG_U16_TILE_SCAN
+      k_transcode16<<<grid, nt, sm, s>>>(a);
+#else
+      k_transcode<U16Pol><<<grid, nt, sm, s>>>(a);
+#endif
+      break;
   }
   return cudaGetLastError();
 }
