@@ -793,7 +793,11 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM) k_validate(const TileArgs a) 
 #define UG_PF 1
 #endif
 constexpr int PF = UG_PF;        // tiles loading ahead of the one being classified
-constexpr int RING = PF + 3;     // input tile slots: PF loading, classifying, two awaiting prefix
+#ifndef UG_DEFER
+#define UG_DEFER 3  // measured: 3 beats 2 (c1 -17 %), 5 ring slots still fit 2 CTAs/SM
+#endif
+constexpr int DEFER = UG_DEFER;  // tiles between classification and emit (awaiting the prefix)
+constexpr int RING = PF + 1 + DEFER;  // input slots: PF loading, one classifying, DEFER waiting
 #ifndef UG_NLB
 #define UG_NLB 1
 #endif
@@ -953,7 +957,9 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
     }
   } else {
     // ------------------------------------------------------------ data warps
-    uint32_t ex[2] = {0u, 0u}, cn[2] = {0u, 0u};  // this thread's offset / count, tiles i-1, i-2
+    uint32_t ex[DEFER], cn[DEFER];  // this thread's offset / count of the tiles awaiting emit
+#pragma unroll
+    for (int q = 0; q < DEFER; q++) ex[q] = cn[q] = 0u;
     int i = 0;
     auto emit = [&](int j) {  // decode + store tile j (all data threads)
       const int js = j % RING;
@@ -969,7 +975,14 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
 #endif
       if (tid == 0) bulk_wait_read_all();  // the previous bulk store has read the stage
       named_sync<BAR_DATA, NT>();
-      emit_tile<Pol>(a, ring + js * INBUF, s_t[js], s_pre[js], s_cnt[js], ex[j & 1], cn[j & 1],
+      uint32_t e0 = 0u, c0 = 0u;
+#pragma unroll
+      for (int q = 0; q < DEFER; q++)
+        if (q == j % DEFER) {
+          e0 = ex[q];
+          c0 = cn[q];
+        }
+      emit_tile<Pol>(a, ring + js * INBUF, s_t[js], s_pre[js], s_cnt[js], e0, c0,
                      stage, tid, lane);
     };
     while (true) {
@@ -1008,7 +1021,7 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
       }
       if (Pol::hint(st)) s_flag[i % 3] = 1;
       if (tid == 0) {
-        // ring slot (i + PF) % RING held tile i - 3, emitted last iteration
+        // ring slot (i + PF) % RING held tile i - DEFER - 1, emitted last iteration
         start_tile((i + PF) % RING, tn);
         // flag slot of tile i + 1: last read after the block scan of i - 2 (every thread has
         // passed the block scan of i - 1 since), next written after the block scan of i
@@ -1033,12 +1046,16 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
 #ifdef UG_TRACE
       if (tid == 0 && i < TR_IT && blockIdx.x < 1024) g_trace[blockIdx.x][i][10] = gtime();  // AGG
 #endif
-      if (i >= 2) emit(i - 2);  // a7, a8
+      if (i >= DEFER) emit(i - DEFER);  // a7, a8
 #ifdef UG_TRACE
       if (tid == 0 && i < TR_IT && blockIdx.x < 1024) g_trace[blockIdx.x][i][11] = gtime();  // end
 #endif
-      ex[i & 1] = excl;  // tile i - 2's slot is free now
-      cn[i & 1] = cnt;
+#pragma unroll
+      for (int q = 0; q < DEFER; q++)  // tile i - DEFER's entry is free now
+        if (q == i % DEFER) {
+          ex[q] = excl;
+          cn[q] = cnt;
+        }
       i++;
     }
     // every look-back agent must see a past-the-end ticket to stop: the one owning tile i has;
@@ -1050,8 +1067,8 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
         mbar_arrive(&mb_tick[(i + k) % RING]);
       }
     }
-    // drain: tiles i - 2 and i - 1
-    for (int j = (i >= 2 ? i - 2 : 0); j < i; j++) emit(j);
+    // drain: tiles i - DEFER .. i - 1
+    for (int j = (i >= DEFER ? i - DEFER : 0); j < i; j++) emit(j);
     if (tid == 0) bulk_wait_all();  // all output written before the CTA retires
   }
   __syncthreads();
