@@ -19,7 +19,7 @@ for r in rows[1:]:
     cnt[name] += 1
 T = sum(tot.values())
 # the bench step launches each of these once (the validators run only in the untimed per-op leg)
-STEP = ("k_len8", "k_transcode<U8Pol>", "k_len16", "k_transcode<U16Pol>", "k_combine")
+STEP = ("k_len8", "k_transcode<U8Pol>", "k_len16", "k_transcode<U16Pol>", "k_transcode16", "k_combine")
 S = sum(tot[k] / cnt[k] for k in STEP if cnt[k])
 print(f"{'kernel':40s} {'launches':>8s} {'total_us':>10s} {'share':>7s} {'avg_us':>9s} {'step_share':>10s}")
 for k, v in tot.most_common():
