@@ -122,6 +122,27 @@ int ug_utf16_length_from_utf8_async(const uint8_t *in, size_t n, uint64_t *d_len
 int ug_utf8_length_from_utf16le_async(const uint16_t *in, size_t n, uint64_t *d_len,
                                       void *stream);
 
+/* ------------------------------------------------------------------ UTF-16BE
+ * The same operations on big-endian UTF-16: word k of the buffer is the code unit
+ * (byte[2k] << 8) | byte[2k + 1] ("utf16be file [0x00,0x41] -> words
+ * [0x0041]").  Results, positions (in words), capacities and error conventions are exactly
+ * those of the LE functions above on the byte-swapped buffer; no BOM handling (a BOM is data).
+ * The kernels are the LE kernels with the byte order folded into their low/high byte split
+ * (input) or unit packing (output), so they run at the LE speed. */
+ug_result utf16be_validate(const uint16_t *in, size_t n, void *stream);
+ug_result utf8_to_utf16be(const uint8_t *in, size_t n, uint16_t *out, size_t out_cap,
+                          void *stream);
+ug_result utf16be_to_utf8(const uint16_t *in, size_t n, uint8_t *out, size_t out_cap,
+                          void *stream);
+uint64_t utf8_length_from_utf16be(const uint16_t *in, size_t n, void *stream);
+int ug_utf16be_validate_async(const uint16_t *in, size_t n, ug_result *d_result, void *stream);
+int ug_utf8_to_utf16be_async(const uint8_t *in, size_t n, uint16_t *out, size_t out_cap,
+                             ug_result *d_result, void *stream);
+int ug_utf16be_to_utf8_async(const uint16_t *in, size_t n, uint8_t *out, size_t out_cap,
+                             ug_result *d_result, void *stream);
+int ug_utf8_length_from_utf16be_async(const uint16_t *in, size_t n, uint64_t *d_len,
+                                      void *stream);
+
 /* ------------------------------------------------------------------ sharded (multi-GPU)
  * One rank's share of a buffer cut at character boundaries (BASELINE
  * north_star item 3).  `in` points at the first OWNED code unit; the owned range is

@@ -176,6 +176,34 @@ def utf8_length_from_utf16le(u) -> int:
     return int(lib().ugo_utf8_length_from_utf16le(_ptr(a), a.size))
 
 
+# ---- UTF-16BE ----
+# SPEC.md S:525-529 (load_file): a utf16be buffer holds each code unit high byte first, and
+# "utf16be file [0x00,0x41] -> words [0x0041]".  So the BE operations are, by definition, the
+# LE operations on the byte-swapped words (the oracle's C codec stays the single source of the
+# codec arithmetic); positions and counts are in words either way.
+def byteswap16(u) -> np.ndarray:
+    """Word k -> (k & 0xFF) << 8 | k >> 8 (the other byte order of the same code unit)."""
+    a = _u16(u)
+    return ((a << 8) | (a >> 8)).astype(np.uint16)
+
+
+def utf16be_validate(u) -> Result:
+    return utf16le_validate(byteswap16(u))
+
+
+def utf16be_to_utf8(u, out_cap: int | None = None):
+    return utf16le_to_utf8(byteswap16(u), out_cap)
+
+
+def utf8_to_utf16be(s, out_cap: int | None = None):
+    r, out = utf8_to_utf16le(s, out_cap)
+    return r, byteswap16(out)
+
+
+def utf8_length_from_utf16be(u) -> int:
+    return utf8_length_from_utf16le(byteswap16(u))
+
+
 # ---- exhaustive sweeps ----
 def sweep_utf8(length: int, part: int = 0, nparts: int = 1):
     hk = np.zeros(7, dtype=np.uint64)

@@ -85,6 +85,14 @@ def _load():
         "utf8_to_utf16le_host": ([P, S, P, S, P], _CResult),
         "utf16le_to_utf8_host": ([P, S, P, S, P], _CResult),
         "ug_set_host_chunk": ([S], S),
+        "utf16be_validate": ([P, S, P], _CResult),
+        "utf8_to_utf16be": ([P, S, P, S, P], _CResult),
+        "utf16be_to_utf8": ([P, S, P, S, P], _CResult),
+        "utf8_length_from_utf16be": ([P, S, P], U64),
+        "ug_utf16be_validate_async": ([P, S, P, P], I),
+        "ug_utf8_to_utf16be_async": ([P, S, P, S, P, P], I),
+        "ug_utf16be_to_utf8_async": ([P, S, P, S, P, P], I),
+        "ug_utf8_length_from_utf16be_async": ([P, S, P, P], I),
         "ug_error_name": ([I], ctypes.c_char_p),
         "ug_launch_count": ([], U64),
         "ug_release_workspaces": ([], None),
@@ -174,6 +182,63 @@ def utf16_length_from_utf8(t_in, n: int | None = None, stream=None) -> int:
 def utf8_length_from_utf16le(t_in, n: int | None = None, stream=None) -> int:
     return int(lib.utf8_length_from_utf16le(_ptr(t_in), _units(t_in) if n is None else n,
                                             _stream(stream)))
+
+
+# --------------------------------------------------------------------------- UTF-16BE
+# Big-endian UTF-16: the tensors hold the raw big-endian
+# words; results are those of the LE functions on the byte-swapped buffer.
+def utf16be_validate(t_in, n: int | None = None, stream=None) -> Result:
+    return _res(lib.utf16be_validate(_ptr(t_in), _units(t_in) if n is None else n,
+                                     _stream(stream)))
+
+
+def utf8_to_utf16be(t_in, t_out, n: int | None = None, out_cap: int | None = None,
+                    stream=None) -> Result:
+    return _res(lib.utf8_to_utf16be(_ptr(t_in), _units(t_in) if n is None else n, _ptr(t_out),
+                                    _units(t_out) if out_cap is None else out_cap,
+                                    _stream(stream)))
+
+
+def utf16be_to_utf8(t_in, t_out, n: int | None = None, out_cap: int | None = None,
+                    stream=None) -> Result:
+    return _res(lib.utf16be_to_utf8(_ptr(t_in), _units(t_in) if n is None else n, _ptr(t_out),
+                                    _units(t_out) if out_cap is None else out_cap,
+                                    _stream(stream)))
+
+
+def utf8_length_from_utf16be(t_in, n: int | None = None, stream=None) -> int:
+    return int(lib.utf8_length_from_utf16be(_ptr(t_in), _units(t_in) if n is None else n,
+                                            _stream(stream)))
+
+
+def utf16be_validate_async(t_in, d_result, n=None, stream=None, result_off=0):
+    _check(lib.ug_utf16be_validate_async(_ptr(t_in), _units(t_in) if n is None else n,
+                                         _at(d_result, result_off), _stream(stream)),
+           "utf16be_validate_async")
+
+
+def utf8_to_utf16be_async(t_in, t_out, d_result, n=None, out_cap=None, stream=None,
+                          result_off=0):
+    _check(lib.ug_utf8_to_utf16be_async(_ptr(t_in), _units(t_in) if n is None else n,
+                                        _ptr(t_out),
+                                        _units(t_out) if out_cap is None else out_cap,
+                                        _at(d_result, result_off), _stream(stream)),
+           "utf8_to_utf16be_async")
+
+
+def utf16be_to_utf8_async(t_in, t_out, d_result, n=None, out_cap=None, stream=None,
+                          result_off=0):
+    _check(lib.ug_utf16be_to_utf8_async(_ptr(t_in), _units(t_in) if n is None else n,
+                                        _ptr(t_out),
+                                        _units(t_out) if out_cap is None else out_cap,
+                                        _at(d_result, result_off), _stream(stream)),
+           "utf16be_to_utf8_async")
+
+
+def utf8_length_from_utf16be_async(t_in, d_len, n=None, stream=None, len_off=0):
+    _check(lib.ug_utf8_length_from_utf16be_async(_ptr(t_in), _units(t_in) if n is None else n,
+                                                 _at(d_len, len_off), _stream(stream)),
+           "utf8_length_from_utf16be_async")
 
 
 # --------------------------------------------------------------------------- asynchronous

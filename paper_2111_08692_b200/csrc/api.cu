@@ -53,7 +53,7 @@ struct Workspace {
 
 struct DeviceInfo {
   int sms = 0;
-  int occ[4] = {0, 0, 0, 0};
+  int occ[NUM_OPS] = {};
   bool configured = false;
 };
 
@@ -67,7 +67,7 @@ cudaError_t device_info(int dev, DeviceInfo **out) {
   if (!d.configured) {
     cudaError_t e = cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
     if (e != cudaSuccess) return e;
-    for (int i = 0; i < 4; i++) {
+    for (int i = 0; i < NUM_OPS; i++) {
       e = tile_configure((Op)i);
       if (e != cudaSuccess) return e;
       e = tile_occupancy((Op)i, &d.occ[i]);
@@ -154,14 +154,13 @@ int enqueue_tile(Op op, const void *in, unsigned long long n, unsigned long long
                  unsigned long long ha, unsigned long long global_off, void *out,
                  unsigned long long out_cap, ResultDev *d_result, RecordDev *d_rec,
                  cudaStream_t s) {
-  const bool u16in = (op == Op::U16_VALIDATE || op == Op::U16_TO_U8);
+  const bool u16in = op_u16_input(op);
   const unsigned long long us = u16in ? 2 : 1;
   if (n > MAX_N) return UG_ERR_ARG;
   if (n > 0 && in == nullptr) return UG_ERR_ARG;
   if (u16in && ((uintptr_t)in & 1u)) return UG_ERR_ARG;
-  if (op == Op::U8_TO_U16 && ((uintptr_t)out & 1u)) return UG_ERR_ARG;
-  if ((op == Op::U8_TO_U16 || op == Op::U16_TO_U8) && out == nullptr && out_cap > 0)
-    return UG_ERR_ARG;
+  if ((op == Op::U8_TO_U16 || op == Op::U8_TO_U16BE) && ((uintptr_t)out & 1u)) return UG_ERR_ARG;
+  if (op_transcodes(op) && out == nullptr && out_cap > 0) return UG_ERR_ARG;
   if (n == 0) {
     if (d_result && cudaMemsetAsync(d_result, 0, sizeof(ResultDev), s) != cudaSuccess)
       return UG_ERR_CUDA;
@@ -183,7 +182,7 @@ int enqueue_tile(Op op, const void *in, unsigned long long n, unsigned long long
   a.ntiles = (unsigned long long)((a.win.n - 1 + a.win.lead) / TILE + 1);
   a.out = out;
   a.out_cap = out ? out_cap : 0;
-  if (op == Op::U8_TO_U16 || op == Op::U16_TO_U8) {
+  if (op_transcodes(op)) {
     if (ensure_status(w, a.ntiles) != cudaSuccess) return UG_ERR_CUDA;
     a.status = w->status;
   }
@@ -230,7 +229,7 @@ ug_result run_sync(Op op, const void *in, unsigned long long n, void *out,
 }
 
 int enqueue_len(bool u16in, const void *in, unsigned long long n, unsigned long long *d_len,
-                cudaStream_t s) {
+                cudaStream_t s, bool be = false) {
   if (d_len == nullptr) return UG_ERR_ARG;
   if (n > 0 && in == nullptr) return UG_ERR_ARG;
   if (u16in && ((uintptr_t)in & 1u)) return UG_ERR_ARG;
@@ -246,18 +245,19 @@ int enqueue_len(bool u16in, const void *in, unsigned long long n, unsigned long 
   unsigned long long want = (bytes + per_block - 1) / per_block;
   unsigned long long maxg = (unsigned long long)di->sms * 4;
   int grid = (int)(want < maxg ? (want ? want : 1) : maxg);
-  cudaError_t e = u16in ? launch_len16((const uint16_t *)in, n, w->ctr, d_len, grid, s)
+  cudaError_t e = u16in ? launch_len16((const uint16_t *)in, n, w->ctr, d_len, grid, s, be)
                         : launch_len8((const uint8_t *)in, n, w->ctr, d_len, grid, s);
   if (e != cudaSuccess) return UG_ERR_CUDA;
   g_launches.fetch_add(1);
   return UG_OK;
 }
 
-uint64_t run_len(bool u16in, const void *in, unsigned long long n, cudaStream_t s) {
+uint64_t run_len(bool u16in, const void *in, unsigned long long n, cudaStream_t s,
+                 bool be = false) {
   if (n == 0) return 0;
   Workspace *w;
   if (get_ws(s, &w) != cudaSuccess) return 0;
-  if (enqueue_len(u16in, in, n, w->d_len, s) != UG_OK) return 0;
+  if (enqueue_len(u16in, in, n, w->d_len, s, be) != UG_OK) return 0;
   std::lock_guard<std::mutex> lk(w->mu);
   if (cudaMemcpyAsync(w->h_len, w->d_len, sizeof(*w->h_len), cudaMemcpyDeviceToHost, s) !=
           cudaSuccess ||
@@ -481,6 +481,47 @@ int ug_utf16_length_from_utf8_async(const uint8_t *in, size_t n, uint64_t *d_len
 int ug_utf8_length_from_utf16le_async(const uint16_t *in, size_t n, uint64_t *d_len,
                                       void *stream) {
   return enqueue_len(true, in, n, (unsigned long long *)d_len, (cudaStream_t)stream);
+}
+
+// ---- UTF-16BE: same kernels, byte order folded into the byte split / unit
+// packing (DESIGN.md f3).
+ug_result utf16be_validate(const uint16_t *in, size_t n, void *stream) {
+  if (n > 0 && in == nullptr) return make_result(UG_ERR_ARG, 0, 0);
+  return run_sync(Op::U16BE_VALIDATE, in, n, nullptr, 0, (cudaStream_t)stream);
+}
+ug_result utf8_to_utf16be(const uint8_t *in, size_t n, uint16_t *out, size_t out_cap,
+                          void *stream) {
+  if (n > 0 && in == nullptr) return make_result(UG_ERR_ARG, 0, 0);
+  return run_sync(Op::U8_TO_U16BE, in, n, out, out_cap, (cudaStream_t)stream);
+}
+ug_result utf16be_to_utf8(const uint16_t *in, size_t n, uint8_t *out, size_t out_cap,
+                          void *stream) {
+  if (n > 0 && in == nullptr) return make_result(UG_ERR_ARG, 0, 0);
+  return run_sync(Op::U16BE_TO_U8, in, n, out, out_cap, (cudaStream_t)stream);
+}
+uint64_t utf8_length_from_utf16be(const uint16_t *in, size_t n, void *stream) {
+  return run_len(true, in, n, (cudaStream_t)stream, true);
+}
+int ug_utf16be_validate_async(const uint16_t *in, size_t n, ug_result *d_result, void *stream) {
+  if (!d_result) return UG_ERR_ARG;
+  return enqueue_tile(Op::U16BE_VALIDATE, in, n, 0, 0, 0, nullptr, 0, (ResultDev *)d_result,
+                      nullptr, (cudaStream_t)stream);
+}
+int ug_utf8_to_utf16be_async(const uint8_t *in, size_t n, uint16_t *out, size_t out_cap,
+                             ug_result *d_result, void *stream) {
+  if (!d_result) return UG_ERR_ARG;
+  return enqueue_tile(Op::U8_TO_U16BE, in, n, 0, 0, 0, out, out_cap, (ResultDev *)d_result,
+                      nullptr, (cudaStream_t)stream);
+}
+int ug_utf16be_to_utf8_async(const uint16_t *in, size_t n, uint8_t *out, size_t out_cap,
+                             ug_result *d_result, void *stream) {
+  if (!d_result) return UG_ERR_ARG;
+  return enqueue_tile(Op::U16BE_TO_U8, in, n, 0, 0, 0, out, out_cap, (ResultDev *)d_result,
+                      nullptr, (cudaStream_t)stream);
+}
+int ug_utf8_length_from_utf16be_async(const uint16_t *in, size_t n, uint64_t *d_len,
+                                      void *stream) {
+  return enqueue_len(true, in, n, (unsigned long long *)d_len, (cudaStream_t)stream, true);
 }
 
 static size_t clamp_halo(size_t h, size_t maxh) { return h < maxh ? h : maxh; }

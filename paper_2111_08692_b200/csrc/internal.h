@@ -39,7 +39,19 @@ struct TileArgs {
   unsigned long long global_off;  // sharded: global offset of position 0 (code units)
 };
 
-enum class Op : int { U8_VALIDATE = 0, U8_TO_U16 = 1, U16_VALIDATE = 2, U16_TO_U8 = 3 };
+enum class Op : int {
+  U8_VALIDATE = 0, U8_TO_U16 = 1, U16_VALIDATE = 2, U16_TO_U8 = 3,
+  U16BE_VALIDATE = 4, U8_TO_U16BE = 5, U16BE_TO_U8 = 6  // UTF-16BE
+};
+constexpr int NUM_OPS = 7;
+inline bool op_u16_input(Op op) {
+  return op == Op::U16_VALIDATE || op == Op::U16_TO_U8 || op == Op::U16BE_VALIDATE ||
+         op == Op::U16BE_TO_U8;
+}
+inline bool op_transcodes(Op op) {
+  return op == Op::U8_TO_U16 || op == Op::U16_TO_U8 || op == Op::U8_TO_U16BE ||
+         op == Op::U16BE_TO_U8;
+}
 
 size_t tile_smem_bytes(Op op);
 cudaError_t tile_configure(Op op);  // set max dynamic smem (idempotent)
@@ -49,7 +61,7 @@ cudaError_t launch_tile(Op op, const TileArgs &a, int grid, cudaStream_t s);
 cudaError_t launch_len8(const uint8_t *in, unsigned long long n, Counters *ctr,
                         unsigned long long *d_len, int grid, cudaStream_t s);
 cudaError_t launch_len16(const uint16_t *in, unsigned long long n, Counters *ctr,
-                         unsigned long long *d_len, int grid, cudaStream_t s);
+                         unsigned long long *d_len, int grid, cudaStream_t s, bool be = false);
 cudaError_t launch_combine(const RecordDev *recs, int nranks, int rank,
                            unsigned long long total_in, ResultDev *res,
                            unsigned long long *out_off, cudaStream_t s);

@@ -205,7 +205,9 @@ __device__ __forceinline__ uint32_t bit_range(long long pos0, long long lo, long
   return mb & ~ma;
 }
 
-struct U8Pol {
+// BE: UTF-16BE output; only the unit packing differs.
+template <bool BE>
+struct U8PolT {
   using Out = uint16_t;
   static constexpr int UNIT = 1;                      // input bytes per position
   static constexpr int STAGE = 2 * (TILE + 32);        // stage bytes per buffer
@@ -305,22 +307,23 @@ struct U8Pol {
         for (int j = 0; j < 8; j++) {
           const uint32_t x = wb[32 * j];
           *reinterpret_cast<uint2 *>(sb + 128 * j) =
-              make_uint2(prmt(x, 0u, 0x4140u), prmt(x, 0u, 0x4342u));
+              make_uint2(prmt(x, 0u, BE ? 0x1404u : 0x4140u), prmt(x, 0u, BE ? 0x3424u : 0x4342u));
         }
       } else if ((o0 & 1u) == 0u) {
 #pragma unroll
         for (int j = 0; j < 8; j++) {
           const uint32_t x = wb[32 * j];
           uint32_t *d = reinterpret_cast<uint32_t *>(sb + 128 * j);
-          d[0] = prmt(x, 0u, 0x4140u);
-          d[1] = prmt(x, 0u, 0x4342u);
+          d[0] = prmt(x, 0u, BE ? 0x1404u : 0x4140u);
+          d[1] = prmt(x, 0u, BE ? 0x3424u : 0x4342u);
         }
       } else {
 #pragma unroll
         for (int j = 0; j < 8; j++) {
           const uint32_t x = wb[32 * j];
 #pragma unroll
-          for (int q = 0; q < 4; q++) sb[128 * j + q] = (uint16_t)((x >> (8 * q)) & 0xFFu);
+          for (int q = 0; q < 4; q++)
+            sb[128 * j + q] = (uint16_t)(((x >> (8 * q)) & 0xFFu) << (BE ? 8 : 0));
         }
       }
       return;
@@ -343,7 +346,7 @@ struct U8Pol {
 #pragma unroll
     for (int k = 0; k < 8; k++) {
       uint32_t u01, u23;
-      uint32_t em = u8::units4(s.w[k], cy, &u01, &u23);
+      uint32_t em = u8::units4<BE>(s.w[k], cy, &u01, &u23);
       if (!IN) em &= range_bytes(s.pos0 + 4 * k, 0, s.n) & 0x01010101u;
       const uint32_t inc2 = em * 0x02020202u;  // byte j: 2 x units emitted by positions <= j
       const uint32_t a1 = mad(prmt(inc2, 0u, 0x4440u), 1u, p);
@@ -388,6 +391,9 @@ struct U8Pol {
   }
 };
 
+using U8Pol = U8PolT<false>;
+using U8PolBE = U8PolT<true>;
+
 // ============================================================================ UTF-16 policy
 // Positions are words.  Thread `tid` owns tile words [16 tid, 16 tid + 16), two per register.
 // Position of the first set lane bit among 8 registers of lane masks (cold path).
@@ -401,9 +407,15 @@ __device__ __noinline__ unsigned long long first_error_lane(uint32_t e0, uint32_
   return NONE;
 }
 
-struct U16Pol {
+// BE: UTF-16BE input: the low/high byte split of the classes swaps its
+// selectors (u16::classes4<BE>), the two scalar context words are byte-swapped.
+template <bool BE>
+struct U16PolT {
   using Out = uint8_t;
   static constexpr int UNIT = 2;
+  __device__ static __forceinline__ uint32_t native(uint32_t w) {  // a stored word's value
+    return BE ? (((w >> 8) | (w << 8)) & 0xFFFFu) : w;
+  }
   static constexpr int STAGE = 3 * (TILE / 2) + 64;
   struct St {
     uint32_t w[8];                   // words 2k (low half), 2k + 1 (high half) of w[k]
@@ -435,12 +447,12 @@ struct U16Pol {
     uint32_t nx = __shfl_down_sync(FULL, s.w[0], 1);
     if (lane == 0) pv = *reinterpret_cast<const uint32_t *>(my - 4);
     if (lane == 31) nx = *reinterpret_cast<const uint32_t *>(my + BPT);
-    s.prev_word = pv >> 16;
-    s.next_word = nx & 0xFFFFu;
+    s.prev_word = native(pv >> 16);
+    s.next_word = native(nx & 0xFFFFu);
     s.pos0 = tpw + (BPT / 2) * tid;
     s.own = IN ? 0xFFFFu : (bit_range(s.pos0, 0, nw) & 0xFFFFu);
     const uint32_t orv = s.w[0] | s.w[1] | s.w[2] | s.w[3] | s.w[4] | s.w[5] | s.w[6] | s.w[7];
-    s.wasc = __all_sync(FULL, (orv & 0xFF80FF80u) == 0u);
+    s.wasc = __all_sync(FULL, (orv & (BE ? 0x80FF80FFu : 0xFF80FF80u)) == 0u);
   }
 
   // a9 pairing predicate (exact) and a5 widths, byte-SWAR over 4 words.
@@ -455,14 +467,14 @@ struct U16Pol {
       return xc ? 16u : 0u;
     }
     uint32_t Hprev = u16::is_high(s.prev_word) ? 0x80000000u : 0u;  // byte 3 = word -1
-    u16::Cls4 c = u16::classes4(s.w[0], s.w[1]);
+    u16::Cls4 c = u16::classes4<BE>(s.w[0], s.w[1]);
     uint32_t acc = 0, anyerr = 0, errm[4];
 #pragma unroll
     for (int g = 0; g < 4; g++) {
       u16::Cls4 cn;
       uint32_t Lnext;
       if (g < 3) {
-        cn = u16::classes4(s.w[2 * g + 2], s.w[2 * g + 3]);
+        cn = u16::classes4<BE>(s.w[2 * g + 2], s.w[2 * g + 3]);
         Lnext = cn.L;
       } else {
         Lnext = u16::is_low(s.next_word) ? 0x80u : 0u;
@@ -513,13 +525,13 @@ struct U16Pol {
 #pragma unroll
         for (int j = 0; j < 4; j++) {
           const uint2 x = wb[32 * j];
-          *reinterpret_cast<uint32_t *>(sb + 128 * j) = prmt(x.x, x.y, 0x6420u);
+          *reinterpret_cast<uint32_t *>(sb + 128 * j) = prmt(x.x, x.y, BE ? 0x7531u : 0x6420u);
         }
       } else {
 #pragma unroll
         for (int j = 0; j < 4; j++) {
           const uint2 x = wb[32 * j];
-          const uint32_t v = prmt(x.x, x.y, 0x6420u);
+          const uint32_t v = prmt(x.x, x.y, BE ? 0x7531u : 0x6420u);
 #pragma unroll
           for (int q = 0; q < 4; q++) sb[128 * j + q] = (uint8_t)(v >> (8 * q));
         }
@@ -539,7 +551,7 @@ struct U16Pol {
     uint32_t lprev = (s.prev_word & 0xFFu) << 24;
 #pragma unroll
     for (int g = 0; g < 4; g++) {
-      const u16::Cls4 c = u16::classes4(s.w[2 * g], s.w[2 * g + 1]);
+      const u16::Cls4 c = u16::classes4<BE>(s.w[2 * g], s.w[2 * g + 1]);
       const uint32_t lp = fsl(lprev, c.lo, 8);
       lprev = c.lo;
       uint32_t O0, O1, O2;
@@ -601,13 +613,13 @@ struct U16Pol {
     uint32_t Hprev = u16::is_high(s.prev_word) ? 0x80000000u : 0u;
     uint32_t errm[4];
     uint32_t anyerr = 0;
-    u16::Cls4 c = u16::classes4(s.w[0], s.w[1]);
+    u16::Cls4 c = u16::classes4<BE>(s.w[0], s.w[1]);
 #pragma unroll
     for (int g = 0; g < 4; g++) {
       u16::Cls4 cn;
       uint32_t Lnext;
       if (g < 3) {
-        cn = u16::classes4(s.w[2 * g + 2], s.w[2 * g + 3]);
+        cn = u16::classes4<BE>(s.w[2 * g + 2], s.w[2 * g + 3]);
         Lnext = cn.L;
       } else {
         Lnext = u16::is_low(s.next_word) ? 0x80u : 0u;
@@ -673,10 +685,13 @@ struct U16Pol {
     if (from < 0) from = 0;
     unsigned long long c = 0;
     for (long long i = from + lane; i < (long long)e; i += 32)
-      c += u16::width(word_at(win, i), word_at(win, i - 1));
+      c += u16::width(native(word_at(win, i)), native(word_at(win, i - 1)));
     *wr = base + warp_sum64(c);
   }
 };
+
+using U16Pol = U16PolT<false>;
+using U16PolBE = U16PolT<true>;
 
 // Last CTA to finish: outcome + counter reset.  n_units in input code units.
 template <class Pol>
@@ -1146,8 +1161,9 @@ __global__ void __launch_bounds__(LNT) k_len8(const uint8_t *in, unsigned long l
 // [u >= 0x80] + [u >= 0x800 and not a surrogate] (the width minus 1; a surrogate counts 2, so a
 // pair counts 4), added into a byte-lane accumulator by IMAD.HI (FMA pipe; the compares use the
 // ALU pipe).  Lane sums stay below 256 for up to 127 calls.
+template <bool BE = false>
 __device__ __forceinline__ uint32_t len16_acc4(uint32_t a, uint32_t b, uint32_t acc) {
-  const uint32_t lo = prmt(a, b, 0x6420u), hi = prmt(a, b, 0x7531u);
+  const uint32_t lo = prmt(a, b, BE ? 0x7531u : 0x6420u), hi = prmt(a, b, BE ? 0x6420u : 0x7531u);
   const uint32_t h7 = hi & 0x7F7F7F7Fu;
   const uint32_t ge80 = (mad(h7, 1u, 0x7F7F7F7Fu) | hi | lo) & HI;   // hi != 0 or lo >= 0x80
   const uint32_t ge800 = (mad(h7, 1u, 0x78787878u) | hi) & HI;       // hi >= 8
@@ -1158,6 +1174,7 @@ __device__ __forceinline__ uint32_t len16_acc4(uint32_t a, uint32_t b, uint32_t 
 }
 __device__ __forceinline__ uint32_t lane_sum(uint32_t acc) { return (acc * 0x01010101u) >> 24; }
 
+template <bool BE>
 __global__ void __launch_bounds__(LNT) k_len16(const uint16_t *in, unsigned long long n,
                                               Counters *ctr, unsigned long long *d_len) {
   const uintptr_t addr = (uintptr_t)in;
@@ -1168,8 +1185,9 @@ __global__ void __launch_bounds__(LNT) k_len16(const uint16_t *in, unsigned long
   const unsigned long long stride = (unsigned long long)gridDim.x * blockDim.x;
   unsigned long long sum = 0;
   auto quad = [](const uint4 &v) {  // 8 words
-    return 8u + lane_sum(len16_acc4(v.z, v.w, len16_acc4(v.x, v.y, 0u)));
+    return 8u + lane_sum(len16_acc4<BE>(v.z, v.w, len16_acc4<BE>(v.x, v.y, 0u)));
   };
+  auto word = [](uint32_t w) { return BE ? (((w >> 8) | (w << 8)) & 0xFFFFu) : w; };
   unsigned long long i = (unsigned long long)blockIdx.x * blockDim.x + threadIdx.x;
   for (; i + 3 * stride < nb; i += 4 * stride) {
     uint4 v[4];
@@ -1177,14 +1195,16 @@ __global__ void __launch_bounds__(LNT) k_len16(const uint16_t *in, unsigned long
     for (int j = 0; j < 4; j++) v[j] = __ldcs(body + i + j * stride);
     uint32_t acc = 0;
 #pragma unroll
-    for (int j = 0; j < 4; j++) acc = len16_acc4(v[j].z, v[j].w, len16_acc4(v[j].x, v[j].y, acc));
+    for (int j = 0; j < 4; j++)
+      acc = len16_acc4<BE>(v[j].z, v[j].w, len16_acc4<BE>(v[j].x, v[j].y, acc));
     sum += 32u + lane_sum(acc);
   }
   for (; i < nb; i += stride) sum += quad(__ldcs(body + i));
   if (blockIdx.x == 0) {
-    for (unsigned long long j = threadIdx.x; j < head; j += blockDim.x) sum += len16_word(in[j]);
+    for (unsigned long long j = threadIdx.x; j < head; j += blockDim.x)
+      sum += len16_word(word(in[j]));
     for (unsigned long long j = head + nb * 8 + threadIdx.x; j < n; j += blockDim.x)
-      sum += len16_word(in[j]);
+      sum += len16_word(word(in[j]));
   }
   finish_reduction(sum, ctr, d_len);
 }
@@ -1214,6 +1234,7 @@ constexpr int D16 = RING16 - PF16 - 1;  // tiles awaiting their prefix (emit def
 static_assert(PF16 >= 1 && D16 >= 1, "ring: loads in flight + the tile counted + deferral");
 constexpr int T16_THREADS = NT + 32;
 
+template <bool BE>
 __device__ __forceinline__ void emit_tile16(const TileArgs &a, const uint8_t *img, long long t,
                                             unsigned long long P, uint32_t C, uint32_t excl,
                                             uint32_t cnt, uint8_t *stage, int tid, int lane) {
@@ -1222,14 +1243,15 @@ __device__ __forceinline__ void emit_tile16(const TileArgs &a, const uint8_t *im
   const long long tp = tile_pos(win, t);
   uint8_t *out = reinterpret_cast<uint8_t *>(a.out);
   const uint32_t ph = (uint32_t)(((uintptr_t)(out + P)) & 15u);
-  U16Pol::St st;
+  using P16 = U16PolT<BE>;
+  typename P16::St st;
   unsigned long long f;
   if (tp >= 0 && tp + TILE <= win.n) {  // tile-uniform
-    U16Pol::load<true>(st, img, tid, lane, tp, win.n);
-    f = U16Pol::decode_validate<true>(st, stage, ph + excl, ph + excl + cnt);
+    P16::template load<true>(st, img, tid, lane, tp, win.n);
+    f = P16::template decode_validate<true>(st, stage, ph + excl, ph + excl + cnt);
   } else {
-    U16Pol::load<false>(st, img, tid, lane, tp, win.n);
-    f = U16Pol::decode_validate<false>(st, stage, ph + excl, ph + excl + cnt);
+    P16::template load<false>(st, img, tid, lane, tp, win.n);
+    f = P16::template decode_validate<false>(st, stage, ph + excl, ph + excl + cnt);
   }
   if (f != NONE) atomicMin(&a.ctr->err_min, f);  // a4 (cold)
   named_sync<BAR_DATA, NT>();  // the whole tile is in the stage
@@ -1253,6 +1275,7 @@ __device__ __forceinline__ void emit_tile16(const TileArgs &a, const uint8_t *im
   }
 }
 
+template <bool BE>
 __global__ void __launch_bounds__(T16_THREADS, CTAS_PER_SM) k_transcode16(const TileArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t *ring = smem;
@@ -1342,7 +1365,7 @@ __global__ void __launch_bounds__(T16_THREADS, CTAS_PER_SM) k_transcode16(const 
 #pragma unroll
       for (int q = 0; q <= D16; q++)
         if (q == j % (D16 + 1)) v = oc[q];
-      emit_tile16(a, ring + js * INBUF, s_t[js], s_pre[js], s_cnt[js],
+      emit_tile16<BE>(a, ring + js * INBUF, s_t[js], s_pre[js], s_cnt[js],
                   s_wsum[js][warp] + (v >> 8), v & 0xFFu, stage, tid, lane);
     };
     int i = 0;
@@ -1365,15 +1388,15 @@ __global__ void __launch_bounds__(T16_THREADS, CTAS_PER_SM) k_transcode16(const 
       const uint4 q0 = my[0], q1 = my[1];
       uint32_t cnt;
       if (tp >= 0 && tp + TILE <= win.n) {
-        cnt = 16u + lane_sum(len16_acc4(q1.z, q1.w, len16_acc4(q1.x, q1.y,
-                             len16_acc4(q0.z, q0.w, len16_acc4(q0.x, q0.y, 0u)))));
+        cnt = 16u + lane_sum(len16_acc4<BE>(q1.z, q1.w, len16_acc4<BE>(q1.x, q1.y,
+                             len16_acc4<BE>(q0.z, q0.w, len16_acc4<BE>(q0.x, q0.y, 0u)))));
       } else {
         const uint32_t q[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
         const long long w0 = (tp + BPT * tid) / 2, nw = win.n / 2;
         cnt = 0;
 #pragma unroll
         for (int k = 0; k < 16; k++)
-          if (w0 + k >= 0 && w0 + k < nw) cnt += len16_word((q[k >> 1] >> (16 * (k & 1))) & 0xFFFFu);
+          if (w0 + k >= 0 && w0 + k < nw) cnt += len16_word(U16PolT<BE>::native((q[k >> 1] >> (16 * (k & 1))) & 0xFFFFu));
       }
       uint32_t sc = cnt;  // in-warp inclusive scan
 #pragma unroll
@@ -1407,7 +1430,7 @@ __global__ void __launch_bounds__(T16_THREADS, CTAS_PER_SM) k_transcode16(const 
     if (tid == 0) bulk_wait_all();
   }
   __syncthreads();
-  finish_call<U16Pol>(a, true, tid, warp, lane, &s_last);
+  finish_call<U16PolT<BE>>(a, true, tid, warp, lane, &s_last);
 }
 
 // ============================================================================ combine
@@ -1470,9 +1493,12 @@ cudaError_t trace_read(void *host, size_t bytes) {
 size_t tile_smem_bytes(Op op) {
   switch (op) {
     case Op::U8_VALIDATE:
-    case Op::U16_VALIDATE: return VRING * INBUF;
-    case Op::U8_TO_U16: return RING * INBUF + U8Pol::STAGE;
+    case Op::U16_VALIDATE:
+    case Op::U16BE_VALIDATE: return VRING * INBUF;
+    case Op::U8_TO_U16:
+    case Op::U8_TO_U16BE: return RING * INBUF + U8Pol::STAGE;
     case Op::U16_TO_U8:
+    case Op::U16BE_TO_U8:
 #ifndef UG_U16_TILE_SCAN
       return RING16 * INBUF + U16Pol::STAGE;
 #else
@@ -1483,23 +1509,45 @@ size_t tile_smem_bytes(Op op) {
 }
 
 static int tile_threads(Op op) {
+  switch (op) {
+    case Op::U8_TO_U16:
+    case Op::U8_TO_U16BE: return NT + 32 * NLB;
+    case Op::U16_TO_U8:
+    case Op::U16BE_TO_U8:
 #ifndef UG_U16_TILE_SCAN
-  if (op == Op::U16_TO_U8) return T16_THREADS;
+      return T16_THREADS;
+#else
+      return NT + 32 * NLB;
 #endif
-  return (op == Op::U8_TO_U16 || op == Op::U16_TO_U8) ? NT + 32 * NLB : NT;
+    default: return NT;
+  }
 }
+
+#ifndef UG_U16_TILE_SCAN
+template <bool BE>
+static const void *rev_fn() { return (const void *)k_transcode16<BE>; }
+template <bool BE>
+static void rev_launch(const TileArgs &a, int grid, int nt, size_t sm, cudaStream_t s) {
+  k_transcode16<BE><<<grid, nt, sm, s>>>(a);
+}
+#else
+template <bool BE>
+static const void *rev_fn() { return (const void *)k_transcode<U16PolT<BE>>; }
+template <bool BE>
+static void rev_launch(const TileArgs &a, int grid, int nt, size_t sm, cudaStream_t s) {
+  k_transcode<U16PolT<BE>><<<grid, nt, sm, s>>>(a);
+}
+#endif
 
 static const void *tile_fn(Op op) {
   switch (op) {
     case Op::U8_VALIDATE: return (const void *)k_validate<U8Pol>;
     case Op::U8_TO_U16: return (const void *)k_transcode<U8Pol>;
     case Op::U16_VALIDATE: return (const void *)k_validate<U16Pol>;
-    case Op::U16_TO_U8:
-#ifndef UG_U16_TILE_SCAN
-      return (const void *)k_transcode16;
-#else
-      return (const void *)k_transcode<U16Pol>;
-#endif
+    case Op::U16_TO_U8: return rev_fn<false>();
+    case Op::U16BE_VALIDATE: return (const void *)k_validate<U16PolBE>;
+    case Op::U8_TO_U16BE: return (const void *)k_transcode<U8PolBE>;
+    case Op::U16BE_TO_U8: return rev_fn<true>();
   }
   return nullptr;
 }
@@ -1521,13 +1569,10 @@ cudaError_t launch_tile(Op op, const TileArgs &a, int grid, cudaStream_t s) {
     case Op::U8_VALIDATE: k_validate<U8Pol><<<grid, nt, sm, s>>>(a); break;
     case Op::U16_VALIDATE: k_validate<U16Pol><<<grid, nt, sm, s>>>(a); break;
     case Op::U8_TO_U16: k_transcode<U8Pol><<<grid, nt, sm, s>>>(a); break;
-    case Op::U16_TO_U8:
-#ifndef UG_U16_TILE_SCAN
-      k_transcode16<<<grid, nt, sm, s>>>(a);
-#else
-      k_transcode<U16Pol><<<grid, nt, sm, s>>>(a);
-#endif
-      break;
+    case Op::U16_TO_U8: rev_launch<false>(a, grid, nt, sm, s); break;
+    case Op::U16BE_VALIDATE: k_validate<U16PolBE><<<grid, nt, sm, s>>>(a); break;
+    case Op::U8_TO_U16BE: k_transcode<U8PolBE><<<grid, nt, sm, s>>>(a); break;
+    case Op::U16BE_TO_U8: rev_launch<true>(a, grid, nt, sm, s); break;
   }
   return cudaGetLastError();
 }
@@ -1538,8 +1583,11 @@ cudaError_t launch_len8(const uint8_t *in, unsigned long long n, Counters *ctr,
   return cudaGetLastError();
 }
 cudaError_t launch_len16(const uint16_t *in, unsigned long long n, Counters *ctr,
-                         unsigned long long *d_len, int grid, cudaStream_t s) {
-  k_len16<<<grid, LNT, 0, s>>>(in, n, ctr, d_len);
+                         unsigned long long *d_len, int grid, cudaStream_t s, bool be) {
+  if (be)
+    k_len16<true><<<grid, LNT, 0, s>>>(in, n, ctr, d_len);
+  else
+    k_len16<false><<<grid, LNT, 0, s>>>(in, n, ctr, d_len);
   return cudaGetLastError();
 }
 cudaError_t launch_combine(const RecordDev *recs, int nranks, int rank,

@@ -133,10 +133,13 @@ struct Cls4 {
   uint32_t ge80, ge800, S, H;   // u >= 0x80, u >= 0x800, surrogate, high surrogate
   uint32_t L;                   // low surrogate
 };
+// BE: the words are stored big-endian (UTF-16BE): the byte order is folded
+// into the split by swapping the two selectors, everything after it is unchanged.
+template <bool BE = false>
 UG_HD Cls4 classes4(uint32_t wa, uint32_t wb) {
   Cls4 c;
-  c.lo = prmt(wa, wb, 0x6420u);
-  c.hi = prmt(wa, wb, 0x7531u);
+  c.lo = prmt(wa, wb, BE ? 0x7531u : 0x6420u);
+  c.hi = prmt(wa, wb, BE ? 0x6420u : 0x7531u);
   const uint32_t h7 = c.hi & 0x7F7F7F7Fu;
   c.ge800 = ((h7 + 0x78787878u) | c.hi) & HI;         // hi >= 8 (no carries: 7-bit adds)
   c.ge80 = ((h7 + 0x7F7F7F7Fu) | c.hi | c.lo) & HI;    // hi != 0 or lo >= 0x80

@@ -128,6 +128,9 @@ UG_HD Carry carry_of(uint32_t x) {
 // every emitting byte.  Units at non-emitting positions are garbage.
 // The class masks are taken in lsb-per-byte form straight from a funnel shift by 8d + 1
 // (d = distance to the lead), so every per-byte constant is one multiply (FMA pipe).
+// BE: units stored big-endian (UTF-16BE output): the two PRMT that pair
+// low and high bytes into units take the bytes in the other order - no extra instruction.
+template <bool BE = false>
 UG_HD uint32_t units4(uint32_t x, Carry &c, uint32_t *u01, uint32_t *u23) {
   const Carry n = carry_of(x);
   const uint32_t bp1 = fsl(c.x, x, 8), bp2 = fsl(c.x, x, 16);  // bytes e-1, e-2
@@ -147,8 +150,8 @@ UG_HD uint32_t units4(uint32_t x, Carry &c, uint32_t *u01, uint32_t *u23) {
   const uint32_t hbm = (hb | HI) - 0x04040404u;  // per byte 0x80 + hb - 4, no borrows
   lb = mux(Mh, mux(0xF0F0F0F0u, hbm << 4, shr_fma<4>(lb)), lb);
   hb = mux(Mh, (shr_fma<4>(hbm) & 0x03030303u) | 0xD8D8D8D8u, hb);
-  *u01 = prmt(lb, hb, 0x5140u);
-  *u23 = prmt(lb, hb, 0x7362u);
+  *u01 = prmt(lb, hb, BE ? 0x1504u : 0x5140u);
+  *u23 = prmt(lb, hb, BE ? 0x3726u : 0x7362u);
   return em;
 }
 

@@ -446,3 +446,106 @@ def test_length_from_large_random(kind):
     b = u.view(np.uint8)
     _, t8 = to_dev(b, pad_before=5)
     assert ug.utf16_length_from_utf8(t8) == oracle.utf16_length_from_utf8(b)
+
+
+# ----------------------------------------------------------------------------- UTF-16BE (f3)
+def be_raw(u_native: np.ndarray) -> np.ndarray:
+    """Memory words of the big-endian encoding of the code units u_native."""
+    return np.frombuffer(u_native.astype(">u2").tobytes(), dtype="<u2").copy()
+
+
+def check_utf16be(w: np.ndarray, offset=0, cap=None):
+    """w: raw big-endian words as stored in memory."""
+    ref_r, ref_o = oracle.utf16be_to_utf8(w, out_cap=cap)
+    _, t = to_dev(w.astype(np.uint16), pad_before=offset, pad_after=32)
+    cap_ = 3 * w.size if cap is None else cap
+    big_out = torch.full((cap_ + 64,), 0x5A, dtype=torch.uint8, device=DEV)
+    r = ug.utf16be_to_utf8(t, big_out[:cap_], out_cap=cap_)
+    o = big_out.cpu().numpy()
+    assert np.all(o[cap_:] == 0x5A), "wrote past out_cap"
+    assert tuple(r) == tuple(ref_r), (r, ref_r)
+    if r.error >= 0:
+        assert np.array_equal(o[: r.written], ref_o)
+    assert tuple(ug.utf16be_validate(t)) == tuple(oracle.utf16be_validate(w))
+    assert ug.utf8_length_from_utf16be(t) == oracle.utf8_length_from_utf16be(w)
+    return r
+
+
+def check_utf8_be(a: np.ndarray, offset=0, cap=None):
+    ref_r, ref_o = oracle.utf8_to_utf16be(a, out_cap=cap)
+    _, t = to_dev(a, pad_before=offset, pad_after=64)
+    cap_ = a.size if cap is None else cap
+    big_out = torch.full((cap_ + 64,), 0x5A5A, dtype=torch.int16, device=DEV)
+    r = ug.utf8_to_utf16be(t, big_out[:cap_], out_cap=cap_)
+    o = big_out.cpu().numpy().view(np.uint16)
+    assert np.all(o[cap_:] == 0x5A5A), "wrote past out_cap"
+    assert tuple(r) == tuple(ref_r), (r, ref_r)
+    if r.error >= 0:
+        assert np.array_equal(o[: r.written], ref_o)
+    return r
+
+
+def test_utf16be_fuzz():
+    rng = np.random.default_rng(0xBE)
+    alpha = np.array([0x0041, 0x007F, 0x0080, 0x07FF, 0x0800, 0xD7FF, 0xD800, 0xDBFF, 0xDC00,
+                      0xDFFF, 0xE000, 0xFFFF, 0x0100, 0x1234], dtype=np.uint16)
+    for k in range(300):
+        n = int(rng.integers(0, 200))
+        cu = alpha[rng.integers(0, alpha.size, n)] if k % 2 else \
+            rng.integers(0, 65536, n).astype(np.uint16)
+        check_utf16be(be_raw(cu), offset=2 * int(rng.integers(0, 8)))
+
+
+def test_utf8_to_utf16be_fuzz():
+    rng = np.random.default_rng(0xBE8)
+    for k in range(300):
+        n = int(rng.integers(0, 300))
+        a = np.frombuffer(synth.gen_chunk("mixed", "utf8", n, 98, k), dtype=np.uint8).copy()
+        if n and k % 3 == 0:
+            a[rng.integers(0, n)] = rng.integers(0x80, 0x100)
+        check_utf8_be(a, offset=int(rng.integers(0, 16)))
+
+
+@pytest.mark.parametrize("key", ["c0", "c1", "c3"])
+def test_utf16be_configs(key):
+    """Config text (several tiles, ragged tail) both ways in BE, element by element, plus an
+    error copy, the ASCII warp paths (c1) and capacity clipping."""
+    x = synth.generate(key, size=None if key == "c0" else (4 << 20) + (5 if key == "c1" else 6))
+    if x.dtype == np.uint8:
+        r = check_utf8_be(x, offset=3)
+        assert r.error == 0
+        u = oracle.utf8_to_utf16le(x)[1]
+    else:
+        u = x
+    w = be_raw(u)
+    assert check_utf16be(w, offset=2).error == 0
+    v = u.copy()
+    p, _ = synth.inject_utf16_error(v, v.size // 3, v.size // 3 + 999, np.random.default_rng(5))
+    r = check_utf16be(be_raw(v))
+    assert (r.error, r.position) == (ug.SURROGATE, p)
+    need = oracle.utf16le_to_utf8(u)[0].written
+    check_utf16be(w, cap=need - 1)
+    if x.dtype == np.uint8:
+        check_utf8_be(x, cap=u.size // 2)
+
+
+def test_utf16be_async():
+    x = synth.generate("c0")
+    u = oracle.utf8_to_utf16le(x)[1]
+    w = be_raw(u)
+    _, tw = to_dev(w)
+    _, t8 = to_dev(x)
+    res = ug.result_buffer(DEV, 3)
+    out8 = torch.zeros(3 * w.size, dtype=torch.uint8, device=DEV)
+    out16 = torch.zeros(x.size, dtype=torch.int16, device=DEV)
+    lens = torch.zeros(1, dtype=torch.int64, device=DEV)
+    ug.utf16be_to_utf8_async(tw, out8, res)
+    ug.utf16be_validate_async(tw, res, result_off=ug.RESULT_BYTES)
+    ug.utf8_to_utf16be_async(t8, out16, res, result_off=2 * ug.RESULT_BYTES)
+    ug.utf8_length_from_utf16be_async(tw, lens)
+    torch.cuda.synchronize()
+    r = ug.decode_results(res)
+    assert tuple(r[0]) == (0, w.size, x.size) and tuple(r[1])[:2] == (0, w.size)
+    assert tuple(r[2]) == (0, x.size, u.size) and int(lens[0]) == x.size
+    assert bytes(out8[: x.size].cpu().numpy()) == x.tobytes()
+    assert np.array_equal(out16[: u.size].cpu().numpy().view(np.uint16), w)

@@ -351,3 +351,48 @@ def test_capacity_contract():
     assert r == (HEADER_BITS, 6, need)
     r, _ = oracle.utf8_to_utf16le(bad, out_cap=need - 1)
     assert r == (OUTPUT_TOO_SMALL, need, 0)
+
+
+# ------------------------------------------------------------------ UTF-16BE
+def be_words(b: bytes) -> np.ndarray:
+    """The words of a big-endian UTF-16 byte string as they sit in (little-endian) memory."""
+    return np.frombuffer(b, dtype="<u2").copy()
+
+
+def test_utf16be_spec_example():
+    """utf16be file [0x00,0x41] -> words [0x0041]."""
+    u = be_words(bytes([0x00, 0x41]))
+    assert list(oracle.byteswap16(u)) == [0x0041]
+    r, out = oracle.utf16be_to_utf8(u)
+    assert tuple(r) == (OK, 1, 1) and out.tobytes() == b"A"
+    r, out = oracle.utf8_to_utf16be(b"A")
+    assert tuple(r) == (OK, 1, 1) and out.astype("<u2").tobytes() == bytes([0x00, 0x41])
+
+
+def test_fuzz_utf16be_vs_cpython():
+    """BE against CPython's own utf-16-be codec (independent of the oracle's byte swap):
+    decode of valid and invalid word strings, encode of valid text, lengths."""
+    rng = np.random.default_rng(0xBE16)
+    alphabet = np.array([0x0041, 0x007F, 0x0080, 0x07FF, 0x0800, 0xD7FF, 0xD800, 0xDBFF,
+                         0xDC00, 0xDFFF, 0xE000, 0xFFFF, 0x0100, 0x1234], dtype=np.uint16)
+    for _ in range(20000):
+        n = int(rng.integers(0, 24))
+        cu = alphabet[rng.integers(0, alphabet.size, n)] if rng.integers(0, 2) else \
+            rng.integers(0, 65536, n).astype(np.uint16)
+        raw = cu.astype(">u2").tobytes()          # big-endian bytes of the code units
+        u = be_words(raw)
+        try:
+            ref = raw.decode("utf-16-be").encode("utf-8")
+            e = -1
+        except UnicodeDecodeError as x:
+            e = x.start // 2
+            ref = raw[: 2 * e].decode("utf-16-be").encode("utf-8")
+        r, out = oracle.utf16be_to_utf8(u)
+        assert (r.error == OK) == (e < 0), cu
+        assert r.position == (n if e < 0 else e), cu
+        assert out.tobytes() == ref and r.written == len(ref), cu
+        assert oracle.utf16be_validate(u)[:2] == r[:2]
+        if e < 0:
+            assert oracle.utf8_length_from_utf16be(u) == len(ref)
+            r2, back = oracle.utf8_to_utf16be(ref)
+            assert r2.error == OK and back.astype("<u2").tobytes() == raw

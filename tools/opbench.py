@@ -33,6 +33,8 @@ else:
     r = ug.utf8_to_utf16le(t8, u16)
     assert r.error == 0 or os.environ.get("UG_LIB_OVERRIDE", "").find("_no") >= 0 or os.environ.get("UG_LIB_OVERRIDE", "").find("_both") >= 0 or os.environ.get("UG_LIB_OVERRIDE", "").find("nolb") >= 0 or os.environ.get("UG_LIB_OVERRIDE", "").find("bothp") >= 0 or os.environ.get("UG_LIB_OVERRIDE", "").find("both") >= 0 or os.environ.get("UG_LIB_OVERRIDE", "").find("slong") >= 0 or os.environ.get("UG_LIB_OVERRIDE", "").find("sshort") >= 0, r
 n8, n16 = t8.numel(), u16.numel()
+# big-endian copies of the same text for the UTF-16BE ops
+u16be = u16.view(torch.uint8).view(-1, 2).flip(1).contiguous().view(torch.int16).view(-1)
 o16 = torch.empty(n8, dtype=torch.int16, device=dev)
 o8 = torch.empty(3 * n16, dtype=torch.uint8, device=dev)
 ops = {
@@ -42,6 +44,9 @@ ops = {
     "utf16le_to_utf8": (lambda: ug.utf16le_to_utf8(u16, o8), 2 * n16, 2 * n16 + n8),
     "utf16_length_from_utf8": (lambda: ug.utf16_length_from_utf8(t8), n8, n8),
     "utf8_length_from_utf16le": (lambda: ug.utf8_length_from_utf16le(u16), 2 * n16, 2 * n16),
+    "utf8_to_utf16be": (lambda: ug.utf8_to_utf16be(t8, o16), n8, n8 + 2 * n16),
+    "utf16be_to_utf8": (lambda: ug.utf16be_to_utf8(u16be, o8), 2 * n16, 2 * n16 + n8),
+    "utf16be_validate": (lambda: ug.utf16be_validate(u16be), 2 * n16, 2 * n16),
 }
 only = os.environ.get("OPS")
 res = {"lib": os.path.basename(os.environ.get("UG_LIB_OVERRIDE", "libunigpu.so")), "cfg": cfg,
