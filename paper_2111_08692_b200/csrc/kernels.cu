@@ -726,9 +726,13 @@ __device__ __forceinline__ void finish_call(const TileArgs &a, bool xc, int tid,
 #define UG_VRING 4
 #endif
 constexpr int VRING = UG_VRING;
+#ifndef UG_VCPS
+#define UG_VCPS 3  // 38-40 registers: 3 CTAs/SM measured +3 % (UTF-8) / +6 % (UTF-16) over 2
+#endif
+constexpr int VCPS = UG_VCPS;  // validator CTAs per SM (register budget)
 
 template <class Pol>
-__global__ void __launch_bounds__(NT, CTAS_PER_SM) k_validate(const TileArgs a) {
+__global__ void __launch_bounds__(NT, VCPS) k_validate(const TileArgs a) {
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t mb_full[VRING], mb_empty[VRING];
   __shared__ int s_last;
