@@ -976,11 +976,13 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
     }
   } else {
     // ------------------------------------------------------------ data warps
-    uint32_t ex[DEFER], cn[DEFER];  // this thread's offset / count of the tiles awaiting emit
+    // this thread's offset << 8 | count of the tiles awaiting emit, newest first (a shift
+    // register: constant indices keep it in registers; offset < 2^15, count <= 32)
+    uint32_t hist[DEFER];
 #pragma unroll
-    for (int q = 0; q < DEFER; q++) ex[q] = cn[q] = 0u;
+    for (int q = 0; q < DEFER; q++) hist[q] = 0u;
     int i = 0;
-    auto emit = [&](int j) {  // decode + store tile j (all data threads)
+    auto emit = [&](int j, uint32_t v) {  // decode + store tile j (all data threads)
       const int js = j % RING;
 #ifdef UG_TRACE
       unsigned long long w0 = gtime();
@@ -994,14 +996,7 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
 #endif
       if (tid == 0) bulk_wait_read_all();  // the previous bulk store has read the stage
       named_sync<BAR_DATA, NT>();
-      uint32_t e0 = 0u, c0 = 0u;
-#pragma unroll
-      for (int q = 0; q < DEFER; q++)
-        if (q == j % DEFER) {
-          e0 = ex[q];
-          c0 = cn[q];
-        }
-      emit_tile<Pol>(a, ring + js * INBUF, s_t[js], s_pre[js], s_cnt[js], e0, c0,
+      emit_tile<Pol>(a, ring + js * INBUF, s_t[js], s_pre[js], s_cnt[js], v >> 8, v & 0xFFu,
                      stage, tid, lane);
     };
     while (true) {
@@ -1065,16 +1060,14 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
 #ifdef UG_TRACE
       if (tid == 0 && i < TR_IT && blockIdx.x < 1024) g_trace[blockIdx.x][i][10] = gtime();  // AGG
 #endif
-      if (i >= DEFER) emit(i - DEFER);  // a7, a8
+      const uint32_t oldest = hist[DEFER - 1];  // tile i - DEFER
+#pragma unroll
+      for (int q = DEFER - 1; q > 0; q--) hist[q] = hist[q - 1];
+      hist[0] = (excl << 8) | cnt;
+      if (i >= DEFER) emit(i - DEFER, oldest);  // a7, a8
 #ifdef UG_TRACE
       if (tid == 0 && i < TR_IT && blockIdx.x < 1024) g_trace[blockIdx.x][i][11] = gtime();  // end
 #endif
-#pragma unroll
-      for (int q = 0; q < DEFER; q++)  // tile i - DEFER's entry is free now
-        if (q == i % DEFER) {
-          ex[q] = excl;
-          cn[q] = cnt;
-        }
       i++;
     }
     // every look-back agent must see a past-the-end ticket to stop: the one owning tile i has;
@@ -1086,8 +1079,10 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
         mbar_arrive(&mb_tick[(i + k) % RING]);
       }
     }
-    // drain: tiles i - DEFER .. i - 1
-    for (int j = (i >= DEFER ? i - DEFER : 0); j < i; j++) emit(j);
+    // drain: tiles i - DEFER .. i - 1 (hist[DEFER - 1] is the oldest)
+#pragma unroll
+    for (int q = DEFER - 1; q >= 0; q--)
+      if (i - 1 - q >= 0) emit(i - 1 - q, hist[q]);
     if (tid == 0) bulk_wait_all();  // all output written before the CTA retires
   }
   __syncthreads();
@@ -1356,19 +1351,16 @@ __global__ void __launch_bounds__(T16_THREADS, CTAS_PER_SM) k_transcode16(const 
     }
   } else {
     // ------------------------------------------------------------ data warps
-    // this thread's in-warp offset << 8 | count for the D16 + 1 tiles between count and emit
-    uint32_t oc[D16 + 1];
+    // this thread's in-warp offset << 8 | count of the tiles awaiting emit, newest first (a
+    // shift register: constant indices keep it in registers)
+    uint32_t hist[D16];
 #pragma unroll
-    for (int j = 0; j <= D16; j++) oc[j] = 0u;
-    auto emit = [&](int j) {
+    for (int j = 0; j < D16; j++) hist[j] = 0u;
+    auto emit = [&](int j, uint32_t v) {
       const int js = j % RING16;
       mbar_wait(&mb_pre[js], (j / RING16) & 1);
       if (tid == 0) bulk_wait_read_all();  // the previous bulk store has read the stage
       named_sync<BAR_DATA, NT>();
-      uint32_t v = 0;
-#pragma unroll
-      for (int q = 0; q <= D16; q++)
-        if (q == j % (D16 + 1)) v = oc[q];
       emit_tile16<BE>(a, ring + js * INBUF, s_t[js], s_pre[js], s_cnt[js],
                   s_wsum[js][warp] + (v >> 8), v & 0xFFu, stage, tid, lane);
     };
@@ -1422,15 +1414,19 @@ __global__ void __launch_bounds__(T16_THREADS, CTAS_PER_SM) k_transcode16(const 
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&mb_agg[sl]);
+      const uint32_t oldest = hist[D16 - 1];  // tile i - D16
 #pragma unroll
-      for (int q = 0; q <= D16; q++)
-        if (q == i % (D16 + 1)) oc[q] = ((sc - cnt) << 8) | cnt;  // count <= 48, offset < 2^11
+      for (int q = D16 - 1; q > 0; q--) hist[q] = hist[q - 1];
+      hist[0] = ((sc - cnt) << 8) | cnt;  // count <= 48, offset < 2^11
       // slot of tile i + PF16 held tile i + PF16 - RING16 = i - D - 1, emitted last iteration
       if (tid == 0) start_tile((i + PF16) % RING16, tn);
-      if (i >= D16) emit(i - D16);  // a7-a9, a8
+      if (i >= D16) emit(i - D16, oldest);  // a7-a9, a8
       i++;
     }
-    for (int j = (i >= D16 ? i - D16 : 0); j < i; j++) emit(j);
+    // drain: tiles i - D16 .. i - 1 (hist[D16 - 1] is the oldest)
+#pragma unroll
+    for (int q = D16 - 1; q >= 0; q--)
+      if (i - 1 - q >= 0) emit(i - 1 - q, hist[q]);
     if (tid == 0) bulk_wait_all();
   }
   __syncthreads();
