@@ -1230,6 +1230,7 @@ constexpr int RING16 = UG_RING16;
 #endif
 constexpr int PF16 = UG_PF16;  // tiles loading ahead of the one being counted
 constexpr int D16 = RING16 - PF16 - 1;  // tiles awaiting their prefix (emit deferral)
+static_assert(3 * (TILE / 2) < (1 << 24) && NT / 32 < 256, "s_acc packing");
 static_assert(PF16 >= 1 && D16 >= 1, "ring: loads in flight + the tile counted + deferral");
 constexpr int T16_THREADS = NT + 32;
 
@@ -1285,7 +1286,9 @@ __global__ void __launch_bounds__(T16_THREADS, CTAS_PER_SM) k_transcode16(const 
   __shared__ uint64_t mb_pre[RING16];   // look-back warp -> data warps: prefix known
   __shared__ long long s_t[RING16];
   __shared__ uint32_t s_wsum[RING16][NT / 32];  // warp totals, then exclusive warp offsets
-  __shared__ unsigned long long s_acc[RING16];   // arrivals << 32 | running sum of warp totals
+  // arrivals << 24 | running sum of warp totals (a tile emits <= 3 * TILE / 2 < 2^24 bytes):
+  // one native 32-bit shared atomic (a 64-bit one is a CAS loop, ATOMS.CAST.SPIN.64)
+  __shared__ uint32_t s_acc[RING16];
   __shared__ uint32_t s_cnt[RING16];
   __shared__ unsigned long long s_pre[RING16];
   __shared__ int s_last;
@@ -1310,7 +1313,7 @@ __global__ void __launch_bounds__(T16_THREADS, CTAS_PER_SM) k_transcode16(const 
       mbar_init(&mb_tick[j], 1);
       mbar_init(&mb_agg[j], NT / 32);
       mbar_init(&mb_pre[j], 1);
-      s_acc[j] = 0ull;
+      s_acc[j] = 0u;
     }
     fence_mbar_init();
 #pragma unroll 1
@@ -1405,11 +1408,11 @@ __global__ void __launch_bounds__(T16_THREADS, CTAS_PER_SM) k_transcode16(const 
         // the last warp to add its total publishes the tile aggregate at once (a6): the
         // look-back warp may still be busy with the previous tile, and every successor's
         // look-back waits for this word
-        const unsigned long long old = atomicAdd(&s_acc[sl], (1ull << 32) | sc);
-        if ((old >> 32) == NT / 32 - 1) {
-          st_relaxed(a.status + t,
-                     pack_status(a.epoch, t == 0 ? FLAG_PREFIX : FLAG_AGG, (uint32_t)old + sc));
-          s_acc[sl] = 0ull;  // next use of the slot is RING16 tiles later
+        const uint32_t old = atomicAdd(&s_acc[sl], (1u << 24) | sc);
+        if ((old >> 24) == NT / 32 - 1) {
+          st_relaxed(a.status + t, pack_status(a.epoch, t == 0 ? FLAG_PREFIX : FLAG_AGG,
+                                               (old & 0xFFFFFFu) + sc));
+          s_acc[sl] = 0u;  // next use of the slot is RING16 tiles later
         }
       }
       __syncwarp();
