@@ -726,6 +726,11 @@ __device__ __forceinline__ void finish_call(const TileArgs &a, bool xc, int tid,
 #define UG_VRING 4
 #endif
 constexpr int VRING = UG_VRING;
+#ifndef UG_VAHEAD
+#define UG_VAHEAD (UG_VRING - 2)
+#endif
+constexpr int VAHEAD = UG_VAHEAD;  // tiles loading ahead of the one being validated
+static_assert(VAHEAD >= 1 && VAHEAD <= VRING - 1, "validator ring");
 #ifndef UG_VCPS
 #define UG_VCPS 3  // 38-40 registers: 3 CTAs/SM measured +3 % (UTF-8) / +6 % (UTF-16) over 2
 #endif
@@ -750,7 +755,7 @@ __global__ void __launch_bounds__(NT, VCPS) k_validate(const TileArgs a) {
     }
     fence_mbar_init();
 #pragma unroll
-    for (int j = 0; j < VRING - 1; j++) {
+    for (int j = 0; j < VAHEAD; j++) {
       const long long t = blockIdx.x + j * G;
       if (t < ntiles) issue_tile_load(win, t, smem + j * INBUF, &mb_full[j]);
     }
@@ -759,11 +764,14 @@ __global__ void __launch_bounds__(NT, VCPS) k_validate(const TileArgs a) {
   int k = 0;
   for (long long t = blockIdx.x; t < ntiles; t += G, k++) {
     const int sl = k % VRING;
-    if (tid == 0) {  // refill the slot freed by tile k - 1 with tile k + VRING - 1
-      const long long tn = t + (VRING - 1) * G;
-      const int sn = (k + VRING - 1) % VRING;
+    if (tid == 0) {
+      // refill the slot of tile k + VAHEAD - VRING (two tiles back: every warp has long left
+      // it, so thread 0 does not wait for the slowest warp of the previous tile)
+      const long long tn = t + VAHEAD * G;
+      const int sn = (k + VAHEAD) % VRING;
+      const int kf = k + VAHEAD - VRING;
       if (tn < ntiles) {
-        if (k >= 1) mbar_wait(&mb_empty[sn], ((k - 1) / VRING) & 1);
+        if (kf >= 0) mbar_wait(&mb_empty[sn], (kf / VRING) & 1);
         fence_proxy_async_smem();
         issue_tile_load(win, tn, smem + sn * INBUF, &mb_full[sn]);
       }
