@@ -21,6 +21,8 @@
  *    first use and reused; calls on different streams never share a workspace.
  *  - Lengths are in CODE UNITS: bytes for UTF-8, 16-bit words for UTF-16LE.  UTF-16LE is
  *    little-endian, the GPU's native order; a BOM is ordinary data (R7, R9).
+ *    n <= 2^38 - 1 units per call (tile status words carry 38-bit counts); a larger n is API
+ *    misuse (UG_ERR_ARG) - split the input with the sharded entry points instead.
  *  - `stream` is a cudaStream_t passed as void* (NULL = the legacy default stream).
  *  - Validity failures are DATA, returned in ug_result, not API failures.
  *  - API misuse (NULL pointer with n > 0, odd address for a UTF-16 pointer, output capacity

@@ -149,6 +149,17 @@ Window make_window(const void *base, unsigned long long nbytes, unsigned long lo
   return w;
 }
 
+// API-misuse checks of a tile op (include/unigpu.h conventions), before any CUDA call.
+int check_tile_args(Op op, const void *in, unsigned long long n, const void *out,
+                    unsigned long long out_cap) {
+  if (n > MAX_N) return UG_ERR_ARG;
+  if (n > 0 && in == nullptr) return UG_ERR_ARG;
+  if (op_u16_input(op) && ((uintptr_t)in & 1u)) return UG_ERR_ARG;
+  if ((op == Op::U8_TO_U16 || op == Op::U8_TO_U16BE) && ((uintptr_t)out & 1u)) return UG_ERR_ARG;
+  if (op_transcodes(op) && out == nullptr && out_cap > 0) return UG_ERR_ARG;
+  return UG_OK;
+}
+
 // Enqueue one tile kernel.  Units: n / halos in code units of the input encoding.
 int enqueue_tile(Op op, const void *in, unsigned long long n, unsigned long long hb,
                  unsigned long long ha, unsigned long long global_off, void *out,
@@ -156,11 +167,8 @@ int enqueue_tile(Op op, const void *in, unsigned long long n, unsigned long long
                  cudaStream_t s) {
   const bool u16in = op_u16_input(op);
   const unsigned long long us = u16in ? 2 : 1;
-  if (n > MAX_N) return UG_ERR_ARG;
-  if (n > 0 && in == nullptr) return UG_ERR_ARG;
-  if (u16in && ((uintptr_t)in & 1u)) return UG_ERR_ARG;
-  if ((op == Op::U8_TO_U16 || op == Op::U8_TO_U16BE) && ((uintptr_t)out & 1u)) return UG_ERR_ARG;
-  if (op_transcodes(op) && out == nullptr && out_cap > 0) return UG_ERR_ARG;
+  const int rc = check_tile_args(op, in, n, out, out_cap);
+  if (rc != UG_OK) return rc;
   if (n == 0) {
     if (d_result && cudaMemsetAsync(d_result, 0, sizeof(ResultDev), s) != cudaSuccess)
       return UG_ERR_CUDA;
@@ -210,10 +218,9 @@ ug_result make_result(int err, uint64_t pos, uint64_t wr) {
 // Run an async tile op into the workspace's result slot and wait for it.
 ug_result run_sync(Op op, const void *in, unsigned long long n, void *out,
                    unsigned long long out_cap, cudaStream_t s) {
-  if (n == 0) {
-    if (in == nullptr && n > 0) return make_result(UG_ERR_ARG, 0, 0);
-    return make_result(UG_OK, 0, 0);
-  }
+  const int arc = check_tile_args(op, in, n, out, out_cap);
+  if (arc != UG_OK) return make_result(arc, 0, 0);
+  if (n == 0) return make_result(UG_OK, 0, 0);
   Workspace *w;
   if (get_ws(s, &w) != cudaSuccess) return make_result(UG_ERR_CUDA, 0, 0);
   int rc = enqueue_tile(op, in, n, 0, 0, 0, out, out_cap, w->d_res, nullptr, s);
@@ -233,6 +240,7 @@ int enqueue_len(bool u16in, const void *in, unsigned long long n, unsigned long 
   if (d_len == nullptr) return UG_ERR_ARG;
   if (n > 0 && in == nullptr) return UG_ERR_ARG;
   if (u16in && ((uintptr_t)in & 1u)) return UG_ERR_ARG;
+  if (n > (1ull << 62)) return UG_ERR_ARG;  // byte counts must not overflow
   if (n == 0) return cudaMemsetAsync(d_len, 0, sizeof(*d_len), s) == cudaSuccess ? UG_OK
                                                                                  : UG_ERR_CUDA;
   Workspace *w;
@@ -340,7 +348,8 @@ ug_result run_host(Op op, const void *in_host, unsigned long long n, void *out_h
   if (n == 0) return make_result(UG_OK, 0, 0);
   if (in_host == nullptr || (out_host == nullptr && out_cap > 0))
     return make_result(UG_ERR_ARG, 0, 0);
-  if (n > MAX_N) return make_result(UG_ERR_ARG, 0, 0);
+  if (n > MAX_N || (u16in && ((uintptr_t)in_host & 1u)) || (!u16in && ((uintptr_t)out_host & 1u)))
+    return make_result(UG_ERR_ARG, 0, 0);
   Workspace *w;
   if (get_ws(s, &w) != cudaSuccess) return make_result(UG_ERR_CUDA, 0, 0);
   // chunk cuts at character starts (the kernel is exact at any cut; this keeps chunks whole)

@@ -125,3 +125,41 @@ def test_product_does_not_import_oracle():
             txt = open(os.path.join(ROOT, "oracle", f)).read()
             assert not re.search(r"^\s*(import|from)\s+paper_2111_08692_b200", txt, re.M), f
             assert not re.search(r'#include\s+".*(unigpu|csrc)', txt), f
+
+
+def test_argument_errors_exhaustive_need_no_gpu(ug):
+    """Every documented API-misuse case of include/unigpu.h returns UG_ERR_ARG from the host
+    checks, before any CUDA call (so also on a machine without a GPU)."""
+    V, L = ctypes.c_void_p, ug.lib
+    big = (1 << 38)  # one past the largest n
+    odd = V(0x1001)
+    for fn in (L.utf16le_validate, L.utf16be_validate):
+        assert fn(odd, 4, V(0)).error == ug.ERR_ARG            # odd UTF-16 pointer
+        assert fn(V(0), 4, V(0)).error == ug.ERR_ARG           # NULL with n > 0
+        assert fn(V(0x1000), big, V(0)).error == ug.ERR_ARG    # n too large
+    assert L.utf8_validate(V(0x1000), big, V(0)).error == ug.ERR_ARG
+    for fn in (L.utf8_to_utf16le, L.utf8_to_utf16be):
+        assert fn(V(0x1000), 4, odd, 4, V(0)).error == ug.ERR_ARG   # odd UTF-16 output
+        assert fn(V(0x1000), 4, V(0), 4, V(0)).error == ug.ERR_ARG  # NULL output, cap > 0
+        assert fn(V(0x1000), big, V(0x2000), 4, V(0)).error == ug.ERR_ARG
+    for fn in (L.utf16le_to_utf8, L.utf16be_to_utf8):
+        assert fn(odd, 4, V(0x2000), 12, V(0)).error == ug.ERR_ARG
+        assert fn(V(0x1000), 4, V(0), 12, V(0)).error == ug.ERR_ARG
+    for fn in (L.ug_utf8_to_utf16le_async, L.ug_utf8_to_utf16be_async):
+        assert fn(V(0x1000), 4, odd, 4, V(0x3000), V(0)) == ug.ERR_ARG
+        assert fn(V(0x1000), 4, V(0x2000), 4, V(0), V(0)) == ug.ERR_ARG   # no result slot
+    for fn in (L.ug_utf16le_validate_async, L.ug_utf16be_validate_async):
+        assert fn(odd, 4, V(0x3000), V(0)) == ug.ERR_ARG
+    assert L.ug_utf16_length_from_utf8_async(V(0x1000), 4, V(0), V(0)) == ug.ERR_ARG
+    assert L.ug_utf8_length_from_utf16be_async(odd, 4, V(0x3000), V(0)) == ug.ERR_ARG
+    assert L.ug_utf8_to_utf16le_shard_async(V(0x1000), 4, 0, 0, 0, V(0x2000), 4, V(0),
+                                            V(0)) == ug.ERR_ARG  # no record slot
+    # host-buffer variants
+    assert L.utf8_to_utf16le_host(V(0), 4, V(0x2000), 4, V(0)).error == ug.ERR_ARG
+    assert L.utf8_to_utf16le_host(V(0x1000), 4, odd, 4, V(0)).error == ug.ERR_ARG
+    assert L.utf16le_to_utf8_host(odd, 4, V(0x2000), 12, V(0)).error == ug.ERR_ARG
+    assert L.utf16le_to_utf8_host(V(0x1000), big, V(0x2000), 12, V(0)).error == ug.ERR_ARG
+    # n = 0 succeeds without touching memory or the GPU, whatever the pointers
+    for fn in (L.utf8_to_utf16be, L.utf16be_to_utf8):
+        r = fn(V(0), 0, V(0), 0, V(0))
+        assert (r.error, r.position, r.written) == (0, 0, 0)
