@@ -61,7 +61,9 @@ typedef enum {
   UG_SURROGATE = 6,   /* rule 6 (D800..DFFF in UTF-8) and unpaired UTF-16 surrogates   */
   UG_ERR_ARG = -1,
   UG_ERR_CUDA = -2,
-  UG_ERR_OUTPUT_TOO_SMALL = -3
+  UG_ERR_OUTPUT_TOO_SMALL = -3,
+  UG_ERR_NCCL = -4 /* reserved for the collective layer; this library makes no
+                      NCCL calls - the record all-gather runs in the caller's torch.distributed */
 } ug_error;
 
 /* 24-byte result, SPEC.md S:39-44 / BASELINE north_star ("output length or a validity

@@ -21,7 +21,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("UG_LIB_OVERRIDE") or os.path.join(_HERE, "libunigpu.so")
 
 OK, HEADER_BITS, TOO_SHORT, TOO_LONG, OVERLONG, TOO_LARGE, SURROGATE = range(7)
-ERR_ARG, ERR_CUDA, ERR_OUTPUT_TOO_SMALL = -1, -2, -3
+ERR_ARG, ERR_CUDA, ERR_OUTPUT_TOO_SMALL, ERR_NCCL = -1, -2, -3, -4
 NONE = (1 << 64) - 1
 
 

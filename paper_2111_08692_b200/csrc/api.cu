@@ -627,6 +627,7 @@ const char *ug_error_name(int err) {
     case UG_ERR_ARG: return "ErrArg";
     case UG_ERR_CUDA: return "ErrCuda";
     case UG_ERR_OUTPUT_TOO_SMALL: return "OutputTooSmall";
+    case UG_ERR_NCCL: return "ErrNccl";
   }
   return "Unknown";
 }
