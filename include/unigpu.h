@@ -205,6 +205,19 @@ ug_result ug_combine_records_host(const ug_shard_record *recs, int nranks, int r
  * surrogate. */
 size_t ug_utf8_cut_backoff(const uint8_t *at, size_t avail_before);
 size_t ug_utf16_cut_backoff(const uint16_t *at, size_t avail_before);
+/* The same rule on big-endian UTF-16 words (f3). */
+size_t ug_utf16be_cut_backoff(const uint16_t *at, size_t avail_before);
+
+/* Sharded UTF-16BE variants (f3): the shard contract above, on big-endian words. */
+int ug_utf8_to_utf16be_shard_async(const uint8_t *in, size_t n, size_t halo_before,
+                                   size_t halo_after, uint64_t in_global_offset, uint16_t *out,
+                                   size_t out_cap, ug_shard_record *d_rec, void *stream);
+int ug_utf16be_to_utf8_shard_async(const uint16_t *in, size_t n, size_t halo_before,
+                                   size_t halo_after, uint64_t in_global_offset, uint8_t *out,
+                                   size_t out_cap, ug_shard_record *d_rec, void *stream);
+int ug_utf16be_validate_shard_async(const uint16_t *in, size_t n, size_t halo_before,
+                                    size_t halo_after, uint64_t in_global_offset,
+                                    ug_shard_record *d_rec, void *stream);
 
 /* ------------------------------------------------------------------ host buffers
  * End-to-end variants on HOST memory (pinned memory gives DMA-speed copies in both
@@ -220,6 +233,11 @@ size_t ug_utf16_cut_backoff(const uint16_t *at, size_t avail_before);
 ug_result utf8_to_utf16le_host(const uint8_t *in_host, size_t n, uint16_t *out_host,
                                size_t out_cap, void *stream);
 ug_result utf16le_to_utf8_host(const uint16_t *in_host, size_t n, uint8_t *out_host,
+                               size_t out_cap, void *stream);
+/* UTF-16BE host-buffer variants (f3). */
+ug_result utf8_to_utf16be_host(const uint8_t *in_host, size_t n, uint16_t *out_host,
+                               size_t out_cap, void *stream);
+ug_result utf16be_to_utf8_host(const uint16_t *in_host, size_t n, uint8_t *out_host,
                                size_t out_cap, void *stream);
 
 /* Chunk size of the host-buffer pipeline, in input code units (default 32 Mi units); returns

@@ -85,6 +85,12 @@ def _load():
         "utf8_to_utf16le_host": ([P, S, P, S, P], _CResult),
         "utf16le_to_utf8_host": ([P, S, P, S, P], _CResult),
         "ug_set_host_chunk": ([S], S),
+        "ug_utf8_to_utf16be_shard_async": ([P, S, S, S, U64, P, S, P, P], I),
+        "ug_utf16be_to_utf8_shard_async": ([P, S, S, S, U64, P, S, P, P], I),
+        "ug_utf16be_validate_shard_async": ([P, S, S, S, U64, P, P], I),
+        "ug_utf16be_cut_backoff": ([P, S], S),
+        "utf8_to_utf16be_host": ([P, S, P, S, P], _CResult),
+        "utf16be_to_utf8_host": ([P, S, P, S, P], _CResult),
         "utf16be_validate": ([P, S, P], _CResult),
         "utf8_to_utf16be": ([P, S, P, S, P], _CResult),
         "utf16be_to_utf8": ([P, S, P, S, P], _CResult),
@@ -351,6 +357,30 @@ def utf16le_validate_shard_async(t_in, offset, n, halo_before, halo_after, globa
            "utf16le_validate_shard_async")
 
 
+def utf8_to_utf16be_shard_async(t_in, offset, n, halo_before, halo_after, global_off, t_out,
+                                d_rec, out_cap=None, stream=None, rec_off=0):
+    _check(lib.ug_utf8_to_utf16be_shard_async(
+        _at(t_in, offset), n, halo_before, halo_after, global_off, _ptr(t_out),
+        _units(t_out) if out_cap is None else out_cap, _at(d_rec, rec_off), _stream(stream)),
+        "utf8_to_utf16be_shard_async")
+
+
+def utf16be_to_utf8_shard_async(t_in, offset, n, halo_before, halo_after, global_off, t_out,
+                                d_rec, out_cap=None, stream=None, rec_off=0):
+    _check(lib.ug_utf16be_to_utf8_shard_async(
+        _at(t_in, 2 * offset), n, halo_before, halo_after, global_off, _ptr(t_out),
+        _units(t_out) if out_cap is None else out_cap, _at(d_rec, rec_off), _stream(stream)),
+        "utf16be_to_utf8_shard_async")
+
+
+def utf16be_validate_shard_async(t_in, offset, n, halo_before, halo_after, global_off, d_rec,
+                                 stream=None, rec_off=0):
+    _check(lib.ug_utf16be_validate_shard_async(_at(t_in, 2 * offset), n, halo_before,
+                                               halo_after, global_off, _at(d_rec, rec_off),
+                                               _stream(stream)),
+           "utf16be_validate_shard_async")
+
+
 def combine_records_async(d_recs, nranks, rank, total_in, d_result, d_out_offset=None,
                           stream=None):
     _check(lib.ug_combine_records_async(_ptr(d_recs), nranks, rank, total_in, _ptr(d_result),
@@ -397,3 +427,19 @@ def utf8_to_utf16le_host(t_in_host, t_out_host, stream=None) -> Result:
 def utf16le_to_utf8_host(t_in_host, t_out_host, stream=None) -> Result:
     return _res(lib.utf16le_to_utf8_host(_ptr(t_in_host), _units(t_in_host), _ptr(t_out_host),
                                          _units(t_out_host), _stream(stream)))
+
+
+def utf8_to_utf16be_host(t_in_host, t_out_host, stream=None) -> Result:
+    return _res(lib.utf8_to_utf16be_host(_ptr(t_in_host), _units(t_in_host), _ptr(t_out_host),
+                                         _units(t_out_host), _stream(stream)))
+
+
+def utf16be_to_utf8_host(t_in_host, t_out_host, stream=None) -> Result:
+    return _res(lib.utf16be_to_utf8_host(_ptr(t_in_host), _units(t_in_host), _ptr(t_out_host),
+                                         _units(t_out_host), _stream(stream)))
+
+
+def utf16be_cut_backoff(words, at: int) -> int:
+    import numpy as np
+    a = np.ascontiguousarray(words, dtype=np.uint16)
+    return int(lib.ug_utf16be_cut_backoff(ctypes.c_void_p(a.ctypes.data + 2 * at), at))

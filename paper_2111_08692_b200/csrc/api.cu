@@ -341,7 +341,7 @@ cudaError_t ensure_pipeline(Workspace *w, size_t nchunks) {
 // exactly as the unsharded kernel states it (first error, written, output too small).
 ug_result run_host(Op op, const void *in_host, unsigned long long n, void *out_host,
                    unsigned long long out_cap, cudaStream_t s) {
-  const bool u16in = op == Op::U16_TO_U8;
+  const bool u16in = op_u16_input(op);
   const size_t ius = u16in ? 2 : 1, ous = u16in ? 1 : 2;
   const unsigned long long ub = u16in ? 3 : 1;  // output units per input unit, at most
   const unsigned long long halo = u16in ? 1 : 3;
@@ -357,8 +357,10 @@ ug_result run_host(Op op, const void *in_host, unsigned long long n, void *out_h
   std::vector<unsigned long long> cut;
   cut.push_back(0);
   for (unsigned long long c = C; c < n; c += C) {
-    unsigned long long k = u16in ? ug_utf16_cut_backoff((const uint16_t *)in_host + c, c)
-                                 : ug_utf8_cut_backoff((const uint8_t *)in_host + c, c);
+    unsigned long long k =
+        op == Op::U16BE_TO_U8 ? ug_utf16be_cut_backoff((const uint16_t *)in_host + c, c)
+        : u16in               ? ug_utf16_cut_backoff((const uint16_t *)in_host + c, c)
+                              : ug_utf8_cut_backoff((const uint8_t *)in_host + c, c);
     if (c - k > cut.back()) cut.push_back(c - k);
   }
   cut.push_back(n);
@@ -591,6 +593,31 @@ ug_result ug_combine_records_host(const ug_shard_record *recs, int nranks, int r
   return o;
 }
 
+int ug_utf8_to_utf16be_shard_async(const uint8_t *in, size_t n, size_t halo_before,
+                                   size_t halo_after, uint64_t in_global_offset, uint16_t *out,
+                                   size_t out_cap, ug_shard_record *d_rec, void *stream) {
+  if (!d_rec) return UG_ERR_ARG;
+  return enqueue_tile(Op::U8_TO_U16BE, in, n, clamp_halo(halo_before, 3),
+                      clamp_halo(halo_after, 3), in_global_offset, out, out_cap, nullptr,
+                      (RecordDev *)d_rec, (cudaStream_t)stream);
+}
+int ug_utf16be_to_utf8_shard_async(const uint16_t *in, size_t n, size_t halo_before,
+                                   size_t halo_after, uint64_t in_global_offset, uint8_t *out,
+                                   size_t out_cap, ug_shard_record *d_rec, void *stream) {
+  if (!d_rec) return UG_ERR_ARG;
+  return enqueue_tile(Op::U16BE_TO_U8, in, n, clamp_halo(halo_before, 1),
+                      clamp_halo(halo_after, 1), in_global_offset, out, out_cap, nullptr,
+                      (RecordDev *)d_rec, (cudaStream_t)stream);
+}
+int ug_utf16be_validate_shard_async(const uint16_t *in, size_t n, size_t halo_before,
+                                    size_t halo_after, uint64_t in_global_offset,
+                                    ug_shard_record *d_rec, void *stream) {
+  if (!d_rec) return UG_ERR_ARG;
+  return enqueue_tile(Op::U16BE_VALIDATE, in, n, clamp_halo(halo_before, 1),
+                      clamp_halo(halo_after, 1), in_global_offset, nullptr, 0, nullptr,
+                      (RecordDev *)d_rec, (cudaStream_t)stream);
+}
+
 size_t ug_utf8_cut_backoff(const uint8_t *at, size_t avail_before) {
   // at[-k] is the candidate cut byte; step back while it is a continuation byte (<= 3 steps)
   size_t k = 0;
@@ -600,6 +627,10 @@ size_t ug_utf8_cut_backoff(const uint8_t *at, size_t avail_before) {
 size_t ug_utf16_cut_backoff(const uint16_t *at, size_t avail_before) {
   return ((at[0] & 0xFC00u) == 0xDC00u && avail_before >= 1) ? 1 : 0;
 }
+size_t ug_utf16be_cut_backoff(const uint16_t *at, size_t avail_before) {
+  const uint32_t w = ((at[0] >> 8) | (at[0] << 8)) & 0xFFFFu;  // the big-endian unit
+  return ((w & 0xFC00u) == 0xDC00u && avail_before >= 1) ? 1 : 0;
+}
 
 ug_result utf8_to_utf16le_host(const uint8_t *in_host, size_t n, uint16_t *out_host,
                                size_t out_cap, void *stream) {
@@ -608,6 +639,14 @@ ug_result utf8_to_utf16le_host(const uint8_t *in_host, size_t n, uint16_t *out_h
 ug_result utf16le_to_utf8_host(const uint16_t *in_host, size_t n, uint8_t *out_host,
                                size_t out_cap, void *stream) {
   return run_host(Op::U16_TO_U8, in_host, n, out_host, out_cap, (cudaStream_t)stream);
+}
+ug_result utf8_to_utf16be_host(const uint8_t *in_host, size_t n, uint16_t *out_host,
+                               size_t out_cap, void *stream) {
+  return run_host(Op::U8_TO_U16BE, in_host, n, out_host, out_cap, (cudaStream_t)stream);
+}
+ug_result utf16be_to_utf8_host(const uint16_t *in_host, size_t n, uint8_t *out_host,
+                               size_t out_cap, void *stream) {
+  return run_host(Op::U16BE_TO_U8, in_host, n, out_host, out_cap, (cudaStream_t)stream);
 }
 
 size_t ug_set_host_chunk(size_t units) {

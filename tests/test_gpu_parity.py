@@ -549,3 +549,67 @@ def test_utf16be_async():
     assert tuple(r[2]) == (0, x.size, u.size) and int(lens[0]) == x.size
     assert bytes(out8[: x.size].cpu().numpy()) == x.tobytes()
     assert np.array_equal(out16[: u.size].cpu().numpy().view(np.uint16), w)
+
+
+def test_utf16be_host_pipeline(c0):
+    """UTF-16BE through the chunked host pipeline, both directions, small chunks (cuts inside
+    surrogate pairs are backed off with the BE rule)."""
+    u = oracle.utf8_to_utf16le(c0)[1]
+    w = be_raw(u)
+    prev = ug.set_host_chunk(4097)
+    try:
+        hin = torch.from_numpy(c0.copy()).pin_memory()
+        h16 = torch.zeros(c0.size, dtype=torch.int16).pin_memory()
+        r = ug.utf8_to_utf16be_host(hin, h16)
+        assert tuple(r) == (0, c0.size, u.size)
+        assert np.array_equal(h16[: u.size].numpy().view(np.uint16), w)
+        hw = torch.from_numpy(w.view(np.int16).copy()).pin_memory()
+        h8 = torch.zeros(3 * w.size, dtype=torch.uint8).pin_memory()
+        r = ug.utf16be_to_utf8_host(hw, h8)
+        assert tuple(r) == (0, w.size, c0.size) and bytes(h8[: c0.size].numpy()) == c0.tobytes()
+        v = u.copy()
+        p, _ = synth.inject_utf16_error(v, 4097 * 7 - 2, 4097 * 7 + 2, np.random.default_rng(3))
+        hv = torch.from_numpy(be_raw(v).view(np.int16).copy()).pin_memory()
+        r = ug.utf16be_to_utf8_host(hv, h8)
+        assert tuple(r) == tuple(oracle.utf16be_to_utf8(be_raw(v))[0]) and r.position == p
+    finally:
+        ug.set_host_chunk(prev)
+
+
+@pytest.mark.parametrize("G", [2, 5])
+def test_utf16be_virtual_shards(c0, G):
+    """BE reverse and BE validation as G shards of one buffer (cuts by the BE rule), records
+    combined on the device: equal to the unsharded oracle, including an error near a cut."""
+    u = oracle.utf8_to_utf16le(c0)[1]
+    for inject in (False, True):
+        v = u.copy()
+        n = v.size
+        if inject:
+            c = (n // G) & ~15
+            synth.inject_utf16_error(v, c - 2, c + 2, np.random.default_rng(G))
+        w = be_raw(v)
+        _, t = to_dev(w)
+        cuts = [0] + [((k * (n // G)) & ~15) - ug.utf16be_cut_backoff(w, (k * (n // G)) & ~15)
+                      for k in range(1, G)] + [n]
+        recs = ug.record_buffer(DEV, 2 * G)
+        outs = []
+        for k in range(G):
+            lo, hi = cuts[k], cuts[k + 1]
+            out = torch.zeros(3 * max(hi - lo, 1), dtype=torch.uint8, device=DEV)
+            ug.utf16be_to_utf8_shard_async(t, lo, hi - lo, min(lo, 1), min(n - hi, 1), lo, out,
+                                           recs, rec_off=k * ug.RECORD_BYTES)
+            ug.utf16be_validate_shard_async(t, lo, hi - lo, min(lo, 1), min(n - hi, 1), lo, recs,
+                                            rec_off=(G + k) * ug.RECORD_BYTES)
+            outs.append(out)
+        res = ug.result_buffer(DEV, 2)
+        ug.combine_records_async(recs, G, 0, n, res)
+        ug.combine_records_async(recs[G * ug.RECORD_BYTES:], G, 0, n, res[ug.RESULT_BYTES:])
+        torch.cuda.synchronize()
+        r, rv = ug.decode_results(res)
+        ref_r, ref_o = oracle.utf16be_to_utf8(w)
+        assert tuple(r) == tuple(ref_r)
+        assert tuple(rv)[:2] == tuple(oracle.utf16be_validate(w))[:2]
+        if not inject:
+            records = ug.decode_records(recs)
+            got = np.concatenate([outs[k][: records[k].count].cpu().numpy() for k in range(G)])
+            assert np.array_equal(got, ref_o)

@@ -72,6 +72,10 @@ def test_utf8_cut_backoff(ug):
 def test_utf16_cut_backoff(ug):
     w = [0x41, 0xD83D, 0xDE00, 0x42]
     assert [ug.utf16_cut_backoff(w, i) for i in range(4)] == [0, 0, 1, 0]
+    # the same text stored big-endian: memory words are the byte-swapped units
+    be = [((x >> 8) | (x << 8)) & 0xFFFF for x in w]
+    assert [ug.utf16be_cut_backoff(be, i) for i in range(4)] == [0, 0, 1, 0]
+    assert ug.utf16be_cut_backoff(w, 2) == 0  # LE words read as BE are not low surrogates
 
 
 def test_combine_records_host(ug):
