@@ -52,78 +52,6 @@ __device__ __forceinline__ uint32_t word_at(const Window &w, long long wpos) {
              : 0u;
 }
 
-// out[P + k] = stage[k] for k in [0, C), clipped at out[cap).  The 16-byte aligned interior is
-// written with 128-bit stores; each chunk is two 128-bit shared loads re-aligned by a
-// tile-uniform funnel shift.  Head and tail (< 16 bytes each) use scalar stores.
-__device__ __forceinline__ uint4 shift_window(const uint4 &a, const uint4 &b, uint32_t q,
-                                              uint32_t r) {
-  uint4 o;
-  switch (q) {
-    case 0: o = make_uint4(__funnelshift_r(a.x, a.y, r), __funnelshift_r(a.y, a.z, r),
-                           __funnelshift_r(a.z, a.w, r), __funnelshift_r(a.w, b.x, r)); break;
-    case 1: o = make_uint4(__funnelshift_r(a.y, a.z, r), __funnelshift_r(a.z, a.w, r),
-                           __funnelshift_r(a.w, b.x, r), __funnelshift_r(b.x, b.y, r)); break;
-    case 2: o = make_uint4(__funnelshift_r(a.z, a.w, r), __funnelshift_r(a.w, b.x, r),
-                           __funnelshift_r(b.x, b.y, r), __funnelshift_r(b.y, b.z, r)); break;
-    default: o = make_uint4(__funnelshift_r(a.w, b.x, r), __funnelshift_r(b.x, b.y, r),
-                            __funnelshift_r(b.y, b.z, r), __funnelshift_r(b.z, b.w, r)); break;
-  }
-  return o;
-}
-
-template <typename T>
-__device__ __forceinline__ void copy_out(T *out, unsigned long long cap, unsigned long long P,
-                                         uint32_t C, const T *stage, int tid) {
-  constexpr uint32_t A = 16 / sizeof(T);  // units per 16 bytes
-  unsigned long long hi = P + C;
-  if (hi > cap) hi = cap;
-  if (hi <= P) return;
-  const uint32_t Cc = (uint32_t)(hi - P);
-  const uint32_t mis = (uint32_t)(((uintptr_t)(out + P) & 15u) / sizeof(T));
-  const uint32_t s0 = mis ? A - mis : 0u;  // first stage index landing on a 16B boundary
-  if (s0 >= Cc) {
-    if ((uint32_t)tid < Cc) out[P + tid] = stage[tid];
-    return;
-  }
-  const uint32_t nfull = (Cc - s0) / A;
-  const uint32_t t0 = s0 + nfull * A;
-  if ((uint32_t)tid < s0) out[P + tid] = stage[tid];
-  if (tid >= 64 && (uint32_t)(tid - 64) < Cc - t0) out[P + t0 + (tid - 64)] = stage[t0 + (tid - 64)];
-  const uint32_t sb = s0 * (uint32_t)sizeof(T);  // byte offset of chunk 0 inside stage[0..16)
-  const uint32_t q = sb >> 2, r = (sb & 3u) * 8u;
-  const uint4 *st = reinterpret_cast<const uint4 *>(stage);
-  uint4 *dst = reinterpret_cast<uint4 *>(out + P + s0);
-  for (uint32_t c = tid; c < nfull; c += NT) dst[c] = shift_window(st[c], st[c + 1], q, r);
-}
-
-// One warp copies stage[lo, lo + cnt) to out[G, G + cnt), clipped at out[cap): 128-bit stores
-// for the 16-byte aligned interior (two 128-bit shared loads re-aligned by funnel shifts),
-// scalar head and tail.
-template <typename T>
-__device__ __forceinline__ void copy_out_warp(T *out, unsigned long long cap,
-                                              unsigned long long G, uint32_t lo, uint32_t cnt,
-                                              const T *stage, int lane) {
-  constexpr uint32_t A = 16 / sizeof(T);  // units per 16 bytes
-  unsigned long long hi = G + cnt;
-  if (hi > cap) hi = cap;
-  if (hi <= G) return;
-  const uint32_t Cc = (uint32_t)(hi - G);
-  const uint32_t mis = (uint32_t)(((uintptr_t)(out + G) & 15u) / sizeof(T));
-  const uint32_t s0 = mis ? A - mis : 0u;  // first unit landing on a 16-byte boundary
-  if (s0 >= Cc) {
-    if ((uint32_t)lane < Cc) out[G + lane] = stage[lo + lane];
-    return;
-  }
-  const uint32_t nfull = (Cc - s0) / A;
-  const uint32_t t0 = s0 + nfull * A;
-  if ((uint32_t)lane < s0) out[G + lane] = stage[lo + lane];
-  if ((uint32_t)lane < Cc - t0) out[G + t0 + lane] = stage[lo + t0 + lane];
-  const uint32_t sb = (lo + s0) * (uint32_t)sizeof(T);  // stage byte offset of chunk 0
-  const uint32_t q = (sb & 15u) >> 2, r = (sb & 3u) * 8u;
-  const uint4 *st = reinterpret_cast<const uint4 *>(stage) + (sb >> 4);
-  uint4 *dst = reinterpret_cast<uint4 *>(out + G + s0);
-  for (uint32_t c = lane; c < nfull; c += 32) dst[c] = shift_window(st[c], st[c + 1], q, r);
-}
 
 // Block exclusive scan over the NT data threads: returns the thread's exclusive prefix within
 // the tile and the tile total.  One data-warp barrier inside.
@@ -396,16 +324,6 @@ using U8PolBE = U8PolT<true>;
 
 // ============================================================================ UTF-16 policy
 // Positions are words.  Thread `tid` owns tile words [16 tid, 16 tid + 16), two per register.
-// Position of the first set lane bit among 8 registers of lane masks (cold path).
-__device__ __noinline__ unsigned long long first_error_lane(uint32_t e0, uint32_t e1, uint32_t e2,
-                                                            uint32_t e3, uint32_t e4, uint32_t e5,
-                                                            uint32_t e6, uint32_t e7,
-                                                            long long pos0) {
-  const uint32_t e[8] = {e0, e1, e2, e3, e4, e5, e6, e7};
-  for (int k = 0; k < 8; k++)
-    if (e[k]) return (unsigned long long)(pos0 + 2 * k + ((e[k] & 0x8000u) ? 0 : 1));
-  return NONE;
-}
 
 // BE: UTF-16BE input: the low/high byte split of the classes swaps its
 // selectors (u16::classes4<BE>), the two scalar context words are byte-swapped.

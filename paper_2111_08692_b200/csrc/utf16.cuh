@@ -29,91 +29,7 @@ UG_HD bool err_at(uint32_t prev, uint32_t u, uint32_t next) {
   return (is_high(u) && !is_low(next)) || (is_low(u) && !is_high(prev));
 }
 
-// UTF-8 bytes of word u (little-endian packed, width(u, prev) of them are meaningful).
-// Branch-free: all candidates computed, then selected.
-UG_HD uint32_t utf8_bytes(uint32_t u, uint32_t prev) {
-  const uint32_t t6 = 0x80u | (u & 0x3Fu);         // last continuation byte
-  const uint32_t m6 = 0x80u | ((u >> 6) & 0x3Fu);  // middle continuation byte
-  const uint32_t b2 = (0xC0u | (u >> 6)) | (t6 << 8);
-  const uint32_t b3 = (0xE0u | (u >> 12)) | (m6 << 8) | (t6 << 16);
-  const uint32_t h10 = (u & 0x3FFu) + 0x40u;       // cp >> 10 of a pair
-  const uint32_t bh = (0xF0u | (h10 >> 8)) | ((0x80u | ((h10 >> 2) & 0x3Fu)) << 8);
-  const uint32_t bl = (0x80u | ((prev & 3u) << 4) | ((u >> 6) & 0xFu)) | (t6 << 8);
-  uint32_t v = b3;
-  v = (is_low(u) && is_high(prev)) ? bl : v;
-  v = is_high(u) ? bh : v;
-  v = (u < 0x800u) ? b2 : v;
-  v = (u < 0x80u) ? u : v;
-  return v;
-}
 
-#if defined(__CUDACC__)
-// ---------------------------------------------------------------- SWAR (two words per op)
-// Masks carry one bit per 16-bit lane, at bit 15 (low word) and bit 31 (high word).
-constexpr uint32_t LANE_TOP = 0x80008000u;
-// lane == 0 -> top bit set (exact per lane: no borrow across lanes)
-__device__ __forceinline__ uint32_t zero_lanes(uint32_t x) {
-  return ~(((x & 0x7FFF7FFFu) + 0x7FFF7FFFu) | x) & LANE_TOP;
-}
-// top-bit lane masks -> 0xFFFF per selected lane (PRMT sign replication of bytes 1 and 3)
-__device__ __forceinline__ uint32_t lanes16(uint32_t m) {
-  uint32_t d;
-  asm("prmt.b32 %0, %1, 0, 0xBB99;" : "=r"(d) : "r"(m));
-  return d;
-}
-
-struct Cls2 {
-  uint32_t A;   // u < 0x80
-  uint32_t B;   // u < 0x800
-  uint32_t H;   // high surrogate
-  uint32_t L;   // low surrogate
-};
-// Per-lane compares without cross-lane carries: (u & 0x7FFF) + (0x8000 - k) sets bit 15 iff
-// (u & 0x7FFF) >= k; OR-ing u's own bit 15 gives u >= k for k <= 0x8000.
-__device__ __forceinline__ Cls2 classes2(uint32_t r) {
-  Cls2 c;
-  const uint32_t lo15 = r & 0x7FFF7FFFu;
-  c.A = ~((lo15 + 0x7F807F80u) | r) & LANE_TOP;          // u < 0x80
-  c.B = ~((lo15 + 0x78007800u) | r) & LANE_TOP;          // u < 0x800
-  const uint32_t S = zero_lanes((r & 0xF800F800u) ^ 0xD800D800u);  // D800..DFFF
-  const uint32_t b10 = (r << 5) & LANE_TOP;              // bit 10: low (DC00..) vs high
-  c.H = S & ~b10;
-  c.L = S & b10;
-  return c;
-}
-// three-byte lanes (a5): not < 0x800, not a high surrogate, not a low one after a high one
-__device__ __forceinline__ uint32_t three2(const Cls2 &c, uint32_t Hp) {
-  return ~(c.B | c.H | (c.L & Hp)) & LANE_TOP;
-}
-
-// UTF-8 byte streams of the two words of r: lane k of B0/B1/B2 holds the
-// first / second / third byte of word k (only the first width(word) are meaningful).
-// pl = the two previous words ([word before lane 0, lane 0]); Hp = previous word is high.
-__device__ __forceinline__ void encode2(uint32_t r, uint32_t pl, const Cls2 &c, uint32_t Hp,
-                                        uint32_t *B0, uint32_t *B1, uint32_t *B2) {
-  const uint32_t r6 = r >> 6;
-  const uint32_t t6 = (r & 0x003F003Fu) | 0x00800080u;
-  const uint32_t m6 = (r6 & 0x003F003Fu) | 0x00800080u;
-  const uint32_t c2 = (r6 & 0x001F001Fu) | 0x00C000C0u;
-  const uint32_t e3 = ((r >> 12) & 0x000F000Fu) | 0x00E000E0u;
-  const uint32_t h10 = (r & 0x03FF03FFu) + 0x00400040u;  // cp >> 10 of a pair
-  const uint32_t hl = ((h10 >> 8) & 0x00070007u) | 0x00F000F0u;
-  const uint32_t hm = ((h10 >> 2) & 0x003F003Fu) | 0x00800080u;
-  const uint32_t ll = ((pl & 0x00030003u) << 4) | (r6 & 0x000F000Fu) | 0x00800080u;
-  const uint32_t mB = lanes16(c.B), mA = lanes16(c.A), mH = lanes16(c.H);
-  const uint32_t mLp = lanes16(c.L & Hp);
-  uint32_t b0 = (c2 & mB) | (e3 & ~mB);
-  b0 = (r & mA) | (b0 & ~mA);
-  b0 = (hl & mH) | (b0 & ~mH);
-  *B0 = (ll & mLp) | (b0 & ~mLp);
-  const uint32_t mT = mB | mLp;
-  uint32_t b1 = (t6 & mT) | (m6 & ~mT);
-  *B1 = (hm & mH) | (b1 & ~mH);
-  *B2 = t6;
-}
-
-
-#endif  // __CUDACC__
 
 // ---------------------------------------------------------------- byte-SWAR, 4 words per op
 // The 4 words of two registers (wa = words 0, 1; wb = words 2, 3) are split into their low
