@@ -613,3 +613,39 @@ def test_utf16be_virtual_shards(c0, G):
             records = ug.decode_records(recs)
             got = np.concatenate([outs[k][: records[k].count].cpu().numpy() for k in range(G)])
             assert np.array_equal(got, ref_o)
+
+
+# ----------------------------------------------------------------------------- randomized mix
+def test_randomized_mix_all_entry_points():
+    """60 random cases over every entry point: sizes spanning 0..~3 MiB (many tiles and a
+    ragged tail), random start alignment, 0-3 injected errors of random classes, random output
+    capacity (ample, exact, one short), LE and BE; each result and output prefix against the
+    oracle."""
+    rng = np.random.default_rng(np.random.SeedSequence([0x5EED, 60]))
+    for case in range(60):
+        n = int(rng.choice([0, 1, 7, 33, 1000, 16384, 16385, 70000, 1 << 20, 3 << 20]))
+        n += int(rng.integers(0, 64)) if n > 64 else 0
+        a = np.frombuffer(synth.gen_chunk("mixed", "utf8", n, 77, case), dtype=np.uint8).copy()
+        nerr = int(rng.integers(0, 4)) if n > 200 else 0
+        for _ in range(nerr):
+            cls = synth.UTF8_ERROR_CLASSES[int(rng.integers(0, 5))]
+            synth.inject_utf8_error(a, 0, max(0, a.size - 8), cls, rng)
+        off = int(rng.integers(0, 16))
+        need = oracle.utf8_to_utf16le(a)[0]
+        cap_choice = int(rng.integers(0, 3))
+        written = need.written if need.error >= 0 else 0
+        cap = [None, written, max(0, written - 1)][cap_choice]
+        be = bool(rng.integers(0, 2))
+        if be:
+            check_utf8_be(a, offset=off, cap=cap)
+        else:
+            check_utf8(a, offset=off, cap=cap)
+        # the reverse direction on the valid prefix's units, with a lone surrogate sometimes
+        u = oracle.utf8_to_utf16le(a)[1].copy()
+        if u.size > 10 and rng.integers(0, 2):
+            synth.inject_utf16_error(u, 0, u.size - 1, rng)
+        offw = 2 * int(rng.integers(0, 8))
+        if be:
+            check_utf16be(be_raw(u), offset=offw)
+        else:
+            check_utf16(u, offset=offw)
