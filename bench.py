@@ -483,12 +483,17 @@ def run_reference(args):
     size = cfg.size if not args.size_mib else args.size_mib << 20
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
     nch = max(1, min(cores, 8, size // synth.CHUNK))
-    data = [np.frombuffer(synth.gen_chunk(cfg.mix, cfg.encoding, min(synth.CHUNK, size),
-                                          cfg.seed, c), dtype=np.uint8) for c in range(nch)]
+    # exactly K timed and W warm-up steps; each step is a bounded sample (nch chunks, one per
+    # thread) sized so the whole run stays near REF_BUDGET_S (a 64 MiB chunk takes ~1.2 s)
+    K, W = max(1, args.steps), max(0, args.warmup)
+    REF_BUDGET_S = 90.0
+    frac = min(1.0, REF_BUDGET_S / ((K + W) * 1.3))
+    clen = max(1 << 20, int(min(synth.CHUNK, size) * frac) >> 20 << 20)
+    data = [np.frombuffer(synth.gen_chunk(cfg.mix, cfg.encoding, clen, cfg.seed, c),
+                          dtype=np.uint8) for c in range(nch)]
     ex = ThreadPoolExecutor(nch)
-    for _ in range(min(args.warmup, 1)):
+    for _ in range(W):
         sum(ex.map(lambda c: oracle_step(oracle, c), data))
-    K = max(1, min(args.steps, 3))
     t = time.perf_counter()
     tot = 0
     for _ in range(K):
@@ -496,13 +501,13 @@ def run_reference(args):
     dt = (time.perf_counter() - t) / K
     v = (tot / K) / dt / 1e9
     line = {"impl": "reference", "metric": METRIC, "value": round(v, 4), "unit": UNIT,
-            "n_gpus": G, "steps": K, "warmup": min(args.warmup, 1),
+            "n_gpus": G, "steps": K, "warmup": W,
             "ms_per_step": round(dt * 1e3, 2), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u8/u16 (integer)", "data": "synthetic",
-            "config": {"workload": f"config 4 sample: {nch} x 64 MiB of the {cfg.key} stream",
+            "config": {"workload": f"config 4 sample: {nch} x {clen >> 20} MiB of the {cfg.key} stream",
                        "parallelism": f"{nch} host threads"},
             "cpu_baseline": {"value": round(v, 4), "unit": UNIT, "cores": nch, "kind": "oracle",
-                             "sample": f"{nch} x 64 MiB chunks per step"},
+                             "sample": f"{nch} x {clen >> 20} MiB chunks per step"},
             "e2e": {"value": round(v, 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
