@@ -13,6 +13,7 @@ import tempfile
 
 rep, ksub, sidx, nbytes = sys.argv[1], sys.argv[2], int(sys.argv[3]), float(sys.argv[4])
 COL = os.environ.get("COL", "Instructions Executed")  # e.g. COL=stall_barrier
+FN = os.environ.get("FN", "")  # extra mangled-name filter for templates, e.g. FN=ILb0E (LE)
 lib = sys.argv[5] if len(sys.argv) > 5 else "paper_2111_08692_b200/libunigpu.so"
 tmp = tempfile.mkdtemp()
 subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(lib)], cwd=tmp, capture_output=True)
@@ -30,7 +31,7 @@ for cub in glob.glob(os.path.join(tmp, "kernels*.cubin")):
             cur_line = f"{os.path.basename(m.group(1))}:{m.group(2)}"
             continue
         m = re.match(r"\s+/\*([0-9a-f]{4,})\*/\s+\S", ln)
-        if m and cur_fn and ksub in cur_fn:
+        if m and cur_fn and ksub in cur_fn and FN in cur_fn:
             lines[int(m.group(1), 16)] = cur_line
 txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
