@@ -443,3 +443,66 @@ def utf16be_cut_backoff(words, at: int) -> int:
     import numpy as np
     a = np.ascontiguousarray(words, dtype=np.uint16)
     return int(lib.ug_utf16be_cut_backoff(ctypes.c_void_p(a.ctypes.data + 2 * at), at))
+
+
+# --------------------------------------------------------------------------- argument checks
+# The C-ABI takes raw pointers and unit counts; a CPU tensor handed to a device function, a
+# tensor of the wrong element size (units miscounted) or a non-contiguous view would be
+# undefined behaviour there.  Every public entry point above is wrapped so that these are
+# rejected in Python, before the call: the input / output element size follows from the
+# function's name (UTF-8 = 1 byte, UTF-16 = 2), `_host` functions take host tensors, all
+# others CUDA tensors.
+def _expect(fname: str):
+    src = fname.split("_from_")[-1] if "_from_" in fname else fname
+    in_es = 2 if src.startswith("utf16") else 1
+    out_es = 2 if "_to_utf16" in fname else (1 if "_to_utf8" in fname else None)
+    return in_es, out_es, fname.endswith("_host")
+
+
+def _validate(t, es, host, what, fname):
+    import torch
+    if not isinstance(t, torch.Tensor):
+        raise TypeError(f"{fname}: {what} must be a torch.Tensor, got {type(t).__name__}")
+    if t.element_size() != es:
+        raise ValueError(f"{fname}: {what} must have {es}-byte elements "
+                         f"({'uint8' if es == 1 else 'int16/uint16'}), got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{fname}: {what} must be contiguous")
+    if host and t.is_cuda:
+        raise ValueError(f"{fname}: {what} must be a host (pinned) tensor")
+    if not host and not t.is_cuda:
+        raise ValueError(f"{fname}: {what} must be a CUDA tensor (no CPU fallback)")
+
+
+def _checked(fname, fn):
+    import functools
+    in_es, out_es, host = _expect(fname)
+    names = fn.__code__.co_varnames[:fn.__code__.co_argcount]
+    roles = [(i, nm, in_es if nm.startswith("t_in") else out_es)
+             for i, nm in enumerate(names) if nm in ("t_in", "t_out", "t_in_host", "t_out_host")]
+
+    @functools.wraps(fn)
+    def w(*args, **kw):
+        for i, nm, es in roles:
+            t = args[i] if i < len(args) else kw.get(nm)
+            if t is not None and es is not None:
+                _validate(t, es, host, nm, fname)
+        return fn(*args, **kw)
+    return w
+
+
+for _n in ("utf8_validate", "utf16le_validate", "utf8_to_utf16le", "utf16le_to_utf8",
+           "utf16_length_from_utf8", "utf8_length_from_utf16le",
+           "utf16be_validate", "utf8_to_utf16be", "utf16be_to_utf8", "utf8_length_from_utf16be",
+           "utf8_validate_async", "utf16le_validate_async", "utf8_to_utf16le_async",
+           "utf16le_to_utf8_async", "utf16_length_from_utf8_async",
+           "utf8_length_from_utf16le_async", "utf16be_validate_async", "utf8_to_utf16be_async",
+           "utf16be_to_utf8_async", "utf8_length_from_utf16be_async",
+           "utf8_to_utf16le_shard_async", "utf16le_to_utf8_shard_async",
+           "utf8_validate_shard_async", "utf16le_validate_shard_async",
+           "utf8_to_utf16be_shard_async", "utf16be_to_utf8_shard_async",
+           "utf16be_validate_shard_async",
+           "utf8_to_utf16le_host", "utf16le_to_utf8_host", "utf8_to_utf16be_host",
+           "utf16be_to_utf8_host"):
+    globals()[_n] = _checked(_n, globals()[_n])
+del _n

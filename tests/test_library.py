@@ -167,3 +167,28 @@ def test_argument_errors_exhaustive_need_no_gpu(ug):
     for fn in (L.utf8_to_utf16be, L.utf16be_to_utf8):
         r = fn(V(0), 0, V(0), 0, V(0))
         assert (r.error, r.position, r.written) == (0, 0, 0)
+
+
+def test_binding_rejects_wrong_tensors(ug):
+    """The Python binding refuses, before any C call, what the raw-pointer ABI cannot check: a
+    CPU tensor for a device function (no CPU fallback), a host function given a CUDA tensor, a
+    wrong element size (units would be miscounted) and non-contiguous views."""
+    torch = pytest.importorskip("torch")
+    b8, w16 = torch.zeros(8, dtype=torch.uint8), torch.zeros(8, dtype=torch.int16)
+    with pytest.raises(ValueError, match="CUDA tensor"):
+        ug.utf8_validate(b8)
+    with pytest.raises(ValueError, match="CUDA tensor"):
+        ug.utf16be_to_utf8(w16, b8)
+    with pytest.raises(ValueError, match="1-byte"):
+        ug.utf8_validate(w16)
+    with pytest.raises(ValueError, match="2-byte"):
+        ug.utf8_length_from_utf16le(b8)
+    with pytest.raises(ValueError, match="2-byte"):
+        ug.utf8_to_utf16le_host(b8, b8)
+    with pytest.raises(ValueError, match="contiguous"):
+        ug.utf8_to_utf16le_host(b8[::2], w16)
+    with pytest.raises(TypeError):
+        ug.utf8_validate(b"\x41")
+    assert ug._expect("utf8_length_from_utf16be") == (2, None, False)
+    assert ug._expect("utf8_to_utf16le_shard_async") == (1, 2, False)
+    assert ug._expect("utf16le_to_utf8_host") == (2, 1, True)
