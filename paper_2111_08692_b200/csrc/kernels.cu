@@ -1158,7 +1158,16 @@ constexpr int PF16 = UG_PF16;  // tiles loading ahead of the one being counted
 constexpr int D16 = RING16 - PF16 - 1;  // tiles awaiting their prefix (emit deferral)
 static_assert(3 * (TILE / 2) < (1 << 24) && NT / 32 < 256, "s_acc packing");
 static_assert(PF16 >= 1 && D16 >= 1, "ring: loads in flight + the tile counted + deferral");
-constexpr int T16_THREADS = NT + 32;
+#ifndef UG_NLB16
+#define UG_NLB16 1
+#endif
+// look-back agents (warps) of K4, alternating tiles.  One is best: two were measured 7 % (c4)
+// to 21 % (ASCII) slower although the no-look-back ablation is 12 % faster on c4 - the chain
+// costs latency against the 3-tile emit slack, not agent throughput.
+constexpr int NLB16 = UG_NLB16;
+constexpr int T16_THREADS = NT + 32 * NLB16;
+static_assert(NLB16 == 1 || PF16 == 1, "termination ticks assume one tile loading ahead");
+static_assert(NLB16 <= RING16 - D16, "termination ticks use slots of emitted tiles");
 
 template <bool BE>
 __device__ __forceinline__ void emit_tile16(const TileArgs &a, const uint8_t *img, long long t,
@@ -1247,10 +1256,11 @@ __global__ void __launch_bounds__(T16_THREADS, CTAS_PER_SM) k_transcode16(const 
   }
   __syncthreads();
 
-  if (warp == NT / 32) {
-    // ------------------------------------------------------------ look-back warp (a6)
+  if (warp >= NT / 32) {
+    // ------------------------------------------------------------ look-back warps (a6)
+    // agent a = warp - NT/32 takes the tiles k = a (mod NLB16), in ticket order
 #pragma unroll 1
-    for (int k = 0;; k++) {
+    for (int k = warp - NT / 32;; k += NLB16) {
       const int sl = k % RING16;
       const uint32_t ph = (k / RING16) & 1;
       mbar_wait(&mb_tick[sl], ph);
@@ -1267,7 +1277,11 @@ __global__ void __launch_bounds__(T16_THREADS, CTAS_PER_SM) k_transcode16(const 
       }
       const uint32_t C = __shfl_sync(FULL, sc, NT / 32 - 1);  // (published by the last warp)
       if (lane < NT / 32) s_wsum[sl][lane] = sc - wv;
+#ifdef UG_ABL_NOLB
+      const unsigned long long P = (unsigned long long)t * (3 * TILE / 2);  // ablation: no chain
+#else
       const unsigned long long P = tile_excl_prefix(a, t, lane);
+#endif
       const unsigned long long incl = P + C;
       __syncwarp();
       if (lane == 0) {
@@ -1351,6 +1365,15 @@ __global__ void __launch_bounds__(T16_THREADS, CTAS_PER_SM) k_transcode16(const 
       if (tid == 0) start_tile((i + PF16) % RING16, tn);
       if (i >= D16) emit(i - D16, oldest);  // a7-a9, a8
       i++;
+    }
+    // every look-back agent must see a past-the-end ticket to stop: the one owning tile i has;
+    // post the same for the others (slots of tiles i + 1 .., held tiles emitted long ago)
+    if (tid == 0) {
+#pragma unroll
+      for (int k = 1; k < NLB16; k++) {
+        s_t[(i + k) % RING16] = ntiles;
+        mbar_arrive(&mb_tick[(i + k) % RING16]);
+      }
     }
     // drain: tiles i - D16 .. i - 1 (hist[D16 - 1] is the oldest)
 #pragma unroll
