@@ -302,6 +302,11 @@ def run_ours(args):
         d["frac"] = d["achieved"] / peak
         t = traffic.get(k)
         d["traffic"] = round(t["dram_bytes_per_input_byte"] * d["input"]) if t else None
+        # the kernel's issue picture from the same capture (it is issue-bound)
+        d["issue"] = ({"lane_instr_per_input_byte": t.get("lane_instr_per_input_byte"),
+                       "alu_lane_instr_per_input_byte": t.get("alu_lane_instr_per_input_byte"),
+                       "issue_slots_busy": t.get("issue_slots_busy")}
+                      if t and "issue_slots_busy" in t else None)
     dom = max(kern, key=lambda k: kern[k]["ms"])
     D = kern[dom]
 
@@ -345,9 +350,11 @@ def run_ours(args):
                          "kernel": f"{dom} ({D['op']}), the longest launch of the step",
                          "algorithmic_bytes_per_launch": alg_bytes,
                          "avg_launch_ms": round(D["ms"], 4), "peak_source": peak_src,
+                         "issue": D["issue"],
                          "kernels": {k: {"op": d["op"], "avg_launch_ms": round(d["ms"], 4),
                                          "achieved": round(d["achieved"], 1),
-                                         "frac": round(d["frac"], 4), "traffic": d["traffic"]}
+                                         "frac": round(d["frac"], 4), "traffic": d["traffic"],
+                                         "issue": d["issue"]}
                                      for k, d in kern.items()}},
             "per_op": per_op,
             "clocks": clk,
