@@ -649,3 +649,25 @@ def test_randomized_mix_all_entry_points():
             check_utf16be(be_raw(u), offset=offw)
         else:
             check_utf16(u, offset=offw)
+
+
+def test_reverse_dense_3byte_text():
+    """CJK text as UTF-16 (3 output bytes per word: a tile emits ~1.4x its size, near the
+    stage's worst case).  Clean, with lone surrogates in the middle of a tile and at tile
+    edges, and with the output capacity cut inside a tile; LE and BE."""
+    x = synth.generate("c2b", size=(2 << 20) + 7)
+    u = oracle.utf8_to_utf16le(x)[1]
+    assert check_utf16(u).error == 0
+    assert check_utf16be(be_raw(u), offset=2).error == 0
+    rng = np.random.default_rng(0x2B)
+    TILE_W = 8192  # words per 16 KiB tile
+    for centre in (TILE_W * 3 + TILE_W // 2, TILE_W * 7, TILE_W * 11 + TILE_W // 2 + 40):
+        v = u.copy()
+        p, _ = synth.inject_utf16_error(v, centre - 24, centre + 24, rng)
+        r = check_utf16(v)
+        assert (r.error, r.position) == (ug.SURROGATE, p)
+        r = check_utf16be(be_raw(v))
+        assert (r.error, r.position) == (ug.SURROGATE, p)
+    need = oracle.utf16le_to_utf8(u)[0].written
+    for cap in (3 * TILE_W * 5 // 2 + 1000, need - 1):
+        check_utf16(u, cap=cap)
