@@ -710,6 +710,10 @@ void ug_release_workspaces(void) {
 
 int ug_abi_version(void) { return UNIGPU_ABI_VERSION; }
 
+#ifdef UG_PREFIX_EXPT
+cudaError_t ug_pmode_set_impl(int m);
+int ug_debug_prefix_mode(int m) { return (int)ug_pmode_set_impl(m); }
+#endif
 #ifdef UG_TRACE
 cudaError_t ug_trace_read_impl(void *host, size_t bytes);
 int ug_debug_trace(void *host, size_t bytes) { return (int)ug::trace_read(host, bytes); }

@@ -28,9 +28,12 @@ constexpr int TILE = NT * 32;     // input bytes per tile (32 per data thread)
 constexpr int CTAS_PER_SM = UG_CPS;  // transcoder CTAs per SM (register budget)
 constexpr int BPT = TILE / NT;    // 32 contiguous input bytes per thread
 #ifndef UG_LB_PER_LANE
-#define UG_LB_PER_LANE 8
+// measured (tools/exp/exp65-66.sh): 1 beats 2/3/4/8 on every config - with push-forward the
+// nearest inclusive prefix is almost always within 32 tiles, and wider rounds only add polling
+// (reverse c4 -6 %, ASCII -14 %; forward c4 -3 %, ASCII -10 % against 8)
+#define UG_LB_PER_LANE 1
 #endif
-constexpr int LB_PER_LANE = UG_LB_PER_LANE;  // look-back window: 32 lanes x 8 = 256 tiles
+constexpr int LB_PER_LANE = UG_LB_PER_LANE;  // look-back window: 32 lanes x LB_PER_LANE tiles
 constexpr int HALO = 16;          // bytes of context loaded before and after each tile
 constexpr int INBUF = TILE + 2 * HALO;
 
@@ -222,8 +225,8 @@ __device__ __forceinline__ void fix_tile_edges(const Window &w, long long t, uin
 // ---------------------------------------------------------------- decoupled look-back
 // Called by one full warp for tile t whose aggregate is already published (t > 0).  Returns the
 // exclusive prefix (sum of all earlier tiles' aggregates) in every lane.  Each round reads a
-// window of 256 predecessors (8 per lane, nearest first) with independent relaxed loads, so the
-// PREFIX frontier advances 256 tiles per L2 round trip (K2).
+// window of 32 x LB_PER_LANE predecessors (nearest first) with independent relaxed loads; with
+// the push-forward below, the nearest inclusive prefix is almost always in the first 32.
 // One look-back round over K status words per lane: lane l examines tiles
 // idx - K*l, ..., idx - K*l - K + 1 (nearest first).  Waits (re-polling only the words that
 // are not yet published, with a back-off) until every word up to this lane's first inclusive

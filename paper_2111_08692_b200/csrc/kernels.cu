@@ -1134,6 +1134,13 @@ __global__ void __launch_bounds__(LNT) k_len16(const uint16_t *in, unsigned long
   finish_reduction(sum, ctr, d_len);
 }
 
+#ifdef UG_PREFIX_EXPT
+__device__ unsigned long long g_pref[1 << 20];
+__device__ int g_pmode;
+extern "C" cudaError_t ug_pmode_set_impl(int m) {
+  return cudaMemcpyToSymbol(g_pmode, &m, sizeof(m));
+}
+#endif
 // ============================================================================ count-first K4
 // UTF-16LE -> UTF-8 with validation moved off the look-back's critical path.  A word's UTF-8
 // width depends on the word alone (u16::wm1: 1 + [u >= 0x80] + [u >= 0x800, not a surrogate]),
@@ -1279,6 +1286,16 @@ __global__ void __launch_bounds__(T16_THREADS, CTAS_PER_SM) k_transcode16(const 
       if (lane < NT / 32) s_wsum[sl][lane] = sc - wv;
 #ifdef UG_ABL_NOLB
       const unsigned long long P = (unsigned long long)t * (3 * TILE / 2);  // ablation: no chain
+#elif defined(UG_PREFIX_EXPT)
+      // experiment: mode 1 records every tile's true prefix, mode 2 replays them without the
+      // look-back (same output placement as a real run, no chain)
+      unsigned long long P;
+      if (g_pmode == 2 && t < (1 << 20)) {
+        P = g_pref[t];
+      } else {
+        P = tile_excl_prefix(a, t, lane);
+        if (g_pmode == 1 && lane == 0 && t < (1 << 20)) g_pref[t] = P;
+      }
 #else
       const unsigned long long P = tile_excl_prefix(a, t, lane);
 #endif
