@@ -28,8 +28,8 @@ constexpr int TILE = NT * 32;     // input bytes per tile (32 per data thread)
 constexpr int CTAS_PER_SM = UG_CPS;  // transcoder CTAs per SM (register budget)
 constexpr int BPT = TILE / NT;    // 32 contiguous input bytes per thread
 #ifndef UG_LB_PER_LANE
-// measured (tools/exp/exp65-66.sh): 1 beats 2/3/4/8 on every config - with push-forward the
-// nearest inclusive prefix is almost always within 32 tiles, and wider rounds only add polling
+// measured (tools/exp/exp65-66.sh): 1 beats 2/3/4/8 on every config - wider rounds only add
+// polling (each lane re-polls its unpublished words until the window resolves)
 // (reverse c4 -6 %, ASCII -14 %; forward c4 -3 %, ASCII -10 % against 8)
 #define UG_LB_PER_LANE 1
 #endif
@@ -225,8 +225,7 @@ __device__ __forceinline__ void fix_tile_edges(const Window &w, long long t, uin
 // ---------------------------------------------------------------- decoupled look-back
 // Called by one full warp for tile t whose aggregate is already published (t > 0).  Returns the
 // exclusive prefix (sum of all earlier tiles' aggregates) in every lane.  Each round reads a
-// window of 32 x LB_PER_LANE predecessors (nearest first) with independent relaxed loads; with
-// the push-forward below, the nearest inclusive prefix is almost always in the first 32.
+// window of 32 x LB_PER_LANE predecessors (nearest first) with independent relaxed loads.
 // One look-back round over K status words per lane: lane l examines tiles
 // idx - K*l, ..., idx - K*l - K + 1 (nearest first).  Waits (re-polling only the words that
 // are not yet published, with a back-off) until every word up to this lane's first inclusive
@@ -292,8 +291,9 @@ __device__ __forceinline__ bool look_back_round(uint64_t *status, uint32_t epoch
 // Push-forward (after tile t's inclusive prefix `incl` is known): publish the inclusive
 // prefixes of the run of successors t+1, t+2, ... (up to 32) whose aggregates are already
 // published.  An inclusive prefix is unique, so a push racing with the tile's own look-back (or
-// another push) writes the same value.  Keeps the published-prefix frontier close behind the
-// aggregate frontier, so look-backs resolve in their first, 32-wide probe.
+// another push) writes the same value.  It kept the published-prefix frontier close behind the
+// aggregate frontier when look-back rounds were 256 wide; with 32-wide rounds it only adds
+// polling (measured 0.3-11 % slower), so it is compiled only with -DUG_PUSH.
 __device__ __forceinline__ void push_forward(uint64_t *status, uint32_t epoch, long long t,
                                              long long ntiles, uint64_t incl, int lane) {
   const long long j = t + 1 + lane;

@@ -896,7 +896,7 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
         s_pre[sl] = P;
         mbar_arrive(&mb_pre[sl]);
       }
-#ifndef UG_NO_PUSH
+#ifdef UG_PUSH  // push-forward: measured slower with 32-wide look-back rounds
       push_forward(a.status, a.epoch, t, ntiles, incl, lane);
 #endif
     }
@@ -1307,7 +1307,9 @@ __global__ void __launch_bounds__(T16_THREADS, CTAS_PER_SM) k_transcode16(const 
         s_pre[sl] = P;
         mbar_arrive(&mb_pre[sl]);  // release: offsets, count, prefix
       }
+#ifdef UG_PUSH  // push-forward: measured slower with 32-wide look-back rounds
       push_forward(a.status, a.epoch, t, ntiles, incl, lane);
+#endif
     }
   } else {
     // ------------------------------------------------------------ data warps
