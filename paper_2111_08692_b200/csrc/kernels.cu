@@ -1346,8 +1346,13 @@ __global__ void __launch_bounds__(T16_THREADS, CTAS_PER_SM) k_transcode16(const 
       const uint4 q0 = my[0], q1 = my[1];
       uint32_t cnt;
       if (tp >= 0 && tp + TILE <= win.n) {
-        cnt = 16u + lane_sum(len16_acc4<BE>(q1.z, q1.w, len16_acc4<BE>(q1.x, q1.y,
-                             len16_acc4<BE>(q0.z, q0.w, len16_acc4<BE>(q0.x, q0.y, 0u)))));
+        // a2: an all-ASCII warp emits one byte per word (skip the width arithmetic)
+        const uint32_t orv = q0.x | q0.y | q0.z | q0.w | q1.x | q1.y | q1.z | q1.w;
+        if (__all_sync(FULL, (orv & (BE ? 0x80FF80FFu : 0xFF80FF80u)) == 0u))
+          cnt = 16u;
+        else
+          cnt = 16u + lane_sum(len16_acc4<BE>(q1.z, q1.w, len16_acc4<BE>(q1.x, q1.y,
+                               len16_acc4<BE>(q0.z, q0.w, len16_acc4<BE>(q0.x, q0.y, 0u)))));
       } else {
         const uint32_t q[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
         const long long w0 = (tp + BPT * tid) / 2, nw = win.n / 2;
