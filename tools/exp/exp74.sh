@@ -1,0 +1,6 @@
+mkdir -p gpurun_out
+: > gpurun_out/exp74.log
+for v in nobar1 cur; do for c in "c4 1024" "c1 1024"; do set -- $c
+L=build_variants/libunigpu_$v.so; [ $v = cur ] && L=paper_2111_08692_b200/libunigpu.so
+UG_LIB_OVERRIDE=$L OPS=utf8_to_utf16le,utf16le_to_utf8 timeout -s KILL 120 python tools/opbench.py $1 $2 10 2>&1 | tail -1 >> gpurun_out/exp74.log
+done; done
