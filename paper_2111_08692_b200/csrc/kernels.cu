@@ -41,6 +41,13 @@ __device__ __forceinline__ unsigned long long gtime() {
 constexpr unsigned long long VALMASK = (1ull << 38) - 1;
 // named barrier ids (0 is __syncthreads)
 constexpr int BAR_DATA = 1;           // the NT data threads
+#ifndef UG_PRODUCER
+#define UG_PRODUCER (NT - 32)
+#endif
+// the data thread that draws tickets, issues the tile loads and publishes the forward kernel's
+// aggregates: lane 0 of the LAST data warp, so that warp 0 (bulk stores, head / tail bytes)
+// is not also the one the emit barriers wait for
+constexpr int PRODUCER = UG_PRODUCER;
 
 __device__ __forceinline__ uint32_t byte_at(const Window &w, long long pos) {
   return (pos >= w.lo_valid && pos < w.hi_valid) ? (uint32_t)w.base[pos] : 0u;
@@ -931,7 +938,7 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
       // thread's share of the classification, so its L2 round trip is off the critical path
       // (every warp waits for warp 0 at the block scan).
       long long tn = 0;
-      if (tid == 0) tn = (long long)atomicAdd(&a.ctr->ticket, 1u);
+      if (tid == PRODUCER) tn = (long long)atomicAdd(&a.ctr->ticket, 1u);
 #ifdef UG_TRACE
       const unsigned long long lw0 = gtime();
 #endif
@@ -960,7 +967,7 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
         cnt = Pol::template analyze<false>(st, tid, true);
       }
       if (Pol::hint(st)) s_flag[i % 3] = 1;
-      if (tid == 0) {
+      if (tid == PRODUCER) {
         // ring slot (i + PF) % RING held tile i - DEFER - 1, emitted last iteration
         start_tile((i + PF) % RING, tn);
         // flag slot of tile i + 1: last read after the block scan of i - 2 (every thread has
@@ -969,7 +976,7 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
       }
       uint32_t excl = 0, C = 0;
       block_scan(cnt, s_wsum[i & 1], lane, warp, &excl, &C);
-      if (tid == 0) {
+      if (tid == PRODUCER) {
         // publish the tile aggregate at once (a6): successors' look-backs need it
         st_relaxed(a.status + t, pack_status(a.epoch, t == 0 ? FLAG_PREFIX : FLAG_AGG, C));
         s_cnt[sl] = C;
@@ -998,7 +1005,7 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
     }
     // every look-back agent must see a past-the-end ticket to stop: the one owning tile i has;
     // post the same for the others (their slots are free: tiles i - 3.. were emitted)
-    if (tid == 0) {
+    if (tid == PRODUCER) {
 #pragma unroll
       for (int k = 1; k < NLB; k++) {
         s_t[(i + k) % RING] = ntiles;
@@ -1331,7 +1338,7 @@ __global__ void __launch_bounds__(T16_THREADS, CTAS_PER_SM) k_transcode16(const 
     while (true) {
       const int sl = i % RING16;
       long long tn = 0;
-      if (tid == 0) tn = (long long)atomicAdd(&a.ctr->ticket, 1u);
+      if (tid == PRODUCER) tn = (long long)atomicAdd(&a.ctr->ticket, 1u);
       mbar_wait(&mb_load[sl], (i / RING16) & 1);
       const long long t = s_t[sl];
       if (t >= ntiles) break;
@@ -1386,13 +1393,13 @@ __global__ void __launch_bounds__(T16_THREADS, CTAS_PER_SM) k_transcode16(const 
       for (int q = D16 - 1; q > 0; q--) hist[q] = hist[q - 1];
       hist[0] = ((sc - cnt) << 8) | cnt;  // count <= 48, offset < 2^11
       // slot of tile i + PF16 held tile i + PF16 - RING16 = i - D - 1, emitted last iteration
-      if (tid == 0) start_tile((i + PF16) % RING16, tn);
+      if (tid == PRODUCER) start_tile((i + PF16) % RING16, tn);
       if (i >= D16) emit(i - D16, oldest);  // a7-a9, a8
       i++;
     }
     // every look-back agent must see a past-the-end ticket to stop: the one owning tile i has;
     // post the same for the others (slots of tiles i + 1 .., held tiles emitted long ago)
-    if (tid == 0) {
+    if (tid == PRODUCER) {
 #pragma unroll
       for (int k = 1; k < NLB16; k++) {
         s_t[(i + k) % RING16] = ntiles;
