@@ -48,6 +48,11 @@ constexpr int BAR_DATA = 1;           // the NT data threads
 // aggregates: lane 0 of the LAST data warp, so that warp 0 (bulk stores, head / tail bytes)
 // is not also the one the emit barriers wait for
 constexpr int PRODUCER = UG_PRODUCER;
+#ifndef UG_SHIP_WARP
+#define UG_SHIP_WARP 0
+#endif
+// lane 0 of this warp issues the TMA bulk stores of the stage; its lanes store head / tail
+constexpr int SHIPPER = 32 * UG_SHIP_WARP;
 
 __device__ __forceinline__ uint32_t byte_at(const Window &w, long long pos) {
   return (pos >= w.lo_valid && pos < w.hi_valid) ? (uint32_t)w.base[pos] : 0u;
@@ -787,14 +792,15 @@ __device__ __forceinline__ void emit_tile(const TileArgs &a, const uint8_t *img,
   const uint32_t Cc = (uint32_t)(hi - P);
   const uint32_t h = ph ? A - ph : 0u;  // head units (before the first 16-byte boundary)
   if (h >= Cc) {
-    if ((uint32_t)tid < Cc) out[P + tid] = stage[ph + tid];
+    if ((uint32_t)(tid - SHIPPER) < Cc) out[P + tid - SHIPPER] = stage[ph + tid - SHIPPER];
     return;
   }
   const uint32_t nb = (Cc - h) / A;  // whole 16-byte granules
   const uint32_t tl = h + nb * A;    // first tail unit
-  if ((uint32_t)tid < h) out[P + tid] = stage[ph + tid];
-  if ((uint32_t)tid < Cc - tl) out[P + tl + tid] = stage[ph + tl + tid];
-  if (tid == 0 && nb) {
+  const uint32_t sid = (uint32_t)(tid - SHIPPER);  // head / tail bytes: the shipping warp
+  if (sid < h) out[P + sid] = stage[ph + sid];
+  if (sid < Cc - tl) out[P + tl + sid] = stage[ph + tl + sid];
+  if (tid == SHIPPER && nb) {
     fence_proxy_async_smem();  // the stage writes above (generic proxy) before the TMA read
     bulk_s2g(out + P + h, stage + ph + h, nb * 16u);
     bulk_commit();
@@ -927,7 +933,7 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
         g_trace[blockIdx.x][j][5] = gtime();
       }
 #endif
-      if (tid == 0) bulk_wait_read_all();  // the previous bulk store has read the stage
+      if (tid == SHIPPER) bulk_wait_read_all();  // the previous bulk store has read the stage
       named_sync<BAR_DATA, NT>();
       emit_tile<Pol>(a, ring + js * INBUF, s_t[js], s_pre[js], s_cnt[js], v >> 8, v & 0xFFu,
                      stage, tid, lane);
@@ -1016,7 +1022,7 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
 #pragma unroll
     for (int q = DEFER - 1; q >= 0; q--)
       if (i - 1 - q >= 0) emit(i - 1 - q, hist[q]);
-    if (tid == 0) bulk_wait_all();  // all output written before the CTA retires
+    if (tid == SHIPPER) bulk_wait_all();  // all output written before the CTA retires
   }
   __syncthreads();
   finish_call<Pol>(a, true, tid, warp, lane, &s_last);
@@ -1210,14 +1216,15 @@ __device__ __forceinline__ void emit_tile16(const TileArgs &a, const uint8_t *im
   const uint32_t Cc = (uint32_t)(hi - P);
   const uint32_t h = ph ? A - ph : 0u;
   if (h >= Cc) {
-    if ((uint32_t)tid < Cc) out[P + tid] = stage[ph + tid];
+    if ((uint32_t)(tid - SHIPPER) < Cc) out[P + tid - SHIPPER] = stage[ph + tid - SHIPPER];
     return;
   }
   const uint32_t nb = (Cc - h) / A;
   const uint32_t tl = h + nb * A;
-  if ((uint32_t)tid < h) out[P + tid] = stage[ph + tid];
-  if ((uint32_t)tid < Cc - tl) out[P + tl + tid] = stage[ph + tl + tid];
-  if (tid == 0 && nb) {
+  const uint32_t sid = (uint32_t)(tid - SHIPPER);  // head / tail bytes: the shipping warp
+  if (sid < h) out[P + sid] = stage[ph + sid];
+  if (sid < Cc - tl) out[P + tl + sid] = stage[ph + tl + sid];
+  if (tid == SHIPPER && nb) {
     fence_proxy_async_smem();
     bulk_s2g(out + P + h, stage + ph + h, nb * 16u);
     bulk_commit();
@@ -1328,7 +1335,7 @@ __global__ void __launch_bounds__(T16_THREADS, CTAS_PER_SM) k_transcode16(const 
     auto emit = [&](int j, uint32_t v) {
       const int js = j % RING16;
       mbar_wait(&mb_pre[js], (j / RING16) & 1);
-      if (tid == 0) bulk_wait_read_all();  // the previous bulk store has read the stage
+      if (tid == SHIPPER) bulk_wait_read_all();  // the previous bulk store has read the stage
       named_sync<BAR_DATA, NT>();
       emit_tile16<BE>(a, ring + js * INBUF, s_t[js], s_pre[js], s_cnt[js],
                   s_wsum[js][warp] + (v >> 8), v & 0xFFu, stage, tid, lane);
@@ -1410,7 +1417,7 @@ __global__ void __launch_bounds__(T16_THREADS, CTAS_PER_SM) k_transcode16(const 
 #pragma unroll
     for (int q = D16 - 1; q >= 0; q--)
       if (i - 1 - q >= 0) emit(i - 1 - q, hist[q]);
-    if (tid == 0) bulk_wait_all();
+    if (tid == SHIPPER) bulk_wait_all();
   }
   __syncthreads();
   finish_call<U16PolT<BE>>(a, true, tid, warp, lane, &s_last);
