@@ -827,7 +827,13 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
   __shared__ uint64_t mb_tick[RING];  // thread 0 -> look-back warp: ticket of slot taken
   __shared__ uint64_t mb_agg[RING];   // thread 0 -> look-back warp: aggregate of slot
   __shared__ uint64_t mb_pre[RING];   // look-back warp -> data warps: prefix of slot
+#ifndef UG_FWD_BLOCK_SCAN  // warp-level publish (measured: forward -2 to -3 %)
+  // warp totals, turned in place into exclusive warp offsets by the look-back warp
+  __shared__ uint32_t s_wsum[RING][NT / 32];
+  __shared__ uint32_t s_acc[RING];  // arrivals << 24 | running sum of warp totals
+#else
   __shared__ uint32_t s_wsum[2][NT / 32];
+#endif
   __shared__ long long s_t[RING];
   __shared__ uint32_t s_cnt[RING];
   __shared__ unsigned long long s_pre[RING];
@@ -855,7 +861,12 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
     for (int j = 0; j < RING; j++) {
       mbar_init(&mb_load[j], 1);
       mbar_init(&mb_tick[j], 1);
+#ifndef UG_FWD_BLOCK_SCAN
+      mbar_init(&mb_agg[j], NT / 32);
+      s_acc[j] = 0u;
+#else
       mbar_init(&mb_agg[j], 1);
+#endif
       mbar_init(&mb_pre[j], 1);
     }
     s_flag[0] = s_flag[1] = s_flag[2] = 0;
@@ -879,6 +890,20 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
       // start when the tile itself is classified: its predecessors were ticketed earlier and
       // are classified around the same time, so an earlier start would only poll L2 longer
       mbar_wait(&mb_agg[sl], ph);
+#endif
+#ifndef UG_FWD_BLOCK_SCAN
+      {  // exclusive warp offsets and the tile count from the warp totals
+        const uint32_t wv = lane < NT / 32 ? s_wsum[sl][lane] : 0u;
+        uint32_t sc = wv;
+#pragma unroll
+        for (int d = 1; d < NT / 32; d <<= 1) {
+          const uint32_t y = __shfl_up_sync(FULL, sc, d);
+          if (lane >= d) sc += y;
+        }
+        if (lane < NT / 32) s_wsum[sl][lane] = sc - wv;
+        if (lane == NT / 32 - 1) s_cnt[sl] = sc;
+        __syncwarp();
+      }
 #endif
 #ifdef UG_TRACE
       unsigned long long t0 = gtime();
@@ -935,7 +960,12 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
 #endif
       if (tid == SHIPPER) bulk_wait_read_all();  // the previous bulk store has read the stage
       named_sync<BAR_DATA, NT>();
+#ifndef UG_FWD_BLOCK_SCAN
+      emit_tile<Pol>(a, ring + js * INBUF, s_t[js], s_pre[js], s_cnt[js],
+                     s_wsum[js][warp] + (v >> 8), v & 0xFFu,
+#else
       emit_tile<Pol>(a, ring + js * INBUF, s_t[js], s_pre[js], s_cnt[js], v >> 8, v & 0xFFu,
+#endif
                      stage, tid, lane);
     };
     while (true) {
@@ -972,6 +1002,32 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
         Pol::template load<false>(st, img, tid, lane, tp, win.n);
         cnt = Pol::template analyze<false>(st, tid, true);
       }
+#ifndef UG_FWD_BLOCK_SCAN
+      // in-warp scan; the warp that completes the tile's (arrivals | sum) word publishes the
+      // aggregate (no CTA barrier between the classification and the publish)
+      uint32_t sc = cnt;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, sc, d);
+        if (lane >= d) sc += y;
+      }
+      const uint32_t excl = sc - cnt;  // in-warp
+      if (lane == 31) {
+        s_wsum[sl][warp] = sc;
+        const uint32_t old = atomicAdd(&s_acc[sl], (1u << 24) | sc);
+        if ((old >> 24) == NT / 32 - 1) {
+          st_relaxed(a.status + t, pack_status(a.epoch, t == 0 ? FLAG_PREFIX : FLAG_AGG,
+                                               (old & 0xFFFFFFu) + sc));
+          s_acc[sl] = 0u;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&mb_agg[sl]);
+      if (tid == PRODUCER) start_tile((i + PF) % RING, tn);
+      // a4 (cold): a flag is resolved inside its warp (every warp's last lane checks the
+      // 3-byte look-ahead), so the warp rescans its own positions
+      if (__any_sync(FULL, Pol::hint(st))) {
+#else
       if (Pol::hint(st)) s_flag[i % 3] = 1;
       if (tid == PRODUCER) {
         // ring slot (i + PF) % RING held tile i - DEFER - 1, emitted last iteration
@@ -989,6 +1045,7 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
         mbar_arrive(&mb_agg[sl]);
       }
       if (s_flag[i % 3]) {  // a4 (cold): straight to the call's minimum
+#endif
 #ifdef UG_TRACE
         if (tid == 0) atomicAdd(&g_dbg[1], 1ull);
         if (Pol::hint(st) && g_dbg[5] == 0) { g_dbg[5] = 1; g_dbg[6] = (unsigned long long)t; g_dbg[7] = tid; }
