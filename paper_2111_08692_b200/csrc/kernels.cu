@@ -807,15 +807,17 @@ __device__ __forceinline__ void emit_tile(const TileArgs &a, const uint8_t *img,
   }
 }
 
-// K2 / K4.  NT data threads + one look-back warp (warp NT/32); up to 4 CTAs per SM.
-//  * Tiles are taken by atomic ticket (issue order keeps the decoupled look-back
-//    deadlock-free) and bulk-loaded (TMA) into a ring of RING input slots, one tile ahead.
-//  * Tile i is classified, block-scanned (the one CTA barrier of the classify stage) and its
-//    aggregate published at once; the look-back warp computes its exclusive prefix P
-//    starting at the ticket (it needs only the predecessors) and publishes P + C when the
-//    aggregate arrives.
-//  * Tile i - 2 - whose prefix had two tiles of time to arrive - is then decoded from its
-//    still-resident input image straight into the stage at its global 16-byte phase and
+// K2 (and K4 in the UG_U16_TILE_SCAN build).  NT data threads + one look-back warp (warp
+// NT/32); two CTAs per SM.
+//  * The producer thread (lane 0 of the last data warp) takes tiles by atomic ticket (issue
+//    order keeps the decoupled look-back deadlock-free) and bulk-loads them (TMA) into a ring
+//    of RING input slots, one tile ahead.
+//  * Tile i is classified; in-warp scans of the thread counts, and the last warp to add its
+//    total publishes the tile aggregate at once (no CTA barrier; UG_FWD_BLOCK_SCAN restores
+//    the block scan); the look-back warp turns the warp totals into offsets, computes the
+//    exclusive prefix P from the predecessors and publishes P + C.
+//  * Tile i - DEFER - whose prefix had DEFER tiles of time to arrive - is then decoded from
+//    its still-resident input image straight into the stage at its global 16-byte phase and
 //    shipped by one TMA bulk store.
 template <class Pol>
 __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const TileArgs a) {
@@ -824,8 +826,8 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
   uint8_t *ring = smem;                                         // RING input tile images
   Out *stage = reinterpret_cast<Out *>(smem + RING * INBUF);   // output stage (global phase)
   __shared__ uint64_t mb_load[RING];  // tile load landed (TMA tx) / no tile (plain arrive)
-  __shared__ uint64_t mb_tick[RING];  // thread 0 -> look-back warp: ticket of slot taken
-  __shared__ uint64_t mb_agg[RING];   // thread 0 -> look-back warp: aggregate of slot
+  __shared__ uint64_t mb_tick[RING];  // producer -> look-back warp: ticket of slot taken
+  __shared__ uint64_t mb_agg[RING];   // data warps -> look-back warp: aggregate of slot
   __shared__ uint64_t mb_pre[RING];   // look-back warp -> data warps: prefix of slot
 #ifndef UG_FWD_BLOCK_SCAN  // warp-level publish (measured: forward -2 to -3 %)
   // warp totals, turned in place into exclusive warp offsets by the look-back warp
@@ -844,7 +846,7 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
   const long long ntiles = (long long)a.ntiles;
   const long long n_units = win.n / Pol::UNIT;
 
-  // Thread 0: publish ticket tn for ring slot `slot` and start loading its tile.
+  // Producer: publish ticket tn for ring slot `slot` and start loading its tile.
   auto start_tile = [&](int slot, long long tn) {
     s_t[slot] = tn;
     mbar_arrive(&mb_tick[slot]);  // the look-back of tile tn can start now
@@ -971,8 +973,7 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
     while (true) {
       const int sl = i % RING;
       // The next ticket: the atomic is issued now and its result used only after this
-      // thread's share of the classification, so its L2 round trip is off the critical path
-      // (every warp waits for warp 0 at the block scan).
+      // thread's share of the classification, so its L2 round trip is off the critical path.
       long long tn = 0;
       if (tid == PRODUCER) tn = (long long)atomicAdd(&a.ctr->ticket, 1u);
 #ifdef UG_TRACE
@@ -1219,7 +1220,7 @@ extern "C" cudaError_t ug_pmode_set_impl(int m) {
 //  * data warps: count only (byte-lane width sums, 4 words per op), an in-warp scan, and the
 //    warp total added to a shared 64-bit (arrivals | sum) word; the warp that completes it
 //    publishes the tile aggregate at once.  No CTA barrier between the load and the publish.
-//  * look-back warp: exclusive prefix (a6) in ticket order, per-warp offsets, push-forward.
+//  * look-back warp: exclusive prefix (a6) in ticket order, per-warp offsets.
 //  * data warps, D16 tiles later: decode + pairing check in one pass (classes computed once,
 //    a7 + a9), stage, TMA bulk store (a8).
 // Against k_transcode<U16Pol> (classify + block scan before the publish) this shortens the
@@ -1294,7 +1295,7 @@ __global__ void __launch_bounds__(T16_THREADS, CTAS_PER_SM) k_transcode16(const 
   uint8_t *ring = smem;
   uint8_t *stage = smem + RING16 * INBUF;
   __shared__ uint64_t mb_load[RING16];  // tile landed (TMA tx) / no tile
-  __shared__ uint64_t mb_tick[RING16];  // thread 0 -> look-back warp: ticket of the slot
+  __shared__ uint64_t mb_tick[RING16];  // producer -> look-back warp: ticket of the slot
   __shared__ uint64_t mb_agg[RING16];   // data warps (one arrival each) -> look-back warp
   __shared__ uint64_t mb_pre[RING16];   // look-back warp -> data warps: prefix known
   __shared__ long long s_t[RING16];
@@ -1309,7 +1310,7 @@ __global__ void __launch_bounds__(T16_THREADS, CTAS_PER_SM) k_transcode16(const 
   const Window &win = a.win;
   const long long ntiles = (long long)a.ntiles;
 
-  auto start_tile = [&](int slot, long long tn) {  // thread 0
+  auto start_tile = [&](int slot, long long tn) {  // producer (thread 0 in the prologue)
     s_t[slot] = tn;
     mbar_arrive(&mb_tick[slot]);
     if (tn < ntiles) {
