@@ -411,7 +411,7 @@ struct U16PolT {
       }
       const uint32_t Hp = fsl(Hprev, c.H, 8), Ln = fsr(c.L, Lnext, 8);
       uint32_t e = (c.H & ~Ln) | (c.L & ~Hp);
-      uint32_t d = u16::wm1(c) + 0x01010101u;  // widths
+      uint32_t d = u16::widths(c);  // widths
       if (!IN) {
         const uint32_t o4 = own4(s, g);
         e &= o4;
@@ -486,7 +486,7 @@ struct U16PolT {
       lprev = c.lo;
       uint32_t O0, O1, O2;
       u16::encode4(c, lp, &O0, &O1, &O2);
-      uint32_t d = u16::wm1(c) + 0x01010101u;
+      uint32_t d = u16::widths(c);
       if (!IN) d &= (own4(s, g) >> 7) * 0xFFu;
       const uint32_t inc = d * 0x01010101u;  // byte j: bytes emitted by words <= j
       const uint32_t a1 = p + prmt(inc, 0u, 0x4440u);
@@ -559,7 +559,7 @@ struct U16PolT {
       const uint32_t lp = fsl(lprev, c.lo, 8);
       uint32_t O0, O1, O2;
       u16::encode4(c, lp, &O0, &O1, &O2);
-      uint32_t d = u16::wm1(c) + 0x01010101u;
+      uint32_t d = u16::widths(c);
       if (!IN) {
         const uint32_t o4 = own4(s, g);
         e &= o4;

@@ -56,11 +56,12 @@ UG_HD Cls4 classes4(uint32_t wa, uint32_t wb) {
   Cls4 c;
   c.lo = prmt(wa, wb, BE ? 0x7531u : 0x6420u);
   c.hi = prmt(wa, wb, BE ? 0x6420u : 0x7531u);
+  // (the byte adds are IMADs: the FMA pipe has room, the ALU pipe is the busy one)
   const uint32_t h7 = c.hi & 0x7F7F7F7Fu;
-  c.ge800 = ((h7 + 0x78787878u) | c.hi) & HI;         // hi >= 8 (no carries: 7-bit adds)
-  c.ge80 = ((h7 + 0x7F7F7F7Fu) | c.hi | c.lo) & HI;    // hi != 0 or lo >= 0x80
+  c.ge800 = (mad(h7, 1u, 0x78787878u) | c.hi) & HI;         // hi >= 8 (7-bit adds)
+  c.ge80 = (mad(h7, 1u, 0x7F7F7F7Fu) | c.hi | c.lo) & HI;    // hi != 0 or lo >= 0x80
   const uint32_t z = (c.hi & 0xF8F8F8F8u) ^ 0xD8D8D8D8u;
-  c.S = ~(((z & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | z) & HI;  // hi in D8..DF
+  c.S = ~(mad(z & 0x7F7F7F7Fu, 1u, 0x7F7F7F7Fu) | z) & HI;  // hi in D8..DF
   const uint32_t b2 = c.hi << 5;                        // bit 2 of hi: DC..DF
   c.L = c.S & b2;
   c.H = c.S & ~b2;
@@ -68,6 +69,10 @@ UG_HD Cls4 classes4(uint32_t wa, uint32_t wb) {
 }
 // width - 1 per byte lane (0..2)
 UG_HD uint32_t wm1(const Cls4 &c) { return (c.ge80 >> 7) + ((c.ge800 & ~c.S) >> 7); }
+// width per byte lane (1..3), both shifts and adds on the FMA pipe (IMAD.HI accumulate)
+UG_HD uint32_t widths(const Cls4 &c) {
+  return mad_hi(c.ge800 & ~c.S, 1u << 25, mad_hi(c.ge80, 1u << 25, 0x01010101u));
+}
 // byte mask (0xFF per lane) from an msb-per-byte mask
 UG_HD uint32_t bmask(uint32_t m) { return prmt(m, 0u, 0xBA98u); }
 
@@ -80,8 +85,8 @@ UG_HD void encode4(const Cls4 &c, uint32_t lp, uint32_t *O0, uint32_t *O1, uint3
   // first byte
   const uint32_t vB = U6 | 0xC0C0C0C0u;
   const uint32_t vC = ((c.hi >> 4) & 0x0F0F0F0Fu) | 0xE0E0E0E0u;
-  const uint32_t cy = (c.lo & (c.lo << 1) & HI) >> 7;           // lo >= 0xC0: h' carries
-  const uint32_t vH = ((c.hi & 0x03030303u) + cy) | 0xF0F0F0F0u;
+  const uint32_t cy = shr_fma<7>(c.lo & (c.lo << 1) & HI);      // lo >= 0xC0: h' carries
+  const uint32_t vH = mad(c.hi & 0x03030303u, 1u, cy) | 0xF0F0F0F0u;
   const uint32_t vL = ((lp << 4) & 0x30303030u) | (U6 & 0x0F0F0F0Fu) | HI;
   const uint32_t mS = bmask(c.S), mH = bmask(c.H);
   const uint32_t mB = bmask(c.ge80 & ~c.ge800), mA = bmask(~c.ge80 & HI);
@@ -90,7 +95,7 @@ UG_HD void encode4(const Cls4 &c, uint32_t lp, uint32_t *O0, uint32_t *O1, uint3
   x = mux(mB, vB, x);
   *O0 = mux(mA, c.lo, x);
   // second byte
-  const uint32_t vH1 = ((((c.lo >> 2) & 0x3F3F3F3Fu) + 0x10101010u) & 0x3F3F3F3Fu) | HI;
+  const uint32_t vH1 = (mad(shr_fma<2>(c.lo) & 0x3F3F3F3Fu, 1u, 0x10101010u) & 0x3F3F3F3Fu) | HI;
   const uint32_t mC = bmask(c.ge800 & ~c.S);
   *O1 = mux(mC, (U6 & 0x3F3F3F3Fu) | HI, mux(mH, vH1, T));
   // third byte
