@@ -128,7 +128,7 @@ int ug_utf8_length_from_utf16le_async(const uint16_t *in, size_t n, uint64_t *d_
 
 /* ------------------------------------------------------------------ UTF-16BE
  * The same operations on big-endian UTF-16: word k of the buffer is the code unit
- * (byte[2k] << 8) | byte[2k + 1] (SPEC.md S:525-529: "utf16be file [0x00,0x41] -> words
+ * (byte[2k] << 8) | byte[2k + 1] (SPEC.md S:525-532: "utf16be file [0x00,0x41] -> words
  * [0x0041]").  Results, positions (in words), capacities and error conventions are exactly
  * those of the LE functions above on the byte-swapped buffer; no BOM handling (a BOM is data).
  * The kernels are the LE kernels with the byte order folded into their low/high byte split

@@ -177,7 +177,7 @@ def utf8_length_from_utf16le(u) -> int:
 
 
 # ---- UTF-16BE ----
-# SPEC.md S:525-529 (load_file): a utf16be buffer holds each code unit high byte first, and
+# SPEC.md S:525-532 (load_file): a utf16be buffer holds each code unit high byte first, and
 # "utf16be file [0x00,0x41] -> words [0x0041]".  So the BE operations are, by definition, the
 # LE operations on the byte-swapped words (the oracle's C codec stays the single source of the
 # codec arithmetic); positions and counts are in words either way.

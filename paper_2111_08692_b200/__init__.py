@@ -191,7 +191,7 @@ def utf8_length_from_utf16le(t_in, n: int | None = None, stream=None) -> int:
 
 
 # --------------------------------------------------------------------------- UTF-16BE
-# Big-endian UTF-16 (SURVEY 8(f) f3; SPEC.md S:525-529): the tensors hold the raw big-endian
+# Big-endian UTF-16 (SURVEY 8(f) f3; SPEC.md S:525-532): the tensors hold the raw big-endian
 # words; results are those of the LE functions on the byte-swapped buffer.
 def utf16be_validate(t_in, n: int | None = None, stream=None) -> Result:
     return _res(lib.utf16be_validate(_ptr(t_in), _units(t_in) if n is None else n,

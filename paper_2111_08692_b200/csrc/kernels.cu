@@ -145,7 +145,7 @@ __device__ __forceinline__ uint32_t bit_range(long long pos0, long long lo, long
   return mb & ~ma;
 }
 
-// BE: UTF-16BE output (SPEC.md S:525-529); only the unit packing differs.
+// BE: UTF-16BE output (SPEC.md S:525-532); only the unit packing differs.
 template <bool BE>
 struct U8PolT {
   using Out = uint16_t;
@@ -332,7 +332,7 @@ using U8PolBE = U8PolT<true>;
 // ============================================================================ UTF-16 policy
 // Positions are words.  Thread `tid` owns tile words [16 tid, 16 tid + 16), two per register.
 
-// BE: UTF-16BE input (SPEC.md S:525-529): the low/high byte split of the classes swaps its
+// BE: UTF-16BE input (SPEC.md S:525-532): the low/high byte split of the classes swaps its
 // selectors (u16::classes4<BE>), the two scalar context words are byte-swapped.
 template <bool BE>
 struct U16PolT {
@@ -610,7 +610,7 @@ struct U16PolT {
     if (from < 0) from = 0;
     unsigned long long c = 0;
     for (long long i = from + lane; i < (long long)e; i += 32)
-      c += u16::width(native(word_at(win, i)), native(word_at(win, i - 1)));
+      c += u16::width(native(word_at(win, i)));
     *wr = base + warp_sum64(c);
   }
 };

@@ -5,7 +5,7 @@
 //    ("During validation, only the possible surrogate pairs require attention").
 //  * Widths in UTF-8 bytes: 1 below 0x80, 2 below 0x800, 2 for each half of a surrogate pair
 //    (the pair's 4 bytes split 2 + 2 so each word emits its own bytes), 3 otherwise; a lone
-//    high gets 2 and a lone low 3.  At most 3 bytes per word on ANY input.
+//    surrogate also gets 2.  At most 3 bytes per word on ANY input.
 //  * Bytes: minimal UTF-8 encoding.  For a pair (h, l) the code point is
 //    0x10000 + ((h & 0x3FF) << 10 | (l & 0x3FF)), so bytes 1-2 depend only on h
 //    (cp >> 10 = 0x40 + (h & 0x3FF)) and bytes 3-4 on l and the low 2 bits of h.
@@ -20,8 +20,10 @@ namespace u16 {
 UG_HD bool is_high(uint32_t u) { return (u & 0xFC00u) == 0xD800u; }
 UG_HD bool is_low(uint32_t u) { return (u & 0xFC00u) == 0xDC00u; }
 
-UG_HD uint32_t width(uint32_t u, uint32_t prev) {
-  const bool two = u < 0x800u || is_high(u) || (is_low(u) && is_high(prev));
+// UTF-8 bytes emitted for word u: the same rule as widths() / len16_word (a surrogate 2, so a
+// pair 4, a lone surrogate 2 as well).  On a valid prefix this is the minimal encoding length.
+UG_HD uint32_t width(uint32_t u) {
+  const bool two = u < 0x800u || (u & 0xF800u) == 0xD800u;
   return 1u + (u >= 0x80u ? 1u : 0u) + (two ? 0u : 1u);
 }
 
@@ -49,7 +51,7 @@ struct Cls4 {
   uint32_t ge80, ge800, S, H;   // u >= 0x80, u >= 0x800, surrogate, high surrogate
   uint32_t L;                   // low surrogate
 };
-// BE: the words are stored big-endian (UTF-16BE, SPEC.md S:525-529): the byte order is folded
+// BE: the words are stored big-endian (UTF-16BE, SPEC.md S:525-532): the byte order is folded
 // into the split by swapping the two selectors, everything after it is unchanged.
 template <bool BE = false>
 UG_HD Cls4 classes4(uint32_t wa, uint32_t wb) {

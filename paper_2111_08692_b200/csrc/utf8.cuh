@@ -128,7 +128,7 @@ UG_HD Carry carry_of(uint32_t x) {
 // every emitting byte.  Units at non-emitting positions are garbage.
 // The class masks are taken in lsb-per-byte form straight from a funnel shift by 8d + 1
 // (d = distance to the lead), so every per-byte constant is one multiply (FMA pipe).
-// BE: units stored big-endian (UTF-16BE output, SPEC.md S:525-529): the two PRMT that pair
+// BE: units stored big-endian (UTF-16BE output, SPEC.md S:525-532): the two PRMT that pair
 // low and high bytes into units take the bytes in the other order - no extra instruction.
 template <bool BE = false>
 UG_HD uint32_t units4(uint32_t x, Carry &c, uint32_t *u01, uint32_t *u23) {

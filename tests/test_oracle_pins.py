@@ -360,7 +360,7 @@ def be_words(b: bytes) -> np.ndarray:
 
 
 def test_utf16be_spec_example():
-    """SPEC.md S:529: utf16be file [0x00,0x41] -> words [0x0041]."""
+    """SPEC.md S:532: utf16be file [0x00,0x41] -> words [0x0041]."""
     u = be_words(bytes([0x00, 0x41]))
     assert list(oracle.byteswap16(u)) == [0x0041]
     r, out = oracle.utf16be_to_utf8(u)
