@@ -1,6 +1,6 @@
 // swar.cuh -- the handful of sm_100a integer primitives the codec arithmetic is written in
 // (PRMT, funnel shifts, POPC, IMAD.HI), each with a bit-exact host definition so the same
-// per-thread code (utf8.cuh / utf16.cuh) can be compiled for the host by tools/emu_*.cpp and
+// per-thread code (utf8.cuh / utf16.cuh) can be compiled for the host by tests/emu/kernel_math_emu.cpp and
 // checked against the oracle without a GPU.  Nothing here is method arithmetic.
 #pragma once
 #include <cstdint>

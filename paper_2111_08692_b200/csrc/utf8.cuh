@@ -1,4 +1,4 @@
-// utf8.cuh -- UTF-8 arithmetic of the hot path (host-compilable: tools/emu_u8.cpp).
+// utf8.cuh -- UTF-8 arithmetic of the hot path (host-compilable: tests/emu/kernel_math_emu.cpp).
 //
 // Two representations, each used where it is cheapest (D3/D4):
 //

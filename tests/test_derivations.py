@@ -4,11 +4,15 @@ the CUDA kernels (which implement the same mathematics in their own code):
 
 (i)  local first-error predicate: e = min{i : A(i) or B(i)}, each term reading only bytes
      [i-3, i+3] -- what makes the first error exact across tiles and shards;
-(ii) the classifier: nibble-table classes for the six value rules (PAPER.md:80-82 and the
-     C0/C1 and F5..FF leads) AND-ed from three 16-entry tables keyed by hi(prev1), lo(prev1),
-     hi(cur), plus bit logic for the structural rules and the continuation-count check.  It
-     flags iff the input is invalid, and the first flagged position r obeys e <= r <= e + 3
-     when positions n, n+1, n+2 are classified against 0x00 padding;
+(ii) HISTORICAL -- the paper's (Keiser-Lemire) nibble-table classifier that the first GPU
+     kernels ran (round 1; replaced by the bit-plane classifier, D3): classes for
+     the six value rules (PAPER.md:80-82 and the C0/C1 and F5..FF leads) AND-ed from three
+     16-entry tables keyed by hi(prev1), lo(prev1), hi(cur), plus bit logic for the structural
+     rules and the continuation-count check.  It flags iff the input is invalid, and the first
+     flagged position r obeys e <= r <= e + 3 when positions n, n+1, n+2 are classified
+     against 0x00 padding.  Kept as the derivation of the flag-window argument; the classifier
+     the kernels RUN is pinned by tests/test_kernel_math_cpu.py (the product's own utf8.cuh
+     compiled for the host, in the kernels' warp layout);
 (iii) the UTF-16 pairing predicate.
 """
 import itertools
