@@ -112,6 +112,13 @@ uint64_t utf16_length_from_utf8(const uint8_t *in, size_t n, void *stream);
  * 1 (< 0x80), 2 (< 0x800), 2 (surrogate), 3 (other); exact on valid input. */
 uint64_t utf8_length_from_utf16le(const uint16_t *in, size_t n, void *stream);
 
+/* The two length-from functions with an error channel: return UG_OK and *len, or UG_ERR_ARG
+ * (NULL `len`, NULL `in` with n > 0, odd UTF-16 pointer, n > 2^62) / UG_ERR_CUDA with
+ * *len = 0.  (The plain forms above return 0 in those cases, indistinguishable from an empty
+ * count.)  Synchronous. */
+int ug_utf16_length_from_utf8_ex(const uint8_t *in, size_t n, uint64_t *len, void *stream);
+int ug_utf8_length_from_utf16le_ex(const uint16_t *in, size_t n, uint64_t *len, void *stream);
+
 /* ------------------------------------------------------------------ asynchronous, device
  * Same operations; the result is written by the GPU into *d_result (a device pointer, or
  * pinned host memory mapped into the device).  Return UG_OK once enqueued, or UG_ERR_ARG /
@@ -144,6 +151,7 @@ int ug_utf8_to_utf16be_async(const uint8_t *in, size_t n, uint16_t *out, size_t 
                              ug_result *d_result, void *stream);
 int ug_utf16be_to_utf8_async(const uint16_t *in, size_t n, uint8_t *out, size_t out_cap,
                              ug_result *d_result, void *stream);
+int ug_utf8_length_from_utf16be_ex(const uint16_t *in, size_t n, uint64_t *len, void *stream);
 int ug_utf8_length_from_utf16be_async(const uint16_t *in, size_t n, uint64_t *d_len,
                                       void *stream);
 
@@ -226,10 +234,13 @@ int ug_utf16be_validate_shard_async(const uint16_t *in, size_t n, size_t halo_be
  * (DESIGN.md f2): chunk i is copied in on one copy stream, transcoded as a shard (the sharded
  * kernel is exact at any cut, D2) on `stream`, and its output copied out on a second
  * copy stream as soon as its 32-byte record has fixed its output offset, so host->device
- * copies, kernels and device->host copies overlap.  Uses library-owned device staging (input
- * + worst-case output) per (device, stream), grown on demand; synchronous (returns when the
- * output is in out_host).  out_host[0..written) is exact; nothing at or beyond
- * out_host[out_cap] is written. */
+ * copies, kernels and device->host copies overlap.  Chunks stream through 4 library-owned
+ * device staging slots per (device, stream) (a chunk with its halos + its worst-case output
+ * each), reused round robin: device memory is O(chunk), not O(n), so inputs larger than HBM
+ * stream through.  Synchronous (returns when the output is in out_host).
+ * out_host[0..written) is exact; nothing at or beyond out_host[out_cap] is written.
+ * Thread safety (all entry points): calls on one (device, stream) serialise on its workspace
+ * mutex, a synchronous call holding it from its launch through its result read-back. */
 ug_result utf8_to_utf16le_host(const uint8_t *in_host, size_t n, uint16_t *out_host,
                                size_t out_cap, void *stream);
 ug_result utf16le_to_utf8_host(const uint16_t *in_host, size_t n, uint8_t *out_host,
@@ -252,6 +263,14 @@ const char *ug_error_name(int err);
 uint64_t ug_launch_count(void);
 /* Free the workspaces of the current device (all streams). */
 void ug_release_workspaces(void);
+/* Input bytes per tile of the transcoding kernels (16 KiB in this build): tile t of a call
+ * covers input bytes [t * T - lead, (t + 1) * T - lead) where lead = (input address mod 16).
+ * Exposed so tests can place inputs across real tile edges. */
+size_t ug_tile_bytes(void);
+/* Device bytes currently held by the library's workspace for (current device, stream): tile
+ * status words, counters, result slots, and the host pipeline's staging slots (bounded:
+ * 4 slots of one chunk each, whatever n is) and per-chunk records.  0 if none exists. */
+size_t ug_workspace_bytes(void *stream);
 int ug_abi_version(void);
 
 #ifdef __cplusplus

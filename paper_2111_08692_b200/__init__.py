@@ -103,6 +103,11 @@ def _load():
         "ug_launch_count": ([], U64),
         "ug_release_workspaces": ([], None),
         "ug_abi_version": ([], I),
+        "ug_tile_bytes": ([], S),
+        "ug_workspace_bytes": ([P], S),
+        "ug_utf16_length_from_utf8_ex": ([P, S, P, P], I),
+        "ug_utf8_length_from_utf16le_ex": ([P, S, P, P], I),
+        "ug_utf8_length_from_utf16be_ex": ([P, S, P, P], I),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -152,6 +157,16 @@ def launch_count() -> int:
     return int(lib.ug_launch_count())
 
 
+def workspace_bytes(stream=None) -> int:
+    """Device bytes the library's workspace holds for (current device, stream)."""
+    return int(lib.ug_workspace_bytes(_stream(stream)))
+
+
+def tile_bytes() -> int:
+    """Input bytes per tile of the transcoding kernels (tiles start at 16-byte addresses)."""
+    return int(lib.ug_tile_bytes())
+
+
 # --------------------------------------------------------------------------- synchronous
 def utf8_validate(t_in, n: int | None = None, stream=None) -> Result:
     """Validate UTF-8 bytes (CUDA uint8 tensor).  PAPER.md:76-83."""
@@ -180,14 +195,22 @@ def utf16le_to_utf8(t_in, t_out, n: int | None = None, out_cap: int | None = Non
                                     _stream(stream)))
 
 
+def _len_ex(fn, t_in, n, stream, what):
+    out = ctypes.c_uint64(0)
+    _check(fn(_ptr(t_in), _units(t_in) if n is None else n, ctypes.byref(out), _stream(stream)),
+           what)
+    return int(out.value)
+
+
 def utf16_length_from_utf8(t_in, n: int | None = None, stream=None) -> int:
-    return int(lib.utf16_length_from_utf8(_ptr(t_in), _units(t_in) if n is None else n,
-                                          _stream(stream)))
+    """UTF-16 units of the UTF-8 input (any input; R15).  Raises on API / CUDA
+    failure (through ug_utf16_length_from_utf8_ex's error channel)."""
+    return _len_ex(lib.ug_utf16_length_from_utf8_ex, t_in, n, stream, "utf16_length_from_utf8")
 
 
 def utf8_length_from_utf16le(t_in, n: int | None = None, stream=None) -> int:
-    return int(lib.utf8_length_from_utf16le(_ptr(t_in), _units(t_in) if n is None else n,
-                                            _stream(stream)))
+    return _len_ex(lib.ug_utf8_length_from_utf16le_ex, t_in, n, stream,
+                   "utf8_length_from_utf16le")
 
 
 # --------------------------------------------------------------------------- UTF-16BE
@@ -213,8 +236,8 @@ def utf16be_to_utf8(t_in, t_out, n: int | None = None, out_cap: int | None = Non
 
 
 def utf8_length_from_utf16be(t_in, n: int | None = None, stream=None) -> int:
-    return int(lib.utf8_length_from_utf16be(_ptr(t_in), _units(t_in) if n is None else n,
-                                            _stream(stream)))
+    return _len_ex(lib.ug_utf8_length_from_utf16be_ex, t_in, n, stream,
+                   "utf8_length_from_utf16be")
 
 
 def utf16be_validate_async(t_in, d_result, n=None, stream=None, result_off=0):
@@ -474,19 +497,67 @@ def _validate(t, es, host, what, fname):
         raise ValueError(f"{fname}: {what} must be a CUDA tensor (no CPU fallback)")
 
 
+_SLOT_BYTES = {"d_result": ("result_off", 24), "d_len": ("len_off", 8), "d_rec": ("rec_off", 32)}
+
+
 def _checked(fname, fn):
+    """Wrap a public entry point: element sizes, contiguity and placement of the tensors; the
+    unit count n (with a shard's element offset) and out_cap within the tensors' extents; the
+    device result / length / record slots inside CUDA tensors; and every CUDA tensor on ONE
+    device, the call then made with that device current (the library picks its workspace and
+    torch's stream from the current device)."""
     import functools
+    import inspect
     in_es, out_es, host = _expect(fname)
-    names = fn.__code__.co_varnames[:fn.__code__.co_argcount]
-    roles = [(i, nm, in_es if nm.startswith("t_in") else out_es)
-             for i, nm in enumerate(names) if nm in ("t_in", "t_out", "t_in_host", "t_out_host")]
+    sig = inspect.signature(fn)
+    roles = {nm: (in_es if nm.startswith("t_in") else out_es)
+             for nm in sig.parameters if nm in ("t_in", "t_out", "t_in_host", "t_out_host")}
 
     @functools.wraps(fn)
     def w(*args, **kw):
-        for i, nm, es in roles:
-            t = args[i] if i < len(args) else kw.get(nm)
+        import torch
+        b = sig.bind(*args, **kw)
+        b.apply_defaults()
+        a = b.arguments
+        devs = set()
+        for nm, es in roles.items():
+            t = a.get(nm)
             if t is not None and es is not None:
                 _validate(t, es, host, nm, fname)
+                if t.is_cuda:
+                    devs.add(t.device.index)
+        t_in = a.get("t_in", a.get("t_in_host"))
+        t_out = a.get("t_out", a.get("t_out_host"))
+        off = a.get("offset") or 0
+        if a.get("n") is not None and t_in is not None:
+            if a["n"] < 0 or off < 0 or off + a["n"] > t_in.numel():
+                raise ValueError(f"{fname}: offset {off} + n {a['n']} exceeds the input "
+                                 f"tensor's {t_in.numel()} elements")
+        if "halo_before" in a and t_in is not None and \
+                (off - a["halo_before"] < 0 or
+                 off + (a.get("n") or 0) + a["halo_after"] > t_in.numel()):
+            raise ValueError(f"{fname}: the halos reach outside the input tensor")
+        if a.get("out_cap") is not None and t_out is not None and \
+                not (0 <= a["out_cap"] <= t_out.numel()):
+            raise ValueError(f"{fname}: out_cap {a['out_cap']} exceeds the output tensor's "
+                             f"{t_out.numel()} elements")
+        for nm, (offnm, size) in _SLOT_BYTES.items():
+            t = a.get(nm)
+            if nm in a and t is None:
+                raise ValueError(f"{fname}: {nm} is required")
+            if t is None:
+                continue
+            if not isinstance(t, torch.Tensor) or not t.is_cuda or not t.is_contiguous():
+                raise ValueError(f"{fname}: {nm} must be a contiguous CUDA tensor")
+            if (a.get(offnm) or 0) + size > t.numel() * t.element_size():
+                raise ValueError(f"{fname}: {nm} holds no {size}-byte slot at byte offset "
+                                 f"{a.get(offnm) or 0}")
+            devs.add(t.device.index)
+        if len(devs) > 1:
+            raise ValueError(f"{fname}: tensors on several devices {sorted(devs)}")
+        if devs and devs != {torch.cuda.current_device()}:
+            with torch.cuda.device(devs.pop()):
+                return fn(*args, **kw)
         return fn(*args, **kw)
     return w
 

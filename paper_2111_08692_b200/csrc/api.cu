@@ -24,6 +24,7 @@ namespace {
 std::atomic<uint64_t> g_launches{0};
 constexpr size_t HOST_CHUNK_DEFAULT = 32ull << 20;  // input units per pipelined host chunk
 std::atomic<size_t> g_host_chunk{HOST_CHUNK_DEFAULT};
+constexpr int HOST_SLOTS = 4;  // staging slots of the host pipeline (chunks in flight)
 constexpr unsigned long long MAX_N = (1ull << 38) - 1;  // status words carry 38-bit values
 
 struct Workspace {
@@ -45,7 +46,7 @@ struct Workspace {
   // host-buffer pipeline (run_host): copy streams, per-chunk events and shard records
   cudaStream_t h2d = nullptr, d2h = nullptr;
   cudaEvent_t ev_start = nullptr;
-  std::vector<cudaEvent_t> ev_in, ev_done;
+  std::vector<cudaEvent_t> ev_in, ev_done, ev_free;  // per staging slot
   RecordDev *d_recs = nullptr;
   RecordDev *h_recs = nullptr;  // pinned
   size_t rec_cap = 0;
@@ -160,30 +161,16 @@ int check_tile_args(Op op, const void *in, unsigned long long n, const void *out
   return UG_OK;
 }
 
-// Enqueue one tile kernel.  Units: n / halos in code units of the input encoding.
-int enqueue_tile(Op op, const void *in, unsigned long long n, unsigned long long hb,
-                 unsigned long long ha, unsigned long long global_off, void *out,
-                 unsigned long long out_cap, ResultDev *d_result, RecordDev *d_rec,
-                 cudaStream_t s) {
+// Enqueue one tile kernel on workspace w, whose mutex the CALLER holds (so a synchronous
+// call keeps it from its launch through its result read-back: two host threads sharing a
+// stream, e.g. torch's legacy default stream, cannot read each other's result slot).
+// Units: n / halos in code units of the input encoding.
+int enqueue_tile_ws(Workspace *w, DeviceInfo *di, Op op, const void *in, unsigned long long n,
+                    unsigned long long hb, unsigned long long ha, unsigned long long global_off,
+                    void *out, unsigned long long out_cap, ResultDev *d_result, RecordDev *d_rec,
+                    cudaStream_t s) {
   const bool u16in = op_u16_input(op);
   const unsigned long long us = u16in ? 2 : 1;
-  const int rc = check_tile_args(op, in, n, out, out_cap);
-  if (rc != UG_OK) return rc;
-  if (n == 0) {
-    if (d_result && cudaMemsetAsync(d_result, 0, sizeof(ResultDev), s) != cudaSuccess)
-      return UG_ERR_CUDA;
-    if (d_rec) {  // {count 0, first_err NONE, written 0, kind OK}
-      if (cudaMemsetAsync(d_rec, 0, sizeof(RecordDev), s) != cudaSuccess ||
-          cudaMemsetAsync(&d_rec->first_err, 0xFF, sizeof(d_rec->first_err), s) != cudaSuccess)
-        return UG_ERR_CUDA;
-    }
-    return UG_OK;
-  }
-  Workspace *w;
-  if (get_ws(s, &w) != cudaSuccess) return UG_ERR_CUDA;
-  DeviceInfo *di;
-  if (device_info(w->device, &di) != cudaSuccess) return UG_ERR_CUDA;
-  std::lock_guard<std::mutex> lk(w->mu);
   TileArgs a;
   std::memset(&a, 0, sizeof(a));
   a.win = make_window(in, n * us, hb * us, ha * us);
@@ -206,6 +193,34 @@ int enqueue_tile(Op op, const void *in, unsigned long long n, unsigned long long
   return UG_OK;
 }
 
+// n = 0: the empty result / record without a launch.
+int enqueue_empty(ResultDev *d_result, RecordDev *d_rec, cudaStream_t s) {
+  if (d_result && cudaMemsetAsync(d_result, 0, sizeof(ResultDev), s) != cudaSuccess)
+    return UG_ERR_CUDA;
+  if (d_rec) {  // {count 0, first_err NONE, written 0, kind OK}
+    if (cudaMemsetAsync(d_rec, 0, sizeof(RecordDev), s) != cudaSuccess ||
+        cudaMemsetAsync(&d_rec->first_err, 0xFF, sizeof(d_rec->first_err), s) != cudaSuccess)
+      return UG_ERR_CUDA;
+  }
+  return UG_OK;
+}
+
+// The asynchronous entry points: argument checks, workspace, one launch under its mutex.
+int enqueue_tile(Op op, const void *in, unsigned long long n, unsigned long long hb,
+                 unsigned long long ha, unsigned long long global_off, void *out,
+                 unsigned long long out_cap, ResultDev *d_result, RecordDev *d_rec,
+                 cudaStream_t s) {
+  const int rc = check_tile_args(op, in, n, out, out_cap);
+  if (rc != UG_OK) return rc;
+  if (n == 0) return enqueue_empty(d_result, d_rec, s);
+  Workspace *w;
+  if (get_ws(s, &w) != cudaSuccess) return UG_ERR_CUDA;
+  DeviceInfo *di;
+  if (device_info(w->device, &di) != cudaSuccess) return UG_ERR_CUDA;
+  std::lock_guard<std::mutex> lk(w->mu);
+  return enqueue_tile_ws(w, di, op, in, n, hb, ha, global_off, out, out_cap, d_result, d_rec, s);
+}
+
 ug_result make_result(int err, uint64_t pos, uint64_t wr) {
   ug_result r;
   r.error = err;
@@ -215,7 +230,8 @@ ug_result make_result(int err, uint64_t pos, uint64_t wr) {
   return r;
 }
 
-// Run an async tile op into the workspace's result slot and wait for it.
+// Run a tile op into the workspace's result slot and wait for it; the workspace mutex is held
+// from the launch through the read-back.
 ug_result run_sync(Op op, const void *in, unsigned long long n, void *out,
                    unsigned long long out_cap, cudaStream_t s) {
   const int arc = check_tile_args(op, in, n, out, out_cap);
@@ -223,9 +239,11 @@ ug_result run_sync(Op op, const void *in, unsigned long long n, void *out,
   if (n == 0) return make_result(UG_OK, 0, 0);
   Workspace *w;
   if (get_ws(s, &w) != cudaSuccess) return make_result(UG_ERR_CUDA, 0, 0);
-  int rc = enqueue_tile(op, in, n, 0, 0, 0, out, out_cap, w->d_res, nullptr, s);
-  if (rc != UG_OK) return make_result(rc, 0, 0);
+  DeviceInfo *di;
+  if (device_info(w->device, &di) != cudaSuccess) return make_result(UG_ERR_CUDA, 0, 0);
   std::lock_guard<std::mutex> lk(w->mu);
+  int rc = enqueue_tile_ws(w, di, op, in, n, 0, 0, 0, out, out_cap, w->d_res, nullptr, s);
+  if (rc != UG_OK) return make_result(rc, 0, 0);
   if (cudaMemcpyAsync(w->h_res, w->d_res, sizeof(ResultDev), cudaMemcpyDeviceToHost, s) !=
           cudaSuccess ||
       cudaStreamSynchronize(s) != cudaSuccess)
@@ -235,19 +253,16 @@ ug_result run_sync(Op op, const void *in, unsigned long long n, void *out,
   return r;
 }
 
-int enqueue_len(bool u16in, const void *in, unsigned long long n, unsigned long long *d_len,
-                cudaStream_t s, bool be = false) {
-  if (d_len == nullptr) return UG_ERR_ARG;
+int check_len_args(bool u16in, const void *in, unsigned long long n) {
   if (n > 0 && in == nullptr) return UG_ERR_ARG;
   if (u16in && ((uintptr_t)in & 1u)) return UG_ERR_ARG;
   if (n > (1ull << 62)) return UG_ERR_ARG;  // byte counts must not overflow
-  if (n == 0) return cudaMemsetAsync(d_len, 0, sizeof(*d_len), s) == cudaSuccess ? UG_OK
-                                                                                 : UG_ERR_CUDA;
-  Workspace *w;
-  if (get_ws(s, &w) != cudaSuccess) return UG_ERR_CUDA;
-  DeviceInfo *di;
-  if (device_info(w->device, &di) != cudaSuccess) return UG_ERR_CUDA;
-  std::lock_guard<std::mutex> lk(w->mu);
+  return UG_OK;
+}
+
+// Enqueue a length reduction into d_len on workspace w (caller holds w->mu).
+int enqueue_len_ws(Workspace *w, DeviceInfo *di, bool u16in, const void *in,
+                   unsigned long long n, unsigned long long *d_len, cudaStream_t s, bool be) {
   unsigned long long per_block = (unsigned long long)LNT * 16 * 4;  // bytes per block pass
   unsigned long long bytes = n * (u16in ? 2 : 1);
   unsigned long long want = (bytes + per_block - 1) / per_block;
@@ -260,18 +275,42 @@ int enqueue_len(bool u16in, const void *in, unsigned long long n, unsigned long 
   return UG_OK;
 }
 
-uint64_t run_len(bool u16in, const void *in, unsigned long long n, cudaStream_t s,
-                 bool be = false) {
-  if (n == 0) return 0;
+int enqueue_len(bool u16in, const void *in, unsigned long long n, unsigned long long *d_len,
+                cudaStream_t s, bool be = false) {
+  if (d_len == nullptr) return UG_ERR_ARG;
+  const int rc = check_len_args(u16in, in, n);
+  if (rc != UG_OK) return rc;
+  if (n == 0) return cudaMemsetAsync(d_len, 0, sizeof(*d_len), s) == cudaSuccess ? UG_OK
+                                                                                 : UG_ERR_CUDA;
   Workspace *w;
-  if (get_ws(s, &w) != cudaSuccess) return 0;
-  if (enqueue_len(u16in, in, n, w->d_len, s, be) != UG_OK) return 0;
+  if (get_ws(s, &w) != cudaSuccess) return UG_ERR_CUDA;
+  DeviceInfo *di;
+  if (device_info(w->device, &di) != cudaSuccess) return UG_ERR_CUDA;
   std::lock_guard<std::mutex> lk(w->mu);
+  return enqueue_len_ws(w, di, u16in, in, n, d_len, s, be);
+}
+
+// Synchronous length: UG_OK and *len, or an error code (UG_ERR_ARG / UG_ERR_CUDA) and *len = 0.
+int run_len(bool u16in, const void *in, unsigned long long n, cudaStream_t s, uint64_t *len,
+            bool be = false) {
+  if (len) *len = 0;
+  if (len == nullptr) return UG_ERR_ARG;
+  const int rc = check_len_args(u16in, in, n);
+  if (rc != UG_OK) return rc;
+  if (n == 0) return UG_OK;
+  Workspace *w;
+  if (get_ws(s, &w) != cudaSuccess) return UG_ERR_CUDA;
+  DeviceInfo *di;
+  if (device_info(w->device, &di) != cudaSuccess) return UG_ERR_CUDA;
+  std::lock_guard<std::mutex> lk(w->mu);
+  const int e = enqueue_len_ws(w, di, u16in, in, n, w->d_len, s, be);
+  if (e != UG_OK) return e;
   if (cudaMemcpyAsync(w->h_len, w->d_len, sizeof(*w->h_len), cudaMemcpyDeviceToHost, s) !=
           cudaSuccess ||
       cudaStreamSynchronize(s) != cudaSuccess)
-    return 0;
-  return *w->h_len;
+    return UG_ERR_CUDA;
+  *len = *w->h_len;
+  return UG_OK;
 }
 
 cudaError_t ensure_staging(Workspace *w, size_t in_bytes, size_t out_bytes) {
@@ -299,8 +338,9 @@ cudaError_t ensure_staging(Workspace *w, size_t in_bytes, size_t out_bytes) {
   return cudaSuccess;
 }
 
-// Per-chunk resources of the host pipeline: two copy streams, an input-landed and a
-// kernel-done event per chunk, one shard record per chunk (device + pinned copy).
+// Per-slot resources of the host pipeline (HOST_SLOTS staging slots, reused round robin): two
+// copy streams, input-landed / kernel-done / output-drained events per slot, and one shard
+// record per chunk (device + pinned copy; 32 B each).
 cudaError_t ensure_pipeline(Workspace *w, size_t nchunks) {
   cudaError_t e;
   if (!w->h2d) {
@@ -308,13 +348,14 @@ cudaError_t ensure_pipeline(Workspace *w, size_t nchunks) {
     if ((e = cudaStreamCreateWithFlags(&w->d2h, cudaStreamNonBlocking)) != cudaSuccess) return e;
     if ((e = cudaEventCreateWithFlags(&w->ev_start, cudaEventDisableTiming)) != cudaSuccess)
       return e;
-  }
-  while (w->ev_in.size() < nchunks) {
-    cudaEvent_t a, b;
-    if ((e = cudaEventCreateWithFlags(&a, cudaEventDisableTiming)) != cudaSuccess) return e;
-    if ((e = cudaEventCreateWithFlags(&b, cudaEventDisableTiming)) != cudaSuccess) return e;
-    w->ev_in.push_back(a);
-    w->ev_done.push_back(b);
+    for (int k = 0; k < HOST_SLOTS; k++) {
+      cudaEvent_t ev[3];
+      for (auto &x : ev)
+        if ((e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming)) != cudaSuccess) return e;
+      w->ev_in.push_back(ev[0]);
+      w->ev_done.push_back(ev[1]);
+      w->ev_free.push_back(ev[2]);
+    }
   }
   if (nchunks > w->rec_cap) {
     cudaFree(w->d_recs);
@@ -329,16 +370,20 @@ cudaError_t ensure_pipeline(Workspace *w, size_t nchunks) {
   return cudaSuccess;
 }
 
-// Host-buffer transcode as a three-stage pipeline over chunks of the input (DESIGN.md f2):
-//   h2d stream:  copy chunk i into the device staging input (all chunks enqueued up front);
-//   `s`:         once chunks i and i+1 have landed (i+1 holds the after-halo), the fused kernel
-//                transcodes chunk i as a shard (exact at any cut, D2) into the
-//                staging output at an upper-bound offset, and its 32-byte record is copied to
-//                pinned memory;
+// Host-buffer transcode as a pipeline over chunks of the input cut at character starts
+// (DESIGN.md f2), streamed through HOST_SLOTS fixed staging slots, so device memory is
+// O(chunk), not O(n), and inputs larger than HBM stream through:
+//   h2d stream:  copy chunk i WITH its halos ([lo - 3, hi + 3) bytes / [lo - 1, hi + 1) words,
+//                clipped at the ends) into slot i % HOST_SLOTS, once that slot's previous
+//                chunk has been copied out;
+//   `s`:         the fused kernel transcodes chunk i as a shard (exact at any cut, D2)
+//                into the slot's output, and its 32-byte record is copied to pinned memory;
 //   d2h stream:  the host waits for record i, which fixes chunk i's output offset (the prefix
-//                of the earlier chunks' counts), and enqueues the copy of its output units.
-// Copies in both directions and the kernels overlap; the result is combined from the records
-// exactly as the unsharded kernel states it (first error, written, output too small).
+//                of the earlier chunks' counts), and enqueues the copy of its output units;
+//                then the slot is refilled with chunk i + HOST_SLOTS.
+// Copies in both directions and the kernels overlap (HOST_SLOTS - 1 chunks ahead of the host);
+// the result is combined from the records exactly as the unsharded kernel states it (first
+// error, written, output too small).  The workspace mutex is held for the whole call.
 ug_result run_host(Op op, const void *in_host, unsigned long long n, void *out_host,
                    unsigned long long out_cap, cudaStream_t s) {
   const bool u16in = op_u16_input(op);
@@ -352,6 +397,8 @@ ug_result run_host(Op op, const void *in_host, unsigned long long n, void *out_h
     return make_result(UG_ERR_ARG, 0, 0);
   Workspace *w;
   if (get_ws(s, &w) != cudaSuccess) return make_result(UG_ERR_CUDA, 0, 0);
+  DeviceInfo *di;
+  if (device_info(w->device, &di) != cudaSuccess) return make_result(UG_ERR_CUDA, 0, 0);
   // chunk cuts at character starts (the kernel is exact at any cut; this keeps chunks whole)
   const unsigned long long C = g_host_chunk.load() ? g_host_chunk.load() : HOST_CHUNK_DEFAULT;
   std::vector<unsigned long long> cut;
@@ -365,44 +412,53 @@ ug_result run_host(Op op, const void *in_host, unsigned long long n, void *out_h
   }
   cut.push_back(n);
   const size_t nch = cut.size() - 1;
-  {
-    std::lock_guard<std::mutex> lk(w->mu);
-    if (ensure_staging(w, n * ius, n * ub * ous) != cudaSuccess ||
-        ensure_pipeline(w, nch) != cudaSuccess)
-      return make_result(UG_ERR_CUDA, 0, 0);
-  }
+  unsigned long long maxlen = 0;
+  for (size_t i = 0; i < nch; i++)
+    if (cut[i + 1] - cut[i] > maxlen) maxlen = cut[i + 1] - cut[i];
+  // one slot: a chunk plus both halos (input), its worst-case output; 16-byte strides
+  const size_t in_slot = ((maxlen + 2 * halo) * ius + 15) & ~(size_t)15;
+  const size_t out_slot = (maxlen * ub * ous + 15) & ~(size_t)15;
+  const int slots = (int)(nch < (size_t)HOST_SLOTS ? nch : (size_t)HOST_SLOTS);
+  std::lock_guard<std::mutex> lk(w->mu);
+  if (ensure_staging(w, slots * in_slot, slots * out_slot) != cudaSuccess ||
+      ensure_pipeline(w, nch) != cudaSuccess)
+    return make_result(UG_ERR_CUDA, 0, 0);
   const uint8_t *hin = (const uint8_t *)in_host;
   uint8_t *din = (uint8_t *)w->d_in, *dout = (uint8_t *)w->d_out;
-  // stage 1: all input copies, ordered after earlier work on the caller's stream
+  // copy chunk i with its halos into slot i % slots and launch its shard kernel
+  auto stage_chunk = [&](size_t i) -> int {
+    const int k = (int)(i % slots);
+    const unsigned long long lo = cut[i], hi = cut[i + 1];
+    const unsigned long long hb = lo < halo ? lo : halo, ha = n - hi < halo ? n - hi : halo;
+    uint8_t *sin = din + k * in_slot, *sout = dout + k * out_slot;
+    if (cudaMemcpyAsync(sin, hin + (lo - hb) * ius, (hi - lo + hb + ha) * ius,
+                        cudaMemcpyHostToDevice, w->h2d) != cudaSuccess ||
+        cudaEventRecord(w->ev_in[k], w->h2d) != cudaSuccess ||
+        cudaStreamWaitEvent(s, w->ev_in[k], 0) != cudaSuccess)
+      return UG_ERR_CUDA;
+    int rc = enqueue_tile_ws(w, di, op, sin + hb * ius, hi - lo, hb, ha, lo, sout,
+                             (hi - lo) * ub, nullptr, w->d_recs + i, s);
+    if (rc != UG_OK) return rc;
+    if (cudaMemcpyAsync(w->h_recs + i, w->d_recs + i, sizeof(RecordDev), cudaMemcpyDeviceToHost,
+                        s) != cudaSuccess ||
+        cudaEventRecord(w->ev_done[k], s) != cudaSuccess)
+      return UG_ERR_CUDA;
+    return UG_OK;
+  };
+  // the input copies are ordered after earlier work on the caller's stream
   if (cudaEventRecord(w->ev_start, s) != cudaSuccess ||
       cudaStreamWaitEvent(w->h2d, w->ev_start, 0) != cudaSuccess)
     return make_result(UG_ERR_CUDA, 0, 0);
-  for (size_t i = 0; i < nch; i++) {
-    if (cudaMemcpyAsync(din + cut[i] * ius, hin + cut[i] * ius, (cut[i + 1] - cut[i]) * ius,
-                        cudaMemcpyHostToDevice, w->h2d) != cudaSuccess ||
-        cudaEventRecord(w->ev_in[i], w->h2d) != cudaSuccess)
-      return make_result(UG_ERR_CUDA, 0, 0);
-  }
-  // stage 2: one shard kernel per chunk + its record to pinned memory
-  for (size_t i = 0; i < nch; i++) {
-    const unsigned long long lo = cut[i], hi = cut[i + 1];
-    const unsigned long long hb = lo < halo ? lo : halo, ha = n - hi < halo ? n - hi : halo;
-    if (cudaStreamWaitEvent(s, w->ev_in[i + 1 < nch ? i + 1 : i], 0) != cudaSuccess)
-      return make_result(UG_ERR_CUDA, 0, 0);
-    int rc = enqueue_tile(op, din + lo * ius, hi - lo, hb, ha, lo, dout + lo * ub * ous,
-                          (hi - lo) * ub, nullptr, w->d_recs + i, s);
-    if (rc != UG_OK) return make_result(rc, 0, 0);
-    if (cudaMemcpyAsync(w->h_recs + i, w->d_recs + i, sizeof(RecordDev), cudaMemcpyDeviceToHost,
-                        s) != cudaSuccess ||
-        cudaEventRecord(w->ev_done[i], s) != cudaSuccess)
-      return make_result(UG_ERR_CUDA, 0, 0);
-  }
-  // stage 3: as each record lands, place the chunk's output
+  int rc = UG_OK;
+  for (size_t i = 0; i < (size_t)slots && rc == UG_OK; i++) rc = stage_chunk(i);
+  if (rc != UG_OK) return make_result(rc, 0, 0);
+  // as each record lands: place the chunk's output, then refill its slot
   unsigned long long prefix = 0, e = NONE, wr = 0;
   int kind = 0;
   bool fits = true, failed = false;
   for (size_t i = 0; i < nch && !failed; i++) {
-    if (cudaEventSynchronize(w->ev_done[i]) != cudaSuccess) {
+    const int k = (int)(i % slots);
+    if (cudaEventSynchronize(w->ev_done[k]) != cudaSuccess) {
       failed = true;
       break;
     }
@@ -410,9 +466,9 @@ ug_result run_host(Op op, const void *in_host, unsigned long long n, void *out_h
     const unsigned long long units = r.first_err == NONE ? r.count : r.written;
     if (fits && prefix + units > out_cap) fits = false;
     if (fits && units) {
-      if (cudaStreamWaitEvent(w->d2h, w->ev_done[i], 0) != cudaSuccess ||
-          cudaMemcpyAsync((uint8_t *)out_host + prefix * ous, dout + cut[i] * ub * ous,
-                          units * ous, cudaMemcpyDeviceToHost, w->d2h) != cudaSuccess) {
+      if (cudaStreamWaitEvent(w->d2h, w->ev_done[k], 0) != cudaSuccess ||
+          cudaMemcpyAsync((uint8_t *)out_host + prefix * ous, dout + k * out_slot, units * ous,
+                          cudaMemcpyDeviceToHost, w->d2h) != cudaSuccess) {
         failed = true;
         break;
       }
@@ -424,6 +480,14 @@ ug_result run_host(Op op, const void *in_host, unsigned long long n, void *out_h
       break;
     }
     prefix += r.count;
+    if (i + slots < nch) {  // slot k is free once its output has been copied out
+      if (cudaEventRecord(w->ev_free[k], w->d2h) != cudaSuccess ||
+          cudaStreamWaitEvent(w->h2d, w->ev_free[k], 0) != cudaSuccess ||
+          stage_chunk(i + slots) != UG_OK) {
+        failed = true;
+        break;
+      }
+    }
   }
   // every stage drained before the staging buffers can be reused
   if (cudaStreamSynchronize(w->d2h) != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess ||
@@ -458,10 +522,23 @@ ug_result utf16le_to_utf8(const uint16_t *in, size_t n, uint8_t *out, size_t out
   return run_sync(Op::U16_TO_U8, in, n, out, out_cap, (cudaStream_t)stream);
 }
 uint64_t utf16_length_from_utf8(const uint8_t *in, size_t n, void *stream) {
-  return run_len(false, in, n, (cudaStream_t)stream);
+  uint64_t len;
+  run_len(false, in, n, (cudaStream_t)stream, &len);
+  return len;
 }
 uint64_t utf8_length_from_utf16le(const uint16_t *in, size_t n, void *stream) {
-  return run_len(true, in, n, (cudaStream_t)stream);
+  uint64_t len;
+  run_len(true, in, n, (cudaStream_t)stream, &len);
+  return len;
+}
+int ug_utf16_length_from_utf8_ex(const uint8_t *in, size_t n, uint64_t *len, void *stream) {
+  return run_len(false, in, n, (cudaStream_t)stream, len);
+}
+int ug_utf8_length_from_utf16le_ex(const uint16_t *in, size_t n, uint64_t *len, void *stream) {
+  return run_len(true, in, n, (cudaStream_t)stream, len);
+}
+int ug_utf8_length_from_utf16be_ex(const uint16_t *in, size_t n, uint64_t *len, void *stream) {
+  return run_len(true, in, n, (cudaStream_t)stream, len, true);
 }
 
 int ug_utf8_validate_async(const uint8_t *in, size_t n, ug_result *d_result, void *stream) {
@@ -511,7 +588,9 @@ ug_result utf16be_to_utf8(const uint16_t *in, size_t n, uint8_t *out, size_t out
   return run_sync(Op::U16BE_TO_U8, in, n, out, out_cap, (cudaStream_t)stream);
 }
 uint64_t utf8_length_from_utf16be(const uint16_t *in, size_t n, void *stream) {
-  return run_len(true, in, n, (cudaStream_t)stream, true);
+  uint64_t len;
+  run_len(true, in, n, (cudaStream_t)stream, &len, true);
+  return len;
 }
 int ug_utf16be_validate_async(const uint16_t *in, size_t n, ug_result *d_result, void *stream) {
   if (!d_result) return UG_ERR_ARG;
@@ -698,6 +777,7 @@ void ug_release_workspaces(void) {
       }
       for (cudaEvent_t ev : w->ev_in) cudaEventDestroy(ev);
       for (cudaEvent_t ev : w->ev_done) cudaEventDestroy(ev);
+      for (cudaEvent_t ev : w->ev_free) cudaEventDestroy(ev);
       cudaFree(w->d_recs);
       cudaFreeHost(w->h_recs);
       delete w;
@@ -709,6 +789,19 @@ void ug_release_workspaces(void) {
 }
 
 int ug_abi_version(void) { return UNIGPU_ABI_VERSION; }
+size_t ug_tile_bytes(void) { return (size_t)TILE; }
+
+size_t ug_workspace_bytes(void *stream) {
+  int dev;
+  if (cudaGetDevice(&dev) != cudaSuccess) return 0;
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_ws.find(std::make_pair(dev, (uintptr_t)stream));
+  if (it == g_ws.end()) return 0;
+  const Workspace *w = it->second;
+  return w->status_cap * sizeof(uint64_t) + w->d_in_cap + w->d_out_cap +
+         w->rec_cap * sizeof(RecordDev) + sizeof(Counters) + sizeof(ResultDev) +
+         sizeof(unsigned long long);
+}
 
 #ifdef UG_PREFIX_EXPT
 cudaError_t ug_pmode_set_impl(int m);

@@ -1,9 +1,18 @@
 """GPU parity at BASELINE.json's full sizes (tier T1, large).  Configs 1-3 are compared with the
-oracle element by element; config 4 (8 GiB, > 2^32 output units) is checked in the launch
-configuration bench.py times (the shard call at G = 1) on sampled 64 MiB generator chunks against
-the oracle, plus properties that hold at any size (round trip = identity, written = length
-function, injected errors exact).  Each 64 MiB generator chunk is whole valid text, so chunk
-boundaries are character boundaries."""
+oracle element by element.  Config 4 (8 GiB, > 2^32 output units):
+  * the launch bench.py times (the shard call at G = 1) is compared with the oracle element by
+    element over ALL 128 of its 64 MiB generator chunks (each is whole valid text, so chunk
+    boundaries are character boundaries and the oracle's per-chunk outputs concatenate);
+  * the sharded path at G = 2 / 4 / 8 (cuts at character starts, 3-byte halos, one shard
+    launch per rank, records combined on the device by ug_combine_records_async) reproduces
+    that output unit for unit, both directions;
+  * BASELINE.json configs[4]'s 16 seeded error copies PER G, each an injected error of a random
+    class within 3 bytes of a shard cut, patched in place on the device, through the SHARDED
+    path: (error, position, written) against the oracle (written = the oracle's counts of the
+    whole chunks before p plus the oracle on the partial chunk)."""
+import os
+from concurrent.futures import ThreadPoolExecutor
+
 import numpy as np
 import pytest
 
@@ -71,72 +80,148 @@ def c4():
     return synth.generate("c4")
 
 
-def chunk_units_gpu(t, nchunks):
-    """UTF-16 length of each 64 MiB chunk (product length kernel on character-aligned
-    sub-ranges)."""
-    C = synth.CHUNK
-    return [ug.utf16_length_from_utf8(t[c * C:(c + 1) * C]) for c in range(nchunks)]
+def _oracle_chunk(x):
+    r, o = oracle.utf8_to_utf16le(x)
+    assert r.error == 0
+    return o
 
 
-def test_config4_full_size_bench_launch(c4):
+@pytest.fixture(scope="module")
+def c4_ref(c4):
+    """The bench launch at G = 1 and its element-by-element check against the oracle on every
+    64 MiB chunk.  Returns (device input, device output, n16, oracle count per chunk)."""
     n = c4.size
     t = torch.from_numpy(c4).to(DEV)
     out16 = torch.empty(n, dtype=torch.int16, device=DEV)
     rec = ug.record_buffer(DEV, 1)
-    # bench.py's launch at G = 1: the shard call over the whole buffer, no halos
-    ug.utf8_to_utf16le_shard_async(t, 0, n, 0, 0, 0, out16, rec)
+    ug.utf8_to_utf16le_shard_async(t, 0, n, 0, 0, 0, out16, rec)   # bench.py's launch, G = 1
     torch.cuda.synchronize()
     r = ug.decode_records(rec)[0]
     assert r.first_err == ug.NONE and r.too_small == 0
     n16 = r.count
     assert n16 > 2 ** 32                       # 64-bit offsets exercised
+    C = synth.CHUNK
+    nch = n // C
+    workers = max(1, min(32, os.cpu_count() or 1))
+    counts, off = [], 0
+    with ThreadPoolExecutor(workers) as ex:    # the oracle releases the GIL (ctypes)
+        for b0 in range(0, nch, workers):
+            refs = list(ex.map(_oracle_chunk, [c4[c * C:(c + 1) * C]
+                                                for c in range(b0, min(nch, b0 + workers))]))
+            for c, ref in zip(range(b0, b0 + len(refs)), refs):
+                got = out16[off:off + ref.size]
+                assert torch.equal(got, torch.from_numpy(ref.view(np.int16)).to(DEV)), c
+                counts.append(ref.size)
+                off += ref.size
+    assert off == n16
+    return t, out16, n16, counts
+
+
+def test_config4_full_size_bench_launch(c4_ref):
+    t, out16, n16, counts = c4_ref
+    n = t.numel()
     assert ug.utf16_length_from_utf8(t) == n16
-    lens = chunk_units_gpu(t, n // synth.CHUNK)
-    assert sum(lens) == n16
-    offs = np.concatenate([[0], np.cumsum(lens)])
-    rng = np.random.default_rng(45)
-    picks = sorted(set([0, len(lens) - 1] + rng.integers(1, len(lens) - 1, 3).tolist()))
-    for c in picks:
-        x = c4[c * synth.CHUNK:(c + 1) * synth.CHUNK]
-        ref = oracle.utf8_to_utf16le(x)[1]
-        got = out16[int(offs[c]):int(offs[c + 1])]
-        assert torch.equal(got, torch.from_numpy(ref.view(np.int16)).to(DEV)), c
     # reverse through the shard call as well, then the round trip is the identity
     back = torch.empty(n, dtype=torch.uint8, device=DEV)
+    rec = ug.record_buffer(DEV, 1)
     ug.utf16le_to_utf8_shard_async(out16[:n16], 0, n16, 0, 0, 0, back, rec)
     torch.cuda.synchronize()
     r2 = ug.decode_records(rec)[0]
     assert r2.first_err == ug.NONE and r2.count == n
     assert torch.equal(back, t)
+    assert ug.utf8_length_from_utf16le(out16[:n16]) == n
     # the plain API agrees
     assert tuple(ug.utf8_to_utf16le(t, out16)) == (0, n, n16)
 
 
-def test_config4_error_copies_near_shard_cuts(c4):
-    """BASELINE config 4's error copies: one injected error within 3 bytes of an 8-way shard
-    cut; unsharded call on the full 8 GiB gives e = p, the injected kind, and written = units
-    before p (GPU lengths of whole chunks + the oracle on the partial chunk)."""
+def shard_cuts_utf8(host: np.ndarray, G: int):
+    """BASELINE north_star item 3 / DESIGN.md section 7: nominal cuts aligned down to 16 B,
+    backed off to character starts by the library's cut rule."""
+    from paper_2111_08692_b200 import dist as ugd
+    n = host.size
+    get = lambda a, b: host[a:b].tobytes()  # noqa: E731
+    return [ugd.utf8_cut(get, c, n) for c in ugd.nominal_cuts(n, G)]
+
+
+def run_sharded_fwd(t, cuts, out, validate=False):
+    """One shard launch per virtual rank over the device buffer t, then every rank's combine
+    on the device.  Returns (global result, records, per-rank output offsets)."""
+    G = len(cuts) - 1
+    n = t.numel()
+    recs = ug.record_buffer(DEV, G)
+    for k in range(G):
+        lo, hi = cuts[k], cuts[k + 1]
+        hb, ha = min(lo, 3), min(n - hi, 3)
+        if validate:
+            ug.utf8_validate_shard_async(t, lo, hi - lo, hb, ha, lo, recs,
+                                         rec_off=k * ug.RECORD_BYTES)
+        else:
+            ug.utf8_to_utf16le_shard_async(t, lo, hi - lo, hb, ha, lo, out[lo:hi], recs,
+                                           rec_off=k * ug.RECORD_BYTES)
+    res = ug.result_buffer(DEV, G)
+    offs = torch.zeros(G, dtype=torch.int64, device=DEV)
+    for k in range(G):
+        ug.combine_records_async(recs, G, k, n, res[k * ug.RESULT_BYTES:], offs[k:])
+    torch.cuda.synchronize()
+    results = ug.decode_results(res)
+    assert all(r == results[0] for r in results)
+    return results[0], ug.decode_records(recs), offs.cpu().tolist()
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_config4_sharded_matches_oracle(c4, c4_ref, G):
+    """The sharded forward at G ranks places every rank's output exactly where the oracle's
+    (verified unsharded) output has it; the reverse per rank round-trips each rank's bytes."""
+    t, out16, n16, _ = c4_ref
     n = c4.size
-    t = torch.from_numpy(c4).to(DEV)
-    out16 = torch.empty(n, dtype=torch.int16, device=DEV)
-    G = 8
-    rng = np.random.default_rng(np.random.SeedSequence([5, 0xE, G, 0]))
-    for j in range(3):
+    cuts = shard_cuts_utf8(c4, G)
+    outs = torch.empty(n, dtype=torch.int16, device=DEV)
+    r, recs, offs = run_sharded_fwd(t, cuts, outs)
+    assert tuple(r) == (0, n, n16)
+    assert offs == list(np.cumsum([0] + [x.count for x in recs[:-1]]))
+    back = torch.empty(max(cuts[k + 1] - cuts[k] for k in range(G)), dtype=torch.uint8,
+                       device=DEV)
+    rec = ug.record_buffer(DEV, 1)
+    for k in range(G):
+        lo, cnt, off = cuts[k], recs[k].count, offs[k]
+        assert torch.equal(outs[lo:lo + cnt], out16[off:off + cnt]), k
+        ug.utf16le_to_utf8_shard_async(outs[lo:lo + cnt], 0, cnt, 0, 0, off, back, rec)
+        torch.cuda.synchronize()
+        rr = ug.decode_records(rec)[0]
+        assert rr.first_err == ug.NONE and rr.count == cuts[k + 1] - lo
+        assert torch.equal(back[:rr.count], t[lo:cuts[k + 1]]), k
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_config4_error_copies_sharded(c4, c4_ref, G):
+    """BASELINE.json configs[4]: 16 seeded copies per G, each with one injected error of a
+    random class at a character start within 3 bytes of a uniformly chosen interior shard cut
+    (SeedSequence([5, 0xE, G, j])), patched in place on the device and
+    run through the SHARDED forward (cuts recomputed on the patched bytes) and the sharded
+    validator.  Expected: kind = the injected class, position = p, written = the oracle's
+    units before p."""
+    t, _, _, counts = c4_ref
+    n = c4.size
+    C = synth.CHUNK
+    prefix = np.concatenate([[0], np.cumsum(counts)])
+    outs = torch.empty(n, dtype=torch.int16, device=DEV)
+    for j in range(16):
+        rng = np.random.default_rng(np.random.SeedSequence([5, 0xE, G, j]))
         k = int(rng.integers(1, G))
         c = (k * (n // G)) & ~15
-        cls = synth.UTF8_ERROR_CLASSES[int(rng.integers(0, 5))]
+        cls = synth.UTF8_ERROR_CLASSES[int(rng.integers(0, len(synth.UTF8_ERROR_CLASSES)))]
         p, saved = synth.inject_utf8_error(c4, c - 3, c + 3, cls, rng)
+        assert abs(p - c) <= 3
         t[p:p + saved.size] = torch.from_numpy(c4[p:p + saved.size].copy()).to(DEV)
         try:
-            r = ug.utf8_to_utf16le(t, out16)
-            C = synth.CHUNK
+            cuts = shard_cuts_utf8(c4, G)
             ch = p // C
-            before = ug.utf16_length_from_utf8(t[:ch * C])
-            part = oracle.utf8_to_utf16le(c4[ch * C:p])[0].written
-            assert (r.error, r.position, r.written) == \
-                (synth.UTF8_EXPECTED_KIND[cls], p, before + part), (cls, r, p)
-            v = ug.utf8_validate(t)
-            assert (v.error, v.position) == (synth.UTF8_EXPECTED_KIND[cls], p)
+            want_wr = int(prefix[ch]) + oracle.utf8_to_utf16le(c4[ch * C:p])[0].written
+            want = (synth.UTF8_EXPECTED_KIND[cls], p, want_wr)
+            r, *_ = run_sharded_fwd(t, cuts, outs)
+            assert tuple(r) == want, (G, j, cls, r, want)
+            v, *_ = run_sharded_fwd(t, cuts, None, validate=True)
+            assert (v.error, v.position, v.written) == (want[0], p, 0), (G, j, cls, v)
         finally:
             c4[p:p + saved.size] = saved
             t[p:p + saved.size] = torch.from_numpy(saved).to(DEV)

@@ -16,7 +16,10 @@ if not torch.cuda.is_available():
 import paper_2111_08692_b200 as ug  # noqa: E402
 
 DEV = torch.device("cuda:0")
-TILE = 8192
+# the kernels' real tile (16 KiB: 512 threads x 32 bytes), queried from the library; tile t of
+# a call covers input positions [t * TILE - lead, (t + 1) * TILE - lead), lead = address mod 16
+TILE = ug.tile_bytes()
+LEADS = (0, 1, 7, 15)
 
 
 # ----------------------------------------------------------------------------- helpers
@@ -103,7 +106,8 @@ def test_spec_examples(golden):
 
 
 @pytest.mark.parametrize("n", [0, 1, 2, 3, 4, 5, 15, 16, 17, 31, 32, 33, 1023, 1024, 1025,
-                               8191, 8192, 8193, 16384 + 7])
+                               8191, 8192, 8193, TILE - 1, TILE, TILE + 1, TILE + 7,
+                               2 * TILE + 3, 3 * TILE - 5])
 def test_small_sizes(n):
     rng = np.random.default_rng(n)
     a = np.frombuffer(synth.gen_chunk("mixed", "utf8", n, 7, n), dtype=np.uint8) if n else \
@@ -136,32 +140,51 @@ def short_cases():
     return cases
 
 
-@pytest.mark.parametrize("boundary", [32, 1024, TILE])
+@pytest.mark.parametrize("boundary", [32, 1024, TILE, 2 * TILE])
 def test_phase_sweep(boundary):
     """Each short string embedded in ASCII padding so that it straddles a thread (32 B), warp
-    (1 KiB) or tile (8 KiB) boundary at every phase, and at several input alignments."""
+    (1 KiB) or real tile edge (the first and the second tile edge: TMA halos, emit ownership
+    split between two CTAs, the look-back between tiles) at every phase -4..+1, at input
+    alignments (leads) 0 / 1 / 7 / 15.  The edge sits at position boundary - lead."""
     cases = short_cases()
-    rng = np.random.default_rng(boundary)
     for i, c in enumerate(cases):
         c = np.frombuffer(c, dtype=np.uint8)
+        lead = LEADS[i % len(LEADS)]
         for ph in range(-4, 2):
-            pre = boundary + ph
+            pre = boundary - lead + ph
             a = np.concatenate([np.full(pre, 0x41, np.uint8), c, np.full(40, 0x42, np.uint8)])
-            check_utf8(a, offset=int(rng.integers(0, 16)) if i % 5 == 0 else 0)
+            check_utf8(a, offset=lead)
+
+
+def test_phase_sweep_at_input_end():
+    """Errors and truncations in the last bytes of the input right at a real tile edge: the
+    after-halo reads 0x00 (end of stream) and the classifier's look-ahead decides."""
+    reps = [b"\xc3", b"\xe4\xbd", b"\xf0\x9f\x98", b"\xed\xa0\x80", b"\x80", b"\xc0\xaf",
+            "\U0001F600".encode(), "你".encode()]
+    for lead in LEADS:
+        for c in reps:
+            for ph in range(-4, 4):
+                pre = TILE - lead + ph - len(c)
+                if pre < 0:
+                    continue
+                a = np.frombuffer(b"A" * pre + c, dtype=np.uint8)
+                check_utf8(a, offset=lead)
 
 
 def test_valid_text_straddling_every_tile_phase():
-    """Valid 4-byte / 3-byte / 2-byte characters across the 8 KiB tile boundary: S:638."""
+    """Valid 4-byte / 3-byte / 2-byte characters across the first and second real tile edges
+    at every byte phase and alignment: S:638 (round trip), both directions."""
     for ch in ("\U0001F600", "你", "é"):
         e = ch.encode()
-        for ph in range(0, 8):
-            pre = TILE - ph
-            a = np.frombuffer(b"a" * pre + e * 3 + b"z" * 5, dtype=np.uint8)
-            for off in (0, 5):
-                r = check_utf8(a, offset=off)
-                assert r.error == 0
-            u = oracle.utf8_to_utf16le(a)[1]
-            check_utf16(u)
+        for edge in (TILE, 2 * TILE):
+            for lead in LEADS:
+                for ph in range(0, len(e) + 1):
+                    pre = edge - lead - ph
+                    a = np.frombuffer(b"a" * pre + e * 3 + b"z" * 5, dtype=np.uint8)
+                    r = check_utf8(a, offset=lead)
+                    assert r.error == 0
+                    u = oracle.utf8_to_utf16le(a)[1]
+                    check_utf16(u, offset=lead & ~1)
 
 
 # ----------------------------------------------------------------------------- random fuzz
@@ -660,7 +683,7 @@ def test_reverse_dense_3byte_text():
     assert check_utf16(u).error == 0
     assert check_utf16be(be_raw(u), offset=2).error == 0
     rng = np.random.default_rng(0x2B)
-    TILE_W = 8192  # words per 16 KiB tile
+    TILE_W = TILE // 2  # words per tile
     for centre in (TILE_W * 3 + TILE_W // 2, TILE_W * 7, TILE_W * 11 + TILE_W // 2 + 40):
         v = u.copy()
         p, _ = synth.inject_utf16_error(v, centre - 24, centre + 24, rng)
@@ -671,3 +694,99 @@ def test_reverse_dense_3byte_text():
     need = oracle.utf16le_to_utf8(u)[0].written
     for cap in (3 * TILE_W * 5 // 2 + 1000, need - 1):
         check_utf16(u, cap=cap)
+
+
+# ----------------------------------------------------------------------------- API hardening
+def test_binding_bounds_and_slots():
+    """The binding rejects n / out_cap beyond the tensors, shard halos outside the input and
+    result / record slots outside their buffers, before any C call."""
+    t = torch.zeros(64, dtype=torch.uint8, device=DEV)
+    o = torch.zeros(64, dtype=torch.int16, device=DEV)
+    with pytest.raises(ValueError, match="exceeds the input"):
+        ug.utf8_to_utf16le(t, o, n=65)
+    with pytest.raises(ValueError, match="out_cap"):
+        ug.utf8_to_utf16le(t, o, out_cap=65)
+    with pytest.raises(ValueError, match="exceeds the input"):
+        ug.utf8_to_utf16le_shard_async(t, 10, 60, 0, 0, 0, o, ug.record_buffer(DEV, 1))
+    with pytest.raises(ValueError, match="halos"):
+        ug.utf8_to_utf16le_shard_async(t, 1, 10, 3, 0, 0, o, ug.record_buffer(DEV, 1))
+    with pytest.raises(ValueError, match="slot"):
+        ug.utf8_validate_async(t, ug.result_buffer(DEV, 1), result_off=8)
+    with pytest.raises(ValueError, match="CUDA tensor"):
+        ug.utf8_validate_async(t, torch.zeros(24, dtype=torch.uint8))
+    r = ug.utf8_to_utf16le(t, o, n=10, out_cap=10)
+    assert tuple(r) == (0, 10, 10)
+
+
+def test_length_ex_on_device():
+    import ctypes
+    t = torch.zeros(7, dtype=torch.uint8, device=DEV)
+    assert ug.utf16_length_from_utf8(t) == 7
+    out = ctypes.c_uint64(9)
+    s = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    assert ug.lib.ug_utf16_length_from_utf8_ex(ctypes.c_void_p(t.data_ptr()), 7,
+                                               ctypes.byref(out), s) == ug.OK
+    assert out.value == 7
+    assert ug.lib.ug_utf16_length_from_utf8_ex(ctypes.c_void_p(0), 3, ctypes.byref(out),
+                                               s) == ug.ERR_ARG and out.value == 0
+
+
+def test_same_stream_threads_get_their_own_results():
+    """Synchronous calls from several host threads on ONE stream (torch's default): each gets
+    its own input's result (the workspace mutex spans launch -> read-back)."""
+    import threading
+    rng = np.random.default_rng(77)
+    inputs = []
+    for k in range(8):
+        a = np.frombuffer(synth.gen_chunk("mixed", "utf8", 200000 + 1000 * k, 31, k),
+                          dtype=np.uint8).copy()
+        if k % 2:
+            synth.inject_utf8_error(a, 1000, a.size - 8, "surrogate", rng)
+        inputs.append(a)
+    dev_in = [torch.from_numpy(a).to(DEV) for a in inputs]
+    dev_out = [torch.empty(a.size, dtype=torch.int16, device=DEV) for a in inputs]
+    want = [tuple(oracle.utf8_to_utf16le(a)[0]) for a in inputs]
+    want_len = [oracle.utf16_length_from_utf8(a) for a in inputs]
+    torch.cuda.synchronize()
+    errs = []
+
+    def worker(k):
+        try:
+            for _ in range(25):
+                r = ug.utf8_to_utf16le(dev_in[k], dev_out[k], stream=0)
+                if tuple(r) != want[k]:
+                    errs.append((k, r, want[k]))
+                v = ug.utf16_length_from_utf8(dev_in[k], stream=0)
+                if v != want_len[k]:
+                    errs.append((k, "len", v, want_len[k]))
+        except Exception as e:  # noqa: BLE001
+            errs.append((k, repr(e)))
+
+    th = [threading.Thread(target=worker, args=(k,)) for k in range(8)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    assert not errs, errs[:5]
+
+
+def test_host_pipeline_streams_many_chunks_in_bounded_memory(c0):
+    """f2 streaming: ~660 chunks (165x the 4 staging slots) through the bounded ring; the
+    workspace stays O(chunk) and the result equals the oracle, with capacity guards, both
+    directions."""
+    a = np.concatenate([c0, c0[: 400000]])
+    chunk = 2203
+    s = torch.cuda.current_stream()
+    torch.cuda.synchronize()
+    ug.lib.ug_release_workspaces()   # measure this call's allocations only
+    r = check_host(a, chunk)
+    assert r.error == 0
+    held = ug.workspace_bytes(s)
+    slot = (chunk + 3 + 6 + 15) + 2 * (chunk + 3) + 15
+    nch = a.size // chunk + 2
+    assert held <= 4 * slot + nch * 32 + (1 << 20), (held, slot)   # + status words / records
+    u = oracle.utf8_to_utf16le(a)[1]
+    check_host(u, chunk)
+    need8 = oracle.utf16le_to_utf8(u)[0].written
+    check_host(u, chunk, cap=need8 - 1)
+    check_host(a, chunk, cap=r.written // 2)

@@ -42,6 +42,7 @@ def test_library_exports_every_declared_symbol(ug):
 
 def test_abi_and_names(ug):
     assert ug.lib.ug_abi_version() == 1
+    assert ug.tile_bytes() == 16384  # NT (512 threads) x 32 bytes, csrc/device.cuh
     assert ug.error_name(0) == "OK" and ug.error_name(6) == "Surrogate"
     assert ug.error_name(-3) == "OutputTooSmall"
 
@@ -192,3 +193,19 @@ def test_binding_rejects_wrong_tensors(ug):
     assert ug._expect("utf8_length_from_utf16be") == (2, None, False)
     assert ug._expect("utf8_to_utf16le_shard_async") == (1, 2, False)
     assert ug._expect("utf16le_to_utf8_host") == (2, 1, True)
+
+
+def test_length_ex_error_channel_needs_no_gpu(ug):
+    """ug_*_length_*_ex report API misuse as UG_ERR_ARG (the plain forms return 0, which is
+    indistinguishable from an empty count) and leave *len = 0."""
+    V, L = ctypes.c_void_p, ug.lib
+    out = ctypes.c_uint64(77)
+    assert L.ug_utf16_length_from_utf8_ex(V(0), 5, ctypes.byref(out), V(0)) == ug.ERR_ARG
+    assert out.value == 0
+    assert L.ug_utf8_length_from_utf16le_ex(V(0x1001), 4, ctypes.byref(out), V(0)) == ug.ERR_ARG
+    assert L.ug_utf8_length_from_utf16be_ex(V(0x1000), 4, V(0), V(0)) == ug.ERR_ARG  # no len
+    assert L.ug_utf16_length_from_utf8_ex(V(0x1000), (1 << 62) + 1, ctypes.byref(out),
+                                          V(0)) == ug.ERR_ARG
+    out.value = 5
+    assert L.ug_utf16_length_from_utf8_ex(V(0), 0, ctypes.byref(out), V(0)) == ug.OK
+    assert out.value == 0
