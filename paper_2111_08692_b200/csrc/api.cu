@@ -174,7 +174,8 @@ int enqueue_tile_ws(Workspace *w, DeviceInfo *di, Op op, const void *in, unsigne
   TileArgs a;
   std::memset(&a, 0, sizeof(a));
   a.win = make_window(in, n * us, hb * us, ha * us);
-  a.ntiles = (unsigned long long)((a.win.n - 1 + a.win.lead) / TILE + 1);
+  int per_cta = 1;
+  a.ntiles = tile_units(op, a.win.n, a.win.lead, &per_cta);
   a.out = out;
   a.out_cap = out ? out_cap : 0;
   if (op_transcodes(op)) {
@@ -187,7 +188,8 @@ int enqueue_tile_ws(Workspace *w, DeviceInfo *di, Op op, const void *in, unsigne
   a.rec = d_rec;
   a.global_off = global_off;
   unsigned long long maxg = (unsigned long long)di->sms * (unsigned long long)di->occ[(int)op];
-  int grid = (int)(a.ntiles < maxg ? a.ntiles : maxg);
+  const unsigned long long want = (a.ntiles + per_cta - 1) / per_cta;
+  int grid = (int)(want < maxg ? want : maxg);
   if (launch_tile(op, a, grid, s) != cudaSuccess) return UG_ERR_CUDA;
   g_launches.fetch_add(1);
   return UG_OK;

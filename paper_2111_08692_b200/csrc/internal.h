@@ -54,6 +54,8 @@ inline bool op_transcodes(Op op) {
 }
 
 size_t tile_smem_bytes(Op op);
+int tile_threads(Op op);
+unsigned long long tile_units(Op op, long long nbytes, long long lead, int *per_cta);
 cudaError_t tile_configure(Op op);  // set max dynamic smem (idempotent)
 cudaError_t tile_occupancy(Op op, int *blocks_per_sm);
 cudaError_t launch_tile(Op op, const TileArgs &a, int grid, cudaStream_t s);

@@ -190,6 +190,22 @@ struct U8PolT {
     s.wasc = __all_sync(FULL, ((orv & HI) == 0u) && !pend);
   }
 
+  // The same state from registers (streaming validator): q0 / q1 = the thread's 32 bytes,
+  // pv / nx = the 4 bytes before / after.
+  __device__ static __forceinline__ void from_regs(St &s, uint4 q0, uint4 q1, uint32_t pv,
+                                                   uint32_t nx, long long pos0, long long n) {
+    s.w[0] = q0.x; s.w[1] = q0.y; s.w[2] = q0.z; s.w[3] = q0.w;
+    s.w[4] = q1.x; s.w[5] = q1.y; s.w[6] = q1.z; s.w[7] = q1.w;
+    s.prev = pv;
+    s.nxt = nx;
+    s.pos0 = pos0;
+    s.n = n;
+    const uint32_t orv = q0.x | q0.y | q0.z | q0.w | q1.x | q1.y | q1.z | q1.w;
+    const bool pend = (pv >= 0xC0000000u) || ((pv & 0x00FF0000u) >= 0x00E00000u) ||
+                      ((pv & 0x0000FF00u) >= 0x0000F000u);
+    s.wasc = __all_sync(FULL, ((orv & HI) == 0u) && !pend);
+  }
+
   // a3 classification (flags into s.err) and, if xc, the number of units the thread emits.
   template <bool IN>  // IN: the whole tile is owned (tile-uniform)
   __device__ static __forceinline__ uint32_t analyze(St &s, int tid, bool xc) {
@@ -377,6 +393,21 @@ struct U16PolT {
     s.pos0 = tpw + (BPT / 2) * tid;
     s.own = IN ? 0xFFFFu : (bit_range(s.pos0, 0, nw) & 0xFFFFu);
     const uint32_t orv = s.w[0] | s.w[1] | s.w[2] | s.w[3] | s.w[4] | s.w[5] | s.w[6] | s.w[7];
+    s.wasc = __all_sync(FULL, (orv & (BE ? 0x80FF80FFu : 0xFF80FF80u)) == 0u);
+  }
+
+  // The same state from registers (streaming validator): q0 / q1 = the thread's 16 words,
+  // pv / nx = the 32-bit words before / after; pos0 / nw in words; own = words < nw owned.
+  template <bool IN>
+  __device__ static __forceinline__ void from_regs(St &s, uint4 q0, uint4 q1, uint32_t pv,
+                                                   uint32_t nx, long long pos0, long long nw) {
+    s.w[0] = q0.x; s.w[1] = q0.y; s.w[2] = q0.z; s.w[3] = q0.w;
+    s.w[4] = q1.x; s.w[5] = q1.y; s.w[6] = q1.z; s.w[7] = q1.w;
+    s.prev_word = native(pv >> 16);
+    s.next_word = native(nx & 0xFFFFu);
+    s.pos0 = pos0;
+    s.own = IN ? 0xFFFFu : (bit_range(pos0, 0, nw) & 0xFFFFu);
+    const uint32_t orv = q0.x | q0.y | q0.z | q0.w | q1.x | q1.y | q1.z | q1.w;
     s.wasc = __all_sync(FULL, (orv & (BE ? 0x80FF80FFu : 0xFF80FF80u)) == 0u);
   }
 
@@ -727,6 +758,108 @@ __global__ void __launch_bounds__(NT, VCPS) k_validate(const TileArgs a) {
       const unsigned long long e = Pol::find_error(st, n_units);
       if (e != NONE) atomicMin(&a.ctr->err_min, e);
     }
+  }
+  __syncthreads();
+  finish_call<Pol>(a, false, tid, warp, lane, &s_last);
+}
+
+// ---------------------------------------------------------------------------- streaming
+// K1 / K3 as streaming register kernels (-DUG_VALIDATE_STREAM; measured and NOT the default:
+// equal to the TMA ring on mixed text, where the classifier's ALU work binds (config 4
+// utf8_validate 0.383 vs 0.381 ms per GiB), and slower where loads bind (ASCII utf8 0.217 vs
+// 0.196 ms, utf16le 0.415 vs 0.336 ms): two 1 KiB chunks in flight per warp are fewer bytes in
+// flight than the ring's 4 x 16 KiB TMA slots per CTA).  No inter-CTA dependence and no smem
+// ring.  Each warp takes 1 KiB chunks in grid-stride order (chunk c = positions
+// [c * 1024 - lead, ...), so every load is a 16-byte-aligned LDG.128 and the warp / lane
+// layout is exactly the tile kernels': lane l owns 32 contiguous bytes, the classifier's
+// 3-byte look-ahead runs in lane 31), with the next chunk's loads issued before the current
+// chunk is classified.  The 4 bytes before / after a lane come from its neighbours by shuffle,
+// lanes 0 / 31 load them.  Chunks touching the window edges take guarded byte loads (bytes
+// outside the window read as 0x00, as fix_tile_edges makes them in the tile kernels).  A warp
+// that flags rescans its own 1 KiB (a4) and atomicMin's the first error; the last CTA
+// finalises (a10).
+constexpr int VS_THREADS = 256;  // 8 warps per CTA
+constexpr int VS_CHUNK = 1024;   // input bytes per warp per step
+#ifndef UG_VSCPS
+#define UG_VSCPS 4
+#endif
+constexpr int VSCPS = UG_VSCPS;  // CTAs per SM (register budget: 64 registers)
+
+struct VChunk {
+  uint4 q0, q1;
+  uint32_t pv, nx;
+};
+
+// Load chunk c (warp-uniform) into this lane's registers.
+__device__ __forceinline__ void vs_load(const Window &w, long long c, int lane, VChunk &v) {
+  const long long p0 = c * VS_CHUNK - w.lead;  // position of the chunk's byte 0
+  const long long pos = p0 + 32 * lane;
+  if (p0 - 4 >= w.lo_valid && p0 + VS_CHUNK + 4 <= w.hi_valid) {  // interior (warp-uniform)
+    const uint4 *g = reinterpret_cast<const uint4 *>(w.base + pos);
+    v.q0 = __ldcs(g);
+    v.q1 = __ldcs(g + 1);
+    v.pv = lane == 0 ? __ldcs(reinterpret_cast<const uint32_t *>(w.base + pos - 4)) : 0u;
+    v.nx = lane == 31 ? __ldcs(reinterpret_cast<const uint32_t *>(w.base + pos + 32)) : 0u;
+  } else {  // cold: window edges, byte by byte
+    uint32_t b[8];
+#pragma unroll
+    for (int k = 0; k < 8; k++) {
+      uint32_t x = 0;
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        const long long q = pos + 4 * k + j;
+        x |= ((q >= w.lo_valid && q < w.hi_valid) ? (uint32_t)w.base[q] : 0u) << (8 * j);
+      }
+      b[k] = x;
+    }
+    v.q0 = make_uint4(b[0], b[1], b[2], b[3]);
+    v.q1 = make_uint4(b[4], b[5], b[6], b[7]);
+    uint32_t pv = 0, nx = 0;
+#pragma unroll
+    for (int j = 0; j < 4; j++) {
+      const long long qp = pos - 4 + j, qn = pos + 32 + j;
+      pv |= ((qp >= w.lo_valid && qp < w.hi_valid) ? (uint32_t)w.base[qp] : 0u) << (8 * j);
+      nx |= ((qn >= w.lo_valid && qn < w.hi_valid) ? (uint32_t)w.base[qn] : 0u) << (8 * j);
+    }
+    v.pv = lane == 0 ? pv : 0u;
+    v.nx = lane == 31 ? nx : 0u;
+  }
+}
+
+template <class Pol>
+__global__ void __launch_bounds__(VS_THREADS, VSCPS) k_validate_stream(const TileArgs a) {
+  __shared__ int s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const Window &win = a.win;
+  const long long nch = (long long)a.ntiles;  // 1 KiB chunks
+  const long long n_units = win.n / Pol::UNIT;
+  const long long nwarps = (long long)gridDim.x * (VS_THREADS / 32);
+  long long c = (long long)blockIdx.x * (VS_THREADS / 32) + warp;
+  VChunk cur, nxt;
+  if (c < nch) vs_load(win, c, lane, cur);
+  for (; c < nch; c += nwarps) {
+    if (c + nwarps < nch) vs_load(win, c + nwarps, lane, nxt);  // in flight during the check
+    uint32_t pv = __shfl_up_sync(FULL, cur.q1.w, 1);
+    uint32_t nx = __shfl_down_sync(FULL, cur.q0.x, 1);
+    if (lane == 0) pv = cur.pv;
+    if (lane == 31) nx = cur.nx;
+    const long long pos = c * VS_CHUNK - win.lead + 32 * lane;  // bytes
+    typename Pol::St st;
+    const long long p0 = c * VS_CHUNK - win.lead;
+    if (p0 >= 0 && p0 + VS_CHUNK <= win.n) {  // every position owned (warp-uniform)
+      if constexpr (Pol::UNIT == 1) Pol::from_regs(st, cur.q0, cur.q1, pv, nx, pos, win.n);
+      else Pol::template from_regs<true>(st, cur.q0, cur.q1, pv, nx, pos / 2, win.n / 2);
+      Pol::template analyze<true>(st, tid, false);
+    } else {
+      if constexpr (Pol::UNIT == 1) Pol::from_regs(st, cur.q0, cur.q1, pv, nx, pos, win.n);
+      else Pol::template from_regs<false>(st, cur.q0, cur.q1, pv, nx, pos / 2, win.n / 2);
+      Pol::template analyze<false>(st, tid, false);
+    }
+    if (__any_sync(FULL, Pol::hint(st))) {  // a4 (cold)
+      const unsigned long long e = Pol::find_error(st, n_units);
+      if (e != NONE) atomicMin(&a.ctr->err_min, e);
+    }
+    cur = nxt;
   }
   __syncthreads();
   finish_call<Pol>(a, false, tid, warp, lane, &s_last);
@@ -1537,7 +1670,12 @@ size_t tile_smem_bytes(Op op) {
   switch (op) {
     case Op::U8_VALIDATE:
     case Op::U16_VALIDATE:
-    case Op::U16BE_VALIDATE: return VRING * INBUF;
+    case Op::U16BE_VALIDATE:
+#ifndef UG_VALIDATE_STREAM
+      return VRING * INBUF;
+#else
+      return 0;
+#endif
     case Op::U8_TO_U16:
     case Op::U8_TO_U16BE: return RING * INBUF + U8Pol::STAGE;
     case Op::U16_TO_U8:
@@ -1551,8 +1689,13 @@ size_t tile_smem_bytes(Op op) {
   return 0;
 }
 
-static int tile_threads(Op op) {
+int tile_threads(Op op) {
   switch (op) {
+#ifdef UG_VALIDATE_STREAM
+    case Op::U8_VALIDATE:
+    case Op::U16_VALIDATE:
+    case Op::U16BE_VALIDATE: return VS_THREADS;
+#endif
     case Op::U8_TO_U16:
     case Op::U8_TO_U16BE: return NT + 32 * NLB;
     case Op::U16_TO_U8:
@@ -1582,17 +1725,35 @@ static void rev_launch(const TileArgs &a, int grid, int nt, size_t sm, cudaStrea
 }
 #endif
 
+#ifndef UG_VALIDATE_STREAM
+#define UG_KVAL k_validate
+#else
+#define UG_KVAL k_validate_stream
+#endif
 static const void *tile_fn(Op op) {
   switch (op) {
-    case Op::U8_VALIDATE: return (const void *)k_validate<U8Pol>;
+    case Op::U8_VALIDATE: return (const void *)UG_KVAL<U8Pol>;
     case Op::U8_TO_U16: return (const void *)k_transcode<U8Pol>;
-    case Op::U16_VALIDATE: return (const void *)k_validate<U16Pol>;
+    case Op::U16_VALIDATE: return (const void *)UG_KVAL<U16Pol>;
     case Op::U16_TO_U8: return rev_fn<false>();
-    case Op::U16BE_VALIDATE: return (const void *)k_validate<U16PolBE>;
+    case Op::U16BE_VALIDATE: return (const void *)UG_KVAL<U16PolBE>;
     case Op::U8_TO_U16BE: return (const void *)k_transcode<U8PolBE>;
     case Op::U16BE_TO_U8: return rev_fn<true>();
   }
   return nullptr;
+}
+
+// Work items of one launch over a window with `nbytes` owned bytes at address phase `lead`:
+// tiles (tile kernels) or 1 KiB warp chunks (streaming validators); and items per CTA.
+unsigned long long tile_units(Op op, long long nbytes, long long lead, int *per_cta) {
+#ifdef UG_VALIDATE_STREAM
+  if (!op_transcodes(op)) {
+    *per_cta = VS_THREADS / 32;
+    return (unsigned long long)((nbytes - 1 + lead) / VS_CHUNK + 1);
+  }
+#endif
+  *per_cta = 1;
+  return (unsigned long long)((nbytes - 1 + lead) / TILE + 1);
 }
 
 cudaError_t tile_configure(Op op) {
@@ -1609,11 +1770,11 @@ cudaError_t launch_tile(Op op, const TileArgs &a, int grid, cudaStream_t s) {
   size_t sm = tile_smem_bytes(op);
   int nt = tile_threads(op);
   switch (op) {
-    case Op::U8_VALIDATE: k_validate<U8Pol><<<grid, nt, sm, s>>>(a); break;
-    case Op::U16_VALIDATE: k_validate<U16Pol><<<grid, nt, sm, s>>>(a); break;
+    case Op::U8_VALIDATE: UG_KVAL<U8Pol><<<grid, nt, sm, s>>>(a); break;
+    case Op::U16_VALIDATE: UG_KVAL<U16Pol><<<grid, nt, sm, s>>>(a); break;
     case Op::U8_TO_U16: k_transcode<U8Pol><<<grid, nt, sm, s>>>(a); break;
     case Op::U16_TO_U8: rev_launch<false>(a, grid, nt, sm, s); break;
-    case Op::U16BE_VALIDATE: k_validate<U16PolBE><<<grid, nt, sm, s>>>(a); break;
+    case Op::U16BE_VALIDATE: UG_KVAL<U16PolBE><<<grid, nt, sm, s>>>(a); break;
     case Op::U8_TO_U16BE: k_transcode<U8PolBE><<<grid, nt, sm, s>>>(a); break;
     case Op::U16BE_TO_U8: rev_launch<true>(a, grid, nt, sm, s); break;
   }
