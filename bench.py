@@ -52,6 +52,9 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-per-op", action="store_true")
+    p.add_argument("--no-per-config", action="store_true")
+    p.add_argument("--path", default="planned", choices=["planned", "chained"],
+                   help="two-pass (sizing pass plans the transcoder) or single-pass look-back")
     p.add_argument("--out", default="")
     return p.parse_args()
 
@@ -216,21 +219,39 @@ def run_ours(args):
                                      res[(2 + which) * 24:],
                                      offs[which:])
 
+    planned = args.path == "planned"
+    plan8, plan16 = ug.plan_buffer(dev), ug.plan_buffer(dev)
+
     def step(record_events=False):
-        ug.utf16_length_from_utf8_async(t_in, lens)
+        # sizing pass of the forward (+ its plan in the two-pass form)
+        if planned:
+            ug.utf8_shard_plan_async(t_all, lo - base, n8, hb, ha, lens, plan8)
+        else:
+            ug.utf16_length_from_utf8_async(t_in, lens)
         if record_events:
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record(stream)
-        ug.utf8_to_utf16le_shard_async(t_all, lo - base, n8, hb, ha, lo, out16, rec)
+        if planned:
+            ug.utf8_to_utf16le_shard_planned_async(t_all, lo - base, n8, hb, ha, lo, plan8,
+                                                   out16, rec)
+        else:
+            ug.utf8_to_utf16le_shard_async(t_all, lo - base, n8, hb, ha, lo, out16, rec)
         if record_events:
             e1.record(stream)
             ev_f.append((e0, e1))
         gather_combine(0)
-        ug.utf8_length_from_utf16le_async(u16, lens, len_off=8)
+        if planned:
+            ug.utf16le_shard_plan_async(u16, 0, n16, 0, 0, lens, plan16, len_off=8)
+        else:
+            ug.utf8_length_from_utf16le_async(u16, lens, len_off=8)
         if record_events:
             e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e2.record(stream)
-        ug.utf16le_to_utf8_shard_async(u16, 0, n16, 0, 0, off16, out8, rec, rec_off=R)
+        if planned:
+            ug.utf16le_to_utf8_shard_planned_async(u16, 0, n16, 0, 0, off16, plan16, out8, rec,
+                                                   rec_off=R)
+        else:
+            ug.utf16le_to_utf8_shard_async(u16, 0, n16, 0, 0, off16, out8, rec, rec_off=R)
         if record_events:
             e3.record(stream)
             ev_r.append((e2, e3))
@@ -294,8 +315,12 @@ def run_ours(args):
     # roofline of the dominant kernel of the step (the longer transcoder launch); both
     # transcoders move n8 + 2 n16 algorithmic bytes per launch (read one side, write the other)
     alg_bytes = n8 + 2 * n16
-    kern = {"k_transcode<U8Pol>": {"op": "utf8_to_utf16le", "ms": fwd_ms, "input": n8},
-            "k_transcode16": {"op": "utf16le_to_utf8", "ms": rev_ms, "input": 2 * n16}}
+    kfwd, krev = (("k_transcode_planned<U8Pol>", "k_transcode_planned<U16Pol>") if planned
+                  else ("k_transcode<U8Pol>", "k_transcode16"))
+    kern = {kfwd: {"op": "utf8_to_utf16le" + ("_planned" if planned else ""), "ms": fwd_ms,
+                   "input": n8},
+            krev: {"op": "utf16le_to_utf8" + ("_planned" if planned else ""), "ms": rev_ms,
+                   "input": 2 * n16}}
     traffic = ncu_traffic() or {}
     for k, d in kern.items():
         d["achieved"] = alg_bytes / (d["ms"] * 1e-3) / 1e9
@@ -318,10 +343,16 @@ def run_ours(args):
     per_op = None
     if not args.no_per_op:
         per_op = measure_per_op(ug, t_all, lo - base, n8, hb, ha, out16, u16, out8, dev, peak)
+    per_config = None
+    if rank == 0 and not args.no_per_config:
+        del out16, out8, t_all, t_in, u16
+        torch.cuda.empty_cache()
+        per_config = measure_per_config(ug, dev, peak)
 
     cpu = None
     if rank == 0 and G == 1 and not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, size)
+        cpu["single_thread"] = oracle_single_thread(cfg)
 
     if rank == 0:
         line = {
@@ -333,8 +364,13 @@ def run_ours(args):
                                    "(60% ASCII/25% 2B/10% 3B/5% 4B), validate + UTF-8->UTF-16LE "
                                    "and back, sharded at character boundaries",
                        "bytes_utf8": N8, "units_utf16": N16,
-                       "step": "len16 + utf8_to_utf16le + [allgather+combine] + len8 + "
-                               "utf16le_to_utf8 + [allgather+combine]",
+                       "step": ("plan_utf8 (utf16_length_from_utf8 + range offsets) + "
+                                "utf8_to_utf16le_planned + [allgather+combine] + plan_utf16le "
+                                "(utf8_length_from_utf16le + range offsets) + "
+                                "utf16le_to_utf8_planned + [allgather+combine]") if planned else
+                               ("len16 + utf8_to_utf16le + [allgather+combine] + len8 + "
+                                "utf16le_to_utf8 + [allgather+combine]"),
+                       "path": args.path,
                        "parallelism": f"shard{G}", "l2": "inputs >= 1 GiB per rank > 126 MB L2; no flush",
                        "per_gpu_gbs": round(value / G, 2),
                        "gchar_per_s": round(gchar, 2), "gchar_per_s_per_gpu": round(gchar / G, 2),
@@ -344,9 +380,11 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": round(D["achieved"], 1), "peak": peak,
                          "unit": "GB/s", "frac": round(D["frac"], 4),
                          "traffic": D["traffic"],
-                         "traffic_source": (traffic["capture"] + " (" + traffic["config"] +
+                         "traffic_source": ("EXTRAPOLATED, not measured at this size: " +
+                                            traffic["capture"] + " (" + traffic["config"] +
                                             "), DRAM bytes per input byte x this launch's input"
                                             if D["traffic"] is not None else None),
+                         "traffic_extrapolated": D["traffic"] is not None,
                          "kernel": f"{dom} ({D['op']}), the longest launch of the step",
                          "algorithmic_bytes_per_launch": alg_bytes,
                          "avg_launch_ms": round(D["ms"], 4), "peak_source": peak_src,
@@ -357,6 +395,7 @@ def run_ours(args):
                                          "issue": d["issue"]}
                                      for k, d in kern.items()}},
             "per_op": per_op,
+            "per_config": per_config,
             "clocks": clk,
             "gpu_launches": int(launches),
             "e2e": e2e,
@@ -383,6 +422,9 @@ def measure_per_op(ug, t_all, off, n8, hb, ha, out16, u16, out8, dev, peak, reps
     res = ug.result_buffer(dev, 1)
     lens = torch.zeros(1, dtype=torch.int64, device=dev)
     rec = ug.record_buffer(dev, 1)
+    p8, p16 = ug.plan_buffer(dev), ug.plan_buffer(dev)
+    ug.utf8_shard_plan_async(t_all, off, n8, hb, ha, lens, p8)
+    ug.utf16le_shard_plan_async(u16, 0, n16, 0, 0, lens, p16)
     ops = {
         "utf8_validate": (lambda: ug.utf8_validate_async(t_in, res), n8, n8),
         "utf8_to_utf16le": (lambda: ug.utf8_to_utf16le_shard_async(
@@ -393,6 +435,16 @@ def measure_per_op(ug, t_all, off, n8, hb, ha, out16, u16, out8, dev, peak, reps
             u16, 0, n16, 0, 0, 0, out8, rec), 2 * n16, 2 * n16 + n8),
         "utf8_length_from_utf16le": (lambda: ug.utf8_length_from_utf16le_async(u16, lens),
                                      2 * n16, 2 * n16),
+        # the two-pass form: the sizing passes with their plans, the planned transcoders
+        "plan_utf8 (len16 + plan)": (lambda: ug.utf8_shard_plan_async(t_all, off, n8, hb, ha,
+                                                                       lens, p8), n8, n8),
+        "utf8_to_utf16le_planned": (lambda: ug.utf8_to_utf16le_shard_planned_async(
+            t_all, off, n8, hb, ha, 0, p8, out16, rec), n8, n8 + 2 * n16),
+        "plan_utf16le (len8 + plan)": (lambda: ug.utf16le_shard_plan_async(u16, 0, n16, 0, 0,
+                                                                            lens, p16),
+                                       2 * n16, 2 * n16),
+        "utf16le_to_utf8_planned": (lambda: ug.utf16le_to_utf8_shard_planned_async(
+            u16, 0, n16, 0, 0, 0, p16, out8, rec), 2 * n16, 2 * n16 + n8),
     }
     out = {}
     for name, (fn, in_bytes, hbm_bytes) in ops.items():
@@ -408,6 +460,66 @@ def measure_per_op(ug, t_all, off, n8, hb, ha, out16, u16, out8, dev, peak, reps
         out[name] = {"ms": round(ms, 4), "input_gbs": round(in_bytes / ms / 1e6, 1),
                      "hbm_gbs": round(hbm_bytes / ms / 1e6, 1),
                      "frac_of_peak": round(hbm_bytes / ms / 1e6 / peak, 4)}
+    return out
+
+
+def measure_per_config(ug, dev, peak, reps=10):
+    """Every hot-path op on BASELINE configs 1, 2A, 2B and 3 at their BASELINE.json sizes
+    (BASELINE.md section 2's targets): per op the mean CUDA-event time of `reps` async calls
+    (no host sync inside), input GB/s, Gchar/s, algorithmic HBM GB/s and its fraction of the
+    measured copy peak.  Each config's other-encoding counterpart (its transcoded output) is
+    produced by the library on the device first, so every op runs on that config's text."""
+    import torch
+    stream = torch.cuda.current_stream()
+    res = ug.result_buffer(dev, 1)
+    lens = torch.zeros(1, dtype=torch.int64, device=dev)
+    out = {}
+    for key in ("c1", "c2a", "c2b", "c3"):
+        cfg = synth.CONFIGS[key]
+        x = synth.generate(key)
+        if cfg.encoding == "utf8":
+            t8 = torch.from_numpy(x).to(dev)
+            n16 = ug.utf16_length_from_utf8(t8)
+            u16 = torch.empty(n16, dtype=torch.int16, device=dev)
+            assert ug.utf8_to_utf16le(t8, u16).error == 0
+        else:
+            u16 = torch.from_numpy(x.view(np.int16)).to(dev)
+            n8 = ug.utf8_length_from_utf16le(u16)
+            t8 = torch.empty(n8, dtype=torch.uint8, device=dev)
+            assert ug.utf16le_to_utf8(u16, t8).error == 0
+        del x
+        n8, n16 = t8.numel(), u16.numel()
+        chars = int(((t8 & 0xC0) != 0x80).sum())
+        o16 = torch.empty(n8, dtype=torch.int16, device=dev)
+        o8 = torch.empty(n8 + 64, dtype=torch.uint8, device=dev)
+        ops = {
+            "utf8_validate": (lambda: ug.utf8_validate_async(t8, res), n8, n8),
+            "utf8_to_utf16le": (lambda: ug.utf8_to_utf16le_async(t8, o16, res), n8, n8 + 2 * n16),
+            "utf16_length_from_utf8": (lambda: ug.utf16_length_from_utf8_async(t8, lens), n8, n8),
+            "utf16le_validate": (lambda: ug.utf16le_validate_async(u16, res), 2 * n16, 2 * n16),
+            "utf16le_to_utf8": (lambda: ug.utf16le_to_utf8_async(u16, o8, res), 2 * n16,
+                                2 * n16 + n8),
+            "utf8_length_from_utf16le": (lambda: ug.utf8_length_from_utf16le_async(u16, lens),
+                                         2 * n16, 2 * n16),
+        }
+        row = {"input": cfg.desc, "bytes_utf8": n8, "units_utf16": n16, "chars": chars}
+        for name, (fn, in_bytes, hbm_bytes) in ops.items():
+            fn()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for _ in range(reps):
+                fn()
+            e1.record(stream)
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / reps
+            row[name] = {"ms": round(ms, 4), "input_gbs": round(in_bytes / ms / 1e6, 1),
+                         "gchar_per_s": round(chars / ms / 1e6, 1),
+                         "hbm_gbs": round(hbm_bytes / ms / 1e6, 1),
+                         "frac_of_peak": round(hbm_bytes / ms / 1e6 / peak, 4)}
+        out[key] = row
+        del t8, u16, o16, o8
+        torch.cuda.empty_cache()
     return out
 
 
@@ -456,6 +568,38 @@ def oracle_step(oracle, chunk: np.ndarray):
     r2, back = oracle.utf16le_to_utf8(u, out_cap=n8)
     assert r1.error == 0 and r2.error == 0 and back.size == chunk.size
     return chunk.size + 2 * u.size
+
+
+def oracle_single_thread(cfg, nbytes=64 << 20):
+    """the oracle on ONE host core (the process pinned to it for
+    the measurement), the same four-op step on one 64 MiB chunk of the workload."""
+    import oracle
+    oracle.build()
+    data = np.frombuffer(synth.gen_chunk(cfg.mix, cfg.encoding, nbytes, cfg.seed, 0),
+                         dtype=np.uint8)
+    prev = os.sched_getaffinity(0) if hasattr(os, "sched_getaffinity") else None
+    core = min(prev) if prev else None
+    try:
+        if core is not None:
+            os.sched_setaffinity(0, {core})
+        t = time.perf_counter()
+        tot = oracle_step(oracle, data)
+        dt = time.perf_counter() - t
+    finally:
+        if prev is not None:
+            os.sched_setaffinity(0, prev)
+    cpu = ""
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                cpu = ln.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return {"value": round(tot / dt / 1e9, 4), "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": f"1 x {nbytes >> 20} MiB chunk of config {cfg.key}, pinned to core {core}; "
+                      f"step = len16 + utf8->utf16le + len8 + utf16le->utf8",
+            "seconds": round(dt, 2), "cpu_model": cpu}
 
 
 def cpu_baseline(cfg, size, chunks=None):

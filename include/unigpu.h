@@ -206,6 +206,85 @@ int ug_combine_records_async(const ug_shard_record *d_recs, int nranks, int rank
 ug_result ug_combine_records_host(const ug_shard_record *recs, int nranks, int rank,
                                   uint64_t total_in, uint64_t *out_offset);
 
+/* ------------------------------------------------------------------ two-pass (planned)
+ * Reduce-then-scan form of the two transcoders (DESIGN.md section 5,
+ * "planned").  A caller sizes the output with a length-from pass anyway; the *_plan_async
+ * forms of that pass also write a PLAN into the caller's device buffer d_plan
+ * (ug_plan_bytes() bytes, 8-byte aligned): the output count of each contiguous range of
+ * tiles the transcoder's CTAs will take, under the transcoder's own emission rule.  The
+ * *_planned_async transcoders then need no inter-CTA look-back: CTA c starts at the sum of
+ * the earlier ranges' counts.  Results, outputs, capacities and error conventions are exactly
+ * those of the plain calls.
+ *   d_len     receives the length-from value (utf16_length_from_utf8 /
+ *             utf8_length_from_utf16le; may be NULL);
+ *   d_plan    must come from the plan call on the SAME input pointer, n and halos, on the same
+ *             device, and stay unmodified until the planned call has run (stream order);
+ *             a plan of another input makes the planned call's result {UG_ERR_ARG, 0, 0}
+ *             (checked on the device against the plan's header);
+ *   returns   UG_OK once enqueued, UG_ERR_ARG (NULL / misaligned pointers, n too large),
+ *             UG_ERR_CUDA. */
+size_t ug_plan_bytes(void);
+int ug_utf16_length_from_utf8_plan_async(const uint8_t *in, size_t n, uint64_t *d_len,
+                                         void *d_plan, void *stream);
+int ug_utf8_length_from_utf16le_plan_async(const uint16_t *in, size_t n, uint64_t *d_len,
+                                           void *d_plan, void *stream);
+int ug_utf8_to_utf16le_planned_async(const uint8_t *in, size_t n, const void *d_plan,
+                                     uint16_t *out, size_t out_cap, ug_result *d_result,
+                                     void *stream);
+int ug_utf16le_to_utf8_planned_async(const uint16_t *in, size_t n, const void *d_plan,
+                                     uint8_t *out, size_t out_cap, ug_result *d_result,
+                                     void *stream);
+/* Shard forms (the window conventions of ug_*_shard_async; the plan covers the owned range). */
+int ug_utf8_shard_plan_async(const uint8_t *in, size_t n, size_t halo_before, size_t halo_after,
+                             uint64_t *d_len, void *d_plan, void *stream);
+int ug_utf16le_shard_plan_async(const uint16_t *in, size_t n, size_t halo_before,
+                                size_t halo_after, uint64_t *d_len, void *d_plan, void *stream);
+int ug_utf8_to_utf16le_shard_planned_async(const uint8_t *in, size_t n, size_t halo_before,
+                                           size_t halo_after, uint64_t in_global_offset,
+                                           const void *d_plan, uint16_t *out, size_t out_cap,
+                                           ug_shard_record *d_rec, void *stream);
+int ug_utf16le_to_utf8_shard_planned_async(const uint16_t *in, size_t n, size_t halo_before,
+                                           size_t halo_after, uint64_t in_global_offset,
+                                           const void *d_plan, uint8_t *out, size_t out_cap,
+                                           ug_shard_record *d_rec, void *stream);
+
+/* ------------------------------------------------------------------ multi-GPU, one process
+ * The whole sharded step for a C caller that drives several devices from one process
+ * (BASELINE north_star item 3): shard k runs on shards[k].device with its
+ * stream; the 32-byte records are exchanged device to device (cudaMemcpyPeerAsync; a plain
+ * device copy when two shards share a device) and every shard's device combines them
+ * (k_combine), so each device ends with the global result and its own output offset.
+ * Shards must be given in input order; each descriptor is exactly the arguments of the
+ * matching ug_*_shard_async call (cuts at character starts, e.g. by
+ * ug_utf8_cut_backoff), shard k + 1 starting where shard k ends (in_global_offset).
+ * Positions in the result are in that global numbering (success: position = the end offset
+ * of the last shard; error: the global first-error offset); `written` counts output units
+ * from shard 0's output start.  Outputs stay sharded: shard k's units are out[0..count_k) at
+ * global output offset out_offsets[k].
+ *   ug_sharded_*():  synchronous; returns the global ug_result and, if out_offsets is not
+ *                    NULL, each shard's global output offset (host array of nshards);
+ *   errors:          UG_ERR_ARG (nshards < 1 or > 1024, bad descriptor: the shard call's own
+ *                    checks), UG_ERR_CUDA (a launch, peer copy or synchronisation failed;
+ *                    e.g. no peer access between two devices). */
+typedef struct {
+  int device;              /* CUDA device ordinal of this shard                            */
+  const void *in;          /* first OWNED unit (device pointer on `device`)               */
+  size_t n;                /* owned units                                                  */
+  size_t halo_before;      /* readable context units before `in` (<= 3 / 1 used)           */
+  size_t halo_after;       /* readable context units after in[n - 1]                       */
+  uint64_t in_global_offset;  /* offset of in[0] in the whole input                        */
+  void *out;               /* this shard's output (device pointer on `device`), or NULL    */
+  size_t out_cap;          /* output capacity in units                                     */
+  void *stream;            /* a stream of `device` (NULL = its legacy default stream)      */
+} ug_shard_desc;
+
+ug_result ug_sharded_utf8_to_utf16le(const ug_shard_desc *shards, int nshards,
+                                     uint64_t *out_offsets);
+ug_result ug_sharded_utf16le_to_utf8(const ug_shard_desc *shards, int nshards,
+                                     uint64_t *out_offsets);
+ug_result ug_sharded_utf8_validate(const ug_shard_desc *shards, int nshards);
+ug_result ug_sharded_utf16le_validate(const ug_shard_desc *shards, int nshards);
+
 /* Cut rule on HOST memory: how many units to move a nominal cut back
  * so that it falls on a character start.  `at` points at the unit at the nominal cut; up to
  * `avail_before` units before it are readable.  UTF-8: back off over at most 3 continuation

@@ -36,6 +36,13 @@ class _CResult(ctypes.Structure):
                 ("position", ctypes.c_uint64), ("written", ctypes.c_uint64)]
 
 
+class _CShardDesc(ctypes.Structure):
+    _fields_ = [("device", ctypes.c_int), ("in_", ctypes.c_void_p), ("n", ctypes.c_size_t),
+                ("halo_before", ctypes.c_size_t), ("halo_after", ctypes.c_size_t),
+                ("in_global_offset", ctypes.c_uint64), ("out", ctypes.c_void_p),
+                ("out_cap", ctypes.c_size_t), ("stream", ctypes.c_void_p)]
+
+
 class ShardRecord(NamedTuple):
     count: int
     first_err: int
@@ -104,6 +111,19 @@ def _load():
         "ug_release_workspaces": ([], None),
         "ug_abi_version": ([], I),
         "ug_tile_bytes": ([], S),
+        "ug_plan_bytes": ([], S),
+        "ug_utf16_length_from_utf8_plan_async": ([P, S, P, P, P], I),
+        "ug_utf8_length_from_utf16le_plan_async": ([P, S, P, P, P], I),
+        "ug_utf8_to_utf16le_planned_async": ([P, S, P, P, S, P, P], I),
+        "ug_utf16le_to_utf8_planned_async": ([P, S, P, P, S, P, P], I),
+        "ug_utf8_shard_plan_async": ([P, S, S, S, P, P, P], I),
+        "ug_utf16le_shard_plan_async": ([P, S, S, S, P, P, P], I),
+        "ug_utf8_to_utf16le_shard_planned_async": ([P, S, S, S, U64, P, P, S, P, P], I),
+        "ug_utf16le_to_utf8_shard_planned_async": ([P, S, S, S, U64, P, P, S, P, P], I),
+        "ug_sharded_utf8_to_utf16le": ([P, I, P], _CResult),
+        "ug_sharded_utf16le_to_utf8": ([P, I, P], _CResult),
+        "ug_sharded_utf8_validate": ([P, I], _CResult),
+        "ug_sharded_utf16le_validate": ([P, I], _CResult),
         "ug_workspace_bytes": ([P], S),
         "ug_utf16_length_from_utf8_ex": ([P, S, P, P], I),
         "ug_utf8_length_from_utf16le_ex": ([P, S, P, P], I),
@@ -422,6 +442,154 @@ def combine_records_host(records: list, rank: int, total_in: int):
     return _res(r), int(off.value)
 
 
+# --------------------------------------------------------------------------- two-pass (planned)
+def plan_buffer(device=None):
+    """Device buffer for one plan (ug_plan_bytes() bytes)."""
+    import torch
+    return torch.zeros(int(lib.ug_plan_bytes()), dtype=torch.uint8, device=device or "cuda")
+
+
+def utf16_length_from_utf8_plan_async(t_in, d_len, d_plan, n=None, stream=None, len_off=0):
+    """utf16_length_from_utf8 into d_len[len_off] AND the plan of utf8_to_utf16le_planned."""
+    _check(lib.ug_utf16_length_from_utf8_plan_async(
+        _ptr(t_in), _units(t_in) if n is None else n, _at(d_len, len_off), _ptr(d_plan),
+        _stream(stream)), "utf16_length_from_utf8_plan_async")
+
+
+def utf8_length_from_utf16le_plan_async(t_in, d_len, d_plan, n=None, stream=None, len_off=0):
+    _check(lib.ug_utf8_length_from_utf16le_plan_async(
+        _ptr(t_in), _units(t_in) if n is None else n, _at(d_len, len_off), _ptr(d_plan),
+        _stream(stream)), "utf8_length_from_utf16le_plan_async")
+
+
+def utf8_to_utf16le_planned_async(t_in, d_plan, t_out, d_result, n=None, out_cap=None,
+                                  stream=None, result_off=0):
+    _check(lib.ug_utf8_to_utf16le_planned_async(
+        _ptr(t_in), _units(t_in) if n is None else n, _ptr(d_plan), _ptr(t_out),
+        _units(t_out) if out_cap is None else out_cap, _at(d_result, result_off),
+        _stream(stream)), "utf8_to_utf16le_planned_async")
+
+
+def utf16le_to_utf8_planned_async(t_in, d_plan, t_out, d_result, n=None, out_cap=None,
+                                  stream=None, result_off=0):
+    _check(lib.ug_utf16le_to_utf8_planned_async(
+        _ptr(t_in), _units(t_in) if n is None else n, _ptr(d_plan), _ptr(t_out),
+        _units(t_out) if out_cap is None else out_cap, _at(d_result, result_off),
+        _stream(stream)), "utf16le_to_utf8_planned_async")
+
+
+def utf8_shard_plan_async(t_in, offset, n, halo_before, halo_after, d_len, d_plan, stream=None,
+                          len_off=0):
+    _check(lib.ug_utf8_shard_plan_async(_at(t_in, offset), n, halo_before, halo_after,
+                                        _at(d_len, len_off), _ptr(d_plan), _stream(stream)),
+           "utf8_shard_plan_async")
+
+
+def utf16le_shard_plan_async(t_in, offset, n, halo_before, halo_after, d_len, d_plan,
+                             stream=None, len_off=0):
+    _check(lib.ug_utf16le_shard_plan_async(_at(t_in, 2 * offset), n, halo_before, halo_after,
+                                           _at(d_len, len_off), _ptr(d_plan), _stream(stream)),
+           "utf16le_shard_plan_async")
+
+
+def utf8_to_utf16le_shard_planned_async(t_in, offset, n, halo_before, halo_after, global_off,
+                                        d_plan, t_out, d_rec, out_cap=None, stream=None,
+                                        rec_off=0):
+    _check(lib.ug_utf8_to_utf16le_shard_planned_async(
+        _at(t_in, offset), n, halo_before, halo_after, global_off, _ptr(d_plan), _ptr(t_out),
+        _units(t_out) if out_cap is None else out_cap, _at(d_rec, rec_off), _stream(stream)),
+        "utf8_to_utf16le_shard_planned_async")
+
+
+def utf16le_to_utf8_shard_planned_async(t_in, offset, n, halo_before, halo_after, global_off,
+                                        d_plan, t_out, d_rec, out_cap=None, stream=None,
+                                        rec_off=0):
+    _check(lib.ug_utf16le_to_utf8_shard_planned_async(
+        _at(t_in, 2 * offset), n, halo_before, halo_after, global_off, _ptr(d_plan),
+        _ptr(t_out), _units(t_out) if out_cap is None else out_cap, _at(d_rec, rec_off),
+        _stream(stream)), "utf16le_to_utf8_shard_planned_async")
+
+
+def utf8_to_utf16le_two_pass(t_in, t_out, n=None, out_cap=None):
+    """Convenience: plan (with the length) + planned transcode, synchronously.
+    Returns (Result, utf16 length)."""
+    import torch
+    dev = t_in.device
+    plan, lens, res = plan_buffer(dev), torch.zeros(1, dtype=torch.int64, device=dev), \
+        result_buffer(dev, 1)
+    utf16_length_from_utf8_plan_async(t_in, lens, plan, n=n)
+    utf8_to_utf16le_planned_async(t_in, plan, t_out, res, n=n, out_cap=out_cap)
+    return decode_results(res)[0], int(lens[0])
+
+
+def utf16le_to_utf8_two_pass(t_in, t_out, n=None, out_cap=None):
+    import torch
+    dev = t_in.device
+    plan, lens, res = plan_buffer(dev), torch.zeros(1, dtype=torch.int64, device=dev), \
+        result_buffer(dev, 1)
+    utf8_length_from_utf16le_plan_async(t_in, lens, plan, n=n)
+    utf16le_to_utf8_planned_async(t_in, plan, t_out, res, n=n, out_cap=out_cap)
+    return decode_results(res)[0], int(lens[0])
+
+
+# --------------------------------------------------------------------------- multi-GPU (C entry)
+def _shard_descs(shards, unit_bytes):
+    arr = (_CShardDesc * len(shards))()
+    for i, sd in enumerate(shards):
+        t_in, off, n, hb, ha, gofs = sd["t_in"], sd["offset"], sd["n"], sd["halo_before"], \
+            sd["halo_after"], sd["global_off"]
+        if not t_in.is_cuda or t_in.element_size() != unit_bytes or not t_in.is_contiguous():
+            raise ValueError("sharded: t_in must be a contiguous CUDA tensor of "
+                             f"{unit_bytes}-byte units")
+        if off - hb < 0 or off + n + ha > t_in.numel():
+            raise ValueError("sharded: shard range / halos outside its input tensor")
+        t_out = sd.get("t_out")
+        cap = sd.get("out_cap", t_out.numel() if t_out is not None else 0)
+        if t_out is not None and (not t_out.is_cuda or cap > t_out.numel() or
+                                  t_out.device != t_in.device):
+            raise ValueError("sharded: bad output tensor / capacity")
+        stream = sd.get("stream")
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream(t_in.device)
+        arr[i].device = t_in.device.index
+        arr[i].in_ = t_in.data_ptr() + unit_bytes * off
+        arr[i].n, arr[i].halo_before, arr[i].halo_after = n, hb, ha
+        arr[i].in_global_offset = gofs
+        arr[i].out = t_out.data_ptr() if t_out is not None else None
+        arr[i].out_cap = cap
+        arr[i].stream = stream if isinstance(stream, int) else stream.cuda_stream
+    return arr
+
+
+def _sharded(fn, shards, unit_bytes, offsets):
+    arr = _shard_descs(shards, unit_bytes)
+    if offsets:
+        offs = (ctypes.c_uint64 * len(shards))()
+        r = fn(ctypes.cast(arr, ctypes.c_void_p), len(shards), ctypes.cast(offs, ctypes.c_void_p))
+        return _res(r), [int(x) for x in offs]
+    return _res(fn(ctypes.cast(arr, ctypes.c_void_p), len(shards)))
+
+
+def sharded_utf8_to_utf16le(shards):
+    """The whole sharded step from ONE process over several devices (C entry
+    ug_sharded_utf8_to_utf16le): shards = [{t_in, offset, n, halo_before, halo_after,
+    global_off, t_out[, out_cap, stream]}] in input order.  Returns (Result, out_offsets)."""
+    return _sharded(lib.ug_sharded_utf8_to_utf16le, shards, 1, True)
+
+
+def sharded_utf16le_to_utf8(shards):
+    return _sharded(lib.ug_sharded_utf16le_to_utf8, shards, 2, True)
+
+
+def sharded_utf8_validate(shards):
+    return _sharded(lib.ug_sharded_utf8_validate, shards, 1, False)
+
+
+def sharded_utf16le_validate(shards):
+    return _sharded(lib.ug_sharded_utf16le_validate, shards, 2, False)
+
+
 def utf8_cut_backoff(buf: bytes | bytearray, at: int) -> int:
     """Units to move a nominal cut at index `at` of a HOST buffer back to a char start."""
     b = (ctypes.c_uint8 * len(buf)).from_buffer_copy(bytes(buf))
@@ -497,7 +665,8 @@ def _validate(t, es, host, what, fname):
         raise ValueError(f"{fname}: {what} must be a CUDA tensor (no CPU fallback)")
 
 
-_SLOT_BYTES = {"d_result": ("result_off", 24), "d_len": ("len_off", 8), "d_rec": ("rec_off", 32)}
+_SLOT_BYTES = {"d_result": ("result_off", 24), "d_len": ("len_off", 8), "d_rec": ("rec_off", 32),
+               "d_plan": (None, 0)}
 
 
 def _checked(fname, fn):
@@ -549,7 +718,9 @@ def _checked(fname, fn):
                 continue
             if not isinstance(t, torch.Tensor) or not t.is_cuda or not t.is_contiguous():
                 raise ValueError(f"{fname}: {nm} must be a contiguous CUDA tensor")
-            if (a.get(offnm) or 0) + size > t.numel() * t.element_size():
+            if nm == "d_plan":
+                size = int(lib.ug_plan_bytes())
+            if ((a.get(offnm) or 0) if offnm else 0) + size > t.numel() * t.element_size():
                 raise ValueError(f"{fname}: {nm} holds no {size}-byte slot at byte offset "
                                  f"{a.get(offnm) or 0}")
             devs.add(t.device.index)
@@ -574,6 +745,10 @@ for _n in ("utf8_validate", "utf16le_validate", "utf8_to_utf16le", "utf16le_to_u
            "utf8_to_utf16be_shard_async", "utf16be_to_utf8_shard_async",
            "utf16be_validate_shard_async",
            "utf8_to_utf16le_host", "utf16le_to_utf8_host", "utf8_to_utf16be_host",
-           "utf16be_to_utf8_host"):
+           "utf16be_to_utf8_host",
+           "utf16_length_from_utf8_plan_async", "utf8_length_from_utf16le_plan_async",
+           "utf8_to_utf16le_planned_async", "utf16le_to_utf8_planned_async",
+           "utf8_shard_plan_async", "utf16le_shard_plan_async",
+           "utf8_to_utf16le_shard_planned_async", "utf16le_to_utf8_shard_planned_async"):
     globals()[_n] = _checked(_n, globals()[_n])
 del _n

@@ -55,6 +55,7 @@ struct Workspace {
 struct DeviceInfo {
   int sms = 0;
   int occ[NUM_OPS] = {};
+  int occ_planned[2] = {};  // planned transcoders: UTF-8 input, UTF-16 input
   bool configured = false;
 };
 
@@ -74,6 +75,16 @@ cudaError_t device_info(int dev, DeviceInfo **out) {
       e = tile_occupancy((Op)i, &d.occ[i]);
       if (e != cudaSuccess) return e;
       if (d.occ[i] < 1) d.occ[i] = 1;
+    }
+    for (int u = 0; u < 2; u++) {
+      const Op op = u ? Op::U16_TO_U8 : Op::U8_TO_U16;
+      e = planned_configure(op);
+      if (e == cudaSuccess) e = planned_configure(u ? Op::U16BE_TO_U8 : Op::U8_TO_U16BE);
+      if (e != cudaSuccess) return e;
+      e = planned_occupancy(op, &d.occ_planned[u]);
+      if (e != cudaSuccess) return e;
+      if (d.occ_planned[u] < 1) d.occ_planned[u] = 1;
+      if (d.occ_planned[u] > CTAS_PER_SM) d.occ_planned[u] = CTAS_PER_SM;
     }
     d.configured = true;
   }
@@ -204,6 +215,88 @@ int enqueue_empty(ResultDev *d_result, RecordDev *d_rec, cudaStream_t s) {
         cudaMemsetAsync(&d_rec->first_err, 0xFF, sizeof(d_rec->first_err), s) != cudaSuccess)
       return UG_ERR_CUDA;
   }
+  return UG_OK;
+}
+
+// ---- planned (two-pass) path (kernels.cu "planned"): the plan call and the planned call must
+// see the same window; both derive the transcoder grid R and the 2R sub-ranges from the
+// device, so the plan's sub-ranges are exactly the planned kernel's CTA ranges.
+struct PlanGeo {
+  Window win;
+  unsigned long long ntiles;
+  int grid, nsub;
+  unsigned long long tps;
+};
+PlanGeo plan_geo(DeviceInfo *di, bool u16in, const void *in, unsigned long long n,
+                 unsigned long long hb, unsigned long long ha) {
+  const unsigned long long us = u16in ? 2 : 1;
+  PlanGeo g;
+  g.win = make_window(in, n * us, hb * us, ha * us);
+  g.ntiles = (unsigned long long)((g.win.n - 1 + g.win.lead) / TILE + 1);
+  g.grid = di->sms * di->occ_planned[u16in ? 1 : 0];
+  // sub-ranges of tps tiles, PLAN_SUBS_PER_CTA per CTA (taken by ticket: load balance)
+  unsigned long long want = (unsigned long long)g.grid * PLAN_SUBS_PER_CTA;
+  if (want > (unsigned long long)(PLAN_WORDS - 8)) want = PLAN_WORDS - 8;
+  if (want > g.ntiles) want = g.ntiles;
+  g.tps = (g.ntiles + want - 1) / want;
+  g.nsub = (int)((g.ntiles + g.tps - 1) / g.tps);
+  return g;
+}
+
+int enqueue_plan(Op op, const void *in, unsigned long long n, unsigned long long hb,
+                 unsigned long long ha, unsigned long long *d_len, void *d_plan, cudaStream_t s) {
+  const bool u16in = op_u16_input(op);
+  if (d_plan == nullptr) return UG_ERR_ARG;
+  if (n > MAX_N || (n > 0 && in == nullptr) || (u16in && ((uintptr_t)in & 1u)) ||
+      ((uintptr_t)d_plan & 7u))
+    return UG_ERR_ARG;
+  if (n == 0)
+    return (d_len == nullptr || cudaMemsetAsync(d_len, 0, sizeof(*d_len), s) == cudaSuccess)
+               ? UG_OK
+               : UG_ERR_CUDA;
+  Workspace *w;
+  if (get_ws(s, &w) != cudaSuccess) return UG_ERR_CUDA;
+  DeviceInfo *di;
+  if (device_info(w->device, &di) != cudaSuccess) return UG_ERR_CUDA;
+  std::lock_guard<std::mutex> lk(w->mu);
+  const PlanGeo g = plan_geo(di, u16in, in, n, hb, ha);
+  if (launch_plan(u16in, op == Op::U16BE_TO_U8, g.win, g.ntiles, g.nsub, g.tps,
+                  (unsigned long long *)d_plan, w->ctr, d_len, s) != cudaSuccess)
+    return UG_ERR_CUDA;
+  g_launches.fetch_add(1);
+  return UG_OK;
+}
+
+int enqueue_planned(Op op, const void *in, unsigned long long n, unsigned long long hb,
+                    unsigned long long ha, unsigned long long global_off, const void *d_plan,
+                    void *out, unsigned long long out_cap, ResultDev *d_result, RecordDev *d_rec,
+                    cudaStream_t s) {
+  const int rc = check_tile_args(op, in, n, out, out_cap);
+  if (rc != UG_OK) return rc;
+  if (d_plan == nullptr || ((uintptr_t)d_plan & 7u)) return UG_ERR_ARG;
+  if (n == 0) return enqueue_empty(d_result, d_rec, s);
+  Workspace *w;
+  if (get_ws(s, &w) != cudaSuccess) return UG_ERR_CUDA;
+  DeviceInfo *di;
+  if (device_info(w->device, &di) != cudaSuccess) return UG_ERR_CUDA;
+  std::lock_guard<std::mutex> lk(w->mu);
+  const PlanGeo g = plan_geo(di, op_u16_input(op), in, n, hb, ha);
+  TileArgs a;
+  std::memset(&a, 0, sizeof(a));
+  a.win = g.win;
+  a.ntiles = g.ntiles;
+  a.out = out;
+  a.out_cap = out ? out_cap : 0;
+  if (ensure_status(w, a.ntiles) != cudaSuccess) return UG_ERR_CUDA;
+  a.status = w->status;
+  a.epoch = next_epoch(w);
+  a.ctr = w->ctr;
+  a.result = d_result;
+  a.rec = d_rec;
+  a.global_off = global_off;
+  if (launch_planned(op, a, (const unsigned long long *)d_plan, g.grid, s) != cudaSuccess)
+    return UG_ERR_CUDA;
+  g_launches.fetch_add(1);
   return UG_OK;
 }
 
@@ -711,6 +804,201 @@ size_t ug_utf16_cut_backoff(const uint16_t *at, size_t avail_before) {
 size_t ug_utf16be_cut_backoff(const uint16_t *at, size_t avail_before) {
   const uint32_t w = ((at[0] >> 8) | (at[0] << 8)) & 0xFFFFu;  // the big-endian unit
   return ((w & 0xFC00u) == 0xDC00u && avail_before >= 1) ? 1 : 0;
+}
+
+// ---- planned (two-pass) entry points (include/unigpu.h "two-pass")
+size_t ug_plan_bytes(void) { return (size_t)PLAN_WORDS * 8; }
+int ug_utf16_length_from_utf8_plan_async(const uint8_t *in, size_t n, uint64_t *d_len,
+                                         void *d_plan, void *stream) {
+  return enqueue_plan(Op::U8_TO_U16, in, n, 0, 0, (unsigned long long *)d_len, d_plan,
+                      (cudaStream_t)stream);
+}
+int ug_utf8_length_from_utf16le_plan_async(const uint16_t *in, size_t n, uint64_t *d_len,
+                                           void *d_plan, void *stream) {
+  return enqueue_plan(Op::U16_TO_U8, in, n, 0, 0, (unsigned long long *)d_len, d_plan,
+                      (cudaStream_t)stream);
+}
+int ug_utf8_to_utf16le_planned_async(const uint8_t *in, size_t n, const void *d_plan,
+                                     uint16_t *out, size_t out_cap, ug_result *d_result,
+                                     void *stream) {
+  if (!d_result) return UG_ERR_ARG;
+  return enqueue_planned(Op::U8_TO_U16, in, n, 0, 0, 0, d_plan, out, out_cap,
+                         (ResultDev *)d_result, nullptr, (cudaStream_t)stream);
+}
+int ug_utf16le_to_utf8_planned_async(const uint16_t *in, size_t n, const void *d_plan,
+                                     uint8_t *out, size_t out_cap, ug_result *d_result,
+                                     void *stream) {
+  if (!d_result) return UG_ERR_ARG;
+  return enqueue_planned(Op::U16_TO_U8, in, n, 0, 0, 0, d_plan, out, out_cap,
+                         (ResultDev *)d_result, nullptr, (cudaStream_t)stream);
+}
+int ug_utf8_shard_plan_async(const uint8_t *in, size_t n, size_t halo_before, size_t halo_after,
+                             uint64_t *d_len, void *d_plan, void *stream) {
+  return enqueue_plan(Op::U8_TO_U16, in, n, clamp_halo(halo_before, 3), clamp_halo(halo_after, 3),
+                      (unsigned long long *)d_len, d_plan, (cudaStream_t)stream);
+}
+int ug_utf16le_shard_plan_async(const uint16_t *in, size_t n, size_t halo_before,
+                                size_t halo_after, uint64_t *d_len, void *d_plan, void *stream) {
+  return enqueue_plan(Op::U16_TO_U8, in, n, clamp_halo(halo_before, 1), clamp_halo(halo_after, 1),
+                      (unsigned long long *)d_len, d_plan, (cudaStream_t)stream);
+}
+int ug_utf8_to_utf16le_shard_planned_async(const uint8_t *in, size_t n, size_t halo_before,
+                                           size_t halo_after, uint64_t in_global_offset,
+                                           const void *d_plan, uint16_t *out, size_t out_cap,
+                                           ug_shard_record *d_rec, void *stream) {
+  if (!d_rec) return UG_ERR_ARG;
+  return enqueue_planned(Op::U8_TO_U16, in, n, clamp_halo(halo_before, 3),
+                         clamp_halo(halo_after, 3), in_global_offset, d_plan, out, out_cap,
+                         nullptr, (RecordDev *)d_rec, (cudaStream_t)stream);
+}
+int ug_utf16le_to_utf8_shard_planned_async(const uint16_t *in, size_t n, size_t halo_before,
+                                           size_t halo_after, uint64_t in_global_offset,
+                                           const void *d_plan, uint8_t *out, size_t out_cap,
+                                           ug_shard_record *d_rec, void *stream) {
+  if (!d_rec) return UG_ERR_ARG;
+  return enqueue_planned(Op::U16_TO_U8, in, n, clamp_halo(halo_before, 1),
+                         clamp_halo(halo_after, 1), in_global_offset, d_plan, out, out_cap,
+                         nullptr, (RecordDev *)d_rec, (cudaStream_t)stream);
+}
+
+// ---- multi-GPU from one process (include/unigpu.h "multi-GPU, one process")
+namespace {
+constexpr int MAX_SHARDS = 1024;
+struct DevCtx {  // per (device, stream): the gather buffer and per-shard results
+  RecordDev *recs = nullptr;  // nshards records, the all-gather target on this device
+  ResultDev *res = nullptr;   // per shard index (shards may share a device and a stream)
+  unsigned long long *off = nullptr;
+  ResultDev *h_res = nullptr;  // pinned
+  unsigned long long *h_off = nullptr;
+  int cap = 0;
+};
+std::mutex g_shard_mu;
+std::map<std::pair<int, uintptr_t>, DevCtx> g_shard_ctx;  // (device, stream)
+
+cudaError_t shard_ctx(int dev, cudaStream_t s, int nshards, DevCtx **out) {
+  DevCtx &c = g_shard_ctx[std::make_pair(dev, (uintptr_t)s)];
+  if (c.cap < nshards) {
+    cudaError_t e;
+    if (c.recs) {
+      cudaStreamSynchronize(s);
+      cudaFree(c.recs);
+      cudaFree(c.res);
+      cudaFree(c.off);
+      cudaFreeHost(c.h_res);
+      cudaFreeHost(c.h_off);
+    }
+    c = DevCtx();
+    if ((e = cudaMalloc(&c.recs, nshards * sizeof(RecordDev))) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&c.res, nshards * sizeof(ResultDev))) != cudaSuccess) return e;
+    if ((e = cudaMalloc(&c.off, nshards * sizeof(unsigned long long))) != cudaSuccess) return e;
+    if ((e = cudaMallocHost(&c.h_res, nshards * sizeof(ResultDev))) != cudaSuccess) return e;
+    if ((e = cudaMallocHost(&c.h_off, nshards * sizeof(unsigned long long))) != cudaSuccess)
+      return e;
+    c.cap = nshards;
+  }
+  *out = &c;
+  return cudaSuccess;
+}
+
+// All shards' kernels, the record all-gather (peer copies: shard j's record lands in slot j of
+// every shard's gather buffer), every shard's combine, then the result / offsets read back.
+ug_result run_sharded(Op op, const ug_shard_desc *sh, int ns, uint64_t *out_offsets) {
+  if (!sh || ns < 1 || ns > MAX_SHARDS) return make_result(UG_ERR_ARG, 0, 0);
+  const bool u16in = op_u16_input(op);
+  const unsigned long long hmax = u16in ? 1 : 3;
+  for (int k = 0; k < ns; k++) {
+    const int rc = check_tile_args(op, sh[k].in, sh[k].n, sh[k].out, sh[k].out_cap);
+    if (rc != UG_OK) return make_result(rc, 0, 0);
+    if (k > 0 && sh[k].in_global_offset != sh[k - 1].in_global_offset + sh[k - 1].n)
+      return make_result(UG_ERR_ARG, 0, 0);  // shards must tile the input in order
+  }
+  int prev_dev;
+  if (cudaGetDevice(&prev_dev) != cudaSuccess) return make_result(UG_ERR_CUDA, 0, 0);
+  std::lock_guard<std::mutex> lk(g_shard_mu);
+  std::vector<DevCtx *> ctx(ns);
+  std::vector<cudaEvent_t> done(ns, nullptr);
+  int rc = UG_OK;
+  auto fail = [&](int code) {
+    rc = code;
+    return code;
+  };
+  const unsigned long long total_in = sh[ns - 1].in_global_offset + sh[ns - 1].n -
+                                      sh[0].in_global_offset;
+  // 1. every shard's kernel writes its record into slot k of its own gather buffer
+  for (int k = 0; k < ns && rc == UG_OK; k++) {
+    const cudaStream_t s = (cudaStream_t)sh[k].stream;
+    if (cudaSetDevice(sh[k].device) != cudaSuccess ||
+        shard_ctx(sh[k].device, s, ns, &ctx[k]) != cudaSuccess ||
+        cudaEventCreateWithFlags(&done[k], cudaEventDisableTiming) != cudaSuccess) {
+      fail(UG_ERR_CUDA);
+      break;
+    }
+    const unsigned long long hb = sh[k].halo_before < hmax ? sh[k].halo_before : hmax;
+    const unsigned long long ha = sh[k].halo_after < hmax ? sh[k].halo_after : hmax;
+    const int e = enqueue_tile(op, sh[k].in, sh[k].n, hb, ha, sh[k].in_global_offset, sh[k].out,
+                               sh[k].out ? sh[k].out_cap : 0, nullptr, ctx[k]->recs + k, s);
+    if (e != UG_OK || cudaEventRecord(done[k], s) != cudaSuccess) fail(e != UG_OK ? e : UG_ERR_CUDA);
+  }
+  // 2. all-gather: record k from shard k's device into slot k of every other shard's buffer
+  for (int j = 0; j < ns && rc == UG_OK; j++) {
+    const cudaStream_t s = (cudaStream_t)sh[j].stream;
+    if (cudaSetDevice(sh[j].device) != cudaSuccess) {
+      fail(UG_ERR_CUDA);
+      break;
+    }
+    for (int k = 0; k < ns && rc == UG_OK; k++) {
+      if (k == j) continue;
+      if (cudaStreamWaitEvent(s, done[k], 0) != cudaSuccess ||
+          cudaMemcpyPeerAsync(ctx[j]->recs + k, sh[j].device, ctx[k]->recs + k, sh[k].device,
+                              sizeof(RecordDev), s) != cudaSuccess)
+        fail(UG_ERR_CUDA);
+    }
+    // 3. this shard's combine -> global result and its output offset, to pinned memory
+    if (rc == UG_OK &&
+        (launch_combine(ctx[j]->recs, ns, j, sh[0].in_global_offset + total_in, ctx[j]->res + j,
+                        ctx[j]->off + j, s) != cudaSuccess ||
+         cudaMemcpyAsync(ctx[j]->h_res + j, ctx[j]->res + j, sizeof(ResultDev),
+                         cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+         cudaMemcpyAsync(ctx[j]->h_off + j, ctx[j]->off + j, sizeof(unsigned long long),
+                         cudaMemcpyDeviceToHost, s) != cudaSuccess))
+      fail(UG_ERR_CUDA);
+    if (rc == UG_OK) g_launches.fetch_add(1);
+  }
+  // 4. wait for every shard's stream (also after a failure: nothing may still be in flight)
+  for (int j = 0; j < ns; j++) {
+    if (cudaSetDevice(sh[j].device) == cudaSuccess) {
+      if (cudaStreamSynchronize((cudaStream_t)sh[j].stream) != cudaSuccess) fail(UG_ERR_CUDA);
+    }
+    if (done[j]) cudaEventDestroy(done[j]);
+  }
+  cudaSetDevice(prev_dev);
+  if (rc != UG_OK) return make_result(rc, 0, 0);
+  ug_result r;
+  std::memcpy(&r, ctx[0]->h_res, sizeof(r));
+  for (int j = 0; j < ns; j++) {
+    ug_result rj;
+    std::memcpy(&rj, ctx[j]->h_res + j, sizeof(rj));
+    if (rj.error != r.error || rj.written != r.written || rj.position != r.position)
+      return make_result(UG_ERR_CUDA, 0, 0);  // the shards disagree: a transfer went wrong
+    if (out_offsets) out_offsets[j] = ctx[j]->h_off[j];
+  }
+  return r;
+}
+}  // namespace
+
+ug_result ug_sharded_utf8_to_utf16le(const ug_shard_desc *shards, int nshards,
+                                     uint64_t *out_offsets) {
+  return run_sharded(Op::U8_TO_U16, shards, nshards, out_offsets);
+}
+ug_result ug_sharded_utf16le_to_utf8(const ug_shard_desc *shards, int nshards,
+                                     uint64_t *out_offsets) {
+  return run_sharded(Op::U16_TO_U8, shards, nshards, out_offsets);
+}
+ug_result ug_sharded_utf8_validate(const ug_shard_desc *shards, int nshards) {
+  return run_sharded(Op::U8_VALIDATE, shards, nshards, nullptr);
+}
+ug_result ug_sharded_utf16le_validate(const ug_shard_desc *shards, int nshards) {
+  return run_sharded(Op::U16_VALIDATE, shards, nshards, nullptr);
 }
 
 ug_result utf8_to_utf16le_host(const uint8_t *in_host, size_t n, uint16_t *out_host,

@@ -45,7 +45,8 @@ struct Counters {
   uint32_t done;      // CTAs finished
   unsigned long long err_min;  // smallest error position found (NONE = none)
   unsigned long long accum;    // reduction accumulator (length-from kernels)
-  unsigned long long pad;
+  unsigned long long pad;      // second accumulator (plan kernels)
+  unsigned long long flags;    // bit 0: a planned transcoder was given a plan of other input
 };
 
 // ---------------------------------------------------------------- status words

@@ -60,6 +60,21 @@ cudaError_t tile_configure(Op op);  // set max dynamic smem (idempotent)
 cudaError_t tile_occupancy(Op op, int *blocks_per_sm);
 cudaError_t launch_tile(Op op, const TileArgs &a, int grid, cudaStream_t s);
 
+// planned (two-pass) path: plan kernels and the planned transcoders
+constexpr int PLAN_WORDS = 8 + 8192;  // header + sub-range offsets (kernels.cu PLAN_*)
+#ifndef UG_PLAN_SUBS
+#define UG_PLAN_SUBS 8
+#endif
+constexpr int PLAN_SUBS_PER_CTA = UG_PLAN_SUBS;  // sub-ranges per planned-transcoder CTA (tickets)
+size_t planned_smem_bytes(bool u16in);
+cudaError_t planned_configure(Op op);
+cudaError_t planned_occupancy(Op op, int *blocks_per_sm);
+cudaError_t launch_planned(Op op, const TileArgs &a, const unsigned long long *plan, int grid,
+                           cudaStream_t s);
+cudaError_t launch_plan(bool u16in, bool be, const Window &w, unsigned long long ntiles,
+                        int nsub, unsigned long long tps, unsigned long long *plan,
+                        Counters *ctr, unsigned long long *d_len, cudaStream_t s);
+
 cudaError_t launch_len8(const uint8_t *in, unsigned long long n, Counters *ctr,
                         unsigned long long *d_len, int grid, cudaStream_t s);
 cudaError_t launch_len16(const uint16_t *in, unsigned long long n, Counters *ctr,

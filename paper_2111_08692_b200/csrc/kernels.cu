@@ -354,6 +354,7 @@ template <bool BE>
 struct U16PolT {
   using Out = uint8_t;
   static constexpr int UNIT = 2;
+  static constexpr bool kBE = BE;
   __device__ static __forceinline__ uint32_t native(uint32_t w) {  // a stored word's value
     return BE ? (((w >> 8) | (w << 8)) & 0xFFFFu) : w;
   }
@@ -628,6 +629,50 @@ struct U16PolT {
     return f;
   }
 
+  // a7 for a warp whose words hold no surrogate (f1): the BMP-only encode, no pairing check
+  // (nothing to check: only surrogates can be invalid), the same stores and clipping.
+  template <bool IN>
+  __device__ static __forceinline__ void decode_bmp(const St &s, uint8_t *stage, uint32_t o,
+                                                    uint32_t lim) {
+    if (IN && s.wasc) {
+      decode<true>(s, stage, o, lim, 0);
+      return;
+    }
+    uint32_t p = smem_addr(stage + o);
+    const uint32_t pend = smem_addr(stage + lim);
+#pragma unroll
+    for (int g = 0; g < 4; g++) {
+      const u16::Bmp4 c = u16::classes4_bmp<BE>(s.w[2 * g], s.w[2 * g + 1]);
+      uint32_t O0, O1, O2;
+      u16::encode4_bmp(c, &O0, &O1, &O2);
+      uint32_t d = u16::widths_bmp(c);
+      if (!IN) d &= (own4(s, g) >> 7) * 0xFFu;
+      const uint32_t inc = d * 0x01010101u;
+      const uint32_t A[4] = {p, p + prmt(inc, 0u, 0x4440u), p + prmt(inc, 0u, 0x4441u),
+                             p + prmt(inc, 0u, 0x4442u)};
+      const uint32_t B0[4] = {O0, shr_fma<8>(O0), shr_fma<16>(O0), shr_fma<24>(O0)};
+      const uint32_t B1[4] = {O1, shr_fma<8>(O1), shr_fma<16>(O1), shr_fma<24>(O1)};
+      const uint32_t B2[4] = {O2, shr_fma<8>(O2), shr_fma<16>(O2), shr_fma<24>(O2)};
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        if (g < 3) {
+          sts8o<0>(A[j], B0[j]);
+          sts8o<1>(A[j], B1[j]);
+          sts8o<2>(A[j], B2[j]);
+        } else if (IN) {
+          sts8o<0>(A[j], B0[j]);
+          if (j < 3 || A[j] + 1 < pend) sts8o<1>(A[j], B1[j]);
+          if (j < 2 || A[j] + 2 < pend) sts8o<2>(A[j], B2[j]);
+        } else {
+          if (A[j] < pend) sts8o<0>(A[j], B0[j]);
+          if (A[j] + 1 < pend) sts8o<1>(A[j], B1[j]);
+          if (A[j] + 2 < pend) sts8o<2>(A[j], B2[j]);
+        }
+      }
+      p += inc >> 24;
+    }
+  }
+
   __device__ static __forceinline__ void finalize(const TileArgs &a, unsigned long long e,
                                                   bool xc, int lane, int *kind,
                                                   unsigned long long *wr) {
@@ -664,6 +709,19 @@ __device__ __forceinline__ void finish_call(const TileArgs &a, bool xc, int tid,
         *reinterpret_cast<volatile unsigned long long *>(&a.ctr->err_min);
     unsigned long long total = 0, wr = 0;
     int kind = 0;
+    const unsigned long long flags =
+        *reinterpret_cast<volatile unsigned long long *>(&a.ctr->flags);
+    if (flags) {  // a planned call given the plan of another input: API misuse, no result
+      if (lane == 0) {
+        if (a.result) *a.result = ResultDev{-1, 0, 0ull, 0ull};
+        if (a.rec) *a.rec = RecordDev{0ull, 0ull, 0ull, -1, 0};
+        a.ctr->ticket = 0;
+        a.ctr->done = 0;
+        a.ctr->err_min = NONE;
+        a.ctr->flags = 0;
+      }
+      return;
+    }
     if (xc && a.ntiles) total = ld_relaxed(a.status + a.ntiles - 1) & VALMASK;
     if (e != NONE) Pol::finalize(a, e, xc, lane, &kind, &wr);
     if (lane == 0)
@@ -1297,6 +1355,21 @@ __device__ __forceinline__ uint32_t len16_acc4(uint32_t a, uint32_t b, uint32_t 
   return mad_hi(ge800 & ~S, 1u << 25, acc);   // + (ge800 and not S) >> 7
 }
 __device__ __forceinline__ uint32_t lane_sum(uint32_t acc) { return (acc * 0x01010101u) >> 24; }
+// len16_acc4 that also ORs the surrogate mask into *sur (f1: a warp without surrogates takes
+// the BMP-only decode)
+template <bool BE = false>
+__device__ __forceinline__ uint32_t len16_acc4s(uint32_t a, uint32_t b, uint32_t acc,
+                                                uint32_t *sur) {
+  const uint32_t lo = prmt(a, b, BE ? 0x7531u : 0x6420u), hi = prmt(a, b, BE ? 0x6420u : 0x7531u);
+  const uint32_t h7 = hi & 0x7F7F7F7Fu;
+  const uint32_t ge80 = (mad(h7, 1u, 0x7F7F7F7Fu) | hi | lo) & HI;
+  const uint32_t ge800 = (mad(h7, 1u, 0x78787878u) | hi) & HI;
+  const uint32_t z = (hi & 0xF8F8F8F8u) ^ 0xD8D8D8D8u;
+  const uint32_t S = ~(mad(z & 0x7F7F7F7Fu, 1u, 0x7F7F7F7Fu) | z) & HI;
+  *sur |= S;
+  acc = mad_hi(ge80, 1u << 25, acc);
+  return mad_hi(ge800 & ~S, 1u << 25, acc);
+}
 
 template <bool BE>
 __global__ void __launch_bounds__(LNT) k_len16(const uint16_t *in, unsigned long long n,
@@ -1609,6 +1682,547 @@ __global__ void __launch_bounds__(T16_THREADS, CTAS_PER_SM) k_transcode16(const 
   finish_call<U16PolT<BE>>(a, true, tid, warp, lane, &s_last);
 }
 
+// ============================================================================ planned (two-pass)
+// Reduce-then-scan form of the transcoders.  The sizing
+// pass a caller runs anyway (the length-from reduction that sizes the output buffer) also
+// writes a PLAN: the output count of each of 2R contiguous sub-ranges of tiles under the
+// transcoder's own emission rule (R = the transcoder's grid).  The planned transcoder then
+// gives CTA c the tiles of sub-ranges 2c and 2c + 1 in order: its first output offset is the
+// sum of the earlier sub-ranges' counts, and inside its range every tile's offset is the
+// running sum of the tiles it has already processed.  No decoupled look-back, no tickets, no
+// look-back warp, no emit deferral: a tile is counted (classify + validate), its thread
+// offsets are block-scanned and it is decoded and shipped the next iteration, the loads run
+// ahead in static order.  One CTA barrier per tile: the decode of tile t and the count of tile
+// t + 1 are issued between the same two barriers, and the output stage is double-buffered.
+//
+// Plan buffer (device, 8-byte words): [0] tag, [1] input address, [2] n (input bytes),
+// [3] sub-ranges, [4] tiles per sub-range, [5] total under the emission rule, [6] lead,
+// [7] reserved, [8 + j] output offset (exclusive prefix of the counts) of sub-range j.
+constexpr int PLAN_HDR = 8;
+constexpr int PLAN_MAX_SUB = 8192;
+static_assert(PLAN_WORDS == PLAN_HDR + PLAN_MAX_SUB, "plan layout (internal.h PLAN_WORDS)");
+constexpr unsigned long long PLAN_TAG = 0x554750414E563031ull;
+
+struct PlanArgs {
+  Window win;                // the same window the transcoder will see
+  unsigned long long ntiles;
+  int nsub;
+  unsigned long long tps;    // tiles per sub-range
+  unsigned long long *plan;
+  Counters *ctr;
+  unsigned long long *d_len;  // the length-from result (optional)
+};
+
+// Positions [p0, p1) of sub-range j (clipped to the owned range [0, n)), in bytes.
+__device__ __forceinline__ void sub_span(const PlanArgs &a, long long j, long long *p0,
+                                         long long *p1) {
+  const long long t0 = j * (long long)a.tps, t1 = t0 + (long long)a.tps;
+  long long q0 = t0 * TILE - a.win.lead, q1 = t1 * TILE - a.win.lead;
+  if (q0 < 0) q0 = 0;
+  if (q1 > a.win.n) q1 = a.win.n;
+  if (t0 >= (long long)a.ntiles) q0 = q1 = a.win.n;
+  *p0 = q0;
+  *p1 = q1 > q0 ? q1 : q0;
+}
+
+__device__ __forceinline__ void plan_finish(const PlanArgs &a, unsigned long long emit_sum,
+                                            unsigned long long len_sum) {
+  __shared__ unsigned long long s_e[LNT / 32], s_l[LNT / 32];
+  __shared__ int s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  emit_sum = warp_sum64(emit_sum);
+  len_sum = warp_sum64(len_sum);
+  if (lane == 0) {
+    s_e[warp] = emit_sum;
+    s_l[warp] = len_sum;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    unsigned long long e = 0, l = 0;
+    for (int i = 0; i < LNT / 32; i++) {
+      e += s_e[i];
+      l += s_l[i];
+    }
+    st_relaxed(reinterpret_cast<uint64_t *>(a.plan + PLAN_HDR + blockIdx.x), e);
+    atomicAdd(&a.ctr->accum, l);
+    __threadfence();
+    s_last = (atomicAdd(&a.ctr->done, 1u) == gridDim.x - 1) ? 1 : 0;
+  }
+  __syncthreads();
+  if (!s_last) return;
+  // last CTA: the sub-range counts become exclusive prefixes (in place), then the header
+  __threadfence();
+  const int ns = a.nsub, per = (ns + LNT - 1) / LNT;
+  const int j0 = tid * per, j1 = j0 + per < ns ? j0 + per : ns;
+  unsigned long long mine = 0;
+  for (int j = j0; j < j1; j++) mine += ld_relaxed(reinterpret_cast<uint64_t *>(a.plan + PLAN_HDR + j));
+  unsigned long long sc = mine;  // inclusive scan over the 512 threads
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const unsigned long long y = __shfl_up_sync(FULL, sc, d);
+    if (lane >= d) sc += y;
+  }
+  if (lane == 31) s_e[warp] = sc;
+  __syncthreads();
+  unsigned long long wpre = 0, total = 0;
+  for (int i = 0; i < LNT / 32; i++) {
+    if (i < warp) wpre += s_e[i];
+    total += s_e[i];
+  }
+  unsigned long long run = wpre + sc - mine;
+  for (int j = j0; j < j1; j++) {
+    const unsigned long long c = ld_relaxed(reinterpret_cast<uint64_t *>(a.plan + PLAN_HDR + j));
+    a.plan[PLAN_HDR + j] = run;
+    run += c;
+  }
+  if (tid == 0) {
+    const unsigned long long L = *reinterpret_cast<volatile unsigned long long *>(&a.ctr->accum);
+    a.plan[0] = PLAN_TAG;
+    a.plan[1] = (unsigned long long)(uintptr_t)a.win.base;
+    a.plan[2] = (unsigned long long)a.win.n;
+    a.plan[3] = (unsigned long long)a.nsub;
+    a.plan[4] = a.tps;
+    a.plan[5] = total;
+    a.plan[6] = (unsigned long long)a.win.lead;
+    a.plan[7] = 0;
+    if (a.d_len) *a.d_len = L;
+    a.ctr->accum = 0;
+    a.ctr->done = 0;
+  }
+}
+
+// UTF-16 -> UTF-8 plan: per sub-range the width sum (u16::widths rule, = utf8 length on valid
+// input), which is also the transcoder's count; total = utf8_length_from_utf16le.  Read-only,
+// grid = nsub CTAs, 16-byte loads over the aligned interior, 4 in flight per thread.
+template <bool BE>
+__global__ void __launch_bounds__(LNT) k_plan16(const PlanArgs a) {
+  long long p0, p1;
+  sub_span(a, blockIdx.x, &p0, &p1);  // bytes, even
+  const uint8_t *base = a.win.base;
+  unsigned long long sum = 0;
+  // aligned interior [h0, h1) of 16-byte vectors; scalar words before / after
+  long long h0 = p0, h1 = p1;
+  while (h0 < p1 && (((uintptr_t)(base + h0)) & 15u)) h0 += 2;
+  h1 = h0 + ((p1 - h0) & ~15ll);
+  if (h1 < h0) h1 = h0;
+  const uint4 *v = reinterpret_cast<const uint4 *>(base + h0);
+  const long long nv = (h1 - h0) / 16;
+  long long i = threadIdx.x;
+  for (; i + 3 * LNT < nv; i += 4 * LNT) {
+    uint4 q[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) q[j] = __ldcs(v + i + j * LNT);
+    uint32_t acc = 0;
+#pragma unroll
+    for (int j = 0; j < 4; j++)
+      acc = len16_acc4<BE>(q[j].z, q[j].w, len16_acc4<BE>(q[j].x, q[j].y, acc));
+    sum += 32u + lane_sum(acc);
+  }
+  for (; i < nv; i += LNT) {
+    const uint4 q = __ldcs(v + i);
+    sum += 8u + lane_sum(len16_acc4<BE>(q.z, q.w, len16_acc4<BE>(q.x, q.y, 0u)));
+  }
+  const uint16_t *w16 = reinterpret_cast<const uint16_t *>(base);
+  for (long long b = p0 + 2 * threadIdx.x; b < h0; b += 2 * LNT) {
+    const uint32_t u = w16[b / 2];
+    sum += len16_word(BE ? (((u >> 8) | (u << 8)) & 0xFFFFu) : u);
+  }
+  for (long long b = h1 + 2 * threadIdx.x; b < p1; b += 2 * LNT) {
+    const uint32_t u = w16[b / 2];
+    sum += len16_word(BE ? (((u >> 8) | (u << 8)) & 0xFFFFu) : u);
+  }
+  plan_finish(a, sum, sum);
+}
+
+// UTF-8 -> UTF-16 plan: per sub-range the number of EMITTING positions (the transcoder's end-
+// position rule: ASCII, or the end of a 2- / 3-byte character, or the 3rd / 4th byte after an
+// F lead - exactly analyze32's emit mask, also on invalid input); the length total is the
+// utf16_length_from_utf8 formula (R15).  Byte-SWAR over 4 positions per word with
+// the word before (from the window: halo bytes of a shard, 0x00 before the start).
+__device__ __forceinline__ uint32_t word_before(const Window &w, long long pos) {
+  if (pos - 4 >= w.lo_valid && pos <= w.hi_valid && !(((uintptr_t)(w.base + pos)) & 3u))
+    return *reinterpret_cast<const uint32_t *>(w.base + pos - 4);
+  uint32_t x = 0;
+#pragma unroll
+  for (int j = 0; j < 4; j++) x |= byte_at(w, pos - 4 + j) << (8 * j);
+  return x;
+}
+// msb-per-byte masks of one word: >= C0 (L), >= E0 (E), >= F0 (F)
+struct Lef {
+  uint32_t L2, E, F;  // C0..DF, >= E0, >= F0
+};
+__device__ __forceinline__ Lef lef_of(uint32_t x) {
+  const uint32_t L = x & (x << 1) & HI, E = L & (x << 2);
+  return Lef{L & ~E, E, E & (x << 3)};
+}
+// emit count (end-position rule) and R15 length of word x after word p (masks mp of p)
+__device__ __forceinline__ void plan8_word(const Lef &mp, uint32_t x, const Lef &mx, uint32_t own,
+                                           uint32_t *em_acc, uint32_t *len_acc) {
+  const uint32_t em = ((~x & HI) | fsl(mp.L2, mx.L2, 8) | fsl(mp.E, mx.E, 16) |
+                       fsl(mp.F, mx.F, 24)) & own;
+  *em_acc = mad_hi(em, 1u << 25, *em_acc);                      // + em >> 7 per byte
+  const uint32_t nk = (~x | (x << 1)) & HI & own;                // not a continuation byte
+  *len_acc = mad_hi(mx.F & own, 1u << 25, mad_hi(nk, 1u << 25, *len_acc));
+}
+__device__ __forceinline__ unsigned long long bsum(uint32_t acc) {
+  return (acc & 0xFFu) + ((acc >> 8) & 0xFFu) + ((acc >> 16) & 0xFFu) + (acc >> 24);
+}
+
+__global__ void __launch_bounds__(LNT) k_plan8(const PlanArgs a) {
+  long long p0, p1;
+  sub_span(a, blockIdx.x, &p0, &p1);
+  const Window &w = a.win;
+  const uint8_t *base = w.base;
+  const int lane = threadIdx.x & 31;
+  unsigned long long esum = 0, lsum = 0;
+  long long h0 = p0;
+  while (h0 < p1 && (((uintptr_t)(base + h0)) & 15u)) h0++;
+  long long h1 = h0 + ((p1 - h0) & ~15ll);
+  if (h1 < h0) h1 = h0;
+  const uint4 *v = reinterpret_cast<const uint4 *>(base + h0);
+  const long long nv = (h1 - h0) / 16;
+  // a warp takes 32 consecutive vectors per step (lane l: vector l), UNR steps in flight; the
+  // word before a lane's vector is the previous lane's last word (lane 0: one extra load).
+  // Full steps run without bounds checks; the remainder vector by vector.
+#ifndef UG_PLAN_UNR
+#define UG_PLAN_UNR 4
+#endif
+  constexpr int UNR = UG_PLAN_UNR;
+  const uint32_t nvu = (uint32_t)nv;  // < 2^31 vectors per sub-range
+  const uint32_t lanev = (uint32_t)lane;
+  // the word before vector 0 (may lie outside the window); every later one is an aligned load
+  const uint32_t pre0 = word_before(w, h0);
+  const uint32_t *v32 = reinterpret_cast<const uint32_t *>(v);
+  uint32_t g = (threadIdx.x >> 5) * 32u * UNR;
+  for (; g + 32u * UNR <= nvu; g += (uint32_t)LNT * UNR) {
+    uint4 q[UNR];
+    uint32_t pw[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; u++) q[u] = __ldcs(v + g + 32u * u + lanev);
+#pragma unroll
+    for (int u = 0; u < UNR; u++) {
+      const uint32_t vi = g + 32u * u;
+      pw[u] = (lane == 0 && vi != 0u) ? __ldg(v32 + 4u * vi - 1u) : pre0;
+    }
+    uint32_t ea = 0, la = 0;
+#pragma unroll
+    for (int u = 0; u < UNR; u++) {
+      uint32_t prev = __shfl_up_sync(FULL, q[u].w, 1);
+      if (lane == 0) prev = pw[u];
+      const Lef m0 = lef_of(prev), m1 = lef_of(q[u].x), m2 = lef_of(q[u].y), m3 = lef_of(q[u].z),
+                m4 = lef_of(q[u].w);
+      plan8_word(m0, q[u].x, m1, 0xFFFFFFFFu, &ea, &la);
+      plan8_word(m1, q[u].y, m2, 0xFFFFFFFFu, &ea, &la);
+      plan8_word(m2, q[u].z, m3, 0xFFFFFFFFu, &ea, &la);
+      plan8_word(m3, q[u].w, m4, 0xFFFFFFFFu, &ea, &la);
+    }
+    esum += bsum(ea);  // per-byte sums <= 4 x UNR x 2 < 256
+    lsum += bsum(la);
+  }
+  for (uint32_t i = g + lanev; i < nvu; i += 32u) {  // this warp's last, partial step
+    if (i >= g + 32u * UNR) break;
+    const uint4 q = __ldcs(v + i);
+    const Lef m0 = lef_of(word_before(w, h0 + 16ll * i)), m1 = lef_of(q.x), m2 = lef_of(q.y),
+              m3 = lef_of(q.z), m4 = lef_of(q.w);
+    uint32_t ea = 0, la = 0;
+    plan8_word(m0, q.x, m1, 0xFFFFFFFFu, &ea, &la);
+    plan8_word(m1, q.y, m2, 0xFFFFFFFFu, &ea, &la);
+    plan8_word(m2, q.z, m3, 0xFFFFFFFFu, &ea, &la);
+    plan8_word(m3, q.w, m4, 0xFFFFFFFFu, &ea, &la);
+    esum += bsum(ea);
+    lsum += bsum(la);
+  }
+  // the unaligned head / tail bytes, one word at a time with ownership masks
+  for (long long b = p0 + 4 * threadIdx.x; b < h0; b += 4 * LNT) {
+    uint32_t x = 0, own = 0;
+    for (int j = 0; j < 4; j++) {
+      x |= byte_at(w, b + j) << (8 * j);
+      if (b + j < h0) own |= 0xFFu << (8 * j);
+    }
+    uint32_t ea = 0, la = 0;
+    plan8_word(lef_of(word_before(w, b)), x, lef_of(x), own, &ea, &la);
+    esum += bsum(ea);
+    lsum += bsum(la);
+  }
+  for (long long b = h1 + 4 * threadIdx.x; b < p1; b += 4 * LNT) {
+    uint32_t x = 0, own = 0;
+    for (int j = 0; j < 4; j++) {
+      x |= byte_at(w, b + j) << (8 * j);
+      if (b + j < p1) own |= 0xFFu << (8 * j);
+    }
+    uint32_t ea = 0, la = 0;
+    plan8_word(lef_of(word_before(w, b)), x, lef_of(x), own, &ea, &la);
+    esum += bsum(ea);
+    lsum += bsum(la);
+  }
+  plan_finish(a, esum, lsum);
+}
+
+// The planned transcoder (both directions; Pol = U8PolT / U16PolT).
+#ifndef UG_PRING8
+#define UG_PRING8 2
+#endif
+#ifndef UG_PRING16
+#define UG_PRING16 3
+#endif
+template <class Pol>
+struct PlannedGeo {
+  static constexpr int RING = Pol::UNIT == 1 ? UG_PRING8 : UG_PRING16;  // input slots
+  static constexpr size_t SMEM = (size_t)RING * INBUF + 2 * (size_t)Pol::STAGE;
+};
+
+// Count first (the next tile's count before this tile's decode) or decode first: measured per
+// direction (UTF-16 input: count first -9 %; UTF-8 input: decode first, count first +15 %).
+template <class Pol>
+struct PlannedOrder {
+  static constexpr bool COUNT_FIRST = Pol::UNIT == 2;
+};
+
+template <class Pol>
+__global__ void __launch_bounds__(NT, CTAS_PER_SM)
+    k_transcode_planned(const TileArgs a, const unsigned long long *plan) {
+  using Out = typename Pol::Out;
+  using G = PlannedGeo<Pol>;
+  constexpr int PR = G::RING;
+  constexpr uint32_t AU = 16 / sizeof(Out);  // output units per 16 bytes
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t *ring = smem;
+  uint8_t *stage_base = smem + PR * INBUF;  // two output stages of Pol::STAGE bytes
+  __shared__ uint64_t mb_load[PR];
+  __shared__ long long s_tile[PR];             // tile in each slot, -1 = no more tiles
+  __shared__ unsigned long long s_base[PR];    // a sub-range's first tile: its output offset
+  __shared__ uint32_t s_wsum[2][NT / 32];
+  __shared__ int s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const Window &win = a.win;
+  const long long ntiles = (long long)a.ntiles;
+  const long long n_units = win.n / Pol::UNIT;
+  Out *out = reinterpret_cast<Out *>(a.out);
+
+  // the plan must describe this very input (else: UG_ERR_ARG from finish, no work)
+  const bool bad = plan[0] != PLAN_TAG || plan[1] != (unsigned long long)(uintptr_t)win.base ||
+                   plan[2] != (unsigned long long)win.n ||
+                   plan[6] != (unsigned long long)win.lead;
+  const long long nsub = bad ? 0 : (long long)plan[3], tps = bad ? 1 : (long long)plan[4];
+  if (bad && tid == 0 && blockIdx.x == 0) atomicOr(&a.ctr->flags, 1ull);
+  // producer (lane 0 of the last warp, not the shipping warp 0): tiles in sub-range order,
+  // sub-ranges by ticket; the next ticket is drawn as a sub-range starts, so its L2 round trip
+  // is off the critical path
+  long long cur_t = 0, cur_end = 0, next_j = 0;
+  auto produce = [&](int slot) {
+    long long t = -1;
+    unsigned long long b = NONE;
+    if (cur_t < cur_end) {
+      t = cur_t++;
+    } else {
+      const long long j = next_j;
+      if (j < nsub) {
+        next_j = (long long)atomicAdd(&a.ctr->ticket, 1u);
+        t = j * tps;
+        cur_end = t + tps < ntiles ? t + tps : ntiles;
+        cur_t = t + 1;
+        b = plan[PLAN_HDR + j];
+      }
+    }
+    s_tile[slot] = t;
+    s_base[slot] = b;
+    if (t >= 0) {
+      fence_proxy_async_smem();
+      issue_tile_load(win, t, ring + slot * INBUF, &mb_load[slot]);
+    } else {
+      mbar_arrive(&mb_load[slot]);
+    }
+  };
+  if (tid == 0) {
+#pragma unroll
+    for (int j = 0; j < PR; j++) mbar_init(&mb_load[j], 1);
+    fence_mbar_init();
+  }
+  __syncthreads();
+  if (tid == PRODUCER) {
+    next_j = (long long)atomicAdd(&a.ctr->ticket, 1u);
+    for (int j = 0; j < PR; j++) produce(j);
+  }
+
+  // count tile t (slot k % PR): classify / validate (errors to the call's minimum), the
+  // thread's count, its in-warp exclusive offset; the warp total goes to s_wsum[k & 1]
+  // (UTF-16: bit 31 of *wexcl set = this warp's words hold no surrogate, f1)
+  auto count_tile = [&](long long t, int k, uint32_t *cnt, uint32_t *wexcl) {
+    uint32_t nosurr = 0;
+    uint8_t *img = ring + (k % PR) * INBUF;
+    mbar_wait(&mb_load[k % PR], (k / PR) & 1);
+    if (tile_at_edge(win, t)) {  // tile-uniform
+      named_sync<BAR_DATA, NT>();
+      fix_tile_edges(win, t, img, NT);
+      named_sync<BAR_DATA, NT>();
+    }
+    const long long tp = tile_pos(win, t);
+    uint32_t c;
+    if constexpr (Pol::UNIT == 2) {
+      // UTF-16: the count is the width sum alone (exact on any input); the pairing check is
+      // done with the decode (decode_validate), as in the count-first k_transcode16
+      constexpr bool BE = Pol::kBE;
+      const uint4 *my = reinterpret_cast<const uint4 *>(img + HALO + BPT * tid);
+      const uint4 q0 = my[0], q1 = my[1];
+      if (tp >= 0 && tp + TILE <= win.n) {
+        const uint32_t orv = q0.x | q0.y | q0.z | q0.w | q1.x | q1.y | q1.z | q1.w;
+        if (__all_sync(FULL, (orv & (BE ? 0x80FF80FFu : 0xFF80FF80u)) == 0u)) {
+          c = 16u;
+        } else {
+          uint32_t sur = 0;
+          c = 16u + lane_sum(len16_acc4s<BE>(q1.z, q1.w, len16_acc4s<BE>(q1.x, q1.y,
+                             len16_acc4s<BE>(q0.z, q0.w, len16_acc4s<BE>(q0.x, q0.y, 0u, &sur),
+                             &sur), &sur), &sur));
+#ifndef UG_NO_F1
+          nosurr = __any_sync(FULL, sur != 0u) ? 0u : 0x80000000u;
+#endif
+        }
+      } else {
+        const uint32_t q[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+        const long long w0 = (tp + BPT * tid) / 2, nw = win.n / 2;
+        c = 0;
+#pragma unroll
+        for (int k2 = 0; k2 < 16; k2++)
+          if (w0 + k2 >= 0 && w0 + k2 < nw)
+            c += len16_word(Pol::native((q[k2 >> 1] >> (16 * (k2 & 1))) & 0xFFFFu));
+      }
+    } else {
+      typename Pol::St st;
+      if (tp >= 0 && tp + TILE <= win.n) {
+        Pol::template load<true>(st, img, tid, lane, tp, win.n);
+        c = Pol::template analyze<true>(st, tid, true);
+      } else {
+        Pol::template load<false>(st, img, tid, lane, tp, win.n);
+        c = Pol::template analyze<false>(st, tid, true);
+      }
+      if (__any_sync(FULL, Pol::hint(st))) {  // a4 (cold)
+        const unsigned long long e = Pol::find_error(st, n_units);
+        if (e != NONE) atomicMin(&a.ctr->err_min, e);
+      }
+    }
+    uint32_t sc = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, sc, d);
+      if (lane >= d) sc += y;
+    }
+    if (lane == 31) s_wsum[k & 1][warp] = sc;
+    *cnt = c;
+    *wexcl = (sc - c) | nosurr;
+  };
+  // after the barrier: this warp's offset inside the tile and the tile total
+  auto tile_offsets = [&](int k, uint32_t *woff, uint32_t *total) {
+    const uint32_t v = lane < NT / 32 ? s_wsum[k & 1][lane] : 0u;
+    uint32_t sc = v;
+#pragma unroll
+    for (int d = 1; d < NT / 32; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(FULL, sc, d);
+      if (lane >= d) sc += y;
+    }
+    *woff = __shfl_sync(FULL, sc - v, warp);
+    *total = __shfl_sync(FULL, sc, NT / 32 - 1);
+  };
+
+  // the tile of the k-th iteration (after its load has landed) and its sub-range base
+  auto slot_tile = [&](int k, unsigned long long *b) {
+    mbar_wait(&mb_load[k % PR], (k / PR) & 1);
+    *b = s_base[k % PR];
+    return s_tile[k % PR];
+  };
+
+  uint32_t cnt = 0, wex = 0, woff = 0, C = 0;
+  unsigned long long running = 0, base_t;
+  long long t = slot_tile(0, &base_t);
+  if (t >= 0) count_tile(t, 0, &cnt, &wex);
+  named_sync<BAR_DATA, NT>();
+  if (t >= 0) tile_offsets(0, &woff, &C);
+  for (int k = 0; t >= 0; k++) {
+    const unsigned long long P = base_t != NONE ? base_t : running;
+    Out *stage = reinterpret_cast<Out *>(stage_base + (k & 1) * Pol::STAGE);
+    const uint32_t ph = (uint32_t)((((uintptr_t)(out + P)) & 15u) / sizeof(Out));
+    uint32_t cnt2 = 0, wex2 = 0;
+    unsigned long long base2 = NONE;
+    long long t2 = -1;
+    if constexpr (PlannedOrder<Pol>::COUNT_FIRST) {
+      t2 = slot_tile(k + 1, &base2);
+      if (t2 >= 0) count_tile(t2, k + 1, &cnt2, &wex2);
+    }
+    // decode tile t at its global 16-byte phase (its input image is still in slot k % PR)
+    {
+      uint8_t *img = ring + (k % PR) * INBUF;
+      typename Pol::St st;
+      const long long tp = tile_pos(win, t);
+      const uint32_t o = ph + woff + (wex & 0x7FFFFFFFu);
+      if constexpr (Pol::UNIT == 2) {  // encode + pairing check in one pass
+        unsigned long long f = NONE;
+        if (tp >= 0 && tp + TILE <= win.n) {
+          Pol::template load<true>(st, img, tid, lane, tp, win.n);
+          if (wex >> 31)  // warp-uniform (f1)
+            Pol::template decode_bmp<true>(st, stage, o, o + cnt);
+          else
+            f = Pol::template decode_validate<true>(st, stage, o, o + cnt);
+        } else {
+          Pol::template load<false>(st, img, tid, lane, tp, win.n);
+          f = Pol::template decode_validate<false>(st, stage, o, o + cnt);
+        }
+        if (f != NONE) atomicMin(&a.ctr->err_min, f);  // a4 (cold)
+      } else {
+        if (tp >= 0 && tp + TILE <= win.n) {
+          Pol::template load<true>(st, img, tid, lane, tp, win.n);
+          Pol::template decode<true>(st, stage, o, o + cnt, n_units);
+        } else {
+          Pol::template load<false>(st, img, tid, lane, tp, win.n);
+          Pol::template decode<false>(st, stage, o, o + cnt, n_units);
+        }
+      }
+    }
+    if constexpr (!PlannedOrder<Pol>::COUNT_FIRST) {
+      t2 = slot_tile(k + 1, &base2);
+      if (t2 >= 0) count_tile(t2, k + 1, &cnt2, &wex2);
+    }
+    if (tid == SHIPPER) bulk_wait_read_all();  // the store of the previous tile has read its stage
+    named_sync<BAR_DATA, NT>();  // stage k & 1 complete; warp totals of the next tile published
+    // ship tile t: 16-byte aligned interior by one TMA bulk store, head / tail by the warp
+    {
+      unsigned long long hi = P + C;
+      if (hi > a.out_cap) hi = a.out_cap;
+      if (hi > P) {
+        const uint32_t Cc = (uint32_t)(hi - P);
+        const uint32_t h = ph ? AU - ph : 0u;
+        const uint32_t sid = (uint32_t)(tid - SHIPPER);
+        if (h >= Cc) {
+          if (sid < Cc) out[P + sid] = stage[ph + sid];
+        } else {
+          const uint32_t nb = (Cc - h) / AU;
+          const uint32_t tl = h + nb * AU;
+          if (sid < h) out[P + sid] = stage[ph + sid];
+          if (sid < Cc - tl) out[P + tl + sid] = stage[ph + tl + sid];
+          if (tid == SHIPPER && nb) {
+            fence_proxy_async_smem();
+            bulk_s2g(out + P + h, stage + ph + h, nb * 16u);
+            bulk_commit();
+          }
+        }
+      }
+    }
+    // the inclusive prefix of tile t for the finaliser (kind / written at the first error)
+    if (tid == 0) st_relaxed(a.status + t, pack_status(a.epoch, FLAG_PREFIX, P + C));
+    // slot k % PR is free: the producer refills it
+    if (tid == PRODUCER) produce(k % PR);
+    running = P + C;
+    t = t2;
+    base_t = base2;
+    if (t >= 0) {
+      tile_offsets(k + 1, &woff, &C);
+      cnt = cnt2;
+      wex = wex2;
+    }
+  }
+  if (tid == SHIPPER) bulk_wait_all();
+  __syncthreads();
+  finish_call<Pol>(a, true, tid, warp, lane, &s_last);
+}
+
 // ============================================================================ combine
 __host__ __device__ inline void combine_impl(const RecordDev *recs, int nranks, int rank,
                                              unsigned long long total_in, ResultDev *res,
@@ -1778,6 +2392,59 @@ cudaError_t launch_tile(Op op, const TileArgs &a, int grid, cudaStream_t s) {
     case Op::U8_TO_U16BE: k_transcode<U8PolBE><<<grid, nt, sm, s>>>(a); break;
     case Op::U16BE_TO_U8: rev_launch<true>(a, grid, nt, sm, s); break;
   }
+  return cudaGetLastError();
+}
+
+// ---- planned path launchers
+size_t planned_smem_bytes(bool u16in) {
+  return u16in ? PlannedGeo<U16Pol>::SMEM : PlannedGeo<U8Pol>::SMEM;
+}
+static const void *planned_fn(Op op) {
+  switch (op) {
+    case Op::U8_TO_U16: return (const void *)k_transcode_planned<U8Pol>;
+    case Op::U8_TO_U16BE: return (const void *)k_transcode_planned<U8PolBE>;
+    case Op::U16_TO_U8: return (const void *)k_transcode_planned<U16Pol>;
+    case Op::U16BE_TO_U8: return (const void *)k_transcode_planned<U16PolBE>;
+    default: return nullptr;
+  }
+}
+cudaError_t planned_configure(Op op) {
+  return cudaFuncSetAttribute(planned_fn(op), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)planned_smem_bytes(op_u16_input(op)));
+}
+cudaError_t planned_occupancy(Op op, int *blocks_per_sm) {
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      blocks_per_sm, planned_fn(op), NT, planned_smem_bytes(op_u16_input(op)));
+}
+cudaError_t launch_planned(Op op, const TileArgs &a, const unsigned long long *plan, int grid,
+                           cudaStream_t s) {
+  const size_t sm = planned_smem_bytes(op_u16_input(op));
+  switch (op) {
+    case Op::U8_TO_U16: k_transcode_planned<U8Pol><<<grid, NT, sm, s>>>(a, plan); break;
+    case Op::U8_TO_U16BE: k_transcode_planned<U8PolBE><<<grid, NT, sm, s>>>(a, plan); break;
+    case Op::U16_TO_U8: k_transcode_planned<U16Pol><<<grid, NT, sm, s>>>(a, plan); break;
+    case Op::U16BE_TO_U8: k_transcode_planned<U16PolBE><<<grid, NT, sm, s>>>(a, plan); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+cudaError_t launch_plan(bool u16in, bool be, const Window &w, unsigned long long ntiles,
+                        int nsub, unsigned long long tps, unsigned long long *plan,
+                        Counters *ctr, unsigned long long *d_len, cudaStream_t s) {
+  PlanArgs pa;
+  pa.win = w;
+  pa.ntiles = ntiles;
+  pa.nsub = nsub;
+  pa.tps = tps;
+  pa.plan = plan;
+  pa.ctr = ctr;
+  pa.d_len = d_len;
+  if (!u16in)
+    k_plan8<<<nsub, LNT, 0, s>>>(pa);
+  else if (be)
+    k_plan16<true><<<nsub, LNT, 0, s>>>(pa);
+  else
+    k_plan16<false><<<nsub, LNT, 0, s>>>(pa);
   return cudaGetLastError();
 }
 

@@ -104,5 +104,38 @@ UG_HD void encode4(const Cls4 &c, uint32_t lp, uint32_t *O0, uint32_t *O1, uint3
   *O2 = T;
 }
 
+// ---------------------------------------------------------------- surrogate-free fast path
+// (the BMP-only case).  A group whose words hold no
+// surrogate cannot be invalid (only surrogates need attention), and every word is
+// a 1-, 2- or 3-byte character: only the low / high byte split and two class masks are needed.
+struct Bmp4 {
+  uint32_t lo, hi;      // low / high bytes of the 4 words
+  uint32_t ge80, ge800;  // u >= 0x80, u >= 0x800 (msb per byte)
+};
+template <bool BE = false>
+UG_HD Bmp4 classes4_bmp(uint32_t wa, uint32_t wb) {
+  Bmp4 c;
+  c.lo = prmt(wa, wb, BE ? 0x7531u : 0x6420u);
+  c.hi = prmt(wa, wb, BE ? 0x6420u : 0x7531u);
+  const uint32_t h7 = c.hi & 0x7F7F7F7Fu;
+  c.ge800 = (mad(h7, 1u, 0x78787878u) | c.hi) & HI;
+  c.ge80 = (mad(h7, 1u, 0x7F7F7F7Fu) | c.hi | c.lo) & HI;
+  return c;
+}
+UG_HD uint32_t widths_bmp(const Bmp4 &c) {
+  return mad_hi(c.ge800, 1u << 25, mad_hi(c.ge80, 1u << 25, 0x01010101u));
+}
+// Output byte planes as encode4, for surrogate-free words.
+UG_HD void encode4_bmp(const Bmp4 &c, uint32_t *O0, uint32_t *O1, uint32_t *O2) {
+  const uint32_t U6 = mux(0xFCFCFCFCu, c.hi << 2, c.lo >> 6);   // (u >> 6) & 0xFF
+  const uint32_t T = (c.lo & 0x3F3F3F3Fu) | HI;                 // 80 | u & 3F
+  const uint32_t vB = U6 | 0xC0C0C0C0u;                          // 2-byte lead
+  const uint32_t vC = ((c.hi >> 4) & 0x0F0F0F0Fu) | 0xE0E0E0E0u; // 3-byte lead
+  const uint32_t mC = bmask(c.ge800), mA = bmask(~c.ge80 & HI);
+  *O0 = mux(mA, c.lo, mux(mC, vC, vB));
+  *O1 = mux(mC, (U6 & 0x3F3F3F3Fu) | HI, T);
+  *O2 = T;
+}
+
 }  // namespace u16
 }  // namespace ug

@@ -142,9 +142,10 @@ UG_HD uint32_t units4(uint32_t x, Carry &c, uint32_t *u01, uint32_t *u23) {
   const uint32_t n7 = (x >> 7) & 0x01010101u;  // 1 in every non-ASCII byte
   const uint32_t em = ((n7 ^ 0x01010101u) | s1l2 | s2e | s3f);
   uint32_t lb = mux(n7 * 0xC0u, bp1 << 6, x);
-  const uint32_t A1 = mad(s3f, 0xFFFFFFF4u, n7 * 15u);  // 0x0F, or 0x03 at a low surrogate
-  // (right shifts on the FMA pipe as IMAD.HI where the ALU pipe is the bottleneck)
-  uint32_t hb = (shr_fma<2>(bp1) & A1) | (s3f * 0xDCu) | ((bp2 << 4) & (s2e * 0xF0u));
+  // (right shifts on the FMA pipe as IMAD.HI where the ALU pipe is the bottleneck).  At a low
+  // surrogate the payload bits are (b[e-1] >> 2) & 3, but OR-ing all four bits of
+  // (b[e-1] >> 2) & 0xF into 0xDC is the same: 0xDC already has bits 2 and 3 set.
+  uint32_t hb = (shr_fma<2>(bp1) & (n7 * 15u)) | (s3f * 0xDCu) | ((bp2 << 4) & (s2e * 0xF0u));
   // high surrogate: G = hb:lb = cp >> 6, unit = 0xD800 | ((G >> 4) - 0x40)
   const uint32_t Mh = s2f * 0xFFu;
   const uint32_t hbm = (hb | HI) - 0x04040404u;  // per byte 0x80 + hb - 4, no borrows

@@ -29,7 +29,9 @@
 //                     leads 0, 1, 7, 15: first error (flag + rescan) and the decoded units on
 //                     [0, written) against the oracle; the total against the oracle's count.
 //   fuzz16 ITERS      UTF-16 -> UTF-8 (U16PolT::decode_validate): first error, widths and the
-//                     staged bytes on [0, written) against the oracle.
+//                     staged bytes on [0, written) against the oracle; every surrogate-free
+//                     group also through the BMP-only path (f1: classes4_bmp / encode4_bmp),
+//                     which must give the same widths and bytes.
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -363,6 +365,23 @@ static void run16(const std::vector<uint16_t> &u, long long lead16, const char *
       uint32_t O0, O1, O2;
       u16::encode4(cl, lp, &O0, &O1, &O2);
       const uint32_t d = u16::widths(cl) & ((own[k] >> 7) * 0xFFu);
+      if (cl.S == 0) {
+        // f1: a surrogate-free group through the BMP-only path gives the same widths and
+        // the same bytes on every position up to its width
+        const u16::Bmp4 cb = u16::classes4_bmp(w[2 * k], w[2 * k + 1]);
+        uint32_t P0, P1, P2;
+        u16::encode4_bmp(cb, &P0, &P1, &P2);
+        const uint32_t wb = u16::widths_bmp(cb);
+        CHECK(wb == u16::widths(cl), "%s: bmp widths differ (chunk %lld group %d)", name, c, k);
+        for (int j = 0; j < 4; j++) {
+          const uint32_t wj = (wb >> (8 * j)) & 0xFFu;
+          const uint32_t a0 = (O0 >> (8 * j)) & 0xFFu, b0 = (P0 >> (8 * j)) & 0xFFu;
+          const uint32_t a1 = (O1 >> (8 * j)) & 0xFFu, b1 = (P1 >> (8 * j)) & 0xFFu;
+          const uint32_t a2 = (O2 >> (8 * j)) & 0xFFu, b2 = (P2 >> (8 * j)) & 0xFFu;
+          CHECK(a0 == b0 && (wj < 2 || a1 == b1) && (wj < 3 || a2 == b2),
+                "%s: bmp bytes differ (chunk %lld group %d word %d)", name, c, k, j);
+        }
+      }
       const uint32_t inc = d * 0x01010101u;
       for (int j = 0; j < 4; j++) {
         const uint32_t oj = so + (j ? ((inc >> (8 * (j - 1))) & 0xFFu) : 0u);

@@ -790,3 +790,61 @@ def test_host_pipeline_streams_many_chunks_in_bounded_memory(c0):
     need8 = oracle.utf16le_to_utf8(u)[0].written
     check_host(u, chunk, cap=need8 - 1)
     check_host(a, chunk, cap=r.written // 2)
+
+
+# ----------------------------------------------------------------------------- C multi-GPU entry
+@pytest.mark.parametrize("G", [1, 2, 5])
+def test_sharded_c_entry_virtual_shards(c0, G):
+    """ug_sharded_* (one process, record all-gather by device copies + a combine per shard):
+    G shards on this device, clean and with errors injected near the cuts, both directions,
+    against the oracle."""
+    _, t = to_dev(c0)
+    n = c0.size
+    cuts = shard_plan(c0, G)
+
+    def descs(tin, cuts, outs, halo):
+        N = tin.numel()
+        return [dict(t_in=tin, offset=cuts[k], n=cuts[k + 1] - cuts[k],
+                     halo_before=min(cuts[k], halo), halo_after=min(N - cuts[k + 1], halo),
+                     global_off=cuts[k], t_out=outs[k] if outs else None)
+                for k in range(len(cuts) - 1)]
+    outs = [torch.zeros(max(cuts[k + 1] - cuts[k], 1), dtype=torch.int16, device=DEV)
+            for k in range(G)]
+    r, offs = ug.sharded_utf8_to_utf16le(descs(t, cuts, outs, 3))
+    ref_r, ref_o = oracle.utf8_to_utf16le(c0)
+    assert tuple(r) == tuple(ref_r)
+    got = np.concatenate([outs[k][: (offs[k + 1] if k + 1 < G else r.written) - offs[k]]
+                          .cpu().numpy().view(np.uint16) for k in range(G)])
+    assert np.array_equal(got, ref_o)
+    v = ug.sharded_utf8_validate(descs(t, cuts, None, 3))
+    assert tuple(v) == tuple(oracle.utf8_validate(c0))
+    # reverse: shard the UTF-16 output at word cuts backed off a low surrogate
+    u = ref_o
+    tu = torch.from_numpy(u.view(np.int16).copy()).to(DEV)
+    m = u.size
+    wc = [0] + [((k * (m // G)) & ~15) - ug.utf16_cut_backoff(u, (k * (m // G)) & ~15)
+                for k in range(1, G)] + [m]
+    outs8 = [torch.zeros(3 * max(wc[k + 1] - wc[k], 1), dtype=torch.uint8, device=DEV)
+             for k in range(G)]
+    r2, offs2 = ug.sharded_utf16le_to_utf8(descs(tu, wc, outs8, 1))
+    assert tuple(r2) == (0, m, n)
+    back = b"".join(bytes(outs8[k][: (offs2[k + 1] if k + 1 < G else n) - offs2[k]]
+                          .cpu().numpy()) for k in range(G))
+    assert back == c0.tobytes()
+    assert tuple(ug.sharded_utf16le_validate(descs(tu, wc, None, 1))) == (0, m, 0)
+    # errors within 3 bytes of a cut
+    rng = np.random.default_rng(np.random.SeedSequence([0, 0xC, G, 0]))
+    for j in range(6):
+        b = c0.copy()
+        k = int(rng.integers(1, G)) if G > 1 else 0
+        c = cuts[k] if G > 1 else int(rng.integers(8, n - 8))
+        cls = synth.UTF8_ERROR_CLASSES[j % 5]
+        p, _ = synth.inject_utf8_error(b, max(0, c - 3), c + 3, cls, rng)
+        _, tb = to_dev(b)
+        bc = shard_plan(b, G)
+        outs = [torch.zeros(max(bc[k + 1] - bc[k], 1), dtype=torch.int16, device=DEV)
+                for k in range(G)]
+        rb, _ = ug.sharded_utf8_to_utf16le(descs(tb, bc, outs, 3))
+        assert tuple(rb) == tuple(oracle.utf8_to_utf16le(b)[0]) and rb.position == p, (cls, rb)
+        vb = ug.sharded_utf8_validate(descs(tb, bc, None, 3))
+        assert (vb.error, vb.position) == (rb.error, p)

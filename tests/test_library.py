@@ -209,3 +209,16 @@ def test_length_ex_error_channel_needs_no_gpu(ug):
     out.value = 5
     assert L.ug_utf16_length_from_utf8_ex(V(0), 0, ctypes.byref(out), V(0)) == ug.OK
     assert out.value == 0
+
+
+def test_sharded_c_entry_argument_errors_need_no_gpu(ug):
+    """ug_sharded_*: no shards / too many / shards out of order are UG_ERR_ARG on the host."""
+    import ctypes as C
+    assert ug.lib.ug_sharded_utf8_validate(C.c_void_p(0), 1).error == ug.ERR_ARG
+    arr = (ug._CShardDesc * 2)()
+    arr[0].in_, arr[0].n, arr[0].in_global_offset = 0x1000, 10, 0
+    arr[1].in_, arr[1].n, arr[1].in_global_offset = 0x2000, 10, 11   # gap: not in order
+    assert ug.lib.ug_sharded_utf8_validate(C.cast(arr, C.c_void_p), 2).error == ug.ERR_ARG
+    assert ug.lib.ug_sharded_utf8_validate(C.cast(arr, C.c_void_p), 0).error == ug.ERR_ARG
+    assert ug.lib.ug_sharded_utf16le_to_utf8(C.cast(arr, C.c_void_p), 2000,
+                                             C.c_void_p(0)).error == ug.ERR_ARG

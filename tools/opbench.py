@@ -37,7 +37,19 @@ n8, n16 = t8.numel(), u16.numel()
 u16be = u16.view(torch.uint8).view(-1, 2).flip(1).contiguous().view(torch.int16).view(-1)
 o16 = torch.empty(n8, dtype=torch.int16, device=dev)
 o8 = torch.empty(3 * n16, dtype=torch.uint8, device=dev)
+plan8, plan16 = ug.plan_buffer(dev), ug.plan_buffer(dev)
+lens = torch.zeros(2, dtype=torch.int64, device=dev)
+resb = ug.result_buffer(dev, 1)
+ug.utf16_length_from_utf8_plan_async(t8, lens, plan8)
+ug.utf8_length_from_utf16le_plan_async(u16, lens, plan16, len_off=8)
 ops = {
+    "utf8_to_utf16le_planned": (lambda: ug.utf8_to_utf16le_planned_async(t8, plan8, o16, resb),
+                                n8, n8 + 2 * n16),
+    "utf16le_to_utf8_planned": (lambda: ug.utf16le_to_utf8_planned_async(u16, plan16, o8, resb),
+                                2 * n16, 2 * n16 + n8),
+    "plan8": (lambda: ug.utf16_length_from_utf8_plan_async(t8, lens, plan8), n8, n8),
+    "plan16": (lambda: ug.utf8_length_from_utf16le_plan_async(u16, lens, plan16, len_off=8),
+               2 * n16, 2 * n16),
     "utf8_validate": (lambda: ug.utf8_validate(t8), n8, n8),
     "utf8_to_utf16le": (lambda: ug.utf8_to_utf16le(t8, o16), n8, n8 + 2 * n16),
     "utf16le_validate": (lambda: ug.utf16le_validate(u16), 2 * n16, 2 * n16),
