@@ -502,6 +502,19 @@ def measure_per_config(ug, dev, peak, reps=10):
             "utf8_length_from_utf16le": (lambda: ug.utf8_length_from_utf16le_async(u16, lens),
                                          2 * n16, 2 * n16),
         }
+        p8, p16 = ug.plan_buffer(dev), ug.plan_buffer(dev)
+        ug.utf16_length_from_utf8_plan_async(t8, lens, p8)
+        ug.utf8_length_from_utf16le_plan_async(u16, lens, p16)
+        ops.update({
+            "plan_utf8 (len16 + plan)": (lambda: ug.utf16_length_from_utf8_plan_async(
+                t8, lens, p8), n8, n8),
+            "utf8_to_utf16le_planned": (lambda: ug.utf8_to_utf16le_planned_async(
+                t8, p8, o16, res), n8, n8 + 2 * n16),
+            "plan_utf16le (len8 + plan)": (lambda: ug.utf8_length_from_utf16le_plan_async(
+                u16, lens, p16), 2 * n16, 2 * n16),
+            "utf16le_to_utf8_planned": (lambda: ug.utf16le_to_utf8_planned_async(
+                u16, p16, o8, res), 2 * n16, 2 * n16 + n8),
+        })
         row = {"input": cfg.desc, "bytes_utf8": n8, "units_utf16": n16, "chars": chars}
         for name, (fn, in_bytes, hbm_bytes) in ops.items():
             fn()
