@@ -327,6 +327,14 @@ def run_ours(args):
         d["frac"] = d["achieved"] / peak
         t = traffic.get(k)
         d["traffic"] = round(t["dram_bytes_per_input_byte"] * d["input"]) if t else None
+        if t:
+            measured = "MEASURED" in t.get("config", "") and t.get("input_bytes") == d["input"]
+            d["traffic_extrapolated"] = not measured
+            d["traffic_source"] = (
+                ("measured at this launch's size in a separate ncu run of the bench command: "
+                 if measured else "EXTRAPOLATED (DRAM bytes per input byte x this input) from: ")
+                + t.get("capture", traffic.get("capture", "?")) + " (" +
+                t.get("config", traffic.get("config", "")) + ")")
         # the kernel's issue picture from the same capture (it is issue-bound)
         d["issue"] = ({"lane_instr_per_input_byte": t.get("lane_instr_per_input_byte"),
                        "alu_lane_instr_per_input_byte": t.get("alu_lane_instr_per_input_byte"),
@@ -380,11 +388,8 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": round(D["achieved"], 1), "peak": peak,
                          "unit": "GB/s", "frac": round(D["frac"], 4),
                          "traffic": D["traffic"],
-                         "traffic_source": ("EXTRAPOLATED, not measured at this size: " +
-                                            traffic["capture"] + " (" + traffic["config"] +
-                                            "), DRAM bytes per input byte x this launch's input"
-                                            if D["traffic"] is not None else None),
-                         "traffic_extrapolated": D["traffic"] is not None,
+                         "traffic_source": D.get("traffic_source"),
+                         "traffic_extrapolated": D.get("traffic_extrapolated"),
                          "kernel": f"{dom} ({D['op']}), the longest launch of the step",
                          "algorithmic_bytes_per_launch": alg_bytes,
                          "avg_launch_ms": round(D["ms"], 4), "peak_source": peak_src,

@@ -1868,6 +1868,93 @@ __device__ __forceinline__ unsigned long long bsum(uint32_t acc) {
   return (acc & 0xFFu) + ((acc >> 8) & 0xFFu) + ((acc >> 16) & 0xFFu) + (acc >> 24);
 }
 
+#ifndef UG_PLAN8_SWAR
+// UTF-8 plan on bit planes (the classifier's transposition, u8::planes32): a lane's 32 bytes ->
+// 8 planes, then the emit mask of analyze32 (ASCII | end of a 2- / 3-byte character | 3rd /
+// 4th byte after an F lead) and the R15 terms (non-continuation, >= F0) are 32 positions per op.
+__device__ __forceinline__ void plan8_chunk32(const uint32_t w[8], uint32_t prev, uint32_t own,
+                                              uint32_t *em, uint32_t *len) {
+  uint32_t P[8];
+  u8::planes32(w, P);
+  const uint32_t L = P[7] & P[6], E = L & P[5], F = E & P[4];
+  const uint32_t pL = u8::lead_c0(prev), pE = pL & (prev << 2), pF = pE & (prev << 3);
+  const uint32_t cL = u8::carry3(pL), cE = u8::carry3(pE), cF = u8::carry3(pF);
+  const uint32_t emit = ~P[7] | fsl(cL & ~cE, L & ~E, 1) | fsl(cE, E, 2) | fsl(cF, F, 3);
+  *em = popc(emit & own);
+  *len = popc(~(P[7] & ~P[6]) & own) + popc(F & own);  // non-continuation + >= F0
+}
+
+__global__ void __launch_bounds__(LNT) k_plan8(const PlanArgs a) {
+  long long p0, p1;
+  sub_span(a, blockIdx.x, &p0, &p1);
+  const Window &w = a.win;
+  const uint8_t *base = w.base;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long esum = 0, lsum = 0;
+  long long h0 = p0;
+  while (h0 < p1 && (((uintptr_t)(base + h0)) & 15u)) h0++;
+  long long h1 = h0 + ((p1 - h0) & ~15ll);
+  if (h1 < h0) h1 = h0;
+  // 1 KiB warp chunks of [h0, h1): lane l owns its 32 bytes; the 4 bytes before come from lane
+  // l - 1 (lane 0: one load, the window's bytes at the start)
+  const long long nb = h1 - h0;
+  const long long nch = (nb + 1023) / 1024;
+  constexpr int CU = 3;  // chunks per warp step (their loads in flight together)
+  for (long long c0 = warp; c0 < nch; c0 += (LNT / 32) * CU) {
+    uint32_t x[CU][8], own[CU];
+#pragma unroll
+    for (int u = 0; u < CU; u++) {
+      const long long q = h0 + (c0 + (long long)u * (LNT / 32)) * 1024 + 32 * lane;
+      uint4 a0 = make_uint4(0, 0, 0, 0), a1 = a0;
+      if (q + 32 <= h1) {
+        a0 = __ldcs(reinterpret_cast<const uint4 *>(base + q));
+        a1 = __ldcs(reinterpret_cast<const uint4 *>(base + q + 16));
+      } else {  // the partial last chunk (or none): vectors up to h1, zeros after
+        if (q < h1) a0 = __ldcs(reinterpret_cast<const uint4 *>(base + q));
+        if (q + 16 < h1) a1 = __ldcs(reinterpret_cast<const uint4 *>(base + q + 16));
+      }
+      x[u][0] = a0.x; x[u][1] = a0.y; x[u][2] = a0.z; x[u][3] = a0.w;
+      x[u][4] = a1.x; x[u][5] = a1.y; x[u][6] = a1.z; x[u][7] = a1.w;
+      const long long k = h1 - q;
+      own[u] = k <= 0 ? 0u : (k >= 32 ? 0xFFFFFFFFu : ((1u << k) - 1u));
+    }
+#pragma unroll
+    for (int u = 0; u < CU; u++) {
+      const long long q = h0 + (c0 + (long long)u * (LNT / 32)) * 1024 + 32 * lane;
+      uint32_t prev = __shfl_up_sync(FULL, x[u][7], 1);
+      if (lane == 0) prev = q < h1 ? word_before(w, q) : 0u;
+      uint32_t em, ln;
+      plan8_chunk32(x[u], prev, own[u], &em, &ln);
+      esum += em;
+      lsum += ln;
+    }
+  }
+  // the unaligned head / tail bytes, one word at a time with ownership masks
+  for (long long b = p0 + 4 * threadIdx.x; b < h0; b += 4 * LNT) {
+    uint32_t x = 0, own = 0;
+    for (int j = 0; j < 4; j++) {
+      x |= byte_at(w, b + j) << (8 * j);
+      if (b + j < h0) own |= 0xFFu << (8 * j);
+    }
+    uint32_t ea = 0, la = 0;
+    plan8_word(lef_of(word_before(w, b)), x, lef_of(x), own, &ea, &la);
+    esum += bsum(ea);
+    lsum += bsum(la);
+  }
+  for (long long b = h1 + 4 * threadIdx.x; b < p1; b += 4 * LNT) {
+    uint32_t x = 0, own = 0;
+    for (int j = 0; j < 4; j++) {
+      x |= byte_at(w, b + j) << (8 * j);
+      if (b + j < p1) own |= 0xFFu << (8 * j);
+    }
+    uint32_t ea = 0, la = 0;
+    plan8_word(lef_of(word_before(w, b)), x, lef_of(x), own, &ea, &la);
+    esum += bsum(ea);
+    lsum += bsum(la);
+  }
+  plan_finish(a, esum, lsum);
+}
+#else
 __global__ void __launch_bounds__(LNT) k_plan8(const PlanArgs a) {
   long long p0, p1;
   sub_span(a, blockIdx.x, &p0, &p1);
@@ -1957,6 +2044,8 @@ __global__ void __launch_bounds__(LNT) k_plan8(const PlanArgs a) {
   }
   plan_finish(a, esum, lsum);
 }
+
+#endif  // UG_PLAN8_SWAR
 
 // The planned transcoder (both directions; Pol = U8PolT / U16PolT).
 #ifndef UG_PRING8
