@@ -5,7 +5,8 @@ oracle element by element.  Config 4 (8 GiB, > 2^32 output units):
     boundaries are character boundaries and the oracle's per-chunk outputs concatenate);
   * the sharded path at G = 2 / 4 / 8 (cuts at character starts, 3-byte halos, one shard
     launch per rank, records combined on the device by ug_combine_records_async) reproduces
-    that output unit for unit, both directions;
+    that output unit for unit, both directions, in its single-pass and two-pass (plan +
+    planned kernel, the form bench.py times) forms;
   * BASELINE.json configs[4]'s 16 seeded error copies PER G, each an injected error of a random
     class within 3 bytes of a shard cut, patched in place on the device, through the SHARDED
     path: (error, position, written) against the oracle (written = the oracle's counts of the
@@ -51,6 +52,14 @@ def test_full_size_utf8_configs(key):
     assert tuple(ug.utf8_validate(t)) == tuple(oracle.utf8_validate(x))
     assert ug.utf16_length_from_utf8(t) == r.written
     assert ug.utf8_length_from_utf16le(out16[: r.written]) == x.size
+    # the two-pass path (the bench's): same result and the same units, both directions
+    o2 = torch.empty(x.size, dtype=torch.int16, device=DEV)
+    rp, ln = ug.utf8_to_utf16le_two_pass(t, o2)
+    assert tuple(rp) == tuple(ref_r) and ln == r.written
+    assert torch.equal(o2[: r.written], out16[: r.written])
+    b2 = torch.empty(x.size, dtype=torch.uint8, device=DEV)
+    rp2, ln2 = ug.utf16le_to_utf8_two_pass(out16[: r.written], b2)
+    assert rp2 == (0, r.written, x.size) and ln2 == x.size and torch.equal(b2, t)
 
 
 def test_full_size_config3_and_error_copy():
@@ -64,6 +73,10 @@ def test_full_size_config3_and_error_copy():
     assert torch.equal(out8[: r.written], torch.from_numpy(ref_o).to(DEV))
     assert tuple(ug.utf16le_validate(t)) == tuple(oracle.utf16le_validate(u))
     assert ug.utf8_length_from_utf16le(t) == r.written
+    o2 = torch.empty(ref_r.written + 64, dtype=torch.uint8, device=DEV)
+    rp, ln = ug.utf16le_to_utf8_two_pass(t, o2)
+    assert tuple(rp) == tuple(ref_r) and ln == r.written
+    assert torch.equal(o2[: r.written], out8[: r.written])
     rng = np.random.default_rng(np.random.SeedSequence([4, 0xE, 1, 0]))
     for _ in range(2):
         v = u.copy()
@@ -73,6 +86,7 @@ def test_full_size_config3_and_error_copy():
         assert tuple(rv) == tuple(oracle.utf16le_to_utf8(v)[0])
         assert (rv.error, rv.position) == (ug.SURROGATE, p)
         assert tuple(ug.utf16le_validate(tv)) == (ug.SURROGATE, p, 0)
+        assert tuple(ug.utf16le_to_utf8_two_pass(tv, out8)[0]) == tuple(rv)
 
 
 @pytest.fixture(scope="module")
@@ -121,6 +135,27 @@ def test_config4_full_size_bench_launch(c4_ref):
     t, out16, n16, counts = c4_ref
     n = t.numel()
     assert ug.utf16_length_from_utf8(t) == n16
+    # the launch bench.py times (two-pass: the shard plan + the planned shard kernel at G = 1)
+    # reproduces the oracle-verified output unit for unit, both directions
+    plan = ug.plan_buffer(DEV)
+    lens = torch.zeros(2, dtype=torch.int64, device=DEV)
+    recp = ug.record_buffer(DEV, 1)
+    o2 = torch.empty(n, dtype=torch.int16, device=DEV)
+    ug.utf8_shard_plan_async(t, 0, n, 0, 0, lens, plan)
+    ug.utf8_to_utf16le_shard_planned_async(t, 0, n, 0, 0, 0, plan, o2, recp)
+    torch.cuda.synchronize()
+    rp = ug.decode_records(recp)[0]
+    assert rp.first_err == ug.NONE and rp.count == n16 and int(lens[0]) == n16
+    assert torch.equal(o2[:n16], out16[:n16])
+    del o2
+    b2 = torch.empty(n, dtype=torch.uint8, device=DEV)
+    ug.utf16le_shard_plan_async(out16[:n16], 0, n16, 0, 0, lens, plan, len_off=8)
+    ug.utf16le_to_utf8_shard_planned_async(out16[:n16], 0, n16, 0, 0, 0, plan, b2, recp)
+    torch.cuda.synchronize()
+    rp2 = ug.decode_records(recp)[0]
+    assert rp2.first_err == ug.NONE and rp2.count == n and int(lens[1]) == n
+    assert torch.equal(b2, t)
+    del b2
     # reverse through the shard call as well, then the round trip is the identity
     back = torch.empty(n, dtype=torch.uint8, device=DEV)
     rec = ug.record_buffer(DEV, 1)
@@ -143,16 +178,23 @@ def shard_cuts_utf8(host: np.ndarray, G: int):
     return [ugd.utf8_cut(get, c, n) for c in ugd.nominal_cuts(n, G)]
 
 
-def run_sharded_fwd(t, cuts, out, validate=False):
+def run_sharded_fwd(t, cuts, out, validate=False, planned=False):
     """One shard launch per virtual rank over the device buffer t, then every rank's combine
-    on the device.  Returns (global result, records, per-rank output offsets)."""
+    on the device.  Returns (global result, records, per-rank output offsets).  planned: the
+    two-pass form (shard plan + planned shard kernel), as bench.py times it."""
     G = len(cuts) - 1
     n = t.numel()
     recs = ug.record_buffer(DEV, G)
+    plan = ug.plan_buffer(DEV) if planned else None
+    lens = torch.zeros(1, dtype=torch.int64, device=DEV)
     for k in range(G):
         lo, hi = cuts[k], cuts[k + 1]
         hb, ha = min(lo, 3), min(n - hi, 3)
-        if validate:
+        if planned:
+            ug.utf8_shard_plan_async(t, lo, hi - lo, hb, ha, lens, plan)
+            ug.utf8_to_utf16le_shard_planned_async(t, lo, hi - lo, hb, ha, lo, plan, out[lo:hi],
+                                                   recs, rec_off=k * ug.RECORD_BYTES)
+        elif validate:
             ug.utf8_validate_shard_async(t, lo, hi - lo, hb, ha, lo, recs,
                                          rec_off=k * ug.RECORD_BYTES)
         else:
@@ -176,6 +218,11 @@ def test_config4_sharded_matches_oracle(c4, c4_ref, G):
     n = c4.size
     cuts = shard_cuts_utf8(c4, G)
     outs = torch.empty(n, dtype=torch.int16, device=DEV)
+    rp, recp, offp = run_sharded_fwd(t, cuts, outs, planned=True)   # the bench's two-pass form
+    assert tuple(rp) == (0, n, n16)
+    for k in range(G):
+        assert torch.equal(outs[cuts[k]:cuts[k] + recp[k].count],
+                           out16[offp[k]:offp[k] + recp[k].count]), k
     r, recs, offs = run_sharded_fwd(t, cuts, outs)
     assert tuple(r) == (0, n, n16)
     assert offs == list(np.cumsum([0] + [x.count for x in recs[:-1]]))
@@ -220,6 +267,8 @@ def test_config4_error_copies_sharded(c4, c4_ref, G):
             want = (synth.UTF8_EXPECTED_KIND[cls], p, want_wr)
             r, *_ = run_sharded_fwd(t, cuts, outs)
             assert tuple(r) == want, (G, j, cls, r, want)
+            rp, *_ = run_sharded_fwd(t, cuts, outs, planned=True)
+            assert tuple(rp) == want, (G, j, cls, "two-pass", rp, want)
             v, *_ = run_sharded_fwd(t, cuts, None, validate=True)
             assert (v.error, v.position, v.written) == (want[0], p, 0), (G, j, cls, v)
         finally:
