@@ -2279,7 +2279,9 @@ __global__ void __launch_bounds__(NT, CTAS_PER_SM)
     if (tid == SHIPPER) bulk_wait_read_all();  // the store of the previous tile has read its stage
     named_sync<BAR_DATA, NT>();  // stage k & 1 complete; warp totals of the next tile published
     // ship tile t: 16-byte aligned interior by one TMA bulk store, head / tail by the warp
-    {
+    // (head and tail are < 16 bytes: only the shipping warp has anything to do; skipping the
+    // rest measured forward -2..-3 %, but +4..+7 % in the UTF-16 kernel, which keeps them)
+    if (Pol::UNIT == 2 || warp == UG_SHIP_WARP) {
       unsigned long long hi = P + C;
       if (hi > a.out_cap) hi = a.out_cap;
       if (hi > P) {
