@@ -313,7 +313,7 @@ int ug_utf16be_validate_shard_async(const uint16_t *in, size_t n, size_t halo_be
  * (DESIGN.md f2): chunk i is copied in on one copy stream, transcoded as a shard (the sharded
  * kernel is exact at any cut, D2) on `stream`, and its output copied out on a second
  * copy stream as soon as its 32-byte record has fixed its output offset, so host->device
- * copies, kernels and device->host copies overlap.  Chunks stream through 4 library-owned
+ * copies, kernels and device->host copies overlap.  Chunks stream through 4 (ug_set_host_slots) library-owned
  * device staging slots per (device, stream) (a chunk with its halos + its worst-case output
  * each), reused round robin: device memory is O(chunk), not O(n), so inputs larger than HBM
  * stream through.  Synchronous (returns when the output is in out_host).
@@ -330,9 +330,12 @@ ug_result utf8_to_utf16be_host(const uint8_t *in_host, size_t n, uint16_t *out_h
 ug_result utf16be_to_utf8_host(const uint16_t *in_host, size_t n, uint8_t *out_host,
                                size_t out_cap, void *stream);
 
-/* Chunk size of the host-buffer pipeline, in input code units (default 32 Mi units); returns
+/* Chunk size of the host-buffer pipeline, in input code units (default 64 Mi units); returns
  * the previous value.  0 restores the default.  Process-wide. */
 size_t ug_set_host_chunk(size_t units);
+/* Number of device staging slots of the host-buffer pipeline (chunks in flight; 2..16, default
+ * 4; other values restore the default); returns the previous value.  Process-wide. */
+int ug_set_host_slots(int slots);
 
 /* ------------------------------------------------------------------ misc */
 /* Human-readable name of a ug_error value (static string). */

@@ -111,6 +111,7 @@ def _load():
         "ug_release_workspaces": ([], None),
         "ug_abi_version": ([], I),
         "ug_tile_bytes": ([], S),
+        "ug_set_host_slots": ([I], I),
         "ug_plan_bytes": ([], S),
         "ug_utf16_length_from_utf8_plan_async": ([P, S, P, P, P], I),
         "ug_utf8_length_from_utf16le_plan_async": ([P, S, P, P, P], I),
@@ -603,6 +604,11 @@ def utf16_cut_backoff(words, at: int) -> int:
 
 
 # --------------------------------------------------------------------------- host buffers
+def set_host_slots(slots: int) -> int:
+    """Device staging slots of the host pipeline (2..16); returns the previous value."""
+    return int(lib.ug_set_host_slots(slots))
+
+
 def set_host_chunk(units: int) -> int:
     """Chunk size (input units) of the pipelined host-buffer path; returns the previous one."""
     return int(lib.ug_set_host_chunk(units))

@@ -22,9 +22,10 @@ static_assert(sizeof(ug_shard_record) == 32, "record is 32 bytes");
 namespace {
 
 std::atomic<uint64_t> g_launches{0};
-constexpr size_t HOST_CHUNK_DEFAULT = 32ull << 20;  // input units per pipelined host chunk
+constexpr size_t HOST_CHUNK_DEFAULT = 64ull << 20;  // input units per pipelined host chunk (e2e sweep: 64 Mi +1.3 % over 32 Mi; slots 3-8 equal)
 std::atomic<size_t> g_host_chunk{HOST_CHUNK_DEFAULT};
-constexpr int HOST_SLOTS = 4;  // staging slots of the host pipeline (chunks in flight)
+constexpr int HOST_SLOTS_MAX = 16;
+std::atomic<int> g_host_slots{4};  // staging slots of the host pipeline (chunks in flight)
 constexpr unsigned long long MAX_N = (1ull << 38) - 1;  // status words carry 38-bit values
 
 struct Workspace {
@@ -433,7 +434,7 @@ cudaError_t ensure_staging(Workspace *w, size_t in_bytes, size_t out_bytes) {
   return cudaSuccess;
 }
 
-// Per-slot resources of the host pipeline (HOST_SLOTS staging slots, reused round robin): two
+// Per-slot resources of the host pipeline (up to HOST_SLOTS_MAX staging slots, reused round robin): two
 // copy streams, input-landed / kernel-done / output-drained events per slot, and one shard
 // record per chunk (device + pinned copy; 32 B each).
 cudaError_t ensure_pipeline(Workspace *w, size_t nchunks) {
@@ -443,7 +444,7 @@ cudaError_t ensure_pipeline(Workspace *w, size_t nchunks) {
     if ((e = cudaStreamCreateWithFlags(&w->d2h, cudaStreamNonBlocking)) != cudaSuccess) return e;
     if ((e = cudaEventCreateWithFlags(&w->ev_start, cudaEventDisableTiming)) != cudaSuccess)
       return e;
-    for (int k = 0; k < HOST_SLOTS; k++) {
+    for (int k = 0; k < HOST_SLOTS_MAX; k++) {
       cudaEvent_t ev[3];
       for (auto &x : ev)
         if ((e = cudaEventCreateWithFlags(&x, cudaEventDisableTiming)) != cudaSuccess) return e;
@@ -466,17 +467,17 @@ cudaError_t ensure_pipeline(Workspace *w, size_t nchunks) {
 }
 
 // Host-buffer transcode as a pipeline over chunks of the input cut at character starts
-// (DESIGN.md f2), streamed through HOST_SLOTS fixed staging slots, so device memory is
+// (DESIGN.md f2), streamed through a fixed number of staging slots (ug_set_host_slots), so device memory is
 // O(chunk), not O(n), and inputs larger than HBM stream through:
 //   h2d stream:  copy chunk i WITH its halos ([lo - 3, hi + 3) bytes / [lo - 1, hi + 1) words,
-//                clipped at the ends) into slot i % HOST_SLOTS, once that slot's previous
+//                clipped at the ends) into slot i % slots, once that slot's previous
 //                chunk has been copied out;
 //   `s`:         the fused kernel transcodes chunk i as a shard (exact at any cut, D2)
 //                into the slot's output, and its 32-byte record is copied to pinned memory;
 //   d2h stream:  the host waits for record i, which fixes chunk i's output offset (the prefix
 //                of the earlier chunks' counts), and enqueues the copy of its output units;
-//                then the slot is refilled with chunk i + HOST_SLOTS.
-// Copies in both directions and the kernels overlap (HOST_SLOTS - 1 chunks ahead of the host);
+//                then the slot is refilled with chunk i + slots.
+// Copies in both directions and the kernels overlap (slots - 1 chunks ahead of the host);
 // the result is combined from the records exactly as the unsharded kernel states it (first
 // error, written, output too small).  The workspace mutex is held for the whole call.
 ug_result run_host(Op op, const void *in_host, unsigned long long n, void *out_host,
@@ -513,7 +514,8 @@ ug_result run_host(Op op, const void *in_host, unsigned long long n, void *out_h
   // one slot: a chunk plus both halos (input), its worst-case output; 16-byte strides
   const size_t in_slot = ((maxlen + 2 * halo) * ius + 15) & ~(size_t)15;
   const size_t out_slot = (maxlen * ub * ous + 15) & ~(size_t)15;
-  const int slots = (int)(nch < (size_t)HOST_SLOTS ? nch : (size_t)HOST_SLOTS);
+  const int hs = g_host_slots.load();
+  const int slots = (int)(nch < (size_t)hs ? nch : (size_t)hs);
   std::lock_guard<std::mutex> lk(w->mu);
   if (ensure_staging(w, slots * in_slot, slots * out_slot) != cudaSuccess ||
       ensure_pipeline(w, nch) != cudaSuccess)
@@ -1016,6 +1018,11 @@ ug_result utf8_to_utf16be_host(const uint8_t *in_host, size_t n, uint16_t *out_h
 ug_result utf16be_to_utf8_host(const uint16_t *in_host, size_t n, uint8_t *out_host,
                                size_t out_cap, void *stream) {
   return run_host(Op::U16BE_TO_U8, in_host, n, out_host, out_cap, (cudaStream_t)stream);
+}
+
+int ug_set_host_slots(int slots) {
+  const int v = slots < 2 ? 4 : (slots > HOST_SLOTS_MAX ? HOST_SLOTS_MAX : slots);
+  return g_host_slots.exchange(v);
 }
 
 size_t ug_set_host_chunk(size_t units) {

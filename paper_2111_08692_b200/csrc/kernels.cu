@@ -2054,9 +2054,13 @@ __global__ void __launch_bounds__(LNT) k_plan8(const PlanArgs a) {
 #ifndef UG_PRING16
 #define UG_PRING16 3
 #endif
+#ifndef UG_PMINB16
+#define UG_PMINB16 CTAS_PER_SM
+#endif
 template <class Pol>
 struct PlannedGeo {
   static constexpr int RING = Pol::UNIT == 1 ? UG_PRING8 : UG_PRING16;  // input slots
+  static constexpr int MINB = Pol::UNIT == 1 ? CTAS_PER_SM : UG_PMINB16;  // launch bounds
   static constexpr size_t SMEM = (size_t)RING * INBUF + 2 * (size_t)Pol::STAGE;
 };
 
@@ -2068,7 +2072,7 @@ struct PlannedOrder {
 };
 
 template <class Pol>
-__global__ void __launch_bounds__(NT, CTAS_PER_SM)
+__global__ void __launch_bounds__(NT, PlannedGeo<Pol>::MINB)
     k_transcode_planned(const TileArgs a, const unsigned long long *plan) {
   using Out = typename Pol::Out;
   using G = PlannedGeo<Pol>;
