@@ -56,7 +56,7 @@ with open(f"{P}/{tag}_ncu_launches.txt", "w") as f:
             "SHARES.\n# The first k_transcode<U8PolT> launch is bench.py's untimed setup pass (it "
             "learns the UTF-16 length); every step = k_plan8 + k_transcode_planned<U8PolT> + "
             "k_plan16 + k_transcode_planned<U16PolT>.\n\n")
-    step = {k: v for k, v in per.items() if k != "ug::k_transcode<ug::U8PolT<(bool)0>>"}
+    step = {k: v for k, v in per.items() if not k.startswith(("k_transcode<U8PolT", "ug::k_transcode<ug::U8PolT"))}
     tot = sum(sum(v) / len(v) for v in step.values())
     f.write(f"{'kernel':48s} {'launches':>8s} {'avg_us':>10s} {'step_share':>10s}\n")
     for k, v in sorted(per.items(), key=lambda kv: -sum(kv[1]) / len(kv[1])):
