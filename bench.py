@@ -53,6 +53,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-per-op", action="store_true")
     p.add_argument("--no-per-config", action="store_true")
+    p.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                   help="gloo: functional multi-rank check on shared GPUs (not a bench number)")
     p.add_argument("--path", default="planned", choices=["planned", "chained"],
                    help="two-pass (sizing pass plans the transcoder) or single-pass look-back")
     p.add_argument("--out", default="")
@@ -164,10 +166,33 @@ def run_ours(args):
 
     G, rank, local = dist_env()
     assert G == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={G}"
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # --dist-backend gloo: a FUNCTIONAL check of the multi-rank code path when fewer GPUs than
+    # ranks exist (ranks share devices; host-side collectives only, no kernel waits on another
+    # rank).  Its timings are not bench numbers.
+    local_dev = local % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if G > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
+
+    def allreduce(t, op=dist.ReduceOp.SUM):
+        if args.dist_backend == "nccl":
+            dist.all_reduce(t, op=op)
+        else:
+            h = t.cpu()
+            dist.all_reduce(h, op=op)
+            t.copy_(h)
+
+    def allgather_into(out, inp):
+        if args.dist_backend == "nccl":
+            dist.all_gather_into_tensor(out, inp)
+        else:
+            parts = [torch.empty_like(inp, device="cpu") for _ in range(G)]
+            dist.all_gather(parts, inp.cpu())
+            out.copy_(torch.cat(parts))
     cfg = synth.CONFIGS[args.config]
     size = cfg.size if not args.size_mib else args.size_mib << 20
     t_gen = time.time()
@@ -202,7 +227,7 @@ def run_ours(args):
     cnts = torch.zeros(G, dtype=torch.int64, device=dev)
     cnts[rank] = n16
     if G > 1:
-        dist.all_reduce(cnts)
+        allreduce(cnts)
     N16_global = int(cnts.sum())
     off16 = int(cnts[:rank].sum())
 
@@ -212,8 +237,8 @@ def run_ours(args):
     def gather_combine(which):
         if G > 1:
             # one NCCL all-gather of the 32-byte shard records, then the combine kernel
-            dist.all_gather_into_tensor(allrec[which * G * R:(which + 1) * G * R],
-                                        rec[which * R:(which + 1) * R])
+            allgather_into(allrec[which * G * R:(which + 1) * G * R],
+                           rec[which * R:(which + 1) * R])
             ug.combine_records_async(allrec[which * G * R:], G, rank,
                                      size if which == 0 else N16_global,
                                      res[(2 + which) * 24:],
@@ -299,9 +324,9 @@ def run_ours(args):
                        dtype=torch.float64, device=dev)
     if G > 1:
         mx = tot[:3].clone()
-        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        allreduce(mx, op=dist.ReduceOp.MAX)
         sm = tot[3:].clone()
-        dist.all_reduce(sm, op=dist.ReduceOp.SUM)
+        allreduce(sm, op=dist.ReduceOp.SUM)
         ms, fwd_ms, rev_ms = float(mx[0]), float(mx[1]), float(mx[2])
         N8, N16, NCH = int(sm[0]), int(sm[1]), int(sm[2])
     else:
@@ -561,7 +586,8 @@ def run_e2e(args, ug, host_shard, n16, G, rank, dev, dist):
         times.append(time.perf_counter() - t)
         assert r1 == (0, n8, n16) and r2 == (0, n16, n8), (r1, r2)
     dt = min(times[1:]) if len(times) > 1 else times[0]
-    tt = torch.tensor([dt, float(n8), float(n16)], dtype=torch.float64, device=dev)
+    tt = torch.tensor([dt, float(n8), float(n16)], dtype=torch.float64,
+                      device=dev if args.dist_backend == "nccl" else "cpu")
     if G > 1:
         a = tt[:1].clone()
         dist.all_reduce(a, op=dist.ReduceOp.MAX)
