@@ -1052,6 +1052,22 @@ uint64_t ug_launch_count(void) { return g_launches.load(); }
 void ug_release_workspaces(void) {
   int dev;
   if (cudaGetDevice(&dev) != cudaSuccess) return;
+  {  // the multi-device entry's gather buffers on this device
+    std::lock_guard<std::mutex> lk(g_shard_mu);
+    for (auto it = g_shard_ctx.begin(); it != g_shard_ctx.end();) {
+      if (it->first.first == dev) {
+        cudaStreamSynchronize((cudaStream_t)it->first.second);
+        cudaFree(it->second.recs);
+        cudaFree(it->second.res);
+        cudaFree(it->second.off);
+        cudaFreeHost(it->second.h_res);
+        cudaFreeHost(it->second.h_off);
+        it = g_shard_ctx.erase(it);
+      } else {
+        ++it;
+      }
+    }
+  }
   std::lock_guard<std::mutex> lk(g_mu);
   for (auto it = g_ws.begin(); it != g_ws.end();) {
     if (it->first.first == dev) {

@@ -1697,7 +1697,8 @@ __global__ void __launch_bounds__(T16_THREADS, CTAS_PER_SM) k_transcode16(const 
 //
 // Plan buffer (device, 8-byte words): [0] tag, [1] input address, [2] n (input bytes),
 // [3] sub-ranges, [4] tiles per sub-range, [5] total under the emission rule, [6] lead,
-// [7] reserved, [8 + j] output offset (exclusive prefix of the counts) of sub-range j.
+// [7] halos (before << 32 | after, bytes), [8 + j] output offset (exclusive prefix of the
+// counts) of sub-range j.
 constexpr int PLAN_HDR = 8;
 constexpr int PLAN_MAX_SUB = 8192;
 static_assert(PLAN_WORDS == PLAN_HDR + PLAN_MAX_SUB, "plan layout (internal.h PLAN_WORDS)");
@@ -1723,6 +1724,12 @@ __device__ __forceinline__ void sub_span(const PlanArgs &a, long long j, long lo
   if (t0 >= (long long)a.ntiles) q0 = q1 = a.win.n;
   *p0 = q0;
   *p1 = q1 > q0 ? q1 : q0;
+}
+
+// The halos of a window (bytes before / after the owned range that are readable context): part
+// of the plan's identity, since the UTF-8 emit rule at the first positions reads them.
+__device__ __forceinline__ unsigned long long plan_halos(const Window &w) {
+  return ((unsigned long long)(-w.lo_valid) << 32) | (unsigned long long)(w.hi_valid - w.n);
 }
 
 __device__ __forceinline__ void plan_finish(const PlanArgs &a, unsigned long long emit_sum,
@@ -1784,7 +1791,7 @@ __device__ __forceinline__ void plan_finish(const PlanArgs &a, unsigned long lon
     a.plan[4] = a.tps;
     a.plan[5] = total;
     a.plan[6] = (unsigned long long)a.win.lead;
-    a.plan[7] = 0;
+    a.plan[7] = plan_halos(a.win);
     if (a.d_len) *a.d_len = L;
     a.ctr->accum = 0;
     a.ctr->done = 0;
@@ -2095,7 +2102,7 @@ __global__ void __launch_bounds__(NT, PlannedGeo<Pol>::MINB)
   // the plan must describe this very input (else: UG_ERR_ARG from finish, no work)
   const bool bad = plan[0] != PLAN_TAG || plan[1] != (unsigned long long)(uintptr_t)win.base ||
                    plan[2] != (unsigned long long)win.n ||
-                   plan[6] != (unsigned long long)win.lead;
+                   plan[6] != (unsigned long long)win.lead || plan[7] != plan_halos(win);
   const long long nsub = bad ? 0 : (long long)plan[3], tps = bad ? 1 : (long long)plan[4];
   if (bad && tid == 0 && blockIdx.x == 0) atomicOr(&a.ctr->flags, 1ull);
   // producer (lane 0 of the last warp, not the shipping warp 0): tiles in sub-range order,

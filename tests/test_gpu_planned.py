@@ -148,6 +148,10 @@ def test_planned_rejects_a_plan_of_another_input():
     ug.utf16_length_from_utf8_plan_async(t, lens, plan)                 # right plan: OK after
     ug.utf8_to_utf16le_planned_async(t, plan, out, res)
     assert tuple(ug.decode_results(res)[0]) == tuple(oracle.utf8_to_utf16le(a)[0])
+    # the same pointer and n, but planned as a shard window with halos: a different window
+    ug.utf8_shard_plan_async(t, 3, a.size - 6, 3, 3, lens, plan)
+    ug.utf8_to_utf16le_planned_async(t[3:], plan, out, res, n=a.size - 6)
+    assert ug.decode_results(res)[0].error == ug.ERR_ARG
 
 
 @pytest.mark.parametrize("G", [2, 5])
