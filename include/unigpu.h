@@ -345,10 +345,13 @@ const char *ug_error_name(int err);
 uint64_t ug_launch_count(void);
 /* Free the workspaces of the current device (all streams). */
 void ug_release_workspaces(void);
-/* Input bytes per tile of the transcoding kernels (16 KiB in this build): tile t of a call
+/* Input bytes per tile of the single-pass transcoding kernels (16 KiB in this build): tile t of a call
  * covers input bytes [t * T - lead, (t + 1) * T - lead) where lead = (input address mod 16).
  * Exposed so tests can place inputs across real tile edges. */
 size_t ug_tile_bytes(void);
+/* Input bytes per tile of the two-pass (planned) transcoders and of the plan's sub-ranges
+ * (8 KiB in this build), with the same tiling rule as ug_tile_bytes. */
+size_t ug_planned_tile_bytes(void);
 /* Device bytes currently held by the library's workspace for (current device, stream): tile
  * status words, counters, result slots, and the host pipeline's staging slots (bounded:
  * 4 slots of one chunk each, whatever n is) and per-chunk records.  0 if none exists. */

@@ -111,6 +111,7 @@ def _load():
         "ug_release_workspaces": ([], None),
         "ug_abi_version": ([], I),
         "ug_tile_bytes": ([], S),
+        "ug_planned_tile_bytes": ([], S),
         "ug_set_host_slots": ([I], I),
         "ug_plan_bytes": ([], S),
         "ug_utf16_length_from_utf8_plan_async": ([P, S, P, P, P], I),
@@ -131,6 +132,8 @@ def _load():
         "ug_utf8_length_from_utf16be_ex": ([P, S, P, P], I),
     }
     for name, (args, res) in sig.items():
+        if os.environ.get("UG_LIB_OVERRIDE") and not hasattr(L, name):
+            continue  # A/B tooling: an older build (tools/r2_ab.sh) may lack newer entries
         f = getattr(L, name)
         f.argtypes = args
         f.restype = res
@@ -186,6 +189,11 @@ def workspace_bytes(stream=None) -> int:
 def tile_bytes() -> int:
     """Input bytes per tile of the transcoding kernels (tiles start at 16-byte addresses)."""
     return int(lib.ug_tile_bytes())
+
+
+def planned_tile_bytes() -> int:
+    """Input bytes per tile of the two-pass (planned) transcoders and of the plan's sub-ranges."""
+    return int(lib.ug_planned_tile_bytes())
 
 
 # --------------------------------------------------------------------------- synchronous

@@ -85,7 +85,7 @@ cudaError_t device_info(int dev, DeviceInfo **out) {
       e = planned_occupancy(op, &d.occ_planned[u]);
       if (e != cudaSuccess) return e;
       if (d.occ_planned[u] < 1) d.occ_planned[u] = 1;
-      if (d.occ_planned[u] > CTAS_PER_SM) d.occ_planned[u] = CTAS_PER_SM;
+      if (d.occ_planned[u] > CPSP) d.occ_planned[u] = CPSP;
     }
     d.configured = true;
   }
@@ -199,6 +199,7 @@ int enqueue_tile_ws(Workspace *w, DeviceInfo *di, Op op, const void *in, unsigne
   a.result = d_result;
   a.rec = d_rec;
   a.global_off = global_off;
+  a.tile = TILE;
   unsigned long long maxg = (unsigned long long)di->sms * (unsigned long long)di->occ[(int)op];
   const unsigned long long want = (a.ntiles + per_cta - 1) / per_cta;
   int grid = (int)(want < maxg ? want : maxg);
@@ -233,10 +234,12 @@ PlanGeo plan_geo(DeviceInfo *di, bool u16in, const void *in, unsigned long long 
   const unsigned long long us = u16in ? 2 : 1;
   PlanGeo g;
   g.win = make_window(in, n * us, hb * us, ha * us);
-  g.ntiles = (unsigned long long)((g.win.n - 1 + g.win.lead) / TILE + 1);
+  g.ntiles = (unsigned long long)((g.win.n - 1 + g.win.lead) / TILEP + 1);
   g.grid = di->sms * di->occ_planned[u16in ? 1 : 0];
-  // sub-ranges of tps tiles, PLAN_SUBS_PER_CTA per CTA (taken by ticket: load balance)
-  unsigned long long want = (unsigned long long)g.grid * PLAN_SUBS_PER_CTA;
+  // sub-ranges of tps tiles (taken by ticket: load balance), PLAN_SUBS_PER_CTA per
+  // 16 KiB-tile CTA slot: the count does not grow with the planned kernels' CTA count, whose
+  // tiles are smaller -- more sub-ranges only cost the sizing pass
+  unsigned long long want = (unsigned long long)di->sms * CTAS_PER_SM * PLAN_SUBS_PER_CTA;
   if (want > (unsigned long long)(PLAN_WORDS - 8)) want = PLAN_WORDS - 8;
   if (want > g.ntiles) want = g.ntiles;
   g.tps = (g.ntiles + want - 1) / want;
@@ -295,6 +298,7 @@ int enqueue_planned(Op op, const void *in, unsigned long long n, unsigned long l
   a.result = d_result;
   a.rec = d_rec;
   a.global_off = global_off;
+  a.tile = TILEP;
   if (launch_planned(op, a, (const unsigned long long *)d_plan, g.grid, s) != cudaSuccess)
     return UG_ERR_CUDA;
   g_launches.fetch_add(1);
@@ -1103,6 +1107,7 @@ void ug_release_workspaces(void) {
 
 int ug_abi_version(void) { return UNIGPU_ABI_VERSION; }
 size_t ug_tile_bytes(void) { return (size_t)TILE; }
+size_t ug_planned_tile_bytes(void) { return (size_t)TILEP; }
 
 size_t ug_workspace_bytes(void *stream) {
   int dev;

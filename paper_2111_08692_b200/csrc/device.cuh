@@ -36,6 +36,19 @@ constexpr int BPT = TILE / NT;    // 32 contiguous input bytes per thread
 constexpr int LB_PER_LANE = UG_LB_PER_LANE;  // look-back window: 32 lanes x LB_PER_LANE tiles
 constexpr int HALO = 16;          // bytes of context loaded before and after each tile
 constexpr int INBUF = TILE + 2 * HALO;
+// The two-pass (planned) transcoders run their own geometry: 256 threads x 32 bytes = 8 KiB
+// tiles, 4 CTAs per SM (measured against 512 x 32 at 2 CTAs/SM: forward -1.4 %, reverse -2.5 %
+// on config 4, -5..-7 % on ASCII; the same switch for every kernel slowed the validators and
+// the single-pass kernels, which keep NT).
+#ifndef UG_NTP
+#define UG_NTP 256
+#endif
+#ifndef UG_CPSP
+#define UG_CPSP (1024 / UG_NTP)
+#endif
+constexpr int NTP = UG_NTP;
+constexpr int TILEP = NTP * 32;
+constexpr int CPSP = UG_CPSP;
 
 // ---------------------------------------------------------------- workspace counters
 // One per (device, stream); zero-initialised once, self-resetting at the end of every call
@@ -186,15 +199,17 @@ struct Window {
   long long n;             // owned bytes
 };
 
+template <int TB = TILE>
 __device__ __forceinline__ long long tile_pos(const Window &w, long long t) {
-  return t * TILE - w.lead;
+  return t * TB - w.lead;
 }
 
 // Issued by ONE thread: bulk-load the smem image of tile t into buf, completing on bar.
+template <int TB = TILE>
 __device__ __forceinline__ void issue_tile_load(const Window &w, long long t, uint8_t *buf,
                                                 uint64_t *bar) {
-  uintptr_t A = (uintptr_t)(w.base + tile_pos(w, t) - HALO);
-  uintptr_t B = A + INBUF;
+  uintptr_t A = (uintptr_t)(w.base + tile_pos<TB>(w, t) - HALO);
+  uintptr_t B = A + TB + 2 * HALO;
   uintptr_t a = A > w.mem_lo ? A : w.mem_lo;
   uintptr_t b = B < w.mem_hi ? B : w.mem_hi;
   uint32_t bytes = b > a ? (uint32_t)(b - a) : 0u;
@@ -203,20 +218,23 @@ __device__ __forceinline__ void issue_tile_load(const Window &w, long long t, ui
 }
 
 // Does tile t's smem image reach outside the valid window (needs fix_tile_edges)?
+template <int TB = TILE>
 __device__ __forceinline__ bool tile_at_edge(const Window &w, long long t) {
-  const long long p0 = tile_pos(w, t) - HALO;
-  return !(p0 >= w.lo_valid && p0 + INBUF <= w.hi_valid);
+  const long long p0 = tile_pos<TB>(w, t) - HALO;
+  return !(p0 >= w.lo_valid && p0 + TB + 2 * HALO <= w.hi_valid);
 }
 
 // After the load landed: zero every smem byte whose position lies outside the valid window
 // (only tiles touching the window edges do any work).  Called by threads 0..nthreads-1; the
 // caller syncs after.
+template <int TB = TILE>
 __device__ __forceinline__ void fix_tile_edges(const Window &w, long long t, uint8_t *buf,
                                                int nthreads, int first = -1) {
-  long long p0 = tile_pos(w, t) - HALO;
-  if (p0 >= w.lo_valid && p0 + INBUF <= w.hi_valid) return;
+  constexpr int IB = TB + 2 * HALO;
+  long long p0 = tile_pos<TB>(w, t) - HALO;
+  if (p0 >= w.lo_valid && p0 + IB <= w.hi_valid) return;
   uint32_t *b32 = reinterpret_cast<uint32_t *>(buf);
-  for (int q = first >= 0 ? first : (int)threadIdx.x; q < INBUF / 4; q += nthreads) {
+  for (int q = first >= 0 ? first : (int)threadIdx.x; q < IB / 4; q += nthreads) {
     long long pos = p0 + 4 * q;
     if (pos >= w.lo_valid && pos + 4 <= w.hi_valid) continue;
     b32[q] &= range_bytes(pos, w.lo_valid, w.hi_valid);

@@ -330,9 +330,9 @@ struct U8PolT {
     *kind = u8::decode_kind(x);
     *wr = 0;
     if (!xc) return;
-    long long te = ((long long)e + win.lead) / TILE;
+    long long te = ((long long)e + win.lead) / a.tile;
     unsigned long long base = te ? (ld_relaxed(a.status + te - 1) & VALMASK) : 0ull;
-    long long from = te * TILE - win.lead;
+    long long from = te * a.tile - win.lead;
     if (from < 0) from = 0;
     unsigned long long c = 0;
     for (long long i = from + lane; i < (long long)e; i += 32)
@@ -680,9 +680,9 @@ struct U16PolT {
     *kind = u8::SURROGATE;
     *wr = 0;
     if (!xc) return;
-    long long te = (2 * (long long)e + win.lead) / TILE;
+    long long te = (2 * (long long)e + win.lead) / a.tile;
     unsigned long long base = te ? (ld_relaxed(a.status + te - 1) & VALMASK) : 0ull;
-    long long from = (te * TILE - win.lead) / 2;
+    long long from = (te * a.tile - win.lead) / 2;
     if (from < 0) from = 0;
     unsigned long long c = 0;
     for (long long i = from + lane; i < (long long)e; i += 32)
@@ -1718,7 +1718,7 @@ struct PlanArgs {
 __device__ __forceinline__ void sub_span(const PlanArgs &a, long long j, long long *p0,
                                          long long *p1) {
   const long long t0 = j * (long long)a.tps, t1 = t0 + (long long)a.tps;
-  long long q0 = t0 * TILE - a.win.lead, q1 = t1 * TILE - a.win.lead;
+  long long q0 = t0 * TILEP - a.win.lead, q1 = t1 * TILEP - a.win.lead;
   if (q0 < 0) q0 = 0;
   if (q1 > a.win.n) q1 = a.win.n;
   if (t0 >= (long long)a.ntiles) q0 = q1 = a.win.n;
@@ -2062,13 +2062,16 @@ __global__ void __launch_bounds__(LNT) k_plan8(const PlanArgs a) {
 #define UG_PRING16 3
 #endif
 #ifndef UG_PMINB16
-#define UG_PMINB16 CTAS_PER_SM
+#define UG_PMINB16 CPSP
 #endif
 template <class Pol>
 struct PlannedGeo {
   static constexpr int RING = Pol::UNIT == 1 ? UG_PRING8 : UG_PRING16;  // input slots
-  static constexpr int MINB = Pol::UNIT == 1 ? CTAS_PER_SM : UG_PMINB16;  // launch bounds
-  static constexpr size_t SMEM = (size_t)RING * INBUF + 2 * (size_t)Pol::STAGE;
+  static constexpr int MINB = Pol::UNIT == 1 ? CPSP : UG_PMINB16;        // launch bounds
+  static constexpr int INBUFP = TILEP + 2 * HALO;                         // one input slot
+  // an output stage: a tile's worst-case output (1 unit per byte / 3 bytes per word) + phase
+  static constexpr int STAGE = Pol::UNIT == 1 ? 2 * (TILEP + 32) : 3 * (TILEP / 2) + 64;
+  static constexpr size_t SMEM = (size_t)RING * INBUFP + 2 * (size_t)STAGE;
 };
 
 // Count first (the next tile's count before this tile's decode) or decode first: measured per
@@ -2079,19 +2082,22 @@ struct PlannedOrder {
 };
 
 template <class Pol>
-__global__ void __launch_bounds__(NT, PlannedGeo<Pol>::MINB)
+__global__ void __launch_bounds__(NTP, PlannedGeo<Pol>::MINB)
     k_transcode_planned(const TileArgs a, const unsigned long long *plan) {
   using Out = typename Pol::Out;
   using G = PlannedGeo<Pol>;
   constexpr int PR = G::RING;
+  constexpr int INBUFP = G::INBUFP;
+  constexpr int STAGEP = G::STAGE;
+  constexpr int PRODUCERP = NTP - 32;  // lane 0 of the last warp
   constexpr uint32_t AU = 16 / sizeof(Out);  // output units per 16 bytes
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t *ring = smem;
-  uint8_t *stage_base = smem + PR * INBUF;  // two output stages of Pol::STAGE bytes
+  uint8_t *stage_base = smem + PR * INBUFP;  // two output stages of STAGEP bytes
   __shared__ uint64_t mb_load[PR];
   __shared__ long long s_tile[PR];             // tile in each slot, -1 = no more tiles
   __shared__ unsigned long long s_base[PR];    // a sub-range's first tile: its output offset
-  __shared__ uint32_t s_wsum[2][NT / 32];
+  __shared__ uint32_t s_wsum[2][NTP / 32];
   __shared__ int s_last;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const Window &win = a.win;
@@ -2128,7 +2134,7 @@ __global__ void __launch_bounds__(NT, PlannedGeo<Pol>::MINB)
     s_base[slot] = b;
     if (t >= 0) {
       fence_proxy_async_smem();
-      issue_tile_load(win, t, ring + slot * INBUF, &mb_load[slot]);
+      issue_tile_load<TILEP>(win, t, ring + slot * INBUFP, &mb_load[slot]);
     } else {
       mbar_arrive(&mb_load[slot]);
     }
@@ -2139,7 +2145,7 @@ __global__ void __launch_bounds__(NT, PlannedGeo<Pol>::MINB)
     fence_mbar_init();
   }
   __syncthreads();
-  if (tid == PRODUCER) {
+  if (tid == PRODUCERP) {
     next_j = (long long)atomicAdd(&a.ctr->ticket, 1u);
     for (int j = 0; j < PR; j++) produce(j);
   }
@@ -2149,14 +2155,14 @@ __global__ void __launch_bounds__(NT, PlannedGeo<Pol>::MINB)
   // (UTF-16: bit 31 of *wexcl set = this warp's words hold no surrogate, f1)
   auto count_tile = [&](long long t, int k, uint32_t *cnt, uint32_t *wexcl) {
     uint32_t nosurr = 0;
-    uint8_t *img = ring + (k % PR) * INBUF;
+    uint8_t *img = ring + (k % PR) * INBUFP;
     mbar_wait(&mb_load[k % PR], (k / PR) & 1);
-    if (tile_at_edge(win, t)) {  // tile-uniform
-      named_sync<BAR_DATA, NT>();
-      fix_tile_edges(win, t, img, NT);
-      named_sync<BAR_DATA, NT>();
+    if (tile_at_edge<TILEP>(win, t)) {  // tile-uniform
+      named_sync<BAR_DATA, NTP>();
+      fix_tile_edges<TILEP>(win, t, img, NTP);
+      named_sync<BAR_DATA, NTP>();
     }
-    const long long tp = tile_pos(win, t);
+    const long long tp = tile_pos<TILEP>(win, t);
     uint32_t c;
     if constexpr (Pol::UNIT == 2) {
       // UTF-16: the count is the width sum alone (exact on any input); the pairing check is
@@ -2164,7 +2170,7 @@ __global__ void __launch_bounds__(NT, PlannedGeo<Pol>::MINB)
       constexpr bool BE = Pol::kBE;
       const uint4 *my = reinterpret_cast<const uint4 *>(img + HALO + BPT * tid);
       const uint4 q0 = my[0], q1 = my[1];
-      if (tp >= 0 && tp + TILE <= win.n) {
+      if (tp >= 0 && tp + TILEP <= win.n) {
         const uint32_t orv = q0.x | q0.y | q0.z | q0.w | q1.x | q1.y | q1.z | q1.w;
         if (__all_sync(FULL, (orv & (BE ? 0x80FF80FFu : 0xFF80FF80u)) == 0u)) {
           c = 16u;
@@ -2188,7 +2194,7 @@ __global__ void __launch_bounds__(NT, PlannedGeo<Pol>::MINB)
       }
     } else {
       typename Pol::St st;
-      if (tp >= 0 && tp + TILE <= win.n) {
+      if (tp >= 0 && tp + TILEP <= win.n) {
         Pol::template load<true>(st, img, tid, lane, tp, win.n);
         c = Pol::template analyze<true>(st, tid, true);
       } else {
@@ -2212,7 +2218,7 @@ __global__ void __launch_bounds__(NT, PlannedGeo<Pol>::MINB)
   };
   // after the barrier: this warp's offset inside the tile and the tile total
   auto tile_offsets = [&](int k, uint32_t *woff, uint32_t *total) {
-    const uint32_t v = lane < NT / 32 ? s_wsum[k & 1][lane] : 0u;
+    const uint32_t v = lane < NTP / 32 ? s_wsum[k & 1][lane] : 0u;
     // UTF-8 input: two REDUX instead of the shuffle scan (measured: forward -1 %; the same in
     // the UTF-16 kernel +1.4 % on config 4, so it keeps the shuffles)
     if constexpr (Pol::UNIT == 1) {
@@ -2222,12 +2228,12 @@ __global__ void __launch_bounds__(NT, PlannedGeo<Pol>::MINB)
     }
     uint32_t sc = v;
 #pragma unroll
-    for (int d = 1; d < NT / 32; d <<= 1) {
+    for (int d = 1; d < NTP / 32; d <<= 1) {
       const uint32_t y = __shfl_up_sync(FULL, sc, d);
       if (lane >= d) sc += y;
     }
     *woff = __shfl_sync(FULL, sc - v, warp);
-    *total = __shfl_sync(FULL, sc, NT / 32 - 1);
+    *total = __shfl_sync(FULL, sc, NTP / 32 - 1);
   };
 
   // the tile of the k-th iteration (after its load has landed) and its sub-range base
@@ -2241,11 +2247,11 @@ __global__ void __launch_bounds__(NT, PlannedGeo<Pol>::MINB)
   unsigned long long running = 0, base_t;
   long long t = slot_tile(0, &base_t);
   if (t >= 0) count_tile(t, 0, &cnt, &wex);
-  named_sync<BAR_DATA, NT>();
+  named_sync<BAR_DATA, NTP>();
   if (t >= 0) tile_offsets(0, &woff, &C);
   for (int k = 0; t >= 0; k++) {
     const unsigned long long P = base_t != NONE ? base_t : running;
-    Out *stage = reinterpret_cast<Out *>(stage_base + (k & 1) * Pol::STAGE);
+    Out *stage = reinterpret_cast<Out *>(stage_base + (k & 1) * STAGEP);
     const uint32_t ph = (uint32_t)((((uintptr_t)(out + P)) & 15u) / sizeof(Out));
     uint32_t cnt2 = 0, wex2 = 0;
     unsigned long long base2 = NONE;
@@ -2256,13 +2262,13 @@ __global__ void __launch_bounds__(NT, PlannedGeo<Pol>::MINB)
     }
     // decode tile t at its global 16-byte phase (its input image is still in slot k % PR)
     {
-      uint8_t *img = ring + (k % PR) * INBUF;
+      uint8_t *img = ring + (k % PR) * INBUFP;
       typename Pol::St st;
-      const long long tp = tile_pos(win, t);
+      const long long tp = tile_pos<TILEP>(win, t);
       const uint32_t o = ph + woff + (wex & 0x7FFFFFFFu);
       if constexpr (Pol::UNIT == 2) {  // encode + pairing check in one pass
         unsigned long long f = NONE;
-        if (tp >= 0 && tp + TILE <= win.n) {
+        if (tp >= 0 && tp + TILEP <= win.n) {
           Pol::template load<true>(st, img, tid, lane, tp, win.n);
           if (wex >> 31)  // warp-uniform (f1)
             Pol::template decode_bmp<true>(st, stage, o, o + cnt);
@@ -2274,7 +2280,7 @@ __global__ void __launch_bounds__(NT, PlannedGeo<Pol>::MINB)
         }
         if (f != NONE) atomicMin(&a.ctr->err_min, f);  // a4 (cold)
       } else {
-        if (tp >= 0 && tp + TILE <= win.n) {
+        if (tp >= 0 && tp + TILEP <= win.n) {
           Pol::template load<true>(st, img, tid, lane, tp, win.n);
           Pol::template decode<true>(st, stage, o, o + cnt, n_units);
         } else {
@@ -2288,7 +2294,7 @@ __global__ void __launch_bounds__(NT, PlannedGeo<Pol>::MINB)
       if (t2 >= 0) count_tile(t2, k + 1, &cnt2, &wex2);
     }
     if (tid == SHIPPER) bulk_wait_read_all();  // the store of the previous tile has read its stage
-    named_sync<BAR_DATA, NT>();  // stage k & 1 complete; warp totals of the next tile published
+    named_sync<BAR_DATA, NTP>();  // stage k & 1 complete; warp totals of the next tile published
     // ship tile t: 16-byte aligned interior by one TMA bulk store, head / tail by the warp
     // (head and tail are < 16 bytes: only the shipping warp has anything to do; skipping the
     // rest measured forward -2..-3 %, but +4..+7 % in the UTF-16 kernel, which keeps them)
@@ -2317,7 +2323,7 @@ __global__ void __launch_bounds__(NT, PlannedGeo<Pol>::MINB)
     // the inclusive prefix of tile t for the finaliser (kind / written at the first error)
     if (tid == 0) st_relaxed(a.status + t, pack_status(a.epoch, FLAG_PREFIX, P + C));
     // slot k % PR is free: the producer refills it
-    if (tid == PRODUCER) produce(k % PR);
+    if (tid == PRODUCERP) produce(k % PR);
     running = P + C;
     t = t2;
     base_t = base2;
@@ -2523,16 +2529,16 @@ cudaError_t planned_configure(Op op) {
 }
 cudaError_t planned_occupancy(Op op, int *blocks_per_sm) {
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-      blocks_per_sm, planned_fn(op), NT, planned_smem_bytes(op_u16_input(op)));
+      blocks_per_sm, planned_fn(op), NTP, planned_smem_bytes(op_u16_input(op)));
 }
 cudaError_t launch_planned(Op op, const TileArgs &a, const unsigned long long *plan, int grid,
                            cudaStream_t s) {
   const size_t sm = planned_smem_bytes(op_u16_input(op));
   switch (op) {
-    case Op::U8_TO_U16: k_transcode_planned<U8Pol><<<grid, NT, sm, s>>>(a, plan); break;
-    case Op::U8_TO_U16BE: k_transcode_planned<U8PolBE><<<grid, NT, sm, s>>>(a, plan); break;
-    case Op::U16_TO_U8: k_transcode_planned<U16Pol><<<grid, NT, sm, s>>>(a, plan); break;
-    case Op::U16BE_TO_U8: k_transcode_planned<U16PolBE><<<grid, NT, sm, s>>>(a, plan); break;
+    case Op::U8_TO_U16: k_transcode_planned<U8Pol><<<grid, NTP, sm, s>>>(a, plan); break;
+    case Op::U8_TO_U16BE: k_transcode_planned<U8PolBE><<<grid, NTP, sm, s>>>(a, plan); break;
+    case Op::U16_TO_U8: k_transcode_planned<U16Pol><<<grid, NTP, sm, s>>>(a, plan); break;
+    case Op::U16BE_TO_U8: k_transcode_planned<U16PolBE><<<grid, NTP, sm, s>>>(a, plan); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

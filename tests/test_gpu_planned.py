@@ -17,7 +17,9 @@ if not torch.cuda.is_available():
     pytest.skip("no CUDA device", allow_module_level=True)
 
 import paper_2111_08692_b200 as ug  # noqa: E402
-from test_gpu_parity import DEV, LEADS, TILE, short_cases, to_dev  # noqa: E402
+from test_gpu_parity import DEV, LEADS, short_cases, to_dev  # noqa: E402
+
+TILE = ug.planned_tile_bytes()  # the planned kernels' own tile
 
 
 def planned_fwd(a: np.ndarray, cap=None, offset=0):

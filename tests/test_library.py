@@ -43,6 +43,7 @@ def test_library_exports_every_declared_symbol(ug):
 def test_abi_and_names(ug):
     assert ug.lib.ug_abi_version() == 1
     assert ug.tile_bytes() == 16384  # NT (512 threads) x 32 bytes, csrc/device.cuh
+    assert ug.planned_tile_bytes() == 8192  # NTP (256 threads) x 32 bytes
     assert ug.error_name(0) == "OK" and ug.error_name(6) == "Surrogate"
     assert ug.error_name(-3) == "OutputTooSmall"
 
