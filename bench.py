@@ -475,7 +475,12 @@ def measure_per_op(ug, t_all, off, n8, hb, ha, out16, u16, out8, dev, peak, reps
                                        2 * n16, 2 * n16),
         "utf16le_to_utf8_planned": (lambda: ug.utf16le_to_utf8_shard_planned_async(
             u16, 0, n16, 0, 0, 0, p16, out8, rec), 2 * n16, 2 * n16 + n8),
+        # SURVEY 8(f) f4 (research comparison): the planned forward, keyed 12-byte decoder
+        "utf8_to_utf16le_keyed (f4)": (lambda: ug.utf8_to_utf16le_keyed_planned_async(
+            t_in, pk, out16, res), n8, n8 + 2 * n16),
     }
+    pk = ug.plan_buffer(dev)
+    ug.utf16_length_from_utf8_plan_async(t_in, lens, pk)
     out = {}
     for name, (fn, in_bytes, hbm_bytes) in ops.items():
         fn()
@@ -544,6 +549,8 @@ def measure_per_config(ug, dev, peak, reps=10):
                 u16, lens, p16), 2 * n16, 2 * n16),
             "utf16le_to_utf8_planned": (lambda: ug.utf16le_to_utf8_planned_async(
                 u16, p16, o8, res), 2 * n16, 2 * n16 + n8),
+            "utf8_to_utf16le_keyed (f4)": (lambda: ug.utf8_to_utf16le_keyed_planned_async(
+                t8, p8, o16, res), n8, n8 + 2 * n16),
         })
         row = {"input": cfg.desc, "bytes_utf8": n8, "units_utf16": n16, "chars": chars}
         for name, (fn, in_bytes, hbm_bytes) in ops.items():

@@ -234,6 +234,22 @@ int ug_utf8_to_utf16le_planned_async(const uint8_t *in, size_t n, const void *d_
 int ug_utf16le_to_utf8_planned_async(const uint16_t *in, size_t n, const void *d_plan,
                                      uint8_t *out, size_t out_cap, ug_result *d_result,
                                      void *stream);
+
+/* SURVEY 8(f) f4, research comparison: ug_utf8_to_utf16le_planned_async with the a7 decode
+ * replaced by the paper's keyed 12-byte routine (section 4: a 12-bit key of
+ * character ends indexes a table giving the bytes consumed and a shuffle index; index
+ * [0, 64) = six characters of 1-2 bytes, [64, 145) = four of 1-3, [145, 209) = three of
+ * 1-4).  Same arguments, plan (from ug_utf16_length_from_utf8_plan_async), results, outputs
+ * and error conventions as ug_utf8_to_utf16le_planned_async; slower. */
+int ug_utf8_to_utf16le_keyed_planned_async(const uint8_t *in, size_t n, const void *d_plan,
+                                           uint16_t *out, size_t out_cap,
+                                           ug_result *d_result, void *stream);
+/* The f4 tables, built on the host (no GPU): key_table[4096] (bits 0-3 bytes consumed, 0 = no
+ * whole character; bits 4-6 characters decoded; bits 8-15 shuffle index) and
+ * shuffle_table[209 * 8] (per entry: four PRMT selector pairs A | B << 16 and four byte masks
+ * M; output register r = mux(M_r, prmt(w0, w1, A_r), prmt(w2, 0, B_r)) of the 12-byte window
+ * w0..w2).  Returns UG_OK, or UG_ERR_ARG for a NULL pointer. */
+int ug_utf8_keyed_tables(uint16_t *key_table, uint32_t *shuffle_table);
 /* Shard forms (the window conventions of ug_*_shard_async; the plan covers the owned range). */
 int ug_utf8_shard_plan_async(const uint8_t *in, size_t n, size_t halo_before, size_t halo_after,
                              uint64_t *d_len, void *d_plan, void *stream);

@@ -118,6 +118,8 @@ def _load():
         "ug_utf8_length_from_utf16le_plan_async": ([P, S, P, P, P], I),
         "ug_utf8_to_utf16le_planned_async": ([P, S, P, P, S, P, P], I),
         "ug_utf16le_to_utf8_planned_async": ([P, S, P, P, S, P, P], I),
+        "ug_utf8_to_utf16le_keyed_planned_async": ([P, S, P, P, S, P, P], I),
+        "ug_utf8_keyed_tables": ([P, P], I),
         "ug_utf8_shard_plan_async": ([P, S, S, S, P, P, P], I),
         "ug_utf16le_shard_plan_async": ([P, S, S, S, P, P, P], I),
         "ug_utf8_to_utf16le_shard_planned_async": ([P, S, S, S, U64, P, P, S, P, P], I),
@@ -479,6 +481,26 @@ def utf8_to_utf16le_planned_async(t_in, d_plan, t_out, d_result, n=None, out_cap
         _stream(stream)), "utf8_to_utf16le_planned_async")
 
 
+def utf8_to_utf16le_keyed_planned_async(t_in, d_plan, t_out, d_result, n=None, out_cap=None,
+                                        stream=None, result_off=0):
+    """f4 (research comparison): the planned forward with the keyed 12-byte decoder."""
+    _check(lib.ug_utf8_to_utf16le_keyed_planned_async(
+        _ptr(t_in), _units(t_in) if n is None else n, _ptr(d_plan), _ptr(t_out),
+        _units(t_out) if out_cap is None else out_cap, _at(d_result, result_off),
+        _stream(stream)), "utf8_to_utf16le_keyed_planned_async")
+
+
+def keyed_tables():
+    """The f4 tables as built by the library on the host: (key[4096] uint16, shuffle[209, 8]
+    uint32) numpy arrays (include/unigpu.h ug_utf8_keyed_tables)."""
+    import numpy as np
+    key = np.zeros(4096, dtype=np.uint16)
+    shuf = np.zeros((209, 8), dtype=np.uint32)
+    _check(lib.ug_utf8_keyed_tables(key.ctypes.data_as(ctypes.c_void_p),
+                                    shuf.ctypes.data_as(ctypes.c_void_p)), "utf8_keyed_tables")
+    return key, shuf
+
+
 def utf16le_to_utf8_planned_async(t_in, d_plan, t_out, d_result, n=None, out_cap=None,
                                   stream=None, result_off=0):
     _check(lib.ug_utf16le_to_utf8_planned_async(
@@ -528,6 +550,17 @@ def utf8_to_utf16le_two_pass(t_in, t_out, n=None, out_cap=None):
         result_buffer(dev, 1)
     utf16_length_from_utf8_plan_async(t_in, lens, plan, n=n)
     utf8_to_utf16le_planned_async(t_in, plan, t_out, res, n=n, out_cap=out_cap)
+    return decode_results(res)[0], int(lens[0])
+
+
+def utf8_to_utf16le_keyed_two_pass(t_in, t_out, n=None, out_cap=None):
+    """f4: plan + the keyed planned transcode, synchronously.  Returns (Result, utf16 length)."""
+    import torch
+    dev = t_in.device
+    plan, lens, res = plan_buffer(dev), torch.zeros(1, dtype=torch.int64, device=dev), \
+        result_buffer(dev, 1)
+    utf16_length_from_utf8_plan_async(t_in, lens, plan, n=n)
+    utf8_to_utf16le_keyed_planned_async(t_in, plan, t_out, res, n=n, out_cap=out_cap)
     return decode_results(res)[0], int(lens[0])
 
 
@@ -762,7 +795,7 @@ for _n in ("utf8_validate", "utf16le_validate", "utf8_to_utf16le", "utf16le_to_u
            "utf16be_to_utf8_host",
            "utf16_length_from_utf8_plan_async", "utf8_length_from_utf16le_plan_async",
            "utf8_to_utf16le_planned_async", "utf16le_to_utf8_planned_async",
-           "utf8_shard_plan_async", "utf16le_shard_plan_async",
+           "utf8_to_utf16le_keyed_planned_async", "utf8_shard_plan_async", "utf16le_shard_plan_async",
            "utf8_to_utf16le_shard_planned_async", "utf16le_to_utf8_shard_planned_async"):
     globals()[_n] = _checked(_n, globals()[_n])
 del _n

@@ -12,6 +12,7 @@
 
 #include "../../include/unigpu.h"
 #include "internal.h"
+#include "utf8_keyed.cuh"
 
 using namespace ug;
 
@@ -57,6 +58,7 @@ struct DeviceInfo {
   int sms = 0;
   int occ[NUM_OPS] = {};
   int occ_planned[2] = {};  // planned transcoders: UTF-8 input, UTF-16 input
+  int occ_keyed = 0;        // f4: the planned forward with the keyed decoder
   bool configured = false;
 };
 
@@ -87,6 +89,11 @@ cudaError_t device_info(int dev, DeviceInfo **out) {
       if (d.occ_planned[u] < 1) d.occ_planned[u] = 1;
       if (d.occ_planned[u] > CPSP) d.occ_planned[u] = CPSP;
     }
+    e = keyed_upload();
+    if (e == cudaSuccess) e = keyed_occupancy(&d.occ_keyed);
+    if (e != cudaSuccess) return e;
+    if (d.occ_keyed < 1) d.occ_keyed = 1;
+    if (d.occ_keyed > CPSP) d.occ_keyed = CPSP;
     d.configured = true;
   }
   *out = &d;
@@ -274,7 +281,7 @@ int enqueue_plan(Op op, const void *in, unsigned long long n, unsigned long long
 int enqueue_planned(Op op, const void *in, unsigned long long n, unsigned long long hb,
                     unsigned long long ha, unsigned long long global_off, const void *d_plan,
                     void *out, unsigned long long out_cap, ResultDev *d_result, RecordDev *d_rec,
-                    cudaStream_t s) {
+                    cudaStream_t s, bool keyed = false) {
   const int rc = check_tile_args(op, in, n, out, out_cap);
   if (rc != UG_OK) return rc;
   if (d_plan == nullptr || ((uintptr_t)d_plan & 7u)) return UG_ERR_ARG;
@@ -299,8 +306,15 @@ int enqueue_planned(Op op, const void *in, unsigned long long n, unsigned long l
   a.rec = d_rec;
   a.global_off = global_off;
   a.tile = TILEP;
-  if (launch_planned(op, a, (const unsigned long long *)d_plan, g.grid, s) != cudaSuccess)
+  if (keyed) {
+    // same plan geometry (the plan fixes the sub-ranges); the grid may differ
+    if (launch_planned_keyed(a, (const unsigned long long *)d_plan, di->sms * di->occ_keyed,
+                             s) != cudaSuccess)
+      return UG_ERR_CUDA;
+  } else if (launch_planned(op, a, (const unsigned long long *)d_plan, g.grid, s) !=
+             cudaSuccess) {
     return UG_ERR_CUDA;
+  }
   g_launches.fetch_add(1);
   return UG_OK;
 }
@@ -830,6 +844,18 @@ int ug_utf8_to_utf16le_planned_async(const uint8_t *in, size_t n, const void *d_
   if (!d_result) return UG_ERR_ARG;
   return enqueue_planned(Op::U8_TO_U16, in, n, 0, 0, 0, d_plan, out, out_cap,
                          (ResultDev *)d_result, nullptr, (cudaStream_t)stream);
+}
+int ug_utf8_to_utf16le_keyed_planned_async(const uint8_t *in, size_t n, const void *d_plan,
+                                           uint16_t *out, size_t out_cap,
+                                           ug_result *d_result, void *stream) {
+  if (!d_result) return UG_ERR_ARG;
+  return enqueue_planned(Op::U8_TO_U16, in, n, 0, 0, 0, d_plan, out, out_cap,
+                         (ResultDev *)d_result, nullptr, (cudaStream_t)stream, true);
+}
+int ug_utf8_keyed_tables(uint16_t *key_table, uint32_t *shuffle_table) {
+  if (!key_table || !shuffle_table) return UG_ERR_ARG;
+  keyed::build_tables(key_table, shuffle_table);
+  return UG_OK;
 }
 int ug_utf16le_to_utf8_planned_async(const uint16_t *in, size_t n, const void *d_plan,
                                      uint8_t *out, size_t out_cap, ug_result *d_result,

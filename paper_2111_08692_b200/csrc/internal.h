@@ -70,6 +70,11 @@ constexpr int PLAN_SUBS_PER_CTA = UG_PLAN_SUBS;  // sub-ranges per planned-trans
 size_t planned_smem_bytes(bool u16in);
 cudaError_t planned_configure(Op op);
 cudaError_t planned_occupancy(Op op, int *blocks_per_sm);
+// f4: the planned forward with the keyed 12-byte decoder (utf8_keyed.cuh)
+cudaError_t keyed_upload();  // tables to the current device + kernel attributes
+cudaError_t keyed_occupancy(int *blocks_per_sm);
+cudaError_t launch_planned_keyed(const TileArgs &a, const unsigned long long *plan, int grid,
+                                 cudaStream_t s);
 cudaError_t launch_planned(Op op, const TileArgs &a, const unsigned long long *plan, int grid,
                            cudaStream_t s);
 cudaError_t launch_plan(bool u16in, bool be, const Window &w, unsigned long long ntiles,

@@ -23,6 +23,7 @@
 #include "internal.h"
 #include "utf16.cuh"
 #include "utf8.cuh"
+#include "utf8_keyed.cuh"
 
 namespace ug {
 
@@ -344,6 +345,35 @@ struct U8PolT {
 
 using U8Pol = U8PolT<false>;
 using U8PolBE = U8PolT<true>;
+
+// ---------------------------------------------------------------- f4: keyed 12-byte decoder
+// SURVEY 8(f) f4, research comparison: the planned forward with the a7 decode
+// replaced by the paper's keyed 12-byte routine (utf8_keyed.cuh).  Classification, validation,
+// the ASCII warp path, counts, offsets and shipping are U8Pol's.  Tables: global memory, read
+// through L1 (16 KiB + 6.5 KiB), uploaded once per device (keyed_upload).
+__device__ uint16_t g_keyed_key[keyed::KEYS];
+__device__ uint32_t g_keyed_shuf[keyed::SHUFFLES * keyed::SHUF_WORDS];
+
+struct U8KeyPol : U8PolT<false> {
+  template <bool IN>
+  __device__ static __forceinline__ void decode(const St &s, uint16_t *stage, uint32_t o,
+                                                uint32_t lim, long long n) {
+    if (IN && s.wasc) {  // a2: the warp's 1 KiB is ASCII (the paper's ASCII block path)
+      U8PolT<false>::template decode<true>(s, stage, o, lim, n);
+      return;
+    }
+    int lo = 0, hi = BPT;
+    if (!IN) {
+      lo = s.pos0 < 0 ? (int)(-s.pos0 < BPT ? -s.pos0 : BPT) : 0;
+      const long long r = s.n - s.pos0;
+      hi = r < 0 ? 0 : (r > BPT ? BPT : (int)r);
+    }
+    const uint32_t words[10] = {s.prev, s.w[0], s.w[1], s.w[2], s.w[3],
+                                s.w[4], s.w[5], s.w[6], s.w[7], s.nxt};
+    keyed::decode_thread(s.img, words, lo, hi, g_keyed_key, g_keyed_shuf, stage + o,
+                         (int)(lim - o));
+  }
+};
 
 // ============================================================================ UTF-16 policy
 // Positions are words.  Thread `tid` owns tile words [16 tid, 16 tid + 16), two per register.
@@ -2513,6 +2543,28 @@ cudaError_t launch_tile(Op op, const TileArgs &a, int grid, cudaStream_t s) {
 // ---- planned path launchers
 size_t planned_smem_bytes(bool u16in) {
   return u16in ? PlannedGeo<U16Pol>::SMEM : PlannedGeo<U8Pol>::SMEM;
+}
+cudaError_t keyed_upload() {
+  static uint16_t key[keyed::KEYS];
+  static uint32_t shuf[keyed::SHUFFLES * keyed::SHUF_WORDS];
+  static bool built = false;  // (called under the device-info lock)
+  if (!built) keyed::build_tables(key, shuf), built = true;
+  cudaError_t e = cudaMemcpyToSymbol(g_keyed_key, key, sizeof(key));
+  if (e == cudaSuccess) e = cudaMemcpyToSymbol(g_keyed_shuf, shuf, sizeof(shuf));
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute((const void *)k_transcode_planned<U8KeyPol>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)planned_smem_bytes(false));
+  return e;
+}
+cudaError_t keyed_occupancy(int *blocks_per_sm) {
+  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+      blocks_per_sm, (const void *)k_transcode_planned<U8KeyPol>, NTP, planned_smem_bytes(false));
+}
+cudaError_t launch_planned_keyed(const TileArgs &a, const unsigned long long *plan, int grid,
+                                 cudaStream_t s) {
+  k_transcode_planned<U8KeyPol><<<grid, NTP, planned_smem_bytes(false), s>>>(a, plan);
+  return cudaGetLastError();
 }
 static const void *planned_fn(Op op) {
   switch (op) {

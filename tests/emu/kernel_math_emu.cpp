@@ -28,6 +28,9 @@
 //   fuzz8 ITERS       random config-0-mix text, corrupted / truncated copies and byte soup at
 //                     leads 0, 1, 7, 15: first error (flag + rescan) and the decoded units on
 //                     [0, written) against the oracle; the total against the oracle's count.
+//                     The f4 keyed decoder (utf8_keyed.cuh decode_thread) runs on every chunk
+//                     beside units4, into the same slots, and is checked the same way; plus
+//                     width-dense text (one width, or a subset of the four).
 //   fuzz16 ITERS      UTF-16 -> UTF-8 (U16PolT::decode_validate): first error, widths and the
 //                     staged bytes on [0, written) against the oracle; every surrogate-free
 //                     group also through the BMP-only path (f1: classes4_bmp / encode4_bmp),
@@ -41,6 +44,7 @@
 
 #include "utf16.cuh"
 #include "utf8.cuh"
+#include "utf8_keyed.cuh"
 extern "C" {
 #include "../../oracle/oracle.h"
 }
@@ -48,6 +52,8 @@ extern "C" {
 using namespace ug;
 
 static long long g_fails = 0, g_cases = 0;
+static uint16_t g_ktab[keyed::KEYS];  // f4 tables (utf8_keyed.cuh build_tables)
+static uint32_t g_stab[keyed::SHUFFLES * keyed::SHUF_WORDS];
 #define CHECK(c, ...)                  \
   do {                                 \
     if (!(c)) {                        \
@@ -215,7 +221,7 @@ static void run8(const std::vector<uint8_t> &s, long long lead, const char *name
   const long long nch = m.chunks();
   // whole warps: the kernel classifies every chunk of a tile, also those past the input's end
   emulate_flags(m, e, 0, (nch + 31) / 32 * 32, name);
-  std::vector<uint16_t> out(n + 64, 0xEEEE);
+  std::vector<uint16_t> out(n + 64, 0xEEEE), kout(n + 64, 0xEEEE);
   long long o = 0;
   for (long long c = 0; c < nch; c++) {
     const long long p = m.pos0(c);
@@ -228,6 +234,20 @@ static void run8(const std::vector<uint8_t> &s, long long lead, const char *name
     for (int i = 0; i < 32; i++)
       if (p + i >= 0 && p + i < n) own |= 1u << i;
     em_bits &= own;
+    {
+      // f4: the keyed 12-byte decoder (U8KeyPol::decode) on the same chunk, into the same
+      // slots: bytes [p - 4, p + 52) as the smem image, own positions [lo, hi)
+      uint32_t arr[14];
+      for (int i = 0; i < 14; i++) arr[i] = m.word(p - 4 + 4 * i);
+      const uint8_t *img = reinterpret_cast<const uint8_t *>(arr + 1);
+      const int lo = p < 0 ? (int)(-p < 32 ? -p : 32) : 0;
+      const int hi = n - p < 32 ? (int)(n - p > 0 ? n - p : 0) : 32;
+      const int cnt = (int)popc(em_bits);
+      uint16_t kb[64];
+      const int got = keyed::decode_thread(img, arr, lo, hi, g_ktab, g_stab, kb, cnt);
+      if (e < 0) CHECK(got == cnt, "%s: keyed chunk %lld emits %d units, count %d", name, c, got, cnt);
+      for (int i = 0; i < cnt && i < got; i++) kout[o + i] = kb[i];
+    }
     u8::Carry cy = u8::carry_of(m.word(p - 4));
     long long so = o;
     for (int k = 0; k < 8; k++) {
@@ -259,6 +279,12 @@ static void run8(const std::vector<uint8_t> &s, long long lead, const char *name
     if (out[i] != ref[i]) {
       CHECK(false, "%s: unit %llu: %04x vs oracle %04x (n=%lld e=%lld lead=%lld)", name, i,
             out[i], ref[i], n, e, lead);
+      break;
+    }
+  for (unsigned long long i = 0; i < r.written; i++)
+    if (kout[i] != ref[i]) {
+      CHECK(false, "%s: keyed unit %llu: %04x vs oracle %04x (n=%lld e=%lld lead=%lld)", name,
+            i, kout[i], ref[i], n, e, lead);
       break;
     }
   g_cases++;
@@ -303,6 +329,24 @@ static void fuzz8(int iters) {
     const size_t at = g() % a.size();
     a[at] = ALPHABET[9 + g() % 18];
     run8(a, lead, "ascii1");
+    // width-dense text (every path of the keyed decoder, straddles at every chunk phase):
+    // characters of one width, or of widths drawn from a subset of {1, 2, 3, 4}
+    {
+      static const uint32_t LO[4] = {0x20, 0x80, 0x800, 0x10000}, HI_[4] = {0x7F, 0x7FF, 0xFFFF, 0x10FFFF};
+      const int set = 1 + (int)(g() % 15);  // non-empty subset of the four widths
+      std::vector<uint8_t> d;
+      const size_t dl = g() % 2500;
+      while (d.size() < dl) {
+        int w;
+        do w = (int)(g() % 4);
+        while (!(set >> w & 1));
+        uint32_t cp;
+        do cp = LO[w] + (uint32_t)(g() % (HI_[w] - LO[w] + 1));
+        while (cp >= 0xD800 && cp <= 0xDFFF);
+        put8(d, cp);
+      }
+      run8(d, lead, "dense");
+    }
   }
   for (int it = 0; it < iters * 30; it++) {
     std::vector<uint8_t> s;
@@ -456,6 +500,7 @@ static void fuzz16(int iters) {
 int main(int argc, char **argv) {
   const std::string mode = argc > 1 ? argv[1] : "fuzz8";
   const int iters = argc > 2 ? atoi(argv[2]) : 200;
+  keyed::build_tables(g_ktab, g_stab);
   if (mode == "window8") window8(iters, argc > 3 ? atoi(argv[3]) : 1);
   else if (mode == "fuzz8") fuzz8(iters);
   else if (mode == "fuzz16") fuzz16(iters);

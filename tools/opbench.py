@@ -47,6 +47,8 @@ ops = {
                                 n8, n8 + 2 * n16),
     "utf16le_to_utf8_planned": (lambda: ug.utf16le_to_utf8_planned_async(u16, plan16, o8, resb),
                                 2 * n16, 2 * n16 + n8),
+    "utf8_to_utf16le_keyed": (lambda: ug.utf8_to_utf16le_keyed_planned_async(t8, plan8, o16, resb),
+                              n8, n8 + 2 * n16),
     "plan8": (lambda: ug.utf16_length_from_utf8_plan_async(t8, lens, plan8), n8, n8),
     "plan16": (lambda: ug.utf8_length_from_utf16le_plan_async(u16, lens, plan16, len_off=8),
                2 * n16, 2 * n16),
