@@ -102,5 +102,17 @@ UG_HD uint32_t mad_hi(uint32_t a, uint32_t b, uint32_t c) {
 }
 // (a & m) | (b & ~m): one LOP3.
 UG_HD uint32_t mux(uint32_t m, uint32_t a, uint32_t b) { return (a & m) | (b & ~m); }
+// mux with a constant mask, forced into ONE LOP3 (mask as its immediate; left to itself the
+// compiler splits a constant-mask select into two).
+template <uint32_t M>
+UG_HD uint32_t muxc(uint32_t a, uint32_t b) {
+#if defined(__CUDA_ARCH__)
+  uint32_t d;
+  asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(d) : "r"(a), "r"(b), "n"(M));
+  return d;
+#else
+  return (a & M) | (b & ~M);
+#endif
+}
 
 }  // namespace ug

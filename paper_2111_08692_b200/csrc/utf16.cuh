@@ -82,7 +82,7 @@ UG_HD uint32_t bmask(uint32_t m) { return prmt(m, 0u, 0xBA98u); }
 // output byte of word j (meaningful up to its width).  lp: low byte of the previous word
 // in each lane (the high surrogate's low bits for a low surrogate).
 UG_HD void encode4(const Cls4 &c, uint32_t lp, uint32_t *O0, uint32_t *O1, uint32_t *O2) {
-  const uint32_t U6 = mux(0xFCFCFCFCu, c.hi << 2, c.lo >> 6);   // (u >> 6) & 0xFF
+  const uint32_t U6 = muxc<0xFCFCFCFCu>(c.hi << 2, c.lo >> 6);  // (u >> 6) & 0xFF
   const uint32_t T = (c.lo & 0x3F3F3F3Fu) | HI;                 // 80 | u & 3F
   // first byte
   const uint32_t vB = U6 | 0xC0C0C0C0u;
@@ -127,7 +127,7 @@ UG_HD uint32_t widths_bmp(const Bmp4 &c) {
 }
 // Output byte planes as encode4, for surrogate-free words.
 UG_HD void encode4_bmp(const Bmp4 &c, uint32_t *O0, uint32_t *O1, uint32_t *O2) {
-  const uint32_t U6 = mux(0xFCFCFCFCu, c.hi << 2, c.lo >> 6);   // (u >> 6) & 0xFF
+  const uint32_t U6 = muxc<0xFCFCFCFCu>(c.hi << 2, c.lo >> 6);  // (u >> 6) & 0xFF
   const uint32_t T = (c.lo & 0x3F3F3F3Fu) | HI;                 // 80 | u & 3F
   const uint32_t vB = U6 | 0xC0C0C0C0u;                          // 2-byte lead
   const uint32_t vC = ((c.hi >> 4) & 0x0F0F0F0Fu) | 0xE0E0E0E0u; // 3-byte lead

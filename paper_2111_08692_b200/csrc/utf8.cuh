@@ -49,12 +49,15 @@ UG_HD void tr4(uint32_t a, uint32_t b, uint32_t c, uint32_t d, uint32_t &t0, uin
   t3 = prmt(ab1, cd1, 0x7632u);
 }
 // Exchange bit b (b & D set) of every byte of a with bit b - D of the same byte of c.
+// Written as two bit-selects (one LOP3 each) of the operands shifted by D, the shifts on the
+// FMA pipe (IMAD.HI / IMAD): the integer ALU pipe is the one the classifier saturates.
 template <int D>
 UG_HD void dswap(uint32_t &a, uint32_t &c) {
   constexpr uint32_t M = D == 1 ? 0x55555555u : (D == 2 ? 0x33333333u : 0x0F0F0F0Fu);
-  const uint32_t t = ((a >> D) ^ c) & M;
-  c ^= t;
-  a ^= t << D;
+  const uint32_t ad = shr_fma<D>(a), cu = mad(c, 1u << D, 0u);
+  const uint32_t c2 = muxc<M>(ad, c);
+  a = muxc<(M << D)>(cu, a);
+  c = c2;
 }
 // w[0..7] = 32 bytes (position 4r + k = byte k of w[r]) -> P[b] bit i = bit b of byte i.
 // R[r] gathers positions r, 8+r, 16+r, 24+r; the delta swaps then transpose every byte lane's
@@ -149,7 +152,7 @@ UG_HD uint32_t units4(uint32_t x, Carry &c, uint32_t *u01, uint32_t *u23) {
   // high surrogate: G = hb:lb = cp >> 6, unit = 0xD800 | ((G >> 4) - 0x40)
   const uint32_t Mh = s2f * 0xFFu;
   const uint32_t hbm = (hb | HI) - 0x04040404u;  // per byte 0x80 + hb - 4, no borrows
-  lb = mux(Mh, mux(0xF0F0F0F0u, hbm << 4, shr_fma<4>(lb)), lb);
+  lb = mux(Mh, muxc<0xF0F0F0F0u>(hbm << 4, shr_fma<4>(lb)), lb);
   hb = mux(Mh, (shr_fma<4>(hbm) & 0x03030303u) | 0xD8D8D8D8u, hb);
   *u01 = prmt(lb, hb, BE ? 0x1504u : 0x5140u);
   *u23 = prmt(lb, hb, BE ? 0x3726u : 0x7362u);
