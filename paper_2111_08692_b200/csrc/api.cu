@@ -206,7 +206,6 @@ int enqueue_tile_ws(Workspace *w, DeviceInfo *di, Op op, const void *in, unsigne
   a.result = d_result;
   a.rec = d_rec;
   a.global_off = global_off;
-  a.tile = TILE;
   unsigned long long maxg = (unsigned long long)di->sms * (unsigned long long)di->occ[(int)op];
   const unsigned long long want = (a.ntiles + per_cta - 1) / per_cta;
   int grid = (int)(want < maxg ? want : maxg);
@@ -305,7 +304,6 @@ int enqueue_planned(Op op, const void *in, unsigned long long n, unsigned long l
   a.result = d_result;
   a.rec = d_rec;
   a.global_off = global_off;
-  a.tile = TILEP;
   if (keyed) {
     // same plan geometry (the plan fixes the sub-ranges); the grid may differ
     if (launch_planned_keyed(a, (const unsigned long long *)d_plan, di->sms * di->occ_keyed,

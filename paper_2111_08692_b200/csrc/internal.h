@@ -37,7 +37,6 @@ struct TileArgs {
   ResultDev *result;            // non-sharded result slot, or null
   RecordDev *rec;               // sharded record slot, or null
   unsigned long long global_off;  // sharded: global offset of position 0 (code units)
-  long long tile;               // input bytes per tile of this launch (TILE or TILEP)
 };
 
 enum class Op : int {

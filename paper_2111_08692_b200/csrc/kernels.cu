@@ -321,6 +321,7 @@ struct U8PolT {
   }
 
   // a10 (last CTA, warp 0): kind of the first error and units written before it
+  template <int TB = TILE>  // the launch's tile bytes (TILE, or TILEP for the planned kernels)
   __device__ static __forceinline__ void finalize(const TileArgs &a, unsigned long long e,
                                                   bool xc, int lane, int *kind,
                                                   unsigned long long *wr) {
@@ -331,9 +332,9 @@ struct U8PolT {
     *kind = u8::decode_kind(x);
     *wr = 0;
     if (!xc) return;
-    long long te = ((long long)e + win.lead) / a.tile;
+    long long te = ((long long)e + win.lead) / TB;
     unsigned long long base = te ? (ld_relaxed(a.status + te - 1) & VALMASK) : 0ull;
-    long long from = te * a.tile - win.lead;
+    long long from = te * TB - win.lead;
     if (from < 0) from = 0;
     unsigned long long c = 0;
     for (long long i = from + lane; i < (long long)e; i += 32)
@@ -703,6 +704,7 @@ struct U16PolT {
     }
   }
 
+  template <int TB = TILE>  // the launch's tile bytes (TILE, or TILEP for the planned kernels)
   __device__ static __forceinline__ void finalize(const TileArgs &a, unsigned long long e,
                                                   bool xc, int lane, int *kind,
                                                   unsigned long long *wr) {
@@ -710,9 +712,9 @@ struct U16PolT {
     *kind = u8::SURROGATE;
     *wr = 0;
     if (!xc) return;
-    long long te = (2 * (long long)e + win.lead) / a.tile;
+    long long te = (2 * (long long)e + win.lead) / TB;
     unsigned long long base = te ? (ld_relaxed(a.status + te - 1) & VALMASK) : 0ull;
-    long long from = (te * a.tile - win.lead) / 2;
+    long long from = (te * TB - win.lead) / 2;
     if (from < 0) from = 0;
     unsigned long long c = 0;
     for (long long i = from + lane; i < (long long)e; i += 32)
@@ -725,7 +727,7 @@ using U16Pol = U16PolT<false>;
 using U16PolBE = U16PolT<true>;
 
 // Last CTA to finish: outcome + counter reset.  n_units in input code units.
-template <class Pol>
+template <class Pol, int TB = TILE>
 __device__ __forceinline__ void finish_call(const TileArgs &a, bool xc, int tid, int warp,
                                             int lane, int *s_last) {
   if (tid == 0) {
@@ -753,7 +755,7 @@ __device__ __forceinline__ void finish_call(const TileArgs &a, bool xc, int tid,
       return;
     }
     if (xc && a.ntiles) total = ld_relaxed(a.status + a.ntiles - 1) & VALMASK;
-    if (e != NONE) Pol::finalize(a, e, xc, lane, &kind, &wr);
+    if (e != NONE) Pol::template finalize<TB>(a, e, xc, lane, &kind, &wr);
     if (lane == 0)
       write_outcome(a, xc, kind, e, total, wr, (unsigned long long)(a.win.n / Pol::UNIT));
   }
@@ -2365,7 +2367,7 @@ __global__ void __launch_bounds__(NTP, PlannedGeo<Pol>::MINB)
   }
   if (tid == SHIPPER) bulk_wait_all();
   __syncthreads();
-  finish_call<Pol>(a, true, tid, warp, lane, &s_last);
+  finish_call<Pol, TILEP>(a, true, tid, warp, lane, &s_last);
 }
 
 // ============================================================================ combine
