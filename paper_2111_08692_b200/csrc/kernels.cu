@@ -1305,15 +1305,17 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
 }
 
 // ============================================================================ length-from
-__device__ __forceinline__ uint32_t len8_word(uint32_t x) {
-  uint32_t s1 = x << 1;
-  uint32_t cont = x & ~s1 & HI;
-  uint32_t f0 = x & s1 & (x << 2) & (x << 3) & HI;
-  return 4u - __popc(cont) + __popc(f0);
-}
 __device__ __forceinline__ uint32_t len8_byte(uint32_t b) {
   return ((b & 0xC0u) != 0x80u ? 1u : 0u) + (b >= 0xF0u ? 1u : 0u);
 }
+// per byte lane: [non-continuation] + [>= F0], accumulated (IMAD.HI) into acc
+__device__ __forceinline__ uint32_t len8_acc(uint32_t x, uint32_t acc) {
+  const uint32_t x1 = x << 1;
+  const uint32_t nk = (~x | x1) & HI;
+  const uint32_t f = x & x1 & (x << 2) & (x << 3) & HI;
+  return mad_hi(f, 1u << 25, mad_hi(nk, 1u << 25, acc));
+}
+__device__ __forceinline__ uint32_t lane_sum(uint32_t acc) { return (acc * 0x01010101u) >> 24; }
 __device__ __forceinline__ uint32_t len16_word(uint32_t u) {
   return 1u + (u >= 0x80u ? 1u : 0u) + ((u >= 0x800u && (u & 0xF800u) != 0xD800u) ? 1u : 0u);
 }
@@ -1355,13 +1357,15 @@ __global__ void __launch_bounds__(LNT) k_len8(const uint8_t *in, unsigned long l
     uint4 v[4];
 #pragma unroll
     for (int j = 0; j < 4; j++) v[j] = __ldcs(body + i + j * stride);
+    uint32_t acc = 0;  // byte lanes (<= 32 each)
 #pragma unroll
     for (int j = 0; j < 4; j++)
-      sum += len8_word(v[j].x) + len8_word(v[j].y) + len8_word(v[j].z) + len8_word(v[j].w);
+      acc = len8_acc(v[j].w, len8_acc(v[j].z, len8_acc(v[j].y, len8_acc(v[j].x, acc))));
+    sum += lane_sum(acc);
   }
   for (; i < nb; i += stride) {
     uint4 v = __ldcs(body + i);
-    sum += len8_word(v.x) + len8_word(v.y) + len8_word(v.z) + len8_word(v.w);
+    sum += lane_sum(len8_acc(v.w, len8_acc(v.z, len8_acc(v.y, len8_acc(v.x, 0u)))));
   }
   if (blockIdx.x == 0) {
     for (unsigned long long j = threadIdx.x; j < head; j += blockDim.x) sum += len8_byte(in[j]);
@@ -1386,7 +1390,6 @@ __device__ __forceinline__ uint32_t len16_acc4(uint32_t a, uint32_t b, uint32_t 
   acc = mad_hi(ge80, 1u << 25, acc);          // + ge80 >> 7
   return mad_hi(ge800 & ~S, 1u << 25, acc);   // + (ge800 and not S) >> 7
 }
-__device__ __forceinline__ uint32_t lane_sum(uint32_t acc) { return (acc * 0x01010101u) >> 24; }
 // len16_acc4 that also ORs the surrogate mask into *sur (f1: a warp without surrogates takes
 // the BMP-only decode)
 template <bool BE = false>
@@ -1907,7 +1910,63 @@ __device__ __forceinline__ unsigned long long bsum(uint32_t acc) {
   return (acc & 0xFFu) + ((acc >> 8) & 0xFFu) + ((acc >> 16) & 0xFFu) + (acc >> 24);
 }
 
-#ifndef UG_PLAN8_SWAR
+#if !defined(UG_PLAN8_SWAR) && !defined(UG_PLAN8_PLANES)
+// UTF-8 plan as the length-from reduction plus boundary terms.  Summed over positions, the end-
+// position rule's terms (ASCII at i, 2-byte lead at i-1, >= E0 at i-2, >= F0 at i-3: R16) weigh
+// each byte by [non-continuation] + [>= F0] -- the R15 length formula -- but credit a lead's
+// units to the positions where they are emitted, up to 3 bytes later.  So the emit-term sum of
+// [a, b) = formula[a, b) + pending(a) - pending(b), pending(q) = the units leads in the 3
+// bytes before q emit at q or later.  On a prefix free of errors the terms never coincide and
+// this is the transcoder's exact emit count; past an error the sum can only exceed it (a sum of
+// the terms >= their OR), so a later range's offset never falls below the units written before
+// the error, and the range holding the error starts at its exact offset.
+__device__ __forceinline__ long long plan8_pending(const Window &w, long long q) {
+  long long c = 0;
+#pragma unroll
+  for (int d = 1; d <= 3; d++) {
+    const uint32_t b = byte_at(w, q - d);
+    const int l2 = (b >= 0xC0u && b < 0xE0u), e = b >= 0xE0u, f = b >= 0xF0u;
+    c += d == 1 ? l2 + e + f : (d == 2 ? e + f : f);
+  }
+  return c;
+}
+
+__global__ void __launch_bounds__(LNT) k_plan8(const PlanArgs a) {
+  long long p0, p1;
+  sub_span(a, blockIdx.x, &p0, &p1);
+  const Window &w = a.win;
+  const uint8_t *base = w.base;
+  unsigned long long sum = 0;
+  long long h0 = p0;
+  while (h0 < p1 && (((uintptr_t)(base + h0)) & 15u)) h0++;
+  long long h1 = h0 + ((p1 - h0) & ~15ll);
+  if (h1 < h0) h1 = h0;
+  const uint4 *v = reinterpret_cast<const uint4 *>(base + h0);
+  const long long nv = (h1 - h0) / 16;
+  long long i = threadIdx.x;
+  for (; i + 3 * LNT < nv; i += 4 * LNT) {
+    uint4 q[4];
+#pragma unroll
+    for (int j = 0; j < 4; j++) q[j] = __ldcs(v + i + j * LNT);
+    uint32_t acc = 0;
+#pragma unroll
+    for (int j = 0; j < 4; j++)
+      acc = len8_acc(q[j].w, len8_acc(q[j].z, len8_acc(q[j].y, len8_acc(q[j].x, acc))));
+    sum += lane_sum(acc);
+  }
+  for (; i < nv; i += LNT) {
+    const uint4 q = __ldcs(v + i);
+    sum += lane_sum(len8_acc(q.w, len8_acc(q.z, len8_acc(q.y, len8_acc(q.x, 0u)))));
+  }
+  for (long long b = p0 + threadIdx.x; b < h0; b += LNT) sum += len8_byte(base[b]);
+  for (long long b = h1 + threadIdx.x; b < p1; b += LNT) sum += len8_byte(base[b]);
+  // boundary terms (thread 0; modular: a range's count may be "negative", prefixes are not)
+  const unsigned long long emit = threadIdx.x == 0
+      ? sum + (unsigned long long)(plan8_pending(w, p0) - plan8_pending(w, p1))
+      : sum;
+  plan_finish(a, emit, sum);
+}
+#elif defined(UG_PLAN8_PLANES)
 // UTF-8 plan on bit planes (the classifier's transposition, u8::planes32): a lane's 32 bytes ->
 // 8 planes, then the emit mask of analyze32 (ASCII | end of a 2- / 3-byte character | 3rd /
 // 4th byte after an F lead) and the R15 terms (non-continuation, >= F0) are 32 positions per op.
