@@ -43,11 +43,16 @@ constexpr int INBUF = TILE + 2 * HALO;
 #ifndef UG_NTP
 #define UG_NTP 256
 #endif
+#ifndef UG_PHALVES
+#define UG_PHALVES 1
+#endif
 #ifndef UG_CPSP
-#define UG_CPSP (1024 / UG_NTP)
+#define UG_CPSP (1024 / UG_NTP / UG_PHALVES)
 #endif
 constexpr int NTP = UG_NTP;
-constexpr int TILEP = NTP * 32;
+constexpr int PHALVES = UG_PHALVES;     // 32-byte chunks per thread per planned tile
+constexpr int HALFP = NTP * 32;         // one chunk of every thread (warps own 1 KiB each)
+constexpr int TILEP = HALFP * PHALVES;  // input bytes per planned tile
 constexpr int CPSP = UG_CPSP;
 
 // ---------------------------------------------------------------- workspace counters

@@ -1305,9 +1305,7 @@ __global__ void __launch_bounds__(NT + 32 * NLB, CTAS_PER_SM) k_transcode(const 
 }
 
 // ============================================================================ length-from
-__device__ __forceinline__ uint32_t len8_byte(uint32_t b) {
-  return ((b & 0xC0u) != 0x80u ? 1u : 0u) + (b >= 0xF0u ? 1u : 0u);
-}
+__device__ __forceinline__ uint32_t len8_byte(uint32_t b) { return u8::plan_weight(b); }
 // per byte lane: [non-continuation] + [>= F0], accumulated (IMAD.HI) into acc
 __device__ __forceinline__ uint32_t len8_acc(uint32_t x, uint32_t acc) {
   const uint32_t x1 = x << 1;
@@ -1921,14 +1919,7 @@ __device__ __forceinline__ unsigned long long bsum(uint32_t acc) {
 // the terms >= their OR), so a later range's offset never falls below the units written before
 // the error, and the range holding the error starts at its exact offset.
 __device__ __forceinline__ long long plan8_pending(const Window &w, long long q) {
-  long long c = 0;
-#pragma unroll
-  for (int d = 1; d <= 3; d++) {
-    const uint32_t b = byte_at(w, q - d);
-    const int l2 = (b >= 0xC0u && b < 0xE0u), e = b >= 0xE0u, f = b >= 0xF0u;
-    c += d == 1 ? l2 + e + f : (d == 2 ? e + f : f);
-  }
-  return c;
+  return (long long)u8::pending3(byte_at(w, q - 1), byte_at(w, q - 2), byte_at(w, q - 3));
 }
 
 __global__ void __launch_bounds__(LNT) k_plan8(const PlanArgs a) {
@@ -2242,8 +2233,11 @@ __global__ void __launch_bounds__(NTP, PlannedGeo<Pol>::MINB)
   }
 
   // count tile t (slot k % PR): classify / validate (errors to the call's minimum), the
-  // thread's count, its in-warp exclusive offset; the warp total goes to s_wsum[k & 1]
-  // (UTF-16: bit 31 of *wexcl set = this warp's words hold no surrogate, f1)
+  // thread's count, its in-warp exclusive offset; the warp total goes to s_wsum[k & 1].
+  // PHALVES chunks per thread (chunk h = bytes [h * HALFP, (h + 1) * HALFP) of the tile): the
+  // counts are packed 16 bits per chunk (bits 16h.., at most 12288 per tile) so ONE scan and
+  // one barrier serve them all; bit 31 - h of *wexcl set = this warp's chunk h holds no
+  // surrogate (UTF-16, f1)
   auto count_tile = [&](long long t, int k, uint32_t *cnt, uint32_t *wexcl) {
     uint32_t nosurr = 0;
     uint8_t *img = ring + (k % PR) * INBUFP;
@@ -2253,61 +2247,69 @@ __global__ void __launch_bounds__(NTP, PlannedGeo<Pol>::MINB)
       fix_tile_edges<TILEP>(win, t, img, NTP);
       named_sync<BAR_DATA, NTP>();
     }
-    const long long tp = tile_pos<TILEP>(win, t);
-    uint32_t c;
-    if constexpr (Pol::UNIT == 2) {
-      // UTF-16: the count is the width sum alone (exact on any input); the pairing check is
-      // done with the decode (decode_validate), as in the count-first k_transcode16
-      constexpr bool BE = Pol::kBE;
-      const uint4 *my = reinterpret_cast<const uint4 *>(img + HALO + BPT * tid);
-      const uint4 q0 = my[0], q1 = my[1];
-      if (tp >= 0 && tp + TILEP <= win.n) {
-        const uint32_t orv = q0.x | q0.y | q0.z | q0.w | q1.x | q1.y | q1.z | q1.w;
-        if (__all_sync(FULL, (orv & (BE ? 0x80FF80FFu : 0xFF80FF80u)) == 0u)) {
-          c = 16u;
-        } else {
-          uint32_t sur = 0;
-          c = 16u + lane_sum(len16_acc4s<BE>(q1.z, q1.w, len16_acc4s<BE>(q1.x, q1.y,
-                             len16_acc4s<BE>(q0.z, q0.w, len16_acc4s<BE>(q0.x, q0.y, 0u, &sur),
-                             &sur), &sur), &sur));
+    const long long tp0 = tile_pos<TILEP>(win, t);
+    uint32_t cp = 0;
+#pragma unroll
+    for (int h = 0; h < PHALVES; h++) {
+      const long long tp = tp0 + (long long)h * HALFP;
+      uint8_t *im = img + h * HALFP;
+      uint32_t c;
+      if constexpr (Pol::UNIT == 2) {
+        // UTF-16: the count is the width sum alone (exact on any input); the pairing check is
+        // done with the decode (decode_validate), as in the count-first k_transcode16
+        constexpr bool BE = Pol::kBE;
+        const uint4 *my = reinterpret_cast<const uint4 *>(im + HALO + BPT * tid);
+        const uint4 q0 = my[0], q1 = my[1];
+        if (tp >= 0 && tp + HALFP <= win.n) {
+          const uint32_t orv = q0.x | q0.y | q0.z | q0.w | q1.x | q1.y | q1.z | q1.w;
+          if (__all_sync(FULL, (orv & (BE ? 0x80FF80FFu : 0xFF80FF80u)) == 0u)) {
+            c = 16u;
+          } else {
+            uint32_t sur = 0;
+            c = 16u + lane_sum(len16_acc4s<BE>(q1.z, q1.w, len16_acc4s<BE>(q1.x, q1.y,
+                               len16_acc4s<BE>(q0.z, q0.w, len16_acc4s<BE>(q0.x, q0.y, 0u, &sur),
+                               &sur), &sur), &sur));
 #ifndef UG_NO_F1
-          nosurr = __any_sync(FULL, sur != 0u) ? 0u : 0x80000000u;
+            if (!__any_sync(FULL, sur != 0u)) nosurr |= 0x80000000u >> h;
 #endif
+          }
+        } else {
+          const uint32_t q[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
+          const long long w0 = (tp + BPT * tid) / 2, nw = win.n / 2;
+          c = 0;
+#pragma unroll
+          for (int k2 = 0; k2 < 16; k2++)
+            if (w0 + k2 >= 0 && w0 + k2 < nw)
+              c += len16_word(Pol::native((q[k2 >> 1] >> (16 * (k2 & 1))) & 0xFFFFu));
         }
       } else {
-        const uint32_t q[8] = {q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w};
-        const long long w0 = (tp + BPT * tid) / 2, nw = win.n / 2;
-        c = 0;
-#pragma unroll
-        for (int k2 = 0; k2 < 16; k2++)
-          if (w0 + k2 >= 0 && w0 + k2 < nw)
-            c += len16_word(Pol::native((q[k2 >> 1] >> (16 * (k2 & 1))) & 0xFFFFu));
+        typename Pol::St st;
+        if (tp >= 0 && tp + HALFP <= win.n) {
+          Pol::template load<true>(st, im, tid, lane, tp, win.n);
+          c = Pol::template analyze<true>(st, tid, true);
+        } else {
+          Pol::template load<false>(st, im, tid, lane, tp, win.n);
+          c = Pol::template analyze<false>(st, tid, true);
+        }
+        if (__any_sync(FULL, Pol::hint(st))) {  // a4 (cold)
+          const unsigned long long e = Pol::find_error(st, n_units);
+          if (e != NONE) atomicMin(&a.ctr->err_min, e);
+        }
       }
-    } else {
-      typename Pol::St st;
-      if (tp >= 0 && tp + TILEP <= win.n) {
-        Pol::template load<true>(st, img, tid, lane, tp, win.n);
-        c = Pol::template analyze<true>(st, tid, true);
-      } else {
-        Pol::template load<false>(st, img, tid, lane, tp, win.n);
-        c = Pol::template analyze<false>(st, tid, true);
-      }
-      if (__any_sync(FULL, Pol::hint(st))) {  // a4 (cold)
-        const unsigned long long e = Pol::find_error(st, n_units);
-        if (e != NONE) atomicMin(&a.ctr->err_min, e);
-      }
+      cp |= c << (16 * h);
     }
-    uint32_t sc = c;
+    uint32_t sc = cp;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {
       const uint32_t y = __shfl_up_sync(FULL, sc, d);
       if (lane >= d) sc += y;
     }
     if (lane == 31) s_wsum[k & 1][warp] = sc;
-    *cnt = c;
-    *wexcl = (sc - c) | nosurr;
+    *cnt = cp;
+    *wexcl = (sc - cp) | nosurr;
   };
-  // after the barrier: this warp's offset inside the tile and the tile total
+  // after the barrier: this warp's offset inside the tile and the tile total (packed as the
+  // counts)
   auto tile_offsets = [&](int k, uint32_t *woff, uint32_t *total) {
     const uint32_t v = lane < NTP / 32 ? s_wsum[k & 1][lane] : 0u;
     // UTF-8 input: two REDUX instead of the shuffle scan (measured: forward -1 %; the same in
@@ -2334,6 +2336,7 @@ __global__ void __launch_bounds__(NTP, PlannedGeo<Pol>::MINB)
     return s_tile[k % PR];
   };
 
+  constexpr uint32_t FIELD = PHALVES == 1 ? 0x7FFFFFFFu : 0x3FFFu;  // one chunk's packed count
   uint32_t cnt = 0, wex = 0, woff = 0, C = 0;
   unsigned long long running = 0, base_t;
   long long t = slot_tile(0, &base_t);
@@ -2351,32 +2354,37 @@ __global__ void __launch_bounds__(NTP, PlannedGeo<Pol>::MINB)
       t2 = slot_tile(k + 1, &base2);
       if (t2 >= 0) count_tile(t2, k + 1, &cnt2, &wex2);
     }
-    // decode tile t at its global 16-byte phase (its input image is still in slot k % PR)
-    {
-      uint8_t *img = ring + (k % PR) * INBUFP;
+    // decode tile t at its global 16-byte phase (its input image is still in slot k % PR);
+    // chunk h's units follow those of chunks < h
+#pragma unroll
+    for (int h = 0; h < PHALVES; h++) {
+      uint8_t *img = ring + (k % PR) * INBUFP + h * HALFP;
       typename Pol::St st;
-      const long long tp = tile_pos<TILEP>(win, t);
-      const uint32_t o = ph + woff + (wex & 0x7FFFFFFFu);
+      const long long tp = tile_pos<TILEP>(win, t) + (long long)h * HALFP;
+      const uint32_t before = h == 0 ? 0u : (C & 0xFFFFu);  // (PHALVES <= 2)
+      const uint32_t wo = PHALVES == 1 ? woff : ((woff >> (16 * h)) & 0xFFFFu);
+      const uint32_t o = ph + before + wo + ((wex >> (16 * h)) & FIELD);
+      const uint32_t ch = PHALVES == 1 ? cnt : ((cnt >> (16 * h)) & 0xFFFFu);
       if constexpr (Pol::UNIT == 2) {  // encode + pairing check in one pass
         unsigned long long f = NONE;
-        if (tp >= 0 && tp + TILEP <= win.n) {
+        if (tp >= 0 && tp + HALFP <= win.n) {
           Pol::template load<true>(st, img, tid, lane, tp, win.n);
-          if (wex >> 31)  // warp-uniform (f1)
-            Pol::template decode_bmp<true>(st, stage, o, o + cnt);
+          if ((wex << h) >> 31)  // warp-uniform (f1)
+            Pol::template decode_bmp<true>(st, stage, o, o + ch);
           else
-            f = Pol::template decode_validate<true>(st, stage, o, o + cnt);
+            f = Pol::template decode_validate<true>(st, stage, o, o + ch);
         } else {
           Pol::template load<false>(st, img, tid, lane, tp, win.n);
-          f = Pol::template decode_validate<false>(st, stage, o, o + cnt);
+          f = Pol::template decode_validate<false>(st, stage, o, o + ch);
         }
         if (f != NONE) atomicMin(&a.ctr->err_min, f);  // a4 (cold)
       } else {
-        if (tp >= 0 && tp + TILEP <= win.n) {
+        if (tp >= 0 && tp + HALFP <= win.n) {
           Pol::template load<true>(st, img, tid, lane, tp, win.n);
-          Pol::template decode<true>(st, stage, o, o + cnt, n_units);
+          Pol::template decode<true>(st, stage, o, o + ch, n_units);
         } else {
           Pol::template load<false>(st, img, tid, lane, tp, win.n);
-          Pol::template decode<false>(st, stage, o, o + cnt, n_units);
+          Pol::template decode<false>(st, stage, o, o + ch, n_units);
         }
       }
     }
@@ -2389,8 +2397,9 @@ __global__ void __launch_bounds__(NTP, PlannedGeo<Pol>::MINB)
     // ship tile t: 16-byte aligned interior by one TMA bulk store, head / tail by the warp
     // (head and tail are < 16 bytes: only the shipping warp has anything to do; skipping the
     // rest measured forward -2..-3 %, but +4..+7 % in the UTF-16 kernel, which keeps them)
+    const uint32_t Ct = PHALVES == 1 ? C : (C & 0xFFFFu) + (C >> 16);  // the tile's units
     if (Pol::UNIT == 2 || warp == UG_SHIP_WARP) {
-      unsigned long long hi = P + C;
+      unsigned long long hi = P + Ct;
       if (hi > a.out_cap) hi = a.out_cap;
       if (hi > P) {
         const uint32_t Cc = (uint32_t)(hi - P);
@@ -2412,10 +2421,10 @@ __global__ void __launch_bounds__(NTP, PlannedGeo<Pol>::MINB)
       }
     }
     // the inclusive prefix of tile t for the finaliser (kind / written at the first error)
-    if (tid == 0) st_relaxed(a.status + t, pack_status(a.epoch, FLAG_PREFIX, P + C));
+    if (tid == 0) st_relaxed(a.status + t, pack_status(a.epoch, FLAG_PREFIX, P + Ct));
     // slot k % PR is free: the producer refills it
     if (tid == PRODUCERP) produce(k % PR);
-    running = P + C;
+    running = P + Ct;
     t = t2;
     base_t = base2;
     if (t >= 0) {

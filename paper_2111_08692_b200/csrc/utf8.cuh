@@ -208,5 +208,22 @@ UG_HD uint32_t emits_at(uint32_t b0, uint32_t b1, uint32_t b2, uint32_t b3) {
   return (b0 < 0x80u || (b1 >= 0xC0u && b1 < 0xE0u) || b2 >= 0xE0u || b3 >= 0xF0u) ? 1u : 0u;
 }
 
+// The plan's arithmetic (kernels.cu k_plan8, DESIGN.md section 5 "planned").  Summed over
+// positions, emits_at's four terms (ASCII at i, 2-byte lead at i-1, >= E0 at i-2, >= F0 at
+// i-3) weigh each byte by plan_weight = [non-continuation] + [>= F0], the R15 length formula,
+// but credit a lead's units to the positions that emit them, up to 3 bytes later; pending3 =
+// the units that the leads in the 3 bytes before a cut q (b1 = s[q-1], b2 = s[q-2],
+// b3 = s[q-3]) emit at q or later.  So sum of the terms over [a, b) = sum of plan_weight over
+// [a, b) + pending3(at a) - pending3(at b); it equals emits_at's count where the terms never
+// coincide (an error-free prefix) and exceeds it otherwise.
+UG_HD uint32_t plan_weight(uint32_t b) { return ((b & 0xC0u) != 0x80u ? 1u : 0u) + (b >= 0xF0u ? 1u : 0u); }
+UG_HD uint32_t pending3(uint32_t b1, uint32_t b2, uint32_t b3) {
+  const uint32_t l2 = (b1 >= 0xC0u && b1 < 0xE0u) ? 1u : 0u;
+  const uint32_t e1 = b1 >= 0xE0u ? 1u : 0u, f1 = b1 >= 0xF0u ? 1u : 0u;
+  const uint32_t e2 = b2 >= 0xE0u ? 1u : 0u, f2 = b2 >= 0xF0u ? 1u : 0u;
+  const uint32_t f3 = b3 >= 0xF0u ? 1u : 0u;
+  return l2 + e1 + f1 + e2 + f2 + f3;
+}
+
 }  // namespace u8
 }  // namespace ug

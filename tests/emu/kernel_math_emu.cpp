@@ -31,6 +31,8 @@
 //                     The f4 keyed decoder (utf8_keyed.cuh decode_thread) runs on every chunk
 //                     beside units4, into the same slots, and is checked the same way; plus
 //                     width-dense text (one width, or a subset of the four).
+//   plan8 ITERS       the plan's arithmetic (u8::plan_weight / pending3) against emits_at at
+//                     every cut of random / corrupted text and byte soup (see plan8() below).
 //   fuzz16 ITERS      UTF-16 -> UTF-8 (U16PolT::decode_validate): first error, widths and the
 //                     staged bytes on [0, written) against the oracle; every surrogate-free
 //                     group also through the BMP-only path (f1: classes4_bmp / encode4_bmp),
@@ -497,6 +499,43 @@ static void fuzz16(int iters) {
   }
 }
 
+// The plan's arithmetic (u8::plan_weight / pending3, kernels.cu k_plan8) against the kernel's
+// emission rule position by position (u8::emits_at, the rule units4 / analyze32 implement):
+// for cuts 0 <= b <= n, plan(b) = sum of plan_weight over [0, b) + pending3(0) - pending3(b)
+// must EQUAL the emitting positions before b when b <= e (the first error, n if none), and be
+// at least the emitting positions before e when b > e (a later range never starts below the
+// units written before the error).  Random text, corrupted copies, byte soup.
+static void plan8(int iters) {
+  std::mt19937_64 g(0x91A8);
+  for (int it = 0; it < iters; it++) {
+    std::vector<uint8_t> s;
+    const size_t len = g() % 600;
+    if (it % 3 == 2) {
+      for (size_t i = 0; i < len; i++) s.push_back(ALPHABET[g() % 27]);
+    } else {
+      while (s.size() < len) put8(s, draw_cp(g));
+      if (it % 3 == 1 && !s.empty())
+        for (int j = 0; j < 2; j++) s[g() % s.size()] = (uint8_t)g();
+    }
+    const long long n = (long long)s.size();
+    const ugo_result r = ugo_utf8_validate(s.data(), n);
+    const long long e = r.error ? (long long)r.position : n;
+    Emu8 m{s.data(), n, 0};
+    std::vector<long long> em(n + 1, 0), pl(n + 1, 0);  // prefix sums
+    for (long long i = 0; i < n; i++) {
+      em[i + 1] = em[i] + u8::emits_at(m.byte(i), m.byte(i - 1), m.byte(i - 2), m.byte(i - 3));
+      pl[i + 1] = pl[i] + u8::plan_weight(m.byte(i));
+    }
+    for (long long b = 0; b <= n; b++) {
+      const long long plan = pl[b] + (long long)u8::pending3(m.byte(-1), m.byte(-2), m.byte(-3)) -
+                             (long long)u8::pending3(m.byte(b - 1), m.byte(b - 2), m.byte(b - 3));
+      if (b <= e) CHECK(plan == em[b], "plan8: cut %lld (e=%lld n=%lld): %lld vs %lld", b, e, n, plan, em[b]);
+      else CHECK(plan >= em[e], "plan8: cut %lld past e=%lld: %lld < %lld", b, e, plan, em[e]);
+      g_cases++;
+    }
+  }
+}
+
 int main(int argc, char **argv) {
   const std::string mode = argc > 1 ? argv[1] : "fuzz8";
   const int iters = argc > 2 ? atoi(argv[2]) : 200;
@@ -504,6 +543,7 @@ int main(int argc, char **argv) {
   if (mode == "window8") window8(iters, argc > 3 ? atoi(argv[3]) : 1);
   else if (mode == "fuzz8") fuzz8(iters);
   else if (mode == "fuzz16") fuzz16(iters);
+  else if (mode == "plan8") plan8(iters);
   else {
     printf("unknown mode %s\n", mode.c_str());
     return 2;

@@ -19,6 +19,9 @@ code with it.  What it pins (D2-D5):
   own tables) on the same chunks and on width-dense text (one width, or any subset of the
   four): its units, at the same per-thread slots, equal the oracle's on [0, written), and on
   valid input it emits exactly the thread's count;
+* the UTF-8 plan's arithmetic (`u8::plan_weight`, `u8::pending3`): at every cut of random,
+  corrupted and soup text, equal to the emit count (`u8::emits_at`) up to the first error and
+  never below the units written before it past the error;
 * the UTF-16 -> UTF-8 byte-SWAR (`u16::classes4 / widths / encode4`, pairing predicate):
   first error, per-thread counts and staged bytes against the oracle.
 """
@@ -72,4 +75,12 @@ def test_utf8_decode_layout_fuzz(emu):
 
 def test_utf16_encode_layout_fuzz(emu):
     out = subprocess.run([emu, "fuzz16", "600"], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout
+
+
+def test_plan_arithmetic_every_cut(emu):
+    """The UTF-8 plan (length formula + pending units at the cuts, kernels.cu k_plan8) equals
+    the kernel's emit count at every cut up to the first error and never falls below the units
+    written before it past the error ("planned")."""
+    out = subprocess.run([emu, "plan8", "3000"], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout
