@@ -2244,16 +2244,27 @@ __global__ void __launch_bounds__(NTP, PlannedGeo<Pol>::MINB)
   // counts are packed 16 bits per chunk (bits 16h.., at most 12288 per tile) so ONE scan and
   // one barrier serve them all; bit 31 - h of *wexcl set = this warp's chunk h holds no
   // surrogate (UTF-16, f1)
-  auto count_tile = [&](long long t, int k, uint32_t *cnt, uint32_t *wexcl) {
+  auto count_tile = [&](long long t, int k, uint32_t *cnt, uint32_t *wexcl, long long *tpo) {
     uint32_t nosurr = 0;
     uint8_t *img = ring + (k % PR) * INBUFP;
-    mbar_wait(&mb_load[k % PR], (k / PR) & 1);
-    if (tile_at_edge<TILEP>(win, t)) {  // tile-uniform
+    // UTF-16 input: no second wait (the caller's slot_tile has waited for this slot's load) and
+    // the tile position computed once per tile (c4 -0.8 %, c1 -2.6 %); the UTF-8 kernel keeps
+    // the old form (+1.1 % with it)
+    bool edge;
+    if constexpr (Pol::UNIT == 2) {
+      const long long e0 = tile_pos<TILEP>(win, t) - HALO;
+      edge = !(e0 >= win.lo_valid && e0 + TILEP + 2 * HALO <= win.hi_valid);
+    } else {
+      mbar_wait(&mb_load[k % PR], (k / PR) & 1);
+      edge = tile_at_edge<TILEP>(win, t);
+    }
+    if (edge) {  // tile-uniform
       named_sync<BAR_DATA, NTP>();
       fix_tile_edges<TILEP>(win, t, img, NTP);
       named_sync<BAR_DATA, NTP>();
     }
     const long long tp0 = tile_pos<TILEP>(win, t);
+    *tpo = tp0;
     uint32_t cp = 0;
 #pragma unroll
     for (int h = 0; h < PHALVES; h++) {
@@ -2345,8 +2356,9 @@ __global__ void __launch_bounds__(NTP, PlannedGeo<Pol>::MINB)
   constexpr uint32_t FIELD = PHALVES == 1 ? 0x7FFFFFFFu : 0x3FFFu;  // one chunk's packed count
   uint32_t cnt = 0, wex = 0, woff = 0, C = 0;
   unsigned long long running = 0, base_t;
+  long long tpt = 0;  // tile_pos of tile t
   long long t = slot_tile(0, &base_t);
-  if (t >= 0) count_tile(t, 0, &cnt, &wex);
+  if (t >= 0) count_tile(t, 0, &cnt, &wex, &tpt);
   named_sync<BAR_DATA, NTP>();
   if (t >= 0) tile_offsets(0, &woff, &C);
   for (int k = 0; t >= 0; k++) {
@@ -2355,10 +2367,10 @@ __global__ void __launch_bounds__(NTP, PlannedGeo<Pol>::MINB)
     const uint32_t ph = (uint32_t)((((uintptr_t)(out + P)) & 15u) / sizeof(Out));
     uint32_t cnt2 = 0, wex2 = 0;
     unsigned long long base2 = NONE;
-    long long t2 = -1;
+    long long t2 = -1, tp2 = 0;
     if constexpr (PlannedOrder<Pol>::COUNT_FIRST) {
       t2 = slot_tile(k + 1, &base2);
-      if (t2 >= 0) count_tile(t2, k + 1, &cnt2, &wex2);
+      if (t2 >= 0) count_tile(t2, k + 1, &cnt2, &wex2, &tp2);
     }
     // decode tile t at its global 16-byte phase (its input image is still in slot k % PR);
     // chunk h's units follow those of chunks < h
@@ -2366,7 +2378,8 @@ __global__ void __launch_bounds__(NTP, PlannedGeo<Pol>::MINB)
     for (int h = 0; h < PHALVES; h++) {
       uint8_t *img = ring + (k % PR) * INBUFP + h * HALFP;
       typename Pol::St st;
-      const long long tp = tile_pos<TILEP>(win, t) + (long long)h * HALFP;
+      const long long tp =
+          (Pol::UNIT == 2 ? tpt : tile_pos<TILEP>(win, t)) + (long long)h * HALFP;
       const uint32_t before = h == 0 ? 0u : (C & 0xFFFFu);  // (PHALVES <= 2)
       const uint32_t wo = PHALVES == 1 ? woff : ((woff >> (16 * h)) & 0xFFFFu);
       const uint32_t o = ph + before + wo + ((wex >> (16 * h)) & FIELD);
@@ -2396,7 +2409,7 @@ __global__ void __launch_bounds__(NTP, PlannedGeo<Pol>::MINB)
     }
     if constexpr (!PlannedOrder<Pol>::COUNT_FIRST) {
       t2 = slot_tile(k + 1, &base2);
-      if (t2 >= 0) count_tile(t2, k + 1, &cnt2, &wex2);
+      if (t2 >= 0) count_tile(t2, k + 1, &cnt2, &wex2, &tp2);
     }
     if (tid == SHIPPER) bulk_wait_read_all();  // the store of the previous tile has read its stage
     named_sync<BAR_DATA, NTP>();  // stage k & 1 complete; warp totals of the next tile published
@@ -2437,6 +2450,7 @@ __global__ void __launch_bounds__(NTP, PlannedGeo<Pol>::MINB)
       tile_offsets(k + 1, &woff, &C);
       cnt = cnt2;
       wex = wex2;
+      tpt = tp2;
     }
   }
   if (tid == SHIPPER) bulk_wait_all();
