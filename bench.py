@@ -498,18 +498,21 @@ def measure_per_op(ug, t_all, off, n8, hb, ha, out16, u16, out8, dev, peak, reps
     return out
 
 
-def measure_per_config(ug, dev, peak, reps=10):
-    """Every hot-path op on BASELINE configs 1, 2A, 2B and 3 at their BASELINE.json sizes
-    (BASELINE.md section 2's targets): per op the mean CUDA-event time of `reps` async calls
-    (no host sync inside), input GB/s, Gchar/s, algorithmic HBM GB/s and its fraction of the
-    measured copy peak.  Each config's other-encoding counterpart (its transcoded output) is
-    produced by the library on the device first, so every op runs on that config's text."""
+def measure_per_config(ug, dev, peak, reps=50, reps_c0=2000):
+    """Every hot-path op on BASELINE configs 0, 1, 2A, 2B and 3 at their BASELINE.json sizes
+    (BASELINE.md section 2's targets): per op 3 warm-up calls, then
+    `reps` async calls (2000 for config 0, which is L2-resident and launch-bound: reported, not a
+    target), each bracketed by CUDA events on the stream; the minimum and mean call time, input
+    GB/s, Gchar/s, algorithmic HBM GB/s and its fraction of the measured copy peak and of the
+    nominal 8 TB/s (from the mean), and `spread_flag` when (mean - min) / min > 1 %.  Each
+    config's other-encoding counterpart (its transcoded output) is produced by the library on
+    the device first, so every op runs on that config's text."""
     import torch
     stream = torch.cuda.current_stream()
     res = ug.result_buffer(dev, 1)
     lens = torch.zeros(1, dtype=torch.int64, device=dev)
     out = {}
-    for key in ("c1", "c2a", "c2b", "c3"):
+    for key in ("c0", "c1", "c2a", "c2b", "c3"):
         cfg = synth.CONFIGS[key]
         x = synth.generate(key)
         if cfg.encoding == "utf8":
@@ -553,20 +556,26 @@ def measure_per_config(ug, dev, peak, reps=10):
                 t8, p8, o16, res), n8, n8 + 2 * n16),
         })
         row = {"input": cfg.desc, "bytes_utf8": n8, "units_utf16": n16, "chars": chars}
+        nrep = reps_c0 if key == "c0" else reps
         for name, (fn, in_bytes, hbm_bytes) in ops.items():
-            fn()
-            torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record(stream)
-            for _ in range(reps):
+            for _ in range(3):
                 fn()
-            e1.record(stream)
             torch.cuda.synchronize()
-            ms = e0.elapsed_time(e1) / reps
-            row[name] = {"ms": round(ms, 4), "input_gbs": round(in_bytes / ms / 1e6, 1),
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(nrep + 1)]
+            ev[0].record(stream)
+            for r in range(nrep):
+                fn()
+                ev[r + 1].record(stream)
+            torch.cuda.synchronize()
+            t = [ev[r].elapsed_time(ev[r + 1]) for r in range(nrep)]
+            ms, mn = sum(t) / nrep, min(t)
+            row[name] = {"ms": round(ms, 4), "min_ms": round(mn, 4),
+                         "input_gbs": round(in_bytes / ms / 1e6, 1),
                          "gchar_per_s": round(chars / ms / 1e6, 1),
                          "hbm_gbs": round(hbm_bytes / ms / 1e6, 1),
-                         "frac_of_peak": round(hbm_bytes / ms / 1e6 / peak, 4)}
+                         "frac_of_peak": round(hbm_bytes / ms / 1e6 / peak, 4),
+                         "frac_of_8tbs": round(hbm_bytes / ms / 1e6 / 8000.0, 4),
+                         "spread_flag": (ms - mn) / mn > 0.01}
         out[key] = row
         del t8, u16, o16, o8
         torch.cuda.empty_cache()

@@ -2266,6 +2266,7 @@ __global__ void __launch_bounds__(NTP, PlannedGeo<Pol>::MINB)
     const long long tp0 = tile_pos<TILEP>(win, t);
     *tpo = tp0;
     uint32_t cp = 0;
+    int asc = 0;  // chunks in which this warp is all ASCII (warp-uniform)
 #pragma unroll
     for (int h = 0; h < PHALVES; h++) {
       const long long tp = tp0 + (long long)h * HALFP;
@@ -2281,6 +2282,7 @@ __global__ void __launch_bounds__(NTP, PlannedGeo<Pol>::MINB)
           const uint32_t orv = q0.x | q0.y | q0.z | q0.w | q1.x | q1.y | q1.z | q1.w;
           if (__all_sync(FULL, (orv & (BE ? 0x80FF80FFu : 0xFF80FF80u)) == 0u)) {
             c = 16u;
+            asc += 1;
           } else {
             uint32_t sur = 0;
             c = 16u + lane_sum(len16_acc4s<BE>(q1.z, q1.w, len16_acc4s<BE>(q1.x, q1.y,
@@ -2316,10 +2318,19 @@ __global__ void __launch_bounds__(NTP, PlannedGeo<Pol>::MINB)
       cp |= c << (16 * h);
     }
     uint32_t sc = cp;
+#ifndef UG_NO_ASCII_SCAN
+    // (UTF-16 input: config 1 -7.5 %, mixed text +0.5 %; the UTF-8 kernel: -1.7 % / +0.5 %, not
+    // taken)
+    if (Pol::UNIT == 2 && asc == PHALVES) {  // every lane's count is the same: closed form
+      sc = cp * (uint32_t)(lane + 1);
+    } else
+#endif
+    {
 #pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {
-      const uint32_t y = __shfl_up_sync(FULL, sc, d);
-      if (lane >= d) sc += y;
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(FULL, sc, d);
+        if (lane >= d) sc += y;
+      }
     }
     if (lane == 31) s_wsum[k & 1][warp] = sc;
     *cnt = cp;
