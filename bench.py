@@ -3,12 +3,14 @@
 
 Workload: BASELINE config 4, the one the metric is quoted on at
 1/2/4/8 GPUs -- 8 GiB of mixed UTF-8 (config-0 mix), sharded over N ranks at character
-boundaries.  One STEP is one pass of the whole hot path over it:
-    utf16_length_from_utf8            (a11, exact output sizing)
-    utf8_to_utf16le   (validate+transcode, a1-a8, a10)
+boundaries.  One STEP is one pass of the whole hot path over it (default --path planned, the
+two-pass form; --path chained runs the single-pass look-back kernels after plain length-from
+reductions instead):
+    utf16_length_from_utf8 + plan     (a11, exact output sizing; the plan: a6')
+    utf8_to_utf16le   (validate+transcode, a1-a5, a7, a8, a10; planned)
     [N>1: NCCL all-gather of the 32-B shard records + combine kernel]
-    utf8_length_from_utf16le          (a11)
-    utf16le_to_utf8   (validate+transcode back, a9, a5-a8, a10)
+    utf8_length_from_utf16le + plan   (a11, a6')
+    utf16le_to_utf8   (validate+transcode back, a9, a5, a7, a8, a10; planned)
     [N>1: all-gather + combine]
 value = input bytes of both transcoding passes (n8 + 2*n16, all ranks) / step time, in GB/s
 (1e9).  Inputs (>= 1 GiB per rank) exceed the 126 MB L2, so no flush is needed.
