@@ -591,6 +591,10 @@ struct U16PolT {
   __device__ static __forceinline__ unsigned long long decode_validate(const St &s,
                                                                        uint8_t *stage,
                                                                        uint32_t o, uint32_t lim) {
+#ifdef UG_ABL_NODECODE
+    decode<IN>(s, stage, o, lim, 0);  // ablation: no encode, no check
+    return NONE;
+#endif
     if (IN && s.wasc) {  // a2: no surrogate, one byte per word
       decode<true>(s, stage, o, lim, 0);
       return NONE;
@@ -665,6 +669,10 @@ struct U16PolT {
   template <bool IN>
   __device__ static __forceinline__ void decode_bmp(const St &s, uint8_t *stage, uint32_t o,
                                                     uint32_t lim) {
+#ifdef UG_ABL_NODECODE
+    decode<IN>(s, stage, o, lim, 0);
+    return;
+#endif
     if (IN && s.wasc) {
       decode<true>(s, stage, o, lim, 0);
       return;
@@ -2278,6 +2286,12 @@ __global__ void __launch_bounds__(NTP, PlannedGeo<Pol>::MINB)
         constexpr bool BE = Pol::kBE;
         const uint4 *my = reinterpret_cast<const uint4 *>(im + HALO + BPT * tid);
         const uint4 q0 = my[0], q1 = my[1];
+#ifdef UG_ABL_NOVAL
+        if (true) {  // ablation: one byte per word, no width sum
+          c = 16u;
+          asc += 1;
+        } else
+#endif
         if (tp >= 0 && tp + HALFP <= win.n) {
           const uint32_t orv = q0.x | q0.y | q0.z | q0.w | q1.x | q1.y | q1.z | q1.w;
           if (__all_sync(FULL, (orv & (BE ? 0x80FF80FFu : 0xFF80FF80u)) == 0u)) {
