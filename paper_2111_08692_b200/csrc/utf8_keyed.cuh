@@ -19,6 +19,9 @@
 //    the four (A | B << 16) selector pairs and the four byte masks M.  Path (a) places each
 //    character in a 16-bit lane (last byte low, lead byte high, zero for ASCII); paths (b) and
 //    (c) in a 32-bit lane, last byte lowest, zero above the character's length.
+//  * FAST PATHS (-DUG_KEYED_FASTPATHS, off by default: 11-16 % slower on the GPU):
+//    before the lookup, 16 ASCII bytes, 16 bytes of two-byte characters or 12 bytes of
+//    three-byte characters (R23) are decoded directly.
 //  * Emission follows a7 exactly, so the planned kernel's per-thread counts and offsets hold:
 //    a thread emits the units of the positions it owns, a character's unit at its last byte
 //    and a 4-byte character's high surrogate at its third byte.  Characters straddling the
@@ -203,6 +206,50 @@ UG_HD int decode_thread(const uint8_t *img, const uint32_t *words, int lo, int h
     p = e0 + 1;
   }
   while (p < hi) {
+#ifdef UG_KEYED_FASTPATHS
+    {
+    const uint32_t *wp = reinterpret_cast<const uint32_t *>(img + (p & ~3));
+    const uint32_t sh = 8u * (uint32_t)(p & 3);
+    const uint32_t r0 = wp[0], r1 = wp[1], r2 = wp[2], r3 = wp[3];
+    const uint32_t w0 = fsr(r0, r1, sh), w1 = fsr(r1, r2, sh), w2 = fsr(r2, r3, sh);
+    // the routine's three homogeneous fast paths: 16 ASCII bytes, 16 bytes of
+    // two-byte characters, and (R23) 12 bytes of three-byte characters.  Off by default: on
+    // the GPU they cost 11-16 % (the checks run every iteration; a lane that hits one still
+    // waits for the lanes of its warp that do not)
+    if (p + 16 <= hi) {
+      const uint32_t w3 = fsr(r3, wp[4], sh);
+      if (((w0 | w1 | w2 | w3) & HI) == 0u) {
+        const uint32_t w[4] = {w0, w1, w2, w3};
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+#pragma unroll
+          for (int b = 0; b < 4; b++) emit((w[k] >> (8 * b)) & 0xFFu);
+        p += 16;
+        continue;
+      }
+      if ((w0 & 0xC0E0C0E0u) == 0x80C080C0u && (w1 & 0xC0E0C0E0u) == 0x80C080C0u &&
+          (w2 & 0xC0E0C0E0u) == 0x80C080C0u && (w3 & 0xC0E0C0E0u) == 0x80C080C0u) {
+        const uint32_t w[4] = {w0, w1, w2, w3};
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+          emit(((w[k] & 0x1Fu) << 6) | ((w[k] >> 8) & 0x3Fu));
+          emit(((w[k] >> 10) & 0x7C0u) | ((w[k] >> 24) & 0x3Fu));
+        }
+        p += 16;
+        continue;
+      }
+    }
+    if (p + 12 <= hi && (w0 & 0xF0C0C0F0u) == 0xE08080E0u && (w1 & 0xC0F0C0C0u) == 0x80E08080u &&
+        (w2 & 0xC0C0F0C0u) == 0x8080E080u) {
+      emit(code_point(w0, 3));
+      emit(code_point(fsr(w0, w1, 24), 3));
+      emit(code_point(fsr(w1, w2, 16), 3));
+      emit(code_point(w2 >> 8, 3));
+      p += 12;
+      continue;
+    }
+    }
+#endif
     const uint32_t key = (uint32_t)(ENDa >> (p + 4)) & 0xFFFu;
     const uint32_t ke = ktab[key];
     const int consumed = (int)(ke & 15u);

@@ -84,3 +84,17 @@ def test_plan_arithmetic_every_cut(emu):
     written before it past the error ("planned")."""
     out = subprocess.run([emu, "plan8", "3000"], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stdout
+
+
+def test_keyed_fast_paths_build(tmp_path):
+    """The f4 decoder with the paper's three homogeneous fast paths (-DUG_KEYED_FASTPATHS,
+    PAPER.md:96; off in the default build) against the oracle on the same fuzz."""
+    gxx = shutil.which("g++")
+    if gxx is None:
+        pytest.skip("g++ not available")
+    exe = str(tmp_path / "emu_fp")
+    subprocess.check_call([gxx, "-O2", "-std=c++17", "-DUG_KEYED_FASTPATHS",
+                           "-I" + os.path.join(ROOT, "paper_2111_08692_b200", "csrc"),
+                           "-o", exe, SRC, os.path.join(ROOT, "oracle", "oracle.c")])
+    out = subprocess.run([exe, "fuzz8", "300"], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout
