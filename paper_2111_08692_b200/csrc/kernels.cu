@@ -788,7 +788,7 @@ static_assert(VAHEAD >= 1 && VAHEAD <= VRING - 1, "validator ring");
 #ifndef UG_VCPS
 #define UG_VCPS 3  // 38-40 registers: 3 CTAs/SM measured +3 % (UTF-8) / +6 % (UTF-16) over 2
 #endif
-constexpr int VCPS = UG_VCPS;  // validator CTAs per SM (register budget)
+[[maybe_unused]] constexpr int VCPS = UG_VCPS;  // validator CTAs per SM (register budget)
 
 #ifndef UG_NO_VPRODUCER
 // Validator with a dedicated producer warp (NT consumer threads + 32): the producer's lane 0
@@ -800,8 +800,13 @@ constexpr int VCPS = UG_VCPS;  // validator CTAs per SM (register budget)
 // Measured against the round-1 form (1 GiB c4 / c1 / c3): utf8_validate -3.4 / -4.2 / -2.8 %,
 // utf16le_validate -3.8 / +6.2 / -6.4 % (c2a -6.1 %).
 constexpr int VNT = NT + 32;
+#ifndef UG_VRING8
+#define UG_VRING8 VRING
+#endif
+constexpr int VRING8 = UG_VRING8;  // the UTF-8 validator's ring (2 CTAs per SM: room for more)
 template <class Pol>
 __global__ void __launch_bounds__(VNT, Pol::UNIT == 1 ? 2 : 3) k_validate(const TileArgs a) {
+  constexpr int VRING = Pol::UNIT == 1 ? VRING8 : ::ug::VRING;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t mb_full[VRING], mb_empty[VRING];
   __shared__ int s_last;
@@ -2615,6 +2620,9 @@ cudaError_t trace_read(void *host, size_t bytes) {
 size_t tile_smem_bytes(Op op) {
   switch (op) {
     case Op::U8_VALIDATE:
+#if !defined(UG_VALIDATE_STREAM) && !defined(UG_NO_VPRODUCER)
+      return VRING8 * INBUF;
+#endif
     case Op::U16_VALIDATE:
     case Op::U16BE_VALIDATE:
 #ifndef UG_VALIDATE_STREAM
