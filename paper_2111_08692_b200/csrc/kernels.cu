@@ -2431,9 +2431,12 @@ __global__ void __launch_bounds__(NTP, PlannedGeo<Pol>::MINB)
   // counts)
   auto tile_offsets = [&](int k, uint32_t *woff, uint32_t *total) {
     const uint32_t v = lane < NTP / 32 ? s_wsum[k & 1][lane] : 0u;
-    // UTF-8 input: two REDUX instead of the shuffle scan (measured: forward -1 %; the same in
-    // the UTF-16 kernel +1.4 % on config 4, so it keeps the shuffles)
-    if constexpr (Pol::UNIT == 1) {
+    // two REDUX instead of the shuffle scan (forward -1 %; the UTF-16 kernel at 256 threads x 4
+    // CTAs: c4 -0.1 %, c1 -4.2 %, c2a -2.0 %, c3 -1.1 %; at 512 x 2 it had been +1.4 %)
+#ifndef UG_REDUX16
+#define UG_REDUX16 1
+#endif
+    if constexpr (Pol::UNIT == 1 || UG_REDUX16) {
       *woff = __reduce_add_sync(FULL, lane < warp ? v : 0u);
       *total = __reduce_add_sync(FULL, v);
       return;
@@ -2519,7 +2522,10 @@ __global__ void __launch_bounds__(NTP, PlannedGeo<Pol>::MINB)
     // (head and tail are < 16 bytes: only the shipping warp has anything to do; skipping the
     // rest measured forward -2..-3 %, but +4..+7 % in the UTF-16 kernel, which keeps them)
     const uint32_t Ct = PHALVES == 1 ? C : (C & 0xFFFFu) + (C >> 16);  // the tile's units
-    if (Pol::UNIT == 2 || warp == UG_SHIP_WARP) {
+#ifndef UG_SHIP_ALL16  // head / tail by the shipping warp only: c4 +3.7 % (c1 -6.5 %): kept
+#define UG_SHIP_ALL16 1
+#endif
+    if ((UG_SHIP_ALL16 && Pol::UNIT == 2) || warp == UG_SHIP_WARP) {
       unsigned long long hi = P + Ct;
       if (hi > a.out_cap) hi = a.out_cap;
       if (hi > P) {
