@@ -2251,7 +2251,11 @@ struct PlannedGeo {
 // direction (UTF-16 input: count first -9 %; UTF-8 input: decode first, count first +15 %).
 template <class Pol>
 struct PlannedOrder {
+#ifndef UG_PORDER_FLIP
   static constexpr bool COUNT_FIRST = Pol::UNIT == 2;
+#else
+  static constexpr bool COUNT_FIRST = Pol::UNIT == 1;
+#endif
 };
 
 template <class Pol>
