@@ -353,6 +353,22 @@ size_t ug_set_host_chunk(size_t units);
  * 4; other values restore the default); returns the previous value.  Process-wide. */
 int ug_set_host_slots(int slots);
 
+/* f2, file form (SURVEY 8(f) f2 "input ... on NVMe"): validate + transcode the
+ * file in_path (UTF-8 bytes / UTF-16LE words, no BOM handling: the bytes are the text) into the
+ * file out_path (created or truncated), streaming through bounded memory: segments of
+ * ug_set_file_segment() input units (default 128 Mi) are read with pread at character-start
+ * cuts with their halos, the next segment's read overlapping the current one's pipeline (the
+ * *_host chunk pipeline above: pinned host segment -> staging slots -> kernels -> output),
+ * each segment's output appended to out_path.  Host memory: two input segments and one output
+ * segment, pinned; device memory: the *_host staging.  Result as for the device call over the
+ * whole file: {UG_OK, n, units} or {kind, e, units before e} (then out_path holds exactly those
+ * units); UG_ERR_ARG for a NULL / unreadable / uncreatable path, a UTF-16 file of odd size, or a
+ * read / write failure; UG_ERR_CUDA on a CUDA failure. */
+ug_result ug_utf8_to_utf16le_file(const char *in_path, const char *out_path, void *stream);
+ug_result ug_utf16le_to_utf8_file(const char *in_path, const char *out_path, void *stream);
+/* Input units per file segment (0: default 128 Mi); returns the previous value. */
+size_t ug_set_file_segment(size_t units);
+
 /* ------------------------------------------------------------------ misc */
 /* Human-readable name of a ug_error value (static string). */
 const char *ug_error_name(int err);

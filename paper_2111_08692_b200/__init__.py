@@ -120,6 +120,9 @@ def _load():
         "ug_utf16le_to_utf8_planned_async": ([P, S, P, P, S, P, P], I),
         "ug_utf8_to_utf16le_keyed_planned_async": ([P, S, P, P, S, P, P], I),
         "ug_utf8_keyed_tables": ([P, P], I),
+        "ug_utf8_to_utf16le_file": ([ctypes.c_char_p, ctypes.c_char_p, P], _CResult),
+        "ug_utf16le_to_utf8_file": ([ctypes.c_char_p, ctypes.c_char_p, P], _CResult),
+        "ug_set_file_segment": ([S], S),
         "ug_utf8_shard_plan_async": ([P, S, S, S, P, P, P], I),
         "ug_utf16le_shard_plan_async": ([P, S, S, S, P, P, P], I),
         "ug_utf8_to_utf16le_shard_planned_async": ([P, S, S, S, U64, P, P, S, P, P], I),
@@ -488,6 +491,23 @@ def utf8_to_utf16le_keyed_planned_async(t_in, d_plan, t_out, d_result, n=None, o
         _ptr(t_in), _units(t_in) if n is None else n, _ptr(d_plan), _ptr(t_out),
         _units(t_out) if out_cap is None else out_cap, _at(d_result, result_off),
         _stream(stream)), "utf8_to_utf16le_keyed_planned_async")
+
+
+def utf8_to_utf16le_file(in_path, out_path, stream=None) -> Result:
+    """f2 file form: UTF-8 file -> UTF-16LE file, streamed through bounded memory."""
+    return _res(lib.ug_utf8_to_utf16le_file(os.fsencode(in_path), os.fsencode(out_path),
+                                            _stream(stream)))
+
+
+def utf16le_to_utf8_file(in_path, out_path, stream=None) -> Result:
+    """f2 file form: UTF-16LE file -> UTF-8 file, streamed through bounded memory."""
+    return _res(lib.ug_utf16le_to_utf8_file(os.fsencode(in_path), os.fsencode(out_path),
+                                            _stream(stream)))
+
+
+def set_file_segment(units: int) -> int:
+    """Input units per file segment (0 = default); returns the previous value."""
+    return int(lib.ug_set_file_segment(units))
 
 
 def keyed_tables():

@@ -8,7 +8,16 @@
 #include <map>
 #include <mutex>
 #include <utility>
+#include <thread>
+#ifdef UG_FILE_TRACE
+#include <chrono>
+#include <cstdio>
+#endif
 #include <vector>
+
+#include <fcntl.h>
+#include <sys/stat.h>
+#include <unistd.h>
 
 #include "../../include/unigpu.h"
 #include "internal.h"
@@ -496,13 +505,24 @@ cudaError_t ensure_pipeline(Workspace *w, size_t nchunks) {
 // Copies in both directions and the kernels overlap (slots - 1 chunks ahead of the host);
 // the result is combined from the records exactly as the unsharded kernel states it (first
 // error, written, output too small).  The workspace mutex is held for the whole call.
+// The pipeline over a WINDOW of a longer stream (the file form below): in_host[0, n) are units
+// [goff, goff + n) of the stream, with HB units readable before in_host and HA after its end;
+// positions in the result are stream positions.  run_host is the whole-buffer case.
+ug_result run_host_window(Op op, const void *in_host, unsigned long long n, unsigned long long HB,
+                          unsigned long long HA, unsigned long long goff, void *out_host,
+                          unsigned long long out_cap, cudaStream_t s);
 ug_result run_host(Op op, const void *in_host, unsigned long long n, void *out_host,
                    unsigned long long out_cap, cudaStream_t s) {
+  return run_host_window(op, in_host, n, 0, 0, 0, out_host, out_cap, s);
+}
+ug_result run_host_window(Op op, const void *in_host, unsigned long long n, unsigned long long HB,
+                          unsigned long long HA, unsigned long long goff, void *out_host,
+                          unsigned long long out_cap, cudaStream_t s) {
   const bool u16in = op_u16_input(op);
   const size_t ius = u16in ? 2 : 1, ous = u16in ? 1 : 2;
   const unsigned long long ub = u16in ? 3 : 1;  // output units per input unit, at most
   const unsigned long long halo = u16in ? 1 : 3;
-  if (n == 0) return make_result(UG_OK, 0, 0);
+  if (n == 0) return make_result(UG_OK, goff, 0);
   if (in_host == nullptr || (out_host == nullptr && out_cap > 0))
     return make_result(UG_ERR_ARG, 0, 0);
   if (n > MAX_N || (u16in && ((uintptr_t)in_host & 1u)) || (!u16in && ((uintptr_t)out_host & 1u)))
@@ -542,14 +562,15 @@ ug_result run_host(Op op, const void *in_host, unsigned long long n, void *out_h
   auto stage_chunk = [&](size_t i) -> int {
     const int k = (int)(i % slots);
     const unsigned long long lo = cut[i], hi = cut[i + 1];
-    const unsigned long long hb = lo < halo ? lo : halo, ha = n - hi < halo ? n - hi : halo;
+    const unsigned long long hb = lo + HB < halo ? lo + HB : halo;
+    const unsigned long long ha = n - hi + HA < halo ? n - hi + HA : halo;
     uint8_t *sin = din + k * in_slot, *sout = dout + k * out_slot;
     if (cudaMemcpyAsync(sin, hin + (lo - hb) * ius, (hi - lo + hb + ha) * ius,
                         cudaMemcpyHostToDevice, w->h2d) != cudaSuccess ||
         cudaEventRecord(w->ev_in[k], w->h2d) != cudaSuccess ||
         cudaStreamWaitEvent(s, w->ev_in[k], 0) != cudaSuccess)
       return UG_ERR_CUDA;
-    int rc = enqueue_tile_ws(w, di, op, sin + hb * ius, hi - lo, hb, ha, lo, sout,
+    int rc = enqueue_tile_ws(w, di, op, sin + hb * ius, hi - lo, hb, ha, goff + lo, sout,
                              (hi - lo) * ub, nullptr, w->d_recs + i, s);
     if (rc != UG_OK) return rc;
     if (cudaMemcpyAsync(w->h_recs + i, w->d_recs + i, sizeof(RecordDev), cudaMemcpyDeviceToHost,
@@ -608,8 +629,216 @@ ug_result run_host(Op op, const void *in_host, unsigned long long n, void *out_h
     return make_result(UG_ERR_CUDA, 0, 0);
   const unsigned long long required = e == NONE ? prefix : wr;
   if (required > out_cap) return make_result(UG_ERR_OUTPUT_TOO_SMALL, required, 0);
-  if (e == NONE) return make_result(UG_OK, n, prefix);
+  if (e == NONE) return make_result(UG_OK, goff + n, prefix);
   return make_result(kind, e, wr);
+}
+
+// ---------------------------------------------------------------- f2: file streaming
+// in_path -> out_path through bounded host and device memory (DESIGN.md f2):
+// the file is read in segments of g_file_segment units (cut at character starts by the shard
+// rule, each read with its halos), the next segment's read overlapped (a reader thread) with
+// the current one's pipeline (run_host_window: H2D / kernels / D2H of its chunks), its output
+// appended to out_path.  Stops at the first error: out_path then holds the units before it.
+std::atomic<size_t> g_file_segment{128ull << 20};  // input units per file segment
+struct FileBuffers {
+  std::mutex mu;
+  void *in[2] = {nullptr, nullptr}, *out[2] = {nullptr, nullptr};
+  size_t in_bytes = 0, out_bytes = 0;
+  cudaError_t grow(void **b, size_t *have, size_t need) {
+    if (*have >= need) return cudaSuccess;
+    for (int k = 0; k < 2; k++) {
+      if (b[k]) cudaFreeHost(b[k]);
+      b[k] = nullptr;
+    }
+    *have = 0;
+    for (int k = 0; k < 2; k++) {
+      const cudaError_t e = cudaHostAlloc(&b[k], need, cudaHostAllocDefault);
+      if (e != cudaSuccess) return e;
+    }
+    *have = need;
+    return cudaSuccess;
+  }
+  void release() {
+    std::lock_guard<std::mutex> lk(mu);
+    for (int k = 0; k < 2; k++) {
+      if (in[k]) cudaFreeHost(in[k]);
+      if (out[k]) cudaFreeHost(out[k]);
+      in[k] = out[k] = nullptr;
+    }
+    in_bytes = out_bytes = 0;
+  }
+};
+FileBuffers g_file;
+
+bool pread_all(int fd, void *buf, size_t bytes, unsigned long long off) {
+  uint8_t *p = (uint8_t *)buf;
+  while (bytes) {
+    const ssize_t r = pread(fd, p, bytes, (off_t)off);
+    if (r <= 0) return false;
+    p += r, bytes -= (size_t)r, off += (unsigned long long)r;
+  }
+  return true;
+}
+bool pwrite_all(int fd, const void *buf, size_t bytes, unsigned long long off) {
+  const uint8_t *p = (const uint8_t *)buf;
+  while (bytes) {
+    const ssize_t r = pwrite(fd, p, bytes, (off_t)off);
+    if (r <= 0) return false;
+    p += r, bytes -= (size_t)r, off += (unsigned long long)r;
+  }
+  return true;
+}
+
+// pread / pwrite of one large block by IO_THREADS threads (a single thread's page-cache copy
+// tops out near 2-3 GB/s)
+constexpr int IO_THREADS = 4;
+bool io_par(bool rd, int fd, void *buf, size_t bytes, unsigned long long off) {
+  if (bytes < (8u << 20))
+    return rd ? pread_all(fd, buf, bytes, off) : pwrite_all(fd, buf, bytes, off);
+  bool ok[IO_THREADS];
+  std::thread th[IO_THREADS];
+  const size_t part = (((bytes + IO_THREADS - 1) / IO_THREADS) + 4095) & ~(size_t)4095;
+  for (int t = 0; t < IO_THREADS; t++) {
+    const size_t a = (size_t)t * part, b = a + part < bytes ? a + part : bytes;
+    ok[t] = true;
+    if (a >= b) continue;
+    th[t] = std::thread([&, t, a, b] {
+      uint8_t *p = (uint8_t *)buf + a;
+      ok[t] = rd ? pread_all(fd, p, b - a, off + a) : pwrite_all(fd, p, b - a, off + a);
+    });
+  }
+  bool all = true;
+  for (int t = 0; t < IO_THREADS; t++) {
+    if (th[t].joinable()) th[t].join();
+    all = all && ok[t];
+  }
+  return all;
+}
+
+ug_result run_file(Op op, const char *in_path, const char *out_path, cudaStream_t s) {
+  const bool u16in = op_u16_input(op);
+  const size_t ius = u16in ? 2 : 1, ous = u16in ? 1 : 2;
+  const unsigned long long ub = u16in ? 3 : 1, halo = u16in ? 1 : 3;
+  if (!in_path || !out_path) return make_result(UG_ERR_ARG, 0, 0);
+  const int fin = open(in_path, O_RDONLY);
+  if (fin < 0) return make_result(UG_ERR_ARG, 0, 0);
+  struct stat st;
+  if (fstat(fin, &st) != 0 || (u16in && (st.st_size & 1))) {
+    close(fin);
+    return make_result(UG_ERR_ARG, 0, 0);
+  }
+  const int fout = open(out_path, O_WRONLY | O_CREAT | O_TRUNC, 0644);
+  if (fout < 0) {
+    close(fin);
+    return make_result(UG_ERR_ARG, 0, 0);
+  }
+  const unsigned long long n = (unsigned long long)st.st_size / ius;
+  const unsigned long long seg = g_file_segment.load() ? g_file_segment.load() : (128ull << 20);
+  const unsigned long long seg_n = seg < n ? seg : n;
+  // two input buffers (current / prefetch): a segment plus 2 halos and the cut look-ahead
+  const size_t in_bytes = (size_t)(seg_n + 4 * halo + 8) * ius;
+  const size_t out_bytes = (size_t)(seg_n * ub + 8) * ous;
+  // pinned segment buffers, kept across calls (pinning ~1 GB costs a few hundred ms)
+  std::lock_guard<std::mutex> flk(g_file.mu);
+  void **hin = g_file.in, **hout = g_file.out;
+  ug_result res = make_result(UG_OK, 0, 0);
+  bool io_err = false;
+  if (n > 0 && (g_file.grow(g_file.in, &g_file.in_bytes, in_bytes) != cudaSuccess ||
+                g_file.grow(g_file.out, &g_file.out_bytes, out_bytes) != cudaSuccess)) {
+    res = make_result(UG_ERR_CUDA, 0, 0);
+  } else if (n > 0) {
+    // read segment [lo, ...): stream units [lo - hb, min(n, lo + seg + 2 halo)) into buf;
+    // returns its end hi (a character start, by the shard cut rule) and hb
+    auto load = [&](int b, unsigned long long lo, unsigned long long *hi,
+                    unsigned long long *hb) -> bool {
+      *hb = lo < halo ? lo : halo;
+      unsigned long long end = lo + seg + 2 * halo;
+      if (end > n) end = n;
+      if (!io_par(true, fin, hin[b], (size_t)(end - lo + *hb) * ius, (lo - *hb) * ius))
+        return false;
+      const unsigned long long c = lo + seg;
+      if (c >= n) {
+        *hi = n;
+      } else {
+        const uint8_t *at = (const uint8_t *)hin[b] + (c - lo + *hb) * ius;
+        const unsigned long long k =
+            op == Op::U16BE_TO_U8 ? ug_utf16be_cut_backoff((const uint16_t *)at, c)
+            : u16in               ? ug_utf16_cut_backoff((const uint16_t *)at, c)
+                                  : ug_utf8_cut_backoff(at, c);
+        *hi = c - k > lo ? c - k : c;
+      }
+      return true;
+    };
+    // three stages overlap: the reader thread fetches segment k + 1, the GPU pipeline runs
+    // segment k, the writer thread appends segment k - 1's output (double-buffered in / out)
+    unsigned long long lo = 0, hi = 0, hb = 0, prefix = 0;
+    int cur = 0;
+    bool wok = true;
+    std::thread writer;
+    bool ok = load(cur, 0, &hi, &hb);
+    if (!ok) io_err = true;
+    while (ok) {
+      unsigned long long hi2 = 0, hb2 = 0;
+      bool ok2 = true;
+      std::thread reader;
+      if (hi < n) reader = std::thread([&, nxt = cur ^ 1, from = hi] {
+        ok2 = load(nxt, from, &hi2, &hb2);
+      });
+      const unsigned long long ha = n - hi < halo ? n - hi : halo;
+#ifdef UG_FILE_TRACE
+      const auto t0 = std::chrono::steady_clock::now();
+#endif
+      const ug_result r = run_host_window(op, (const uint8_t *)hin[cur] + hb * ius, hi - lo, hb,
+                                          ha, lo, hout[cur], (hi - lo) * ub, s);
+#ifdef UG_FILE_TRACE
+      const auto t1 = std::chrono::steady_clock::now();
+#endif
+      if (reader.joinable()) reader.join();
+#ifdef UG_FILE_TRACE
+      const auto t2 = std::chrono::steady_clock::now();
+#endif
+      if (writer.joinable()) writer.join();  // segment k - 1's output (the other buffer) is out
+#ifdef UG_FILE_TRACE
+      const auto t3 = std::chrono::steady_clock::now();
+      fprintf(stderr, "seg %llu: gpu %.1f ms, read wait %.1f ms, write wait %.1f ms\n", lo,
+              std::chrono::duration<double, std::milli>(t1 - t0).count(),
+              std::chrono::duration<double, std::milli>(t2 - t1).count(),
+              std::chrono::duration<double, std::milli>(t3 - t2).count());
+#endif
+      if (!wok) {
+        io_err = true;
+        break;
+      }
+      if (r.error < 0) {
+        res = r;
+        break;
+      }
+      const unsigned long long units = r.written;
+      if (units) writer = std::thread([&, b = cur, bytes = (size_t)units * ous,
+                                       off = prefix * ous] {
+        if (!io_par(false, fout, hout[b], bytes, off)) wok = false;
+      });
+      if (r.error != UG_OK) {
+        res = make_result(r.error, r.position, prefix + units);
+        break;
+      }
+      prefix += units;
+      res = make_result(UG_OK, hi, prefix);
+      if (hi >= n) break;
+      if (!ok2) {
+        io_err = true;
+        break;
+      }
+      lo = hi, hi = hi2, hb = hb2, cur ^= 1;
+    }
+    if (writer.joinable()) writer.join();
+    if (!wok) io_err = true;
+  }
+
+  if (close(fout) != 0) io_err = true;
+  close(fin);
+  if (io_err) return make_result(UG_ERR_ARG, 0, 0);
+  return res;
 }
 
 }  // namespace
@@ -1048,6 +1277,15 @@ ug_result utf16be_to_utf8_host(const uint16_t *in_host, size_t n, uint8_t *out_h
   return run_host(Op::U16BE_TO_U8, in_host, n, out_host, out_cap, (cudaStream_t)stream);
 }
 
+ug_result ug_utf8_to_utf16le_file(const char *in_path, const char *out_path, void *stream) {
+  return run_file(Op::U8_TO_U16, in_path, out_path, (cudaStream_t)stream);
+}
+ug_result ug_utf16le_to_utf8_file(const char *in_path, const char *out_path, void *stream) {
+  return run_file(Op::U16_TO_U8, in_path, out_path, (cudaStream_t)stream);
+}
+size_t ug_set_file_segment(size_t units) {
+  return g_file_segment.exchange(units ? units : (128ull << 20));
+}
 int ug_set_host_slots(int slots) {
   const int v = slots < 2 ? 4 : (slots > HOST_SLOTS_MAX ? HOST_SLOTS_MAX : slots);
   return g_host_slots.exchange(v);
@@ -1080,6 +1318,7 @@ uint64_t ug_launch_count(void) { return g_launches.load(); }
 void ug_release_workspaces(void) {
   int dev;
   if (cudaGetDevice(&dev) != cudaSuccess) return;
+  g_file.release();  // the file form's pinned segment buffers
   {  // the multi-device entry's gather buffers on this device
     std::lock_guard<std::mutex> lk(g_shard_mu);
     for (auto it = g_shard_ctx.begin(); it != g_shard_ctx.end();) {
