@@ -363,7 +363,8 @@ int ug_set_host_slots(int slots);
  * segment, pinned; device memory: the *_host staging.  Result as for the device call over the
  * whole file: {UG_OK, n, units} or {kind, e, units before e} (then out_path holds exactly those
  * units); UG_ERR_ARG for a NULL / unreadable / uncreatable path, a UTF-16 file of odd size, or a
- * read / write failure; UG_ERR_CUDA on a CUDA failure. */
+ * read / write failure; UG_ERR_CUDA on a CUDA failure.  The pinned segment buffers are kept
+ * for the next call (freed by ug_release_workspaces); concurrent file calls are serialised. */
 ug_result ug_utf8_to_utf16le_file(const char *in_path, const char *out_path, void *stream);
 ug_result ug_utf16le_to_utf8_file(const char *in_path, const char *out_path, void *stream);
 /* Input units per file segment (0: default 128 Mi); returns the previous value. */
