@@ -19,7 +19,7 @@ def f(op):
 
 
 new = f"""**Round 2 (driver-comparable bench line, `profiles/{tag}_bench_default.json`, 8 GiB config 4,
-one B200, clocks 1965 MHz, no throttle reasons; interim builds `profiles/r2a_*` … `r2g_*`):**
+one B200, clocks 1965 MHz, no throttle reasons; interim builds `profiles/r2a_*`, `r2b_*`; r2d–r2g in git history):**
 
 | Step / kernel | round 1 (r1m) | round 2 interim (r2b) | round 2 final two-pass ({tag}) | round 2 single-pass (`--path chained`, {tag}) |
 |---|---|---|---|---|
