@@ -255,7 +255,7 @@ PlanGeo plan_geo(DeviceInfo *di, bool u16in, const void *in, unsigned long long 
   // 16 KiB-tile CTA slot: the count does not grow with the planned kernels' CTA count, whose
   // tiles are smaller -- more sub-ranges only cost the sizing pass
   unsigned long long want = (unsigned long long)di->sms * CTAS_PER_SM * PLAN_SUBS_PER_CTA;
-  if (want > (unsigned long long)(PLAN_WORDS - 8)) want = PLAN_WORDS - 8;
+  if (want > (unsigned long long)(PLAN_WORDS - PLAN_HDR)) want = PLAN_WORDS - PLAN_HDR;
   if (want > g.ntiles) want = g.ntiles;
   g.tps = (g.ntiles + want - 1) / want;
   g.nsub = (int)((g.ntiles + g.tps - 1) / g.tps);

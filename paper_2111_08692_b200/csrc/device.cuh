@@ -63,7 +63,7 @@ struct Counters {
   uint32_t done;      // CTAs finished
   unsigned long long err_min;  // smallest error position found (NONE = none)
   unsigned long long accum;    // reduction accumulator (length-from kernels)
-  unsigned long long pad;      // second accumulator (plan kernels)
+  unsigned long long accf;     // second accumulator (the UTF-8 plan's >= F0 bytes)
   unsigned long long flags;    // bit 0: a planned transcoder was given a plan of other input
 };
 

@@ -61,7 +61,8 @@ cudaError_t tile_occupancy(Op op, int *blocks_per_sm);
 cudaError_t launch_tile(Op op, const TileArgs &a, int grid, cudaStream_t s);
 
 // planned (two-pass) path: plan kernels and the planned transcoders
-constexpr int PLAN_WORDS = 8 + 8192;  // header + sub-range offsets (kernels.cu PLAN_*)
+constexpr int PLAN_HDR = 16;                // header words (kernels.cu plan_finish)
+constexpr int PLAN_WORDS = PLAN_HDR + 8192;  // header + sub-range offsets
 #ifndef UG_PLAN_SUBS
 #define UG_PLAN_SUBS 8
 #endif

@@ -151,12 +151,14 @@ template <bool BE>
 struct U8PolT {
   using Out = uint16_t;
   static constexpr int UNIT = 1;                      // input bytes per position
+  static constexpr bool kNoF = true;  // planned kernel: warps without >= F0 leads decode by units4_nof
   static constexpr int STAGE = 2 * (TILE + 32);        // stage bytes per buffer
   struct St {
     uint32_t w[8];   // own 32 bytes
     uint32_t prev;   // the 4 bytes before
     uint32_t nxt;    // the 4 bytes after
     uint32_t err;    // classifier flags (a3)
+    uint32_t fany;   // nonzero: a >= F0 lead in the chunk or the 3 bytes before (f1, UTF-8)
     long long pos0;  // position of own byte 0
     long long n;
     const uint8_t *img;  // own bytes in the smem tile image
@@ -215,7 +217,8 @@ struct U8PolT {
 #ifdef UG_ABL_NOVAL
     emit = ~s.w[0] & 0x80808080u;
 #else
-    if (!s.wasc) s.err = u8::analyze32(s.w, s.prev, s.nxt, (tid & 31) == 31, &emit);  // a3, a5
+    s.fany = 0;
+    if (!s.wasc) s.err = u8::analyze32(s.w, s.prev, s.nxt, (tid & 31) == 31, &emit, &s.fany);
 #endif
     if (!xc) return 0u;
     if (!IN) emit &= bit_range(s.pos0, 0, s.n);
@@ -245,7 +248,7 @@ struct U8PolT {
 
   // a7: decode the owned characters into stage[o ...] (UTF-16 units).  Each emitting position
   // stores its unit at its exclusive-prefix slot (predicated on the emit mask).
-  template <bool IN>
+  template <bool IN, bool NOF = false>  // NOF: the warp holds no >= F0 lead (units4_nof)
   __device__ static __forceinline__ void decode(const St &s, uint16_t *stage, uint32_t o,
                                                 uint32_t, long long) {
     if (IN && s.wasc) {
@@ -300,7 +303,8 @@ struct U8PolT {
 #pragma unroll
     for (int k = 0; k < 8; k++) {
       uint32_t u01, u23;
-      uint32_t em = u8::units4<BE>(s.w[k], cy, &u01, &u23);
+      uint32_t em = NOF ? u8::units4_nof<BE>(s.w[k], cy, &u01, &u23)
+                        : u8::units4<BE>(s.w[k], cy, &u01, &u23);
       if (!IN) em &= range_bytes(s.pos0 + 4 * k, 0, s.n) & 0x01010101u;
       const uint32_t inc2 = em * 0x02020202u;  // byte j: 2 x units emitted by positions <= j
       const uint32_t a1 = mad(prmt(inc2, 0u, 0x4440u), 1u, p);
@@ -356,6 +360,7 @@ __device__ uint16_t g_keyed_key[keyed::KEYS];
 __device__ uint32_t g_keyed_shuf[keyed::SHUFFLES * keyed::SHUF_WORDS];
 
 struct U8KeyPol : U8PolT<false> {
+  static constexpr bool kNoF = false;  // the comparison keeps its own decode everywhere
   template <bool IN>
   __device__ static __forceinline__ void decode(const St &s, uint16_t *stage, uint32_t o,
                                                 uint32_t lim, long long n) {
@@ -386,6 +391,7 @@ struct U16PolT {
   using Out = uint8_t;
   static constexpr int UNIT = 2;
   static constexpr bool kBE = BE;
+  static constexpr bool kNoF = false;  // (the UTF-8 forward's f1 form)
   __device__ static __forceinline__ uint32_t native(uint32_t w) {  // a stored word's value
     return BE ? (((w >> 8) | (w << 8)) & 0xFFFFu) : w;
   }
@@ -1398,10 +1404,11 @@ __device__ __forceinline__ uint32_t len8_word(uint32_t x) {
 }
 __device__ __forceinline__ uint32_t len8_byte(uint32_t b) { return u8::plan_weight(b); }
 // per byte lane: [non-continuation] + [>= F0], accumulated (IMAD.HI) into acc
-__device__ __forceinline__ uint32_t len8_acc(uint32_t x, uint32_t acc) {
+__device__ __forceinline__ uint32_t len8_acc(uint32_t x, uint32_t acc, uint32_t *fo = nullptr) {
   const uint32_t x1 = x << 1;
   const uint32_t nk = (~x | x1) & HI;
   const uint32_t f = x & x1 & (x << 2) & (x << 3) & HI;
+  if (fo) *fo |= f;
   return mad_hi(f, 1u << 25, mad_hi(nk, 1u << 25, acc));
 }
 __device__ __forceinline__ uint32_t lane_sum(uint32_t acc) { return (acc * 0x01010101u) >> 24; }
@@ -1823,7 +1830,6 @@ __global__ void __launch_bounds__(T16_THREADS, CTAS_PER_SM) k_transcode16(const 
 // [3] sub-ranges, [4] tiles per sub-range, [5] total under the emission rule, [6] lead,
 // [7] halos (before << 32 | after, bytes), [8 + j] output offset (exclusive prefix of the
 // counts) of sub-range j.
-constexpr int PLAN_HDR = 8;
 constexpr int PLAN_MAX_SUB = 8192;
 static_assert(PLAN_WORDS == PLAN_HDR + PLAN_MAX_SUB, "plan layout (internal.h PLAN_WORDS)");
 constexpr unsigned long long PLAN_TAG = 0x554750414E563031ull;
@@ -1857,15 +1863,20 @@ __device__ __forceinline__ unsigned long long plan_halos(const Window &w) {
 }
 
 __device__ __forceinline__ void plan_finish(const PlanArgs &a, unsigned long long emit_sum,
-                                            unsigned long long len_sum) {
+                                            unsigned long long len_sum,
+                                            unsigned long long f_sum = 0) {
   __shared__ unsigned long long s_e[LNT / 32], s_l[LNT / 32];
-  __shared__ int s_last;
+  __shared__ int s_last, s_f;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) s_f = 0;
   emit_sum = warp_sum64(emit_sum);
   len_sum = warp_sum64(len_sum);
+  const bool f_any = __any_sync(FULL, f_sum != 0);
+  __syncthreads();
   if (lane == 0) {
     s_e[warp] = emit_sum;
     s_l[warp] = len_sum;
+    if (f_any) s_f = 1;
   }
   __syncthreads();
   if (tid == 0) {
@@ -1876,6 +1887,9 @@ __device__ __forceinline__ void plan_finish(const PlanArgs &a, unsigned long lon
     }
     st_relaxed(reinterpret_cast<uint64_t *>(a.plan + PLAN_HDR + blockIdx.x), e);
     atomicAdd(&a.ctr->accum, l);
+    // a flag, not a count: one plain store per CTA that saw a >= F0 byte (no atomic traffic)
+    if (s_f && *reinterpret_cast<volatile unsigned long long *>(&a.ctr->accf) == 0)
+      *reinterpret_cast<volatile unsigned long long *>(&a.ctr->accf) = 1;
     __threadfence();
     s_last = (atomicAdd(&a.ctr->done, 1u) == gridDim.x - 1) ? 1 : 0;
   }
@@ -1916,8 +1930,11 @@ __device__ __forceinline__ void plan_finish(const PlanArgs &a, unsigned long lon
     a.plan[5] = total;
     a.plan[6] = (unsigned long long)a.win.lead;
     a.plan[7] = plan_halos(a.win);
+    // nonzero iff the window (with the halo before it) holds a >= F0 byte (UTF-8 plans; f1)
+    a.plan[8] = *reinterpret_cast<volatile unsigned long long *>(&a.ctr->accf);
     if (a.d_len) *a.d_len = L;
     a.ctr->accum = 0;
+    a.ctr->accf = 0;
     a.ctr->done = 0;
   }
 }
@@ -2026,6 +2043,8 @@ __global__ void __launch_bounds__(LNT) k_plan8(const PlanArgs a) {
   const uint4 *v = reinterpret_cast<const uint4 *>(base + h0);
   const long long nv = (h1 - h0) / 16;
   long long i = threadIdx.x;
+  uint32_t fo = 0;  // >= F0 bytes seen (OR of their msb masks: only "any" matters per lane)
+  unsigned long long fsum = 0;
   for (; i + 3 * LNT < nv; i += 4 * LNT) {
     uint4 q[4];
 #pragma unroll
@@ -2033,20 +2052,32 @@ __global__ void __launch_bounds__(LNT) k_plan8(const PlanArgs a) {
     uint32_t acc = 0;
 #pragma unroll
     for (int j = 0; j < 4; j++)
-      acc = len8_acc(q[j].w, len8_acc(q[j].z, len8_acc(q[j].y, len8_acc(q[j].x, acc))));
+      acc = len8_acc(q[j].w, len8_acc(q[j].z, len8_acc(q[j].y, len8_acc(q[j].x, acc, &fo), &fo),
+                                      &fo), &fo);
     sum += lane_sum(acc);
   }
   for (; i < nv; i += LNT) {
     const uint4 q = __ldcs(v + i);
-    sum += lane_sum(len8_acc(q.w, len8_acc(q.z, len8_acc(q.y, len8_acc(q.x, 0u)))));
+    sum += lane_sum(len8_acc(q.w, len8_acc(q.z, len8_acc(q.y, len8_acc(q.x, 0u, &fo), &fo), &fo),
+                             &fo));
   }
-  for (long long b = p0 + threadIdx.x; b < h0; b += LNT) sum += len8_byte(base[b]);
-  for (long long b = h1 + threadIdx.x; b < p1; b += LNT) sum += len8_byte(base[b]);
+  for (long long b = p0 + threadIdx.x; b < h0; b += LNT) {
+    sum += len8_byte(base[b]);
+    fsum += base[b] >= 0xF0u;
+  }
+  for (long long b = h1 + threadIdx.x; b < p1; b += LNT) {
+    sum += len8_byte(base[b]);
+    fsum += base[b] >= 0xF0u;
+  }
+  fsum += fo != 0u;
+  // the window's halo bytes before position 0 count too (a 4-byte character begun there)
+  if (p0 == 0 && threadIdx.x == 0)
+    for (int d = 1; d <= 3; d++) fsum += byte_at(w, -d) >= 0xF0u;
   // boundary terms (thread 0; modular: a range's count may be "negative", prefixes are not)
   const unsigned long long emit = threadIdx.x == 0
       ? sum + (unsigned long long)(plan8_pending(w, p0) - plan8_pending(w, p1))
       : sum;
-  plan_finish(a, emit, sum);
+  plan_finish(a, emit, sum, fsum);
 }
 #elif defined(UG_PLAN8_PLANES)
 // UTF-8 plan on bit planes (the classifier's transposition, u8::planes32): a lane's 32 bytes ->
@@ -2258,7 +2289,7 @@ struct PlannedOrder {
 #endif
 };
 
-template <class Pol>
+template <class Pol, bool NOF = false>
 __global__ void __launch_bounds__(NTP, PlannedGeo<Pol>::MINB)
     k_transcode_planned(const TileArgs a, const unsigned long long *plan) {
   using Out = typename Pol::Out;
@@ -2286,6 +2317,11 @@ __global__ void __launch_bounds__(NTP, PlannedGeo<Pol>::MINB)
   const bool bad = plan[0] != PLAN_TAG || plan[1] != (unsigned long long)(uintptr_t)win.base ||
                    plan[2] != (unsigned long long)win.n ||
                    plan[6] != (unsigned long long)win.lead || plan[7] != plan_halos(win);
+  // f1 for UTF-8: the forward is launched twice, with and without the no-F decode; the plan
+  // (header word 8: the input's >= F0 bytes) picks the one that runs, the other returns here
+  if constexpr (Pol::kNoF) {
+    if ((!bad && plan[8] == 0) != NOF) return;
+  }
   const long long nsub = bad ? 0 : (long long)plan[3], tps = bad ? 1 : (long long)plan[4];
   if (bad && tid == 0 && blockIdx.x == 0) atomicOr(&a.ctr->flags, 1ull);
   // producer (lane 0 of the last warp, not the shipping warp 0): tiles in sub-range order,
@@ -2509,7 +2545,10 @@ __global__ void __launch_bounds__(NTP, PlannedGeo<Pol>::MINB)
       } else {
         if (tp >= 0 && tp + HALFP <= win.n) {
           Pol::template load<true>(st, img, tid, lane, tp, win.n);
-          Pol::template decode<true>(st, stage, o, o + ch, n_units);
+          if constexpr (NOF)  // (f1, UTF-8: the input holds no >= F0 byte)
+            Pol::template decode<true, true>(st, stage, o, o + ch, n_units);
+          else
+            Pol::template decode<true>(st, stage, o, o + ch, n_units);
         } else {
           Pol::template load<false>(st, img, tid, lane, tp, win.n);
           Pol::template decode<false>(st, stage, o, o + ch, n_units);
@@ -2785,9 +2824,20 @@ static const void *planned_fn(Op op) {
     default: return nullptr;
   }
 }
+static const void *planned_fn_nof(Op op) {  // f1 for UTF-8: the no-F forward
+  switch (op) {
+    case Op::U8_TO_U16: return (const void *)k_transcode_planned<U8Pol, true>;
+    case Op::U8_TO_U16BE: return (const void *)k_transcode_planned<U8PolBE, true>;
+    default: return nullptr;
+  }
+}
 cudaError_t planned_configure(Op op) {
-  return cudaFuncSetAttribute(planned_fn(op), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)planned_smem_bytes(op_u16_input(op)));
+  cudaError_t e = cudaFuncSetAttribute(planned_fn(op), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)planned_smem_bytes(op_u16_input(op)));
+  if (e == cudaSuccess && planned_fn_nof(op))
+    e = cudaFuncSetAttribute(planned_fn_nof(op), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)planned_smem_bytes(false));
+  return e;
 }
 cudaError_t planned_occupancy(Op op, int *blocks_per_sm) {
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(
@@ -2797,8 +2847,15 @@ cudaError_t launch_planned(Op op, const TileArgs &a, const unsigned long long *p
                            cudaStream_t s) {
   const size_t sm = planned_smem_bytes(op_u16_input(op));
   switch (op) {
-    case Op::U8_TO_U16: k_transcode_planned<U8Pol><<<grid, NTP, sm, s>>>(a, plan); break;
-    case Op::U8_TO_U16BE: k_transcode_planned<U8PolBE><<<grid, NTP, sm, s>>>(a, plan); break;
+    // both forward forms are launched; the plan's header selects the one that works
+    case Op::U8_TO_U16:
+      k_transcode_planned<U8Pol><<<grid, NTP, sm, s>>>(a, plan);
+      k_transcode_planned<U8Pol, true><<<grid, NTP, sm, s>>>(a, plan);
+      break;
+    case Op::U8_TO_U16BE:
+      k_transcode_planned<U8PolBE><<<grid, NTP, sm, s>>>(a, plan);
+      k_transcode_planned<U8PolBE, true><<<grid, NTP, sm, s>>>(a, plan);
+      break;
     case Op::U16_TO_U8: k_transcode_planned<U16Pol><<<grid, NTP, sm, s>>>(a, plan); break;
     case Op::U16BE_TO_U8: k_transcode_planned<U16PolBE><<<grid, NTP, sm, s>>>(a, plan); break;
     default: return cudaErrorInvalidValue;

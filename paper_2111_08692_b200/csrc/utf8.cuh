@@ -83,7 +83,7 @@ UG_HD uint32_t carry3(uint32_t msb_mask) { return msb_mask * 0x4081u; }
 //   *emit: bit i set iff position i emits a UTF-16 unit (end-position rule above).
 //   tail: also flag continuation bytes missing at positions 32..34 (the last chunk of a tile).
 UG_HD uint32_t analyze32(const uint32_t w[8], uint32_t prev, uint32_t nxt, bool tail,
-                         uint32_t *emit) {
+                         uint32_t *emit, uint32_t *fany = nullptr) {
   uint32_t P[8];
   planes32(w, P);
   const uint32_t L = P[7] & P[6], E = L & P[5], F = E & P[4];
@@ -113,6 +113,7 @@ UG_HD uint32_t analyze32(const uint32_t w[8], uint32_t prev, uint32_t nxt, bool 
     if (Rt & ~Knb) err |= 0x80000000u;
   }
   *emit = ~P[7] | fsl(cL & ~cE, L & ~E, 1) | S2E | S3F;
+  if (fany) *fany = F | cF;  // nonzero iff a >= F0 lead lies in the chunk or the 3 bytes before
   return err;
 }
 
@@ -154,6 +155,25 @@ UG_HD uint32_t units4(uint32_t x, Carry &c, uint32_t *u01, uint32_t *u23) {
   const uint32_t hbm = (hb | HI) - 0x04040404u;  // per byte 0x80 + hb - 4, no borrows
   lb = mux(Mh, muxc<0xF0F0F0F0u>(hbm << 4, shr_fma<4>(lb)), lb);
   hb = mux(Mh, (shr_fma<4>(hbm) & 0x03030303u) | 0xD8D8D8D8u, hb);
+  *u01 = prmt(lb, hb, BE ? 0x1504u : 0x5140u);
+  *u23 = prmt(lb, hb, BE ? 0x3726u : 0x7362u);
+  return em;
+}
+
+// units4 for a warp whose 1 KiB and the 3 bytes before hold no >= F0 lead (no 4-byte
+// character: no surrogate pair to emit, f1 for UTF-8): the same units and emit mask on such
+// input without the surrogate terms.
+template <bool BE = false>
+UG_HD uint32_t units4_nof(uint32_t x, Carry &c, uint32_t *u01, uint32_t *u23) {
+  const Carry n = carry_of(x);
+  const uint32_t bp1 = fsl(c.x, x, 8), bp2 = fsl(c.x, x, 16);
+  const uint32_t s1l2 = fsl(c.L2, n.L2, 1);
+  const uint32_t s2e = fsl(c.E, n.E, 9);
+  c = n;
+  const uint32_t n7 = (x >> 7) & 0x01010101u;
+  const uint32_t em = ((n7 ^ 0x01010101u) | s1l2 | s2e);
+  const uint32_t lb = mux(n7 * 0xC0u, bp1 << 6, x);
+  const uint32_t hb = (shr_fma<2>(bp1) & (n7 * 15u)) | ((bp2 << 4) & (s2e * 0xF0u));
   *u01 = prmt(lb, hb, BE ? 0x1504u : 0x5140u);
   *u23 = prmt(lb, hb, BE ? 0x3726u : 0x7362u);
   return em;

@@ -250,10 +250,34 @@ static void run8(const std::vector<uint8_t> &s, long long lead, const char *name
       if (e < 0) CHECK(got == cnt, "%s: keyed chunk %lld emits %d units, count %d", name, c, got, cnt);
       for (int i = 0; i < cnt && i < got; i++) kout[o + i] = kb[i];
     }
-    u8::Carry cy = u8::carry_of(m.word(p - 4));
+    // f1 for UTF-8: a warp with no >= F0 lead in its 1 KiB or the 3 bytes before decodes by
+    // units4_nof, which must give the same emit mask and units there
+    bool warp_nof = true;
+    for (long long cc = (c / 32) * 32; cc < (c / 32) * 32 + 32 && warp_nof; cc++) {
+      const long long pc = m.pos0(cc);
+      uint32_t wv[8], emx, fany = 0;
+      for (int k = 0; k < 8; k++) wv[k] = m.word(pc + 4 * k);
+      u8::analyze32(wv, m.word(pc - 4), m.word(pc + 32), false, &emx, &fany);
+      if (fany) warp_nof = false;
+    }
+    u8::Carry cy = u8::carry_of(m.word(p - 4)), cyn = cy;
     long long so = o;
     for (int k = 0; k < 8; k++) {
       uint32_t u01, u23;
+      if (warp_nof) {
+        uint32_t v01, v23;
+        const uint32_t emn = u8::units4_nof(m.word(p + 4 * k), cyn, &v01, &v23);
+        uint32_t w01, w23;
+        u8::Carry cc = cy;
+        const uint32_t emf = u8::units4(m.word(p + 4 * k), cc, &w01, &w23);
+        CHECK(emn == emf, "%s: units4_nof emit mask differs, chunk %lld word %d", name, c, k);
+        const uint32_t a[4] = {v01 & 0xFFFFu, v01 >> 16, v23 & 0xFFFFu, v23 >> 16};
+        const uint32_t b[4] = {w01 & 0xFFFFu, w01 >> 16, w23 & 0xFFFFu, w23 >> 16};
+        for (int j = 0; j < 4; j++)
+          if ((emf >> (8 * j)) & 1u)
+            CHECK(a[j] == b[j], "%s: units4_nof unit differs, chunk %lld word %d", name, c, k);
+        g_cases++;
+      }
       uint32_t em = u8::units4(m.word(p + 4 * k), cy, &u01, &u23);
       uint32_t ob = 0;
       for (int j = 0; j < 4; j++)
