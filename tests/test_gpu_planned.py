@@ -198,3 +198,20 @@ def test_planned_shards(G):
             got = np.concatenate([outs[k][0][: recl[k].count].cpu().numpy().view(np.uint16)
                                   for k in range(G)])
             assert np.array_equal(got, ref_o)
+
+
+@pytest.mark.parametrize("key", ["c2a", "c2b"])
+def test_planned_no_four_byte_text_with_errors(key):
+    """Text without 4-byte characters takes the no-F forward (f1 for UTF-8, chosen by the plan):
+    every error class that adds no >= F0 byte, at random places, and the truncated tail."""
+    x = synth.generate(key, size=(6 << 20) + 333)
+    assert not (x >= 0xF0).any()
+    check8(x, offset=7)
+    rng = np.random.default_rng(np.random.SeedSequence([0xF1, len(key)]))
+    for cls in synth.UTF8_ERROR_CLASSES:
+        b = x.copy()
+        p, _ = synth.inject_utf8_error(b, 0, b.size - 8, cls, rng)
+        r = check8(b)
+        assert (r.error, r.position) == (synth.UTF8_EXPECTED_KIND[cls], p)
+    check8(x[:-1])
+

@@ -15,6 +15,8 @@ code with it.  What it pins (D2-D5):
 * the end-position decoder `u8::units4` and its emit mask (equal to the classifier's) on
   random config-0 text, corrupted / truncated copies and byte soup at input alignments
   0 / 1 / 7 / 15: the staged units equal the oracle's output on [0, written);
+* `u8::units4_nof` (f1 for UTF-8): on every warp with no >= F0 lead in its 1 KiB or the 3 bytes
+  before, the same emit mask and units as `u8::units4`;
 * the f4 keyed 12-byte decoder (`keyed::decode_thread`, utf8_keyed.cuh, with the library's
   own tables) on the same chunks and on width-dense text (one width, or any subset of the
   four): its units, at the same per-thread slots, equal the oracle's on [0, written), and on
