@@ -1046,6 +1046,129 @@ __global__ void __launch_bounds__(VS_THREADS, VSCPS) k_validate_stream(const Til
   finish_call<Pol>(a, false, tid, warp, lane, &s_last);
 }
 
+// ---------------------------------------------------------------------------- K3, streaming
+// utf16le_validate / utf16be_validate as a register-streaming kernel (round 2, late; the
+// default, -DUG_VAL16_TMA restores the TMA-ring k_validate<U16Pol>).  The pairing rule
+// ("only the possible surrogate pairs require attention") needs no tile, no
+// ring and no inter-CTA order: a word i is in error iff it is a high surrogate not followed by
+// a low one or a low one not preceded by a high one, so on the whole window the hot check is
+//     H(i - 1) XOR L(i) == 0   for every word i in [0, n]
+// (word -1 / word n: the halo word, 0 outside [lo_valid, hi_valid)), which flags a lone low at
+// i and a lone high at i - 1 at position i.  A lane holds one 16-byte chunk per slot (8 words,
+// two byte-lane groups of 4 split by PRMT as in u16::classes4, ~11 ops per group); the
+// high-surrogate mask of word -1 comes from the lane before by one shuffle (lane 0: from lane
+// 31 of the slot before, or one scalar load for the first slot).  VU chunks per lane are in
+// flight (LDG.128 with the streaming hint).  A flagging warp rescans its lanes' words exactly
+// with u16::err_at from global memory (cold) and atomicMin's the first error; the last CTA
+// finalises as every validator does (a10).  Chunk c covers bytes [16c - lead, 16c - lead + 16)
+// of the window; the chunks cover [-lead, n + 2) so the word at n (a shard's halo, else 0)
+// settles a high surrogate at n - 1.
+#ifndef UG_V16_THREADS
+#define UG_V16_THREADS 512
+#endif
+#ifndef UG_V16_U
+#define UG_V16_U 4
+#endif
+constexpr int V16_THREADS = UG_V16_THREADS;
+constexpr int V16_U = UG_V16_U;  // chunks in flight per lane
+
+__device__ __forceinline__ long long v16_nchunks(const Window &w) {
+  return (w.n + 2 + w.lead + 15) / 16;
+}
+
+// Guarded 32-bit word of the window at byte position p (p even): bytes outside
+// [lo_valid, hi_valid) read as 0 (cold paths and edge chunks only).
+__device__ __forceinline__ uint32_t v16_rd16(const Window &w, long long p) {
+  return (p >= w.lo_valid && p + 2 <= w.hi_valid)
+             ? (uint32_t)*reinterpret_cast<const uint16_t *>(w.base + p)
+             : 0u;
+}
+
+template <bool BE>
+__global__ void __launch_bounds__(V16_THREADS) k_validate16(const TileArgs a) {
+  using Pol = U16PolT<BE>;
+  __shared__ int s_last;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const Window &win = a.win;
+  const long long nch = v16_nchunks(win);
+  const long long nw = win.n / 2;
+  constexpr int GW = 32 * V16_U;  // chunks per warp round
+  const long long nwarps = (long long)gridDim.x * (V16_THREADS / 32);
+  constexpr uint32_t SEL_HI = BE ? 0x6420u : 0x7531u;
+  for (long long g = (long long)blockIdx.x * (V16_THREADS / 32) + warp; g * GW < nch;
+       g += nwarps) {
+    const long long c0 = g * GW;
+    uint4 v[V16_U];
+    // interior round: every chunk of it inside the valid range
+    const bool in = (c0 * 16 - win.lead >= win.lo_valid) &&
+                    ((c0 + GW) * 16 - win.lead <= win.hi_valid);
+    if (in) {
+      const uint4 *gp = reinterpret_cast<const uint4 *>(win.base - win.lead) + c0 + lane;
+#pragma unroll
+      for (int j = 0; j < V16_U; j++) v[j] = __ldcs(gp + 32 * j);
+    } else {  // cold: the window's first / last rounds, word by word with guards
+#pragma unroll
+      for (int j = 0; j < V16_U; j++) {
+        const long long p0 = (c0 + 32 * j + lane) * 16 - win.lead;
+        uint32_t q[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++)
+          q[k] = v16_rd16(win, p0 + 4 * k) | (v16_rd16(win, p0 + 4 * k + 2) << 16);
+        v[j] = make_uint4(q[0], q[1], q[2], q[3]);
+      }
+    }
+    // H of the word before the round (lane 0 of slot 0 only; 0 outside the valid range)
+    uint32_t hcarry = 0;
+    if (lane == 0) {
+      const uint32_t u = Pol::native(v16_rd16(win, c0 * 16 - win.lead - 2));
+      hcarry = u16::is_high(u) ? 0x80000000u : 0u;
+    }
+    uint32_t flag = 0;
+#pragma unroll
+    for (int j = 0; j < V16_U; j++) {
+      const uint32_t his[2] = {prmt(v[j].x, v[j].y, SEL_HI), prmt(v[j].z, v[j].w, SEL_HI)};
+      uint32_t H[2], L[2];
+#pragma unroll
+      for (int h = 0; h < 2; h++) {
+        const uint32_t hi = his[h];
+        const uint32_t z = (hi & 0xF8F8F8F8u) ^ 0xD8D8D8D8u;  // 0 iff hi in D8..DF
+        const uint32_t S = ~(mad(z & 0x7F7F7F7Fu, 1u, 0x7F7F7F7Fu) | z) & HI;
+        const uint32_t b2 = hi << 5;  // bit 2 of hi: DC..DF
+        L[h] = S & b2;
+        H[h] = S & ~b2;
+      }
+      // bit 31 of the word before this chunk: the lane before (lane 0: lane 31 of the slot
+      // before, or the carry for slot 0)
+      uint32_t hp = __shfl_up_sync(FULL, H[1], 1);
+      if (lane == 0) hp = hcarry;
+      hcarry = __shfl_sync(FULL, H[1], 31);  // for lane 0 of the next slot
+      flag |= (fsl(hp, H[0], 8) ^ L[0]) | (fsl(H[0], H[1], 8) ^ L[1]);
+    }
+    if (__any_sync(FULL, flag != 0u)) {  // cold: exact rescan of this lane's flagged chunks
+      unsigned long long e = NONE;
+#pragma unroll 1
+      for (int j = 0; j < V16_U; j++) {
+        const long long p0 = (c0 + 32 * j + lane) * 16 - win.lead;  // bytes
+#pragma unroll 1
+        for (int k = -1; k < 8; k++) {
+          const long long q = p0 / 2 + k;  // word
+          if (q < 0 || q >= nw) continue;
+          const uint32_t pv = Pol::native(v16_rd16(win, 2 * q - 2));
+          const uint32_t u = Pol::native(v16_rd16(win, 2 * q));
+          const uint32_t nx = Pol::native(v16_rd16(win, 2 * q + 2));
+          if (u16::err_at(pv, u, nx)) {
+            if ((unsigned long long)q < e) e = (unsigned long long)q;
+            break;
+          }
+        }
+      }
+      if (e != NONE) atomicMin(&a.ctr->err_min, e);
+    }
+  }
+  __syncthreads();
+  finish_call<Pol>(a, false, tid, warp, lane, &s_last);
+}
+
 // ============================================================================ transcoders
 // K2 / K4.  NT data threads + one look-back warp (warp NT/32); several CTAs per SM.
 // Per tile the data warps take a ticket and bulk-load the tile (TMA), classify, block-scan,
@@ -2674,6 +2797,9 @@ size_t tile_smem_bytes(Op op) {
 #endif
     case Op::U16_VALIDATE:
     case Op::U16BE_VALIDATE:
+#if !defined(UG_VALIDATE_STREAM) && !defined(UG_VAL16_TMA)
+      if (op != Op::U8_VALIDATE) return 0;
+#endif
 #ifndef UG_VALIDATE_STREAM
       return VRING * INBUF;
 #else
@@ -2694,6 +2820,10 @@ size_t tile_smem_bytes(Op op) {
 
 int tile_threads(Op op) {
   switch (op) {
+#if !defined(UG_VALIDATE_STREAM) && !defined(UG_VAL16_TMA)
+    case Op::U16_VALIDATE:
+    case Op::U16BE_VALIDATE: return V16_THREADS;
+#endif
 #ifdef UG_VALIDATE_STREAM
     case Op::U8_VALIDATE:
     case Op::U16_VALIDATE:
@@ -2709,9 +2839,11 @@ int tile_threads(Op op) {
       return NT + 32 * NLB;
 #endif
 #ifndef UG_NO_VPRODUCER
-    case Op::U8_VALIDATE:
+    case Op::U8_VALIDATE: return VNT;
+#if !(!defined(UG_VALIDATE_STREAM) && !defined(UG_VAL16_TMA))
     case Op::U16_VALIDATE:
     case Op::U16BE_VALIDATE: return VNT;
+#endif
 #endif
     default: return NT;
   }
@@ -2738,13 +2870,20 @@ static void rev_launch(const TileArgs &a, int grid, int nt, size_t sm, cudaStrea
 #else
 #define UG_KVAL k_validate_stream
 #endif
+#if !defined(UG_VALIDATE_STREAM) && !defined(UG_VAL16_TMA)
+#define UG_V16_ON 1
+#define UG_KVAL16(BE) k_validate16<BE>
+#else
+#define UG_V16_ON 0
+#define UG_KVAL16(BE) UG_KVAL<U16PolT<BE>>
+#endif
 static const void *tile_fn(Op op) {
   switch (op) {
     case Op::U8_VALIDATE: return (const void *)UG_KVAL<U8Pol>;
     case Op::U8_TO_U16: return (const void *)k_transcode<U8Pol>;
-    case Op::U16_VALIDATE: return (const void *)UG_KVAL<U16Pol>;
+    case Op::U16_VALIDATE: return (const void *)UG_KVAL16(false);
     case Op::U16_TO_U8: return rev_fn<false>();
-    case Op::U16BE_VALIDATE: return (const void *)UG_KVAL<U16PolBE>;
+    case Op::U16BE_VALIDATE: return (const void *)UG_KVAL16(true);
     case Op::U8_TO_U16BE: return (const void *)k_transcode<U8PolBE>;
     case Op::U16BE_TO_U8: return rev_fn<true>();
   }
@@ -2754,6 +2893,12 @@ static const void *tile_fn(Op op) {
 // Work items of one launch over a window with `nbytes` owned bytes at address phase `lead`:
 // tiles (tile kernels) or 1 KiB warp chunks (streaming validators); and items per CTA.
 unsigned long long tile_units(Op op, long long nbytes, long long lead, int *per_cta) {
+#if UG_V16_ON
+  if (op == Op::U16_VALIDATE || op == Op::U16BE_VALIDATE) {  // 16-byte chunks, k_validate16
+    *per_cta = (V16_THREADS / 32) * 32 * V16_U;
+    return (unsigned long long)((nbytes + 2 + lead + 15) / 16);
+  }
+#endif
 #ifdef UG_VALIDATE_STREAM
   if (!op_transcodes(op)) {
     *per_cta = VS_THREADS / 32;
@@ -2779,10 +2924,10 @@ cudaError_t launch_tile(Op op, const TileArgs &a, int grid, cudaStream_t s) {
   int nt = tile_threads(op);
   switch (op) {
     case Op::U8_VALIDATE: UG_KVAL<U8Pol><<<grid, nt, sm, s>>>(a); break;
-    case Op::U16_VALIDATE: UG_KVAL<U16Pol><<<grid, nt, sm, s>>>(a); break;
+    case Op::U16_VALIDATE: UG_KVAL16(false)<<<grid, nt, sm, s>>>(a); break;
     case Op::U8_TO_U16: k_transcode<U8Pol><<<grid, nt, sm, s>>>(a); break;
     case Op::U16_TO_U8: rev_launch<false>(a, grid, nt, sm, s); break;
-    case Op::U16BE_VALIDATE: UG_KVAL<U16PolBE><<<grid, nt, sm, s>>>(a); break;
+    case Op::U16BE_VALIDATE: UG_KVAL16(true)<<<grid, nt, sm, s>>>(a); break;
     case Op::U8_TO_U16BE: k_transcode<U8PolBE><<<grid, nt, sm, s>>>(a); break;
     case Op::U16BE_TO_U8: rev_launch<true>(a, grid, nt, sm, s); break;
   }
