@@ -215,3 +215,28 @@ def test_planned_no_four_byte_text_with_errors(key):
         assert (r.error, r.position) == (synth.UTF8_EXPECTED_KIND[cls], p)
     check8(x[:-1])
 
+
+
+def test_planned_ascii_tiles_output_phases():
+    """All-ASCII tiles of the planned UTF-16 -> UTF-8 kernel (the warps' cooperative a2 path)
+    at every output phase: ASCII runs of several tiles after mixed prefixes of different
+    lengths, at three input address phases, with a mixed tail and an error after the run; an
+    all-ASCII input at capacities around a tile's output."""
+    rng = np.random.default_rng(2024)
+    mixed = oracle.utf8_to_utf16le(
+        np.frombuffer(synth.gen_chunk("mixed", "utf8", 4096, 5, 4096), dtype=np.uint8))[1]
+    mixed = mixed[: np.nonzero((mixed & 0xFC00) != 0xDC00)[0][-1]]  # not ending inside a pair
+    for pre in range(0, 8):
+        run = rng.integers(0x20, 0x7F, 5 * TILE // 2 + int(rng.integers(0, 300))).astype(np.uint16)
+        cut = int(np.nonzero((mixed[: 40 + pre] & 0xFC00) != 0xDC00)[0][-1])  # whole chars
+        u = np.concatenate([mixed[:cut], run, mixed[:777]]).astype(np.uint16)
+        for off in (0, 1, 7):
+            check16(u, offset=off)
+        v = u.copy()
+        v[cut + run.size + 3] = 0xDC00  # a lone low after the run
+        check16(v, offset=1)
+    # all ASCII, every capacity edge around a tile's output
+    a = rng.integers(0, 0x80, 4 * TILE).astype(np.uint16)
+    check16(a)
+    for cap in (TILE // 2 - 1, TILE // 2, TILE // 2 + 3, 3 * TILE // 2 + 1):
+        check16(a, cap=cap)

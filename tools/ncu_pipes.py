@@ -1,17 +1,22 @@
 """Executed SASS instructions of one kernel in an ncu report, grouped by opcode and by pipe.
-usage: ncu_pipes.py report.ncu-rep section_index input_bytes"""
+usage: ncu_pipes.py report.ncu-rep section_index|kernel_regex input_bytes
+(the source page lists each kernel more than once: prefer a kernel-name regex)"""
 import collections, csv, io, re, subprocess, sys
-rep, sidx, nbytes = sys.argv[1], int(sys.argv[2]), float(sys.argv[3])
+rep, sel, nbytes = sys.argv[1], sys.argv[2], float(sys.argv[3])
 txt = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
                      capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(txt)))
-secs, cur = [], None
+secs, names, cur = [], [], None
 for r in rows:
     if r and r[0] == "Kernel Name":
-        cur = []; secs.append(cur)
+        cur = []; secs.append(cur); names.append(r[1] if len(r) > 1 else "")
     elif cur is not None:
         cur.append(r)
-sec = secs[sidx]; h = sec[0]; ix = {k: i for i, k in enumerate(h)}
+if sel.isdigit():
+    sec = secs[int(sel)]
+else:
+    sec = secs[next(i for i, nm in enumerate(names) if re.search(sel, nm))]
+h = sec[0]; ix = {k: i for i, k in enumerate(h)}
 ops = collections.Counter()
 for r in sec[1:]:
     if len(r) != len(h): continue

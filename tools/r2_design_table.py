@@ -14,6 +14,12 @@ i = s.index("**Round 2 (driver-comparable bench line, `profiles/")
 j = s.index("What moved between r2b and")
 
 
+def step(kern):
+    # the transcoders as timed inside the bench step (the launches the roofline line uses)
+    k = b["roofline"]["kernels"][kern]
+    return f"{k['avg_launch_ms']:.2f} ms ({k['frac']:.3f}, in the step)"
+
+
 def f(op):
     return f"{po[op]['ms']:.2f} ms ({po[op]['frac_of_peak']:.3f})"
 
@@ -25,8 +31,8 @@ one B200, clocks 1965 MHz, no throttle reasons; interim builds `profiles/r2a_*`,
 |---|---|---|---|---|
 | bench value (input GB/s of both transcoding passes) | 827.5 | 855.2 | **{b['value']:.1f}** | {c['value']:.1f} |
 | ms per step | 24.01 | 23.23 | {b['ms_per_step']:.2f} | {c['ms_per_step']:.2f} |
-| forward transcoder (8 GiB) | 10.07 ms (0.306) | 9.17 ms (0.336) | {f('utf8_to_utf16le_planned')} | {f('utf8_to_utf16le')} |
-| reverse transcoder (11.3 GB UTF-16) | 10.85 ms (0.284) | 10.62 ms (0.290) | {f('utf16le_to_utf8_planned')} | {f('utf16le_to_utf8')} |
+| forward transcoder (8 GiB) | 10.07 ms (0.306) | 9.17 ms (0.336) | {step('k_transcode_planned<U8Pol>')} | {f('utf8_to_utf16le')} |
+| reverse transcoder (11.3 GB UTF-16) | 10.85 ms (0.284) | 10.62 ms (0.290) | {step('k_transcode_planned<U16Pol>')} | {f('utf16le_to_utf8')} |
 | sizing pass, UTF-8 (len16 / + plan) | 1.31 ms | 1.85 ms (plan) | **{po['plan_utf8 (len16 + plan)']['ms']:.2f} ms (plan)** | {po['utf16_length_from_utf8']['ms']:.2f} ms |
 | sizing pass, UTF-16 (len8 / + plan) | 1.57 ms | 1.65 ms (plan) | {po['plan_utf16le (len8 + plan)']['ms']:.2f} ms (plan) | {po['utf8_length_from_utf16le']['ms']:.2f} ms |
 | utf8_validate / utf16le_validate | 0.49 / 0.72 | 0.47 / 0.71 | {po['utf8_validate']['frac_of_peak']:.2f} / {po['utf16le_validate']['frac_of_peak']:.2f} | — |

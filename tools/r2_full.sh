@@ -11,6 +11,8 @@ timeout -s KILL 600 python bench.py --impl reference > gpurun_out/bench_ref_$TAG
 timeout -s KILL 900 python bench.py --path chained --no-e2e --no-cpu-baseline --no-per-config > gpurun_out/bench_chained_$TAG.log 2>&1; echo "chained=$?"
 CMD="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --no-per-op --no-per-config"
 timeout -s KILL 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_" -c 40 --csv --log-file gpurun_out/launches_$TAG.csv $CMD > gpurun_out/ncu_launch_$TAG.log 2>&1; echo "launches=$?"
-timeout -s KILL 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,smsp__inst_executed.sum --clock-control none -k regex:k_transcode_planned -c 2 --csv --log-file gpurun_out/traffic8g_$TAG.csv $CMD > gpurun_out/ncu_traffic_$TAG.log 2>&1; echo "traffic=$?"
-OPS=pfwd,prev timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:k_transcode_planned -c 2 -o gpurun_out/full_$TAG python tools/ncu_one.py c4 1024 > gpurun_out/ncu_full_$TAG.log 2>&1; echo "full=$?"
+timeout -s KILL 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,smsp__inst_executed.sum --clock-control none --kernel-name-base mangled -k regex:'k_transcode_plannedINS_(6U8PolTILb0EEELb0|7U16PolTILb0)' -c 2 --csv --log-file gpurun_out/traffic8g_$TAG.csv $CMD > gpurun_out/ncu_traffic_$TAG.log 2>&1; echo "traffic=$?"
+# (mangled names: the forward's running form on config 4 - NOF = false, the input has >= F0
+# bytes; its other form returns at once - and the reverse)
+OPS=pfwd,prev timeout -s KILL 900 ncu --set full --clock-control none --import-source on --kernel-name-base mangled -k regex:'k_transcode_plannedINS_(6U8PolTILb0EEELb0|7U16PolTILb0)' -c 2 -o gpurun_out/full_$TAG python tools/ncu_one.py c4 1024 > gpurun_out/ncu_full_$TAG.log 2>&1; echo "full=$?"
 cp paper_2111_08692_b200/libunigpu.so gpurun_out/lib_$TAG.so

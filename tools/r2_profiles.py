@@ -99,8 +99,8 @@ shutil.copy(f"{G}/traffic8g_{tag}.csv", f"{P}/{tag}_ncu_traffic.txt")
 rep = f"{G}/full_{tag}.ncu-rep"
 lib = f"{G}/lib_{tag}.so"
 summ = run("tools/ncu_summary.py", rep, "20")
-pipes_f = run("tools/ncu_pipes.py", rep, "0", "1073741824")
-pipes_r = run("tools/ncu_pipes.py", rep, "1", "1409338390")
+pipes_f = run("tools/ncu_pipes.py", rep, "planned<ug::U8PolT", "1073741824")
+pipes_r = run("tools/ncu_pipes.py", rep, "planned<ug::U16PolT", "1409338390")
 lines_f = run("tools/sass_lines.py", rep, "planned<ug::U8PolT", lib, "1073741824", "30",
               env={"STALLS": "25"})
 lines_r = run("tools/sass_lines.py", rep, "planned<ug::U16PolT", lib, "1409338390", "30",
