@@ -2445,6 +2445,12 @@ __global__ void __launch_bounds__(NTP, PlannedGeo<Pol>::MINB)
   if constexpr (Pol::kNoF) {
     if ((!bad && plan[8] == 0) != NOF) return;
   }
+#ifndef UG_NO_NARROW16
+  // a window of ASCII words only is k_narrow16's (launched after this kernel)
+  if constexpr (Pol::UNIT == 2) {
+    if (!bad && plan[5] == (unsigned long long)(win.n / 2)) return;
+  }
+#endif
   const long long nsub = bad ? 0 : (long long)plan[3], tps = bad ? 1 : (long long)plan[4];
   if (bad && tid == 0 && blockIdx.x == 0) atomicOr(&a.ctr->flags, 1ull);
   // producer (lane 0 of the last warp, not the shipping warp 0): tiles in sub-range order,
@@ -2732,6 +2738,73 @@ __global__ void __launch_bounds__(NTP, PlannedGeo<Pol>::MINB)
   finish_call<Pol, TILEP>(a, true, tid, warp, lane, &s_last);
 }
 
+
+// a2 for a whole window of ASCII words (planned UTF-16 -> UTF-8, round 2 late; -DUG_NO_NARROW16
+// builds without).  The plan's total (header word 5, the width sum of the owned words) equals
+// the word count iff every word is below 0x80 (every width is >= 1): such a window has no
+// error and its output is the low byte of every word, so it needs
+// neither tiles nor offsets: a grid-stride narrowing copy, 8 output bytes per item (one
+// LDG.128 of 8 words -> two PRMT -> one 8-byte store when the input is 16-byte aligned at the
+// output's 8-byte phase, 2-byte loads otherwise), four items per thread in flight, head / tail
+// bytes by block 0.  The result / record is written up front (it does not depend on the
+// data); the planned kernel launched with it returns at once on the same test.
+constexpr int N16_THREADS = 512;
+template <bool BE>
+__global__ void __launch_bounds__(N16_THREADS, 4) k_narrow16(const TileArgs a,
+                                                          const unsigned long long *plan) {
+  const Window &win = a.win;
+  const long long nw = win.n / 2;
+  const bool bad = plan[0] != PLAN_TAG || plan[1] != (unsigned long long)(uintptr_t)win.base ||
+                   plan[2] != (unsigned long long)win.n ||
+                   plan[6] != (unsigned long long)win.lead || plan[7] != plan_halos(win);
+  if (bad || plan[5] != (unsigned long long)nw) return;
+  const unsigned long long total = (unsigned long long)nw;
+  const unsigned long long m = total < a.out_cap ? total : a.out_cap;  // bytes written
+  const int tid = threadIdx.x;
+  if (blockIdx.x == 0 && tid == 0) write_outcome(a, true, 0, NONE, total, 0, total);
+  constexpr uint32_t SEL = BE ? 0x7531u : 0x6420u;
+  constexpr int LB = BE ? 1 : 0;  // the low byte's offset in a stored word
+  const uint8_t *in = win.base;
+  uint8_t *out = reinterpret_cast<uint8_t *>(a.out);
+  unsigned long long h = (8u - ((uintptr_t)out & 7u)) & 7u;  // out + h is 8-byte aligned
+  if (h > m) h = m;
+  const unsigned long long nb = (m - h) / 8, tl = h + 8 * nb;
+  const bool fast = (((uintptr_t)(in + 2 * h)) & 15u) == 0;
+  const unsigned long long stride = (unsigned long long)gridDim.x * N16_THREADS;
+  unsigned long long i = (unsigned long long)blockIdx.x * N16_THREADS + tid;
+  if (fast) {
+    const uint4 *src = reinterpret_cast<const uint4 *>(in + 2 * h);
+    uint2 *dst = reinterpret_cast<uint2 *>(out + h);
+    for (; i + 3 * stride < nb; i += 4 * stride) {
+      uint4 q[4];
+#pragma unroll
+      for (int j = 0; j < 4; j++) q[j] = __ldcs(src + i + j * stride);
+#pragma unroll
+      for (int j = 0; j < 4; j++)
+        __stcs(dst + i + j * stride, make_uint2(prmt(q[j].x, q[j].y, SEL), prmt(q[j].z, q[j].w, SEL)));
+    }
+    for (; i < nb; i += stride) {
+      const uint4 q = __ldcs(src + i);
+      __stcs(dst + i, make_uint2(prmt(q.x, q.y, SEL), prmt(q.z, q.w, SEL)));
+    }
+  } else {  // (unaligned phases: correctness, not speed)
+    for (; i < nb; i += stride) {
+      const uint8_t *s = in + 2 * (h + 8 * i) + LB;
+      uint32_t lo = 0, hi = 0;
+#pragma unroll
+      for (int j = 0; j < 4; j++) {
+        lo |= (uint32_t)s[2 * j] << (8 * j);
+        hi |= (uint32_t)s[8 + 2 * j] << (8 * j);
+      }
+      *reinterpret_cast<uint2 *>(out + h + 8 * i) = make_uint2(lo, hi);
+    }
+  }
+  if (blockIdx.x == 0) {
+    if ((unsigned long long)tid < h) out[tid] = in[2 * tid + LB];
+    if ((unsigned long long)tid < m - tl) out[tl + tid] = in[2 * (tl + tid) + LB];
+  }
+}
+
 // ============================================================================ combine
 __host__ __device__ inline void combine_impl(const RecordDev *recs, int nranks, int rank,
                                              unsigned long long total_in, ResultDev *res,
@@ -3001,8 +3074,20 @@ cudaError_t launch_planned(Op op, const TileArgs &a, const unsigned long long *p
       k_transcode_planned<U8PolBE><<<grid, NTP, sm, s>>>(a, plan);
       k_transcode_planned<U8PolBE, true><<<grid, NTP, sm, s>>>(a, plan);
       break;
-    case Op::U16_TO_U8: k_transcode_planned<U16Pol><<<grid, NTP, sm, s>>>(a, plan); break;
-    case Op::U16BE_TO_U8: k_transcode_planned<U16PolBE><<<grid, NTP, sm, s>>>(a, plan); break;
+    // UTF-16 input: the tile kernel, then the all-ASCII narrowing copy; the plan's total
+    // selects the one that works
+    case Op::U16_TO_U8:
+      k_transcode_planned<U16Pol><<<grid, NTP, sm, s>>>(a, plan);
+#ifndef UG_NO_NARROW16
+      k_narrow16<false><<<grid, N16_THREADS, 0, s>>>(a, plan);
+#endif
+      break;
+    case Op::U16BE_TO_U8:
+      k_transcode_planned<U16PolBE><<<grid, NTP, sm, s>>>(a, plan);
+#ifndef UG_NO_NARROW16
+      k_narrow16<true><<<grid, N16_THREADS, 0, s>>>(a, plan);
+#endif
+      break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();

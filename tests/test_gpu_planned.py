@@ -240,3 +240,66 @@ def test_planned_ascii_tiles_output_phases():
     check16(a)
     for cap in (TILE // 2 - 1, TILE // 2, TILE // 2 + 3, 3 * TILE // 2 + 1):
         check16(a, cap=cap)
+
+
+@pytest.mark.parametrize("n", [1, 7, 8, 9, 100, 4097, 3 * TILE + 5, (1 << 20) + 3])
+def test_planned_all_ascii_narrowing(n):
+    """A window of ASCII words only is the narrowing copy's (k_narrow16, selected by the plan's
+    total = word count): every input and output address phase, capacities below the need, and
+    an input with one non-ASCII word (back on the tile kernel)."""
+    rng = np.random.default_rng(n)
+    u = rng.integers(0, 0x80, n).astype(np.uint16)
+    ref_r, ref_o = oracle.utf16le_to_utf8(u)
+    for off in (0, 1, 3, 7):
+        _, t = to_dev(u, pad_before=off, pad_after=32)
+        for oo in (0, 1, 5, 8):
+            big = torch.full((n + oo + 64,), 0x5A, dtype=torch.uint8, device=DEV)
+            r, ln = ug.utf16le_to_utf8_two_pass(t, big[oo:oo + n], n=n, out_cap=n)
+            o = big.cpu().numpy()
+            assert tuple(r) == tuple(ref_r) and ln == n
+            assert np.array_equal(o[oo:oo + n], ref_o)
+            assert np.all(o[:oo] == 0x5A) and np.all(o[oo + n:] == 0x5A)
+    for cap in (0, n - 1, n // 2):
+        if cap < 0:
+            continue
+        check16(u, cap=cap)
+    v = u.copy()
+    v[n // 2] = 0x00E9
+    check16(v, offset=1)
+    v[n // 2] = 0xDC00
+    check16(v)
+
+
+def test_planned_shards_ascii_and_mixed():
+    """Shards of one buffer through the planned shard form, some all ASCII (narrowing copy),
+    some mixed (tile kernel), records combined on the device: equal to the unsharded oracle."""
+    rng = np.random.default_rng(99)
+    a = rng.integers(0x20, 0x7F, 300000).astype(np.uint16)
+    mixed = oracle.utf8_to_utf16le(
+        np.frombuffer(synth.gen_chunk("mixed", "utf8", 60000, 3, 60000), dtype=np.uint8))[1]
+    mixed = mixed[: np.nonzero((mixed & 0xFC00) != 0xDC00)[0][-1]]
+    u = np.concatenate([a, mixed, a[:123457]]).astype(np.uint16)
+    n = u.size
+    cuts = [0, 150001, 300000, 300000 + mixed.size, 300000 + mixed.size + 60000, n]
+    _, t = to_dev(u)
+    G = len(cuts) - 1
+    recs = ug.record_buffer(DEV, G)
+    outs = []
+    for k in range(G):
+        lo, hi = cuts[k], cuts[k + 1]
+        out = torch.zeros(3 * (hi - lo), dtype=torch.uint8, device=DEV)
+        plan = ug.plan_buffer(DEV)
+        lens = torch.zeros(1, dtype=torch.int64, device=DEV)
+        ug.utf16le_shard_plan_async(t, lo, hi - lo, min(lo, 1), min(n - hi, 1), lens, plan)
+        ug.utf16le_to_utf8_shard_planned_async(t, lo, hi - lo, min(lo, 1), min(n - hi, 1), lo,
+                                               plan, out, recs, rec_off=k * ug.RECORD_BYTES)
+        outs.append(out)
+    res = ug.result_buffer(DEV, 1)
+    ug.combine_records_async(recs, G, 0, n, res)
+    torch.cuda.synchronize()
+    (r,) = ug.decode_results(res)
+    ref_r, ref_o = oracle.utf16le_to_utf8(u)
+    assert tuple(r) == tuple(ref_r)
+    records = ug.decode_records(recs)
+    got = np.concatenate([outs[k][: records[k].count].cpu().numpy() for k in range(G)])
+    assert np.array_equal(got, ref_o)
