@@ -322,7 +322,7 @@ int enqueue_planned(Op op, const void *in, unsigned long long n, unsigned long l
              cudaSuccess) {
     return UG_ERR_CUDA;
   }
-  g_launches.fetch_add(1);
+  g_launches.fetch_add(keyed ? 1 : planned_kernels(op));
   return UG_OK;
 }
 

@@ -75,6 +75,7 @@ cudaError_t keyed_upload();  // tables to the current device + kernel attributes
 cudaError_t keyed_occupancy(int *blocks_per_sm);
 cudaError_t launch_planned_keyed(const TileArgs &a, const unsigned long long *plan, int grid,
                                  cudaStream_t s);
+int planned_kernels(Op op);
 cudaError_t launch_planned(Op op, const TileArgs &a, const unsigned long long *plan, int grid,
                            cudaStream_t s);
 cudaError_t launch_plan(bool u16in, bool be, const Window &w, unsigned long long ntiles,

@@ -3061,6 +3061,15 @@ cudaError_t planned_occupancy(Op op, int *blocks_per_sm) {
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(
       blocks_per_sm, planned_fn(op), NTP, planned_smem_bytes(op_u16_input(op)));
 }
+// kernels one launch_planned enqueues (the two forward forms; the reverse's tile kernel and
+// narrowing copy): what the launch counter adds
+int planned_kernels(Op op) {
+#ifdef UG_NO_NARROW16
+  if (op_u16_input(op)) return 1;
+#endif
+  (void)op;
+  return 2;
+}
 cudaError_t launch_planned(Op op, const TileArgs &a, const unsigned long long *plan, int grid,
                            cudaStream_t s) {
   const size_t sm = planned_smem_bytes(op_u16_input(op));
