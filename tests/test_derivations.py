@@ -158,3 +158,40 @@ def test_utf16_pairing_predicate():
                     or (L(t[i]) and not (i >= 1 and H(t[i - 1])))]
             r = oracle.utf16le_validate(np.array(t, dtype=np.uint16))
             assert (errs[0] if errs else -1) == (r.position if r.error else -1), t
+
+
+def test_utf16_xor_pairing_form():
+    """The streaming validator's form (kernels.cu k_validate16): with H(-1) = L(n) = 0, a
+    string is valid iff H(u_{i-1}) == L(u_i) for every i in [0, n]; the first i where they
+    differ, f, lies at e or e + 1 for the first error e (a lone low flags at itself, a lone high
+    at the next word), so rescanning words f - 1 .. f finds e.  Against the oracle on all
+    strings of length <= 6 over 6 words (every neighbour combination of the two classes)."""
+    words = [0x0041, 0xD800, 0xDBFF, 0xDC00, 0xDFFF, 0xE000]
+    H = lambda w: 0xD800 <= w <= 0xDBFF  # noqa: E731
+    L = lambda w: 0xDC00 <= w <= 0xDFFF  # noqa: E731
+    for n in range(7):
+        for t in itertools.product(words, repeat=n):
+            hp = [False] + [H(w) for w in t]          # H(u_{i-1}), i = 0 .. n
+            lw = [L(w) for w in t] + [False]          # L(u_i),     i = 0 .. n
+            flags = [i for i in range(n + 1) if hp[i] != lw[i]]
+            r = oracle.utf16le_validate(np.array(t, dtype=np.uint16))
+            assert bool(flags) == bool(r.error), t
+            if flags:
+                assert r.position in (flags[0], flags[0] - 1), (t, flags, r)
+
+
+def test_utf16_ascii_window_iff_width_sum_equals_count():
+    """k_narrow16's selection (kernels.cu): the UTF-8 width sum of a UTF-16 window equals its
+    word count iff every word is below 0x80 (every width is >= 1; a surrogate counts 2, so no
+    invalid window qualifies) -- on every single word and on random mixes, against the oracle's
+    utf8_length_from_utf16le."""
+    for w in range(0x10000):
+        u = np.array([w], dtype=np.uint16)
+        assert (oracle.utf8_length_from_utf16le(u) == 1) == (w < 0x80), hex(w)
+    rng = np.random.default_rng(5)
+    for _ in range(2000):
+        n = int(rng.integers(1, 40))
+        u = rng.integers(0, 0x80, n).astype(np.uint16)
+        if rng.integers(0, 2):
+            u[int(rng.integers(0, n))] = int(rng.integers(0x80, 0x10000))
+        assert (oracle.utf8_length_from_utf16le(u) == n) == bool(np.all(u < 0x80))
