@@ -2911,7 +2911,7 @@ int tile_threads(Op op) {
 #else
       return NT + 32 * NLB;
 #endif
-#ifndef UG_NO_VPRODUCER
+#if !defined(UG_NO_VPRODUCER) && !defined(UG_VALIDATE_STREAM)
     case Op::U8_VALIDATE: return VNT;
 #if !(!defined(UG_VALIDATE_STREAM) && !defined(UG_VAL16_TMA))
     case Op::U16_VALIDATE:
