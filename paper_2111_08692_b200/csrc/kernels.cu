@@ -805,14 +805,33 @@ static_assert(VAHEAD >= 1 && VAHEAD <= VRING - 1, "validator ring");
 // UTF-8 2 (48 registers; 3 CTAs force 32 registers and spills: +0..5 %), UTF-16 3 (32).
 // Measured against the round-1 form (1 GiB c4 / c1 / c3): utf8_validate -3.4 / -4.2 / -2.8 %,
 // utf16le_validate -3.8 / +6.2 / -6.4 % (c2a -6.1 %).
+// Round 2 late: the UTF-8 validator's compute threads take VH chunks of 32 bytes per tile each
+// (chunk h of thread tid = tile bytes [h * TILE / VH + 32 tid, ... + 32)), so the per-tile glue
+// (slot wait, tile position and edge test, loop, release) is paid once per VH chunks; VH = 2:
+// 256 compute threads + the producer warp, 4 CTAs per SM.  Measured against one chunk per
+// thread (1 GiB / BASELINE sizes, gpurun_out/vh_ab.log): c4 -5.9 %, c3 -5.6 %, c2a / c2b
+// -0.2 %, c1 +4.9 % (ASCII, at 1.0 of the copy peak either way); four chunks +1..17 %.
+#ifndef UG_VHALVES
+#define UG_VHALVES 2
+#endif
+template <class Pol>
+struct VGeo {
+  static constexpr int VH = Pol::UNIT == 1 ? UG_VHALVES : 1;  // chunks per thread per tile
+  static constexpr int VC = NT / VH;                           // compute threads
+  static constexpr int THREADS = VC + 32;
+  static constexpr int MINB = Pol::UNIT == 1 ? (VH > 1 ? 4 : 2) : 3;
+};
 constexpr int VNT = NT + 32;
 #ifndef UG_VRING8
-#define UG_VRING8 VRING
+#define UG_VRING8 3
 #endif
-constexpr int VRING8 = UG_VRING8;  // the UTF-8 validator's ring (2 CTAs per SM: room for more)
+// the UTF-8 validator's ring: 3 slots (4 CTAs per SM at 49 KiB) measured against 4 (3 CTAs) with
+// two chunks per thread: c4 -2.9 %, c3 -1.2 %, c1 -0.7 %
+constexpr int VRING8 = UG_VRING8;
 template <class Pol>
-__global__ void __launch_bounds__(VNT, Pol::UNIT == 1 ? 2 : 3) k_validate(const TileArgs a) {
+__global__ void __launch_bounds__(VGeo<Pol>::THREADS, VGeo<Pol>::MINB) k_validate(const TileArgs a) {
   constexpr int VRING = Pol::UNIT == 1 ? VRING8 : ::ug::VRING;
+  constexpr int VH = VGeo<Pol>::VH, VC = VGeo<Pol>::VC;
   extern __shared__ __align__(128) uint8_t smem[];
   __shared__ uint64_t mb_full[VRING], mb_empty[VRING];
   __shared__ int s_last;
@@ -825,12 +844,12 @@ __global__ void __launch_bounds__(VNT, Pol::UNIT == 1 ? 2 : 3) k_validate(const 
 #pragma unroll
     for (int j = 0; j < VRING; j++) {
       mbar_init(&mb_full[j], 1);
-      mbar_init(&mb_empty[j], NT / 32);
+      mbar_init(&mb_empty[j], VC / 32);
     }
     fence_mbar_init();
   }
   __syncthreads();
-  if (warp == NT / 32) {  // producer
+  if (warp == VC / 32) {  // producer
     if (lane == 0) {
       int k = 0;
       for (long long t = blockIdx.x; t < ntiles; t += G, k++) {
@@ -847,25 +866,32 @@ __global__ void __launch_bounds__(VNT, Pol::UNIT == 1 ? 2 : 3) k_validate(const 
       uint8_t *buf = smem + sl * INBUF;
       mbar_wait(&mb_full[sl], (k / VRING) & 1);
       if (tile_at_edge(win, t)) {  // tile-uniform
-        named_sync<BAR_DATA, NT>();
-        fix_tile_edges(win, t, buf, NT);
-        named_sync<BAR_DATA, NT>();
+        named_sync<BAR_DATA, VC>();
+        fix_tile_edges(win, t, buf, VC);
+        named_sync<BAR_DATA, VC>();
       }
-      typename Pol::St st;
-      const long long tp = tile_pos(win, t);
-      if (tp >= 0 && tp + TILE <= win.n) {
-        Pol::template load<true>(st, buf, tid, lane, tp, win.n);
-        Pol::template analyze<true>(st, tid, false);
-      } else {
-        Pol::template load<false>(st, buf, tid, lane, tp, win.n);
-        Pol::template analyze<false>(st, tid, false);
+      const long long tp0 = tile_pos(win, t);
+      unsigned long long e = NONE;
+#pragma unroll
+      for (int h = 0; h < VH; h++) {
+        typename Pol::St st;
+        const long long tp = tp0 + (long long)h * (TILE / VH);
+        uint8_t *hb = buf + h * (TILE / VH);
+        if (tp >= 0 && tp + TILE / VH <= win.n) {
+          Pol::template load<true>(st, hb, tid, lane, tp, win.n);
+          Pol::template analyze<true>(st, tid, false);
+        } else {
+          Pol::template load<false>(st, hb, tid, lane, tp, win.n);
+          Pol::template analyze<false>(st, tid, false);
+        }
+        if (__any_sync(FULL, Pol::hint(st))) {  // a4 (cold)
+          const unsigned long long f = Pol::find_error(st, n_units);
+          if (f < e) e = f;
+        }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&mb_empty[sl]);
-      if (__any_sync(FULL, Pol::hint(st))) {  // a4 (cold)
-        const unsigned long long e = Pol::find_error(st, n_units);
-        if (e != NONE) atomicMin(&a.ctr->err_min, e);
-      }
+      if (e != NONE) atomicMin(&a.ctr->err_min, e);
     }
   }
   __syncthreads();
@@ -2912,7 +2938,7 @@ int tile_threads(Op op) {
       return NT + 32 * NLB;
 #endif
 #if !defined(UG_NO_VPRODUCER) && !defined(UG_VALIDATE_STREAM)
-    case Op::U8_VALIDATE: return VNT;
+    case Op::U8_VALIDATE: return VGeo<U8Pol>::THREADS;
 #if !(!defined(UG_VALIDATE_STREAM) && !defined(UG_VAL16_TMA))
     case Op::U16_VALIDATE:
     case Op::U16BE_VALIDATE: return VNT;
