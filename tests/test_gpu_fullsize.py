@@ -167,6 +167,19 @@ def test_config4_full_size_bench_launch(c4_ref):
     assert ug.utf8_length_from_utf16le(out16[:n16]) == n
     # the plain API agrees
     assert tuple(ug.utf8_to_utf16le(t, out16)) == (0, n, n16)
+    # the streaming UTF-16 validator at the bench size (11.3 GB, word indices past 2^32 bytes),
+    # clean and with a high surrogate followed by 'A' planted late in the buffer
+    u = out16[:n16]
+    assert tuple(ug.utf16le_validate(u)) == (0, n16, 0)
+    for p in ((5 << 30) + 7, n16 - 1):
+        keep = u[p - 2:p + 1].clone()
+        prev2 = int(keep[0].item()) & 0xFFFF
+        u[p - 1] = -0x2800  # 0xD800
+        u[p] = 0x41
+        want = p - 2 if (prev2 & 0xFC00) == 0xD800 else p - 1
+        assert tuple(ug.utf16le_validate(u)) == (ug.SURROGATE, want, 0), p
+        u[p - 2:p + 1] = keep
+    assert tuple(ug.utf16le_validate(u)) == (0, n16, 0)
 
 
 def shard_cuts_utf8(host: np.ndarray, G: int):
