@@ -2478,6 +2478,11 @@ __global__ void __launch_bounds__(NTP, PlannedGeo<Pol>::MINB)
   }
 #endif
   const long long nsub = bad ? 0 : (long long)plan[3], tps = bad ? 1 : (long long)plan[4];
+#ifndef UG_NO_PDL
+  // the paired launch (the other forward form / the narrowing copy) only reads the plan, written
+  // before this kernel: let it launch now (programmatic dependent launch)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
   if (bad && tid == 0 && blockIdx.x == 0) atomicOr(&a.ctr->flags, 1ull);
   // producer (lane 0 of the last warp, not the shipping warp 0): tiles in sub-range order,
   // sub-ranges by ticket; the next ticket is drawn as a sub-range starts, so its L2 round trip
@@ -3087,6 +3092,27 @@ cudaError_t planned_occupancy(Op op, int *blocks_per_sm) {
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(
       blocks_per_sm, planned_fn(op), NTP, planned_smem_bytes(op_u16_input(op)));
 }
+#ifndef UG_NO_PDL
+// The second kernel of a planned pair, launched with programmatic stream serialization: it may
+// start before the first completes (it reads only the plan, which both wait for in stream
+// order; exactly one of the two does the work).  The next launch in the stream still waits for
+// both.
+template <class... Args>
+static cudaError_t launch_paired(void (*fn)(Args...), int grid, int threads, size_t sm,
+                                 cudaStream_t s, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(threads);
+  cfg.dynamicSmemBytes = sm;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, fn, args...);
+}
+#endif
 // kernels one launch_planned enqueues (the two forward forms; the reverse's tile kernel and
 // narrowing copy): what the launch counter adds
 int planned_kernels(Op op) {
@@ -3103,24 +3129,40 @@ cudaError_t launch_planned(Op op, const TileArgs &a, const unsigned long long *p
     // both forward forms are launched; the plan's header selects the one that works
     case Op::U8_TO_U16:
       k_transcode_planned<U8Pol><<<grid, NTP, sm, s>>>(a, plan);
+#ifndef UG_NO_PDL
+      launch_paired(k_transcode_planned<U8Pol, true>, grid, NTP, sm, s, a, plan);
+#else
       k_transcode_planned<U8Pol, true><<<grid, NTP, sm, s>>>(a, plan);
+#endif
       break;
     case Op::U8_TO_U16BE:
       k_transcode_planned<U8PolBE><<<grid, NTP, sm, s>>>(a, plan);
+#ifndef UG_NO_PDL
+      launch_paired(k_transcode_planned<U8PolBE, true>, grid, NTP, sm, s, a, plan);
+#else
       k_transcode_planned<U8PolBE, true><<<grid, NTP, sm, s>>>(a, plan);
+#endif
       break;
     // UTF-16 input: the tile kernel, then the all-ASCII narrowing copy; the plan's total
     // selects the one that works
     case Op::U16_TO_U8:
       k_transcode_planned<U16Pol><<<grid, NTP, sm, s>>>(a, plan);
 #ifndef UG_NO_NARROW16
+#ifndef UG_NO_PDL
+      launch_paired(k_narrow16<false>, grid, N16_THREADS, 0, s, a, plan);
+#else
       k_narrow16<false><<<grid, N16_THREADS, 0, s>>>(a, plan);
+#endif
 #endif
       break;
     case Op::U16BE_TO_U8:
       k_transcode_planned<U16PolBE><<<grid, NTP, sm, s>>>(a, plan);
 #ifndef UG_NO_NARROW16
+#ifndef UG_NO_PDL
+      launch_paired(k_narrow16<true>, grid, N16_THREADS, 0, s, a, plan);
+#else
       k_narrow16<true><<<grid, N16_THREADS, 0, s>>>(a, plan);
+#endif
 #endif
       break;
     default: return cudaErrorInvalidValue;
