@@ -2013,19 +2013,21 @@ __device__ __forceinline__ unsigned long long plan_halos(const Window &w) {
 
 __device__ __forceinline__ void plan_finish(const PlanArgs &a, unsigned long long emit_sum,
                                             unsigned long long len_sum,
-                                            unsigned long long f_sum = 0) {
+                                            unsigned long long f_sum = 0,
+                                            unsigned long long a_sum = 1) {  // 1: not known ASCII
   __shared__ unsigned long long s_e[LNT / 32], s_l[LNT / 32];
   __shared__ int s_last, s_f;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) s_f = 0;
   emit_sum = warp_sum64(emit_sum);
   len_sum = warp_sum64(len_sum);
-  const bool f_any = __any_sync(FULL, f_sum != 0);
+  const bool f_any = __any_sync(FULL, f_sum != 0), a_any = __any_sync(FULL, a_sum != 0);
   __syncthreads();
   if (lane == 0) {
     s_e[warp] = emit_sum;
     s_l[warp] = len_sum;
-    if (f_any) s_f = 1;
+    if (f_any) atomicOr(&s_f, 1);
+    if (a_any) atomicOr(&s_f, 2);
   }
   __syncthreads();
   if (tid == 0) {
@@ -2036,9 +2038,11 @@ __device__ __forceinline__ void plan_finish(const PlanArgs &a, unsigned long lon
     }
     st_relaxed(reinterpret_cast<uint64_t *>(a.plan + PLAN_HDR + blockIdx.x), e);
     atomicAdd(&a.ctr->accum, l);
-    // a flag, not a count: one plain store per CTA that saw a >= F0 byte (no atomic traffic)
-    if (s_f && *reinterpret_cast<volatile unsigned long long *>(&a.ctr->accf) == 0)
-      *reinterpret_cast<volatile unsigned long long *>(&a.ctr->accf) = 1;
+    // flags, not counts (bit 0: a >= F0 byte; bit 1: a byte >= 0x80, or not known to be
+    // ASCII): one atomic per CTA that adds a bit not yet set
+    const unsigned long long fl = (unsigned long long)s_f;
+    if (fl & ~*reinterpret_cast<volatile unsigned long long *>(&a.ctr->accf))
+      atomicOr(&a.ctr->accf, fl);
     __threadfence();
     s_last = (atomicAdd(&a.ctr->done, 1u) == gridDim.x - 1) ? 1 : 0;
   }
@@ -2080,7 +2084,10 @@ __device__ __forceinline__ void plan_finish(const PlanArgs &a, unsigned long lon
     a.plan[6] = (unsigned long long)a.win.lead;
     a.plan[7] = plan_halos(a.win);
     // nonzero iff the window (with the halo before it) holds a >= F0 byte (UTF-8 plans; f1)
-    a.plan[8] = *reinterpret_cast<volatile unsigned long long *>(&a.ctr->accf);
+    const unsigned long long fl = *reinterpret_cast<volatile unsigned long long *>(&a.ctr->accf);
+    a.plan[8] = fl & 1u;
+    // 0 iff no owned byte is >= 0x80 (UTF-8 plans: the all-ASCII widening copy's; UTF-16: 1)
+    a.plan[9] = (fl >> 1) & 1u;
     if (a.d_len) *a.d_len = L;
     a.ctr->accum = 0;
     a.ctr->accf = 0;
@@ -2193,6 +2200,7 @@ __global__ void __launch_bounds__(LNT) k_plan8(const PlanArgs a) {
   const long long nv = (h1 - h0) / 16;
   long long i = threadIdx.x;
   uint32_t fo = 0;  // >= F0 bytes seen (OR of their msb masks: only "any" matters per lane)
+  uint32_t ao = 0;  // OR of every owned byte (bit 7: a byte >= 0x80)
   unsigned long long fsum = 0;
   for (; i + 3 * LNT < nv; i += 4 * LNT) {
     uint4 q[4];
@@ -2200,23 +2208,28 @@ __global__ void __launch_bounds__(LNT) k_plan8(const PlanArgs a) {
     for (int j = 0; j < 4; j++) q[j] = __ldcs(v + i + j * LNT);
     uint32_t acc = 0;
 #pragma unroll
-    for (int j = 0; j < 4; j++)
+    for (int j = 0; j < 4; j++) {
       acc = len8_acc(q[j].w, len8_acc(q[j].z, len8_acc(q[j].y, len8_acc(q[j].x, acc, &fo), &fo),
                                       &fo), &fo);
+      ao |= q[j].x | q[j].y | q[j].z | q[j].w;
+    }
     sum += lane_sum(acc);
   }
   for (; i < nv; i += LNT) {
     const uint4 q = __ldcs(v + i);
     sum += lane_sum(len8_acc(q.w, len8_acc(q.z, len8_acc(q.y, len8_acc(q.x, 0u, &fo), &fo), &fo),
                              &fo));
+    ao |= q.x | q.y | q.z | q.w;
   }
   for (long long b = p0 + threadIdx.x; b < h0; b += LNT) {
     sum += len8_byte(base[b]);
     fsum += base[b] >= 0xF0u;
+    ao |= base[b];
   }
   for (long long b = h1 + threadIdx.x; b < p1; b += LNT) {
     sum += len8_byte(base[b]);
     fsum += base[b] >= 0xF0u;
+    ao |= base[b];
   }
   fsum += fo != 0u;
   // the window's halo bytes before position 0 count too (a 4-byte character begun there)
@@ -2226,7 +2239,7 @@ __global__ void __launch_bounds__(LNT) k_plan8(const PlanArgs a) {
   const unsigned long long emit = threadIdx.x == 0
       ? sum + (unsigned long long)(plan8_pending(w, p0) - plan8_pending(w, p1))
       : sum;
-  plan_finish(a, emit, sum, fsum);
+  plan_finish(a, emit, sum, fsum, (ao & HI) != 0u);
 }
 #elif defined(UG_PLAN8_PLANES)
 // UTF-8 plan on bit planes (the classifier's transposition, u8::planes32): a lane's 32 bytes ->
@@ -2462,6 +2475,12 @@ __global__ void __launch_bounds__(NTP, PlannedGeo<Pol>::MINB)
   const long long n_units = win.n / Pol::UNIT;
   Out *out = reinterpret_cast<Out *>(a.out);
 
+#ifndef UG_NO_PDL
+  // the kernels launched after this one in the planned call (the other forward form, the
+  // all-ASCII copy) only read the plan, written before this kernel: let them launch now, before
+  // this one returns early or works (programmatic dependent launch)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
   // the plan must describe this very input (else: UG_ERR_ARG from finish, no work)
   const bool bad = plan[0] != PLAN_TAG || plan[1] != (unsigned long long)(uintptr_t)win.base ||
                    plan[2] != (unsigned long long)win.n ||
@@ -2470,6 +2489,9 @@ __global__ void __launch_bounds__(NTP, PlannedGeo<Pol>::MINB)
   // (header word 8: the input's >= F0 bytes) picks the one that runs, the other returns here
   if constexpr (Pol::kNoF) {
     if ((!bad && plan[8] == 0) != NOF) return;
+#ifndef UG_NO_WIDEN8
+    if (NOF && !bad && plan[9] == 0) return;  // all ASCII: k_widen8's (launched after this one)
+#endif
   }
 #ifndef UG_NO_NARROW16
   // a window of ASCII words only is k_narrow16's (launched after this kernel)
@@ -2478,11 +2500,6 @@ __global__ void __launch_bounds__(NTP, PlannedGeo<Pol>::MINB)
   }
 #endif
   const long long nsub = bad ? 0 : (long long)plan[3], tps = bad ? 1 : (long long)plan[4];
-#ifndef UG_NO_PDL
-  // the paired launch (the other forward form / the narrowing copy) only reads the plan, written
-  // before this kernel: let it launch now (programmatic dependent launch)
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-#endif
   if (bad && tid == 0 && blockIdx.x == 0) atomicOr(&a.ctr->flags, 1ull);
   // producer (lane 0 of the last warp, not the shipping warp 0): tiles in sub-range order,
   // sub-ranges by ticket; the next ticket is drawn as a sub-range starts, so its L2 round trip
@@ -2836,6 +2853,70 @@ __global__ void __launch_bounds__(N16_THREADS, 4) k_narrow16(const TileArgs a,
   }
 }
 
+
+// a2 for a whole window of ASCII bytes (planned UTF-8 -> UTF-16, round 2 late; -DUG_NO_WIDEN8
+// builds without): the UTF-8 plan's header word 9 is 0 iff no owned byte is >= 0x80; such a
+// window is valid (every byte a 1-byte character) and its output is each byte
+// zero-extended.  As k_narrow16: the result written up front, a grid-stride
+// widening copy (one 8-byte load -> four PRMT -> one 16-byte store when the input is 8-byte
+// aligned at the output's 16-byte phase, byte loads otherwise), head / tail by block 0; the
+// third kernel of the forward's planned launch (programmatic dependent launch, like the pair).
+template <bool BE>
+__global__ void __launch_bounds__(N16_THREADS, 4) k_widen8(const TileArgs a,
+                                                         const unsigned long long *plan) {
+  const Window &win = a.win;
+  const long long n = win.n;
+  const bool bad = plan[0] != PLAN_TAG || plan[1] != (unsigned long long)(uintptr_t)win.base ||
+                   plan[2] != (unsigned long long)win.n ||
+                   plan[6] != (unsigned long long)win.lead || plan[7] != plan_halos(win);
+  if (bad || plan[9] != 0 || n <= 0) return;
+  const unsigned long long total = (unsigned long long)n;
+  const unsigned long long m = total < a.out_cap ? total : a.out_cap;  // units written
+  const int tid = threadIdx.x;
+  if (blockIdx.x == 0 && tid == 0) write_outcome(a, true, 0, NONE, total, 0, total);
+  constexpr uint32_t S0 = BE ? 0x1404u : 0x4140u, S1 = BE ? 0x3424u : 0x4342u;
+  const uint8_t *in = win.base;
+  uint16_t *out = reinterpret_cast<uint16_t *>(a.out);
+  unsigned long long h = ((16u - ((uintptr_t)out & 15u)) & 15u) / 2;  // out + h: 16-byte aligned
+  if (h > m) h = m;
+  const unsigned long long nb = (m - h) / 8, tl = h + 8 * nb;  // 8-unit items
+  const bool fast = (((uintptr_t)(in + h)) & 7u) == 0;
+  const unsigned long long stride = (unsigned long long)gridDim.x * N16_THREADS;
+  unsigned long long i = (unsigned long long)blockIdx.x * N16_THREADS + tid;
+  auto unit = [&](unsigned long long q) { return (uint16_t)(BE ? in[q] << 8 : in[q]); };
+  if (fast) {
+    const uint2 *src = reinterpret_cast<const uint2 *>(in + h);
+    uint4 *dst = reinterpret_cast<uint4 *>(out + h);
+    for (; i + 3 * stride < nb; i += 4 * stride) {
+      uint2 q[4];
+#pragma unroll
+      for (int j = 0; j < 4; j++) q[j] = __ldcs(src + i + j * stride);
+#pragma unroll
+      for (int j = 0; j < 4; j++)
+        __stcs(dst + i + j * stride, make_uint4(prmt(q[j].x, 0u, S0), prmt(q[j].x, 0u, S1),
+                                                prmt(q[j].y, 0u, S0), prmt(q[j].y, 0u, S1)));
+    }
+    for (; i < nb; i += stride) {
+      const uint2 q = __ldcs(src + i);
+      __stcs(dst + i, make_uint4(prmt(q.x, 0u, S0), prmt(q.x, 0u, S1), prmt(q.y, 0u, S0),
+                                 prmt(q.y, 0u, S1)));
+    }
+  } else {  // (unaligned phases: correctness, not speed)
+    for (; i < nb; i += stride) {
+      const unsigned long long q0 = h + 8 * i;
+      uint32_t v[4];
+#pragma unroll
+      for (int j = 0; j < 4; j++)
+        v[j] = unit(q0 + 2 * j) | ((uint32_t)unit(q0 + 2 * j + 1) << 16);
+      *reinterpret_cast<uint4 *>(out + q0) = make_uint4(v[0], v[1], v[2], v[3]);
+    }
+  }
+  if (blockIdx.x == 0) {
+    if ((unsigned long long)tid < h) out[tid] = unit(tid);
+    if ((unsigned long long)tid < m - tl) out[tl + tid] = unit(tl + tid);
+  }
+}
+
 // ============================================================================ combine
 __host__ __device__ inline void combine_impl(const RecordDev *recs, int nranks, int rank,
                                              unsigned long long total_in, ResultDev *res,
@@ -3116,11 +3197,16 @@ static cudaError_t launch_paired(void (*fn)(Args...), int grid, int threads, siz
 // kernels one launch_planned enqueues (the two forward forms; the reverse's tile kernel and
 // narrowing copy): what the launch counter adds
 int planned_kernels(Op op) {
+  if (op_u16_input(op)) {
 #ifdef UG_NO_NARROW16
-  if (op_u16_input(op)) return 1;
+    return 1;
 #endif
-  (void)op;
+    return 2;
+  }
+#ifdef UG_NO_WIDEN8
   return 2;
+#endif
+  return 3;
 }
 cudaError_t launch_planned(Op op, const TileArgs &a, const unsigned long long *plan, int grid,
                            cudaStream_t s) {
@@ -3131,16 +3217,28 @@ cudaError_t launch_planned(Op op, const TileArgs &a, const unsigned long long *p
       k_transcode_planned<U8Pol><<<grid, NTP, sm, s>>>(a, plan);
 #ifndef UG_NO_PDL
       launch_paired(k_transcode_planned<U8Pol, true>, grid, NTP, sm, s, a, plan);
+#ifndef UG_NO_WIDEN8
+      launch_paired(k_widen8<false>, grid, N16_THREADS, 0, s, a, plan);
+#endif
 #else
       k_transcode_planned<U8Pol, true><<<grid, NTP, sm, s>>>(a, plan);
+#ifndef UG_NO_WIDEN8
+      k_widen8<false><<<grid, N16_THREADS, 0, s>>>(a, plan);
+#endif
 #endif
       break;
     case Op::U8_TO_U16BE:
       k_transcode_planned<U8PolBE><<<grid, NTP, sm, s>>>(a, plan);
 #ifndef UG_NO_PDL
       launch_paired(k_transcode_planned<U8PolBE, true>, grid, NTP, sm, s, a, plan);
+#ifndef UG_NO_WIDEN8
+      launch_paired(k_widen8<true>, grid, N16_THREADS, 0, s, a, plan);
+#endif
 #else
       k_transcode_planned<U8PolBE, true><<<grid, NTP, sm, s>>>(a, plan);
+#ifndef UG_NO_WIDEN8
+      k_widen8<true><<<grid, N16_THREADS, 0, s>>>(a, plan);
+#endif
 #endif
       break;
     // UTF-16 input: the tile kernel, then the all-ASCII narrowing copy; the plan's total

@@ -303,3 +303,65 @@ def test_planned_shards_ascii_and_mixed():
     records = ug.decode_records(recs)
     got = np.concatenate([outs[k][: records[k].count].cpu().numpy() for k in range(G)])
     assert np.array_equal(got, ref_o)
+
+
+@pytest.mark.parametrize("n", [1, 7, 8, 9, 100, 4097, 3 * TILE + 5, (1 << 20) + 3])
+def test_planned_all_ascii_widening(n):
+    """A window of ASCII bytes only is the widening copy's (k_widen8, selected by the UTF-8
+    plan's header word 9): every input and output address phase, capacities below the need,
+    and inputs with one non-ASCII byte (valid, or invalid) back on the tile kernels."""
+    rng = np.random.default_rng(n + 1)
+    a = rng.integers(0, 0x80, n).astype(np.uint8)
+    ref_r, ref_o = oracle.utf8_to_utf16le(a)
+    for off in (0, 1, 7, 8):
+        _, t = to_dev(a, pad_before=off, pad_after=64)
+        for oo in (0, 1, 3, 8):
+            big = torch.full((n + oo + 64,), 0x5A5A, dtype=torch.int16, device=DEV)
+            r, ln = ug.utf8_to_utf16le_two_pass(t, big[oo:oo + n], n=n, out_cap=n)
+            o = big.cpu().numpy().view(np.uint16)
+            assert tuple(r) == tuple(ref_r) and ln == n
+            assert np.array_equal(o[oo:oo + n], ref_o)
+            assert np.all(o[:oo] == 0x5A5A) and np.all(o[oo + n:] == 0x5A5A)
+    for cap in (0, n - 1, n // 2):
+        check8(a, cap=cap)
+    if n >= 2:
+        v = a.copy()
+        v[n // 2] = 0x80  # a lone continuation byte: an error, on the tile kernel
+        check8(v, offset=1)
+        v[n // 2 - 1:n // 2 + 1] = (0xC3, 0xA9)  # a valid 2-byte character
+        check8(v)
+
+
+def test_planned_fwd_shards_ascii_and_mixed():
+    """UTF-8 shards of one buffer through the planned shard form, some all ASCII (widening
+    copy), some mixed (tile kernels), records combined: equal to the unsharded oracle."""
+    rng = np.random.default_rng(98)
+    asc = rng.integers(0x20, 0x7F, 400000).astype(np.uint8)
+    mixed = np.frombuffer(synth.gen_chunk("mixed", "utf8", 90000, 4, 90000), dtype=np.uint8)
+    a = np.concatenate([asc, mixed, asc[:200001]])
+    n = a.size
+    cuts = [0, 200003, 400000, 400000 + mixed.size, 400000 + mixed.size + 100000, n]
+    _, t = to_dev(a)
+    G = len(cuts) - 1
+    recs = ug.record_buffer(DEV, G)
+    outs = []
+    for k in range(G):
+        lo, hi = cuts[k], cuts[k + 1]
+        hb, ha = min(lo, 3), min(n - hi, 3)
+        out = torch.zeros(hi - lo, dtype=torch.int16, device=DEV)
+        plan = ug.plan_buffer(DEV)
+        lens = torch.zeros(1, dtype=torch.int64, device=DEV)
+        ug.utf8_shard_plan_async(t, lo, hi - lo, hb, ha, lens, plan)
+        ug.utf8_to_utf16le_shard_planned_async(t, lo, hi - lo, hb, ha, lo, plan, out, recs,
+                                               rec_off=k * ug.RECORD_BYTES)
+        outs.append(out)
+    res = ug.result_buffer(DEV, 1)
+    ug.combine_records_async(recs, G, 0, n, res)
+    torch.cuda.synchronize()
+    (r,) = ug.decode_results(res)
+    ref_r, ref_o = oracle.utf8_to_utf16le(a)
+    assert tuple(r) == tuple(ref_r)
+    records = ug.decode_records(recs)
+    got = np.concatenate([outs[k][: records[k].count].cpu().numpy().view(np.uint16)
+                          for k in range(G)])
+    assert np.array_equal(got, ref_o)
