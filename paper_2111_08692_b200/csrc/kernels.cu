@@ -2477,9 +2477,11 @@ __global__ void __launch_bounds__(NTP, PlannedGeo<Pol>::MINB)
 
 #ifndef UG_NO_PDL
   // the kernels launched after this one in the planned call (the other forward form, the
-  // all-ASCII copy) only read the plan, written before this kernel: let them launch now, before
-  // this one returns early or works (programmatic dependent launch)
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  // all-ASCII copies) only read the plan, written before this kernel: let them launch now
+  // (programmatic dependent launch).  UTF-8 input: as the first instruction, so a form that
+  // returns at once does not delay the next; UTF-16 input: after the exit test below (measured:
+  // the narrowing copy of an ASCII window runs best launched once this kernel has returned)
+  if constexpr (Pol::UNIT == 1) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 #endif
   // the plan must describe this very input (else: UG_ERR_ARG from finish, no work)
   const bool bad = plan[0] != PLAN_TAG || plan[1] != (unsigned long long)(uintptr_t)win.base ||
@@ -2500,6 +2502,9 @@ __global__ void __launch_bounds__(NTP, PlannedGeo<Pol>::MINB)
   }
 #endif
   const long long nsub = bad ? 0 : (long long)plan[3], tps = bad ? 1 : (long long)plan[4];
+#ifndef UG_NO_PDL
+  if constexpr (Pol::UNIT == 2) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+#endif
   if (bad && tid == 0 && blockIdx.x == 0) atomicOr(&a.ctr->flags, 1ull);
   // producer (lane 0 of the last warp, not the shipping warp 0): tiles in sub-range order,
   // sub-ranges by ticket; the next ticket is drawn as a sub-range starts, so its L2 round trip
