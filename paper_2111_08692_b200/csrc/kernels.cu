@@ -821,7 +821,6 @@ struct VGeo {
   static constexpr int THREADS = VC + 32;
   static constexpr int MINB = Pol::UNIT == 1 ? (VH > 1 ? 4 : 2) : 3;
 };
-constexpr int VNT = NT + 32;
 #ifndef UG_VRING8
 #define UG_VRING8 3
 #endif
@@ -3032,7 +3031,7 @@ int tile_threads(Op op) {
     case Op::U8_VALIDATE: return VGeo<U8Pol>::THREADS;
 #if !(!defined(UG_VALIDATE_STREAM) && !defined(UG_VAL16_TMA))
     case Op::U16_VALIDATE:
-    case Op::U16BE_VALIDATE: return VNT;
+    case Op::U16BE_VALIDATE: return VGeo<U16Pol>::THREADS;
 #endif
 #endif
     default: return NT;
