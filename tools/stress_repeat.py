@@ -1,6 +1,6 @@
-"""Race check by repetition: run each transcoder many times on the same inputs (several start
-alignments, one input with an injected error) and require bit-identical outputs and results
-every time.  Development tool: python tools/stress_repeat.py [iterations]"""
+"""Race check by repetition: run each transcoder (single-pass and two-pass) many times on the
+same inputs (several start alignments, one input with an injected error) and require
+bit-identical outputs and results every time.  Development tool: python tools/stress_repeat.py [iterations]"""
 import sys
 import numpy as np
 import torch
@@ -37,5 +37,16 @@ for name, buf in (("clean", x), ("error", bad)):
             if tuple(q) != tuple(q0) or not torch.equal(o8[: q.written], ref8):
                 fails += 1
                 print("REVERSE MISMATCH", name, off, k, q, q0)
+            # the two-pass (planned) path, the bench's: the same results and units every time
+            o16.fill_(0 if k % 2 else 0x5A5A)
+            rp, _ = ug.utf8_to_utf16le_two_pass(t8, o16)
+            if tuple(rp) != tuple(r0) or not torch.equal(o16[: rp.written], ref16):
+                fails += 1
+                print("PLANNED FORWARD MISMATCH", name, off, k, rp, r0)
+            o8.fill_(0 if k % 2 else 0x5A)
+            qp, _ = ug.utf16le_to_utf8_two_pass(u16, o8)
+            if tuple(qp) != tuple(q0) or not torch.equal(o8[: qp.written], ref8):
+                fails += 1
+                print("PLANNED REVERSE MISMATCH", name, off, k, qp, q0)
         print(name, off, "forward", tuple(r0), "reverse", tuple(q0), "ok" if not fails else fails)
 print("STRESS", "PASS" if fails == 0 else f"FAIL {fails}")
